@@ -1,0 +1,330 @@
+"""CPU restatement of the reference's calibrate + RX hot path (numpy / LAPACK).
+
+TEST INFRASTRUCTURE (oracle/): this module is the *checker*.  Only tests/,
+``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` / ``--impl
+reference`` legs may import it.  The product (paper_2602_13509_b200) never
+routes through it; its ops fail loudly when the CUDA library is missing.
+
+Each function restates one reference function over plain arrays and cites the
+reference line it follows (paths relative to /root/reference/pkg/src/skyrx).
+Pinned against the reference itself: tests/golden/*.npz were produced by
+importing the real `skyrx` package (tests/golden/make_golden.py) and
+tests/test_oracle.py checks this module against every fixture.
+
+Three rows of SURVEY.md §8(a) have no reference implementation; their frozen
+definitions live here (R-TOPK ``topk_threshold``/``topk_mask``, R-STREAM
+``StreamingStats``, R-GLOBAL ``moments``/``combine_moments``/``finalize_moments``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+from scipy.linalg import cho_solve, solve_triangular
+
+# rx.py:23 — diagonal-loading ladder tried after the unridged attempt
+RIDGE_EPSILONS = (1e-10, 1e-9, 1e-8, 1e-7, 1e-6)
+BAND_KEEP_MIN_NM = 400.0   # calibrate.py:23
+BAND_KEEP_MAX_NM = 1000.0  # calibrate.py:24
+RGB_TARGETS_NM = (640.0, 550.0, 460.0)  # calibrate.py:25
+
+
+# --------------------------------------------------------------------------- calibration
+def line_gains(gains) -> np.ndarray:
+    """calibrate.py:83-87 — per-line gains as float32, all strictly positive."""
+    g = np.asarray(gains, dtype=np.float32)
+    if not (g > 0).all():
+        raise ValueError("every line gain must be positive")
+    return g
+
+
+def _check_tables(shape, dark, coeff):
+    # calibrate.py:92-96 / 150-154
+    if tuple(dark.shape) != (shape[1], shape[2]):
+        raise ValueError(
+            f"invalid tables: shape ({dark.shape[0]}, {dark.shape[1]}) does not "
+            f"match cube ({shape[1]}, {shape[2]})"
+        )
+
+
+def apply_calibration(raw, dark, coeff, gains) -> np.ndarray:
+    """calibrate.py:90-102: max(0, f32(raw) - dark) * coeff / gain[l], each op f32 RN."""
+    raw = np.asarray(raw)
+    dark = np.asarray(dark, np.float32)
+    coeff = np.asarray(coeff, np.float32)
+    _check_tables(raw.shape, dark, coeff)
+    g = line_gains(gains)
+    x = raw.astype(np.float32) - dark[None]
+    np.maximum(x, np.float32(0.0), out=x)
+    x *= coeff[None]
+    x /= g[:, None, None]
+    return x
+
+
+def keep_bands(wavelengths) -> np.ndarray:
+    """calibrate.py:105-114 — boolean keep mask for centres in [400, 1000] nm."""
+    w = np.asarray(wavelengths, dtype=np.float64)
+    return (w >= BAND_KEEP_MIN_NM) & (w <= BAND_KEEP_MAX_NM)
+
+
+def band_nearest(wavelengths, target) -> int:
+    """cube.py:187-195 — argmin |w - target|, ties to the lower index."""
+    w = np.asarray(wavelengths, dtype=np.float64)
+    if w.size == 0:
+        raise ValueError("wavelength list is empty")
+    return int(np.argmin(np.abs(w - target)))
+
+
+def sequential_sum_f32(x: np.ndarray) -> np.ndarray:
+    """Last-axis f32 sum, strictly left to right: ((a0+a1)+a2)+...
+
+    This is the order the reference actually gets at calibrate.py:173 (and
+    bin_bands, calibrate.py:122-124): ``block[:, :, keep]`` is a boolean index
+    on the last axis, which numpy materialises band-major (strides
+    (S*4, 4, L*S*4)), so the reduction over each group of ``factor`` bands
+    accumulates one band at a time for every factor.  Verified bit-exact
+    against the reference for factor 4 and 8 (tests/test_oracle.py)."""
+    x = np.asarray(x, np.float32)
+    acc = x[..., 0].copy()
+    for j in range(1, x.shape[-1]):
+        acc += x[..., j]
+    return acc
+
+
+def binned_centers(wavelengths, factor):
+    keep = keep_bands(wavelengths)
+    kept = int(keep.sum())
+    if factor < 1 or kept % factor != 0:
+        raise ValueError(f"band count {kept} not divisible by factor {factor}")
+    return np.asarray(wavelengths, np.float64)[keep].reshape(kept // factor, factor).mean(axis=1)
+
+
+def calibrate_bin_rgb(raw, wavelengths, dark, coeff, gains, factor=4, chunk_lines=64):
+    """calibrate.py:135-176 — calibrate, drop out-of-range bands, sum ``factor``
+    consecutive bands left to right in f32, then pick RGB planes."""
+    raw = np.asarray(raw)
+    dark = np.asarray(dark, np.float32)
+    coeff = np.asarray(coeff, np.float32)
+    _check_tables(raw.shape, dark, coeff)
+    g = line_gains(gains)
+    keep = keep_bands(wavelengths)
+    centers = binned_centers(wavelengths, factor)
+    nb = centers.shape[0]
+    L, S = raw.shape[:2]
+    out = np.empty((L, S, nb), np.float32)
+    for lo in range(0, L, chunk_lines):
+        hi = min(L, lo + chunk_lines)
+        x = raw[lo:hi].astype(np.float32) - dark[None]
+        np.maximum(x, np.float32(0.0), out=x)
+        x *= coeff[None]
+        x /= g[lo:hi, None, None]
+        x = x[:, :, keep].reshape(hi - lo, S, nb, factor)
+        out[lo:hi] = sequential_sum_f32(x)
+    rgb_idx = [band_nearest(centers, t) for t in RGB_TARGETS_NM]
+    rgb = np.ascontiguousarray(out[:, :, rgb_idx])
+    return out, centers, rgb
+
+
+# --------------------------------------------------------------------------- statistics
+@dataclass(frozen=True)
+class Stats:
+    """rx.py:26-39 CubeStats, as plain arrays."""
+
+    mu: np.ndarray
+    sigma: np.ndarray
+    sigma_inv: np.ndarray
+    ridge_used: float
+    chol_lower: np.ndarray
+
+
+def factor_covariance(mu, cov) -> Stats:
+    """rx.py:68-86 — ridge-escalated Cholesky and the symmetric inverse."""
+    bands = cov.shape[0]
+    trace = float(np.trace(cov))
+    scale = trace / bands if trace > 0 else 1.0
+    chol = None
+    ridge = 0.0
+    for eps in (0.0,) + RIDGE_EPSILONS:
+        ridge = eps * scale
+        try:
+            chol = np.linalg.cholesky(cov + ridge * np.eye(bands))
+            break
+        except np.linalg.LinAlgError:
+            continue
+    if chol is None:
+        raise ValueError("covariance not positive definite even after ridging")
+    inv = cho_solve((chol, True), np.eye(bands), check_finite=False)
+    inv = (inv + inv.T) / 2.0
+    return Stats(mu=mu, sigma=cov, sigma_inv=inv, ridge_used=ridge, chol_lower=chol)
+
+
+def compute_stats(values, chunk: int = 65536) -> Stats:
+    """rx.py:42-86 — two-pass f64 mean and unbiased covariance over all pixels."""
+    values = np.asarray(values, np.float32)
+    bands = values.shape[-1]
+    px = values.reshape(-1, bands)
+    n = px.shape[0]
+    if n <= bands:
+        raise ValueError(f"insufficient samples: {n} pixels for {bands} bands")
+    if not np.isfinite(values).all():
+        raise ValueError("invalid data: cube contains non-finite values")
+    mu = np.zeros(bands)
+    for a in range(0, n, chunk):
+        mu += px[a:a + chunk].astype(np.float64).sum(axis=0)
+    mu /= n
+    cov = np.zeros((bands, bands))
+    for a in range(0, n, chunk):
+        d = px[a:a + chunk].astype(np.float64) - mu
+        cov += d.T @ d
+    cov /= n - 1
+    cov = (cov + cov.T) / 2.0
+    return factor_covariance(mu, cov)
+
+
+# --------------------------------------------------------------------------- scoring
+def mahalanobis_sq(pixels, mu, chol_lower, chunk: int = 65536) -> np.ndarray:
+    """_accel.py:33-47 — delta = ||L^-1 (x - mu)||^2 per row, float64."""
+    pixels = np.asarray(pixels)
+    n = pixels.shape[0]
+    out = np.empty(n)
+    for a in range(0, n, chunk):
+        d = pixels[a:a + chunk].astype(np.float64) - mu
+        y = solve_triangular(chol_lower, d.T, lower=True, check_finite=False)
+        out[a:a + chunk] = np.einsum("bn,bn->n", y, y)
+    return out
+
+
+def rx_scores(values, stats: Stats) -> np.ndarray:
+    """rx.py:89-97 — f64 scores cast to f32, shaped (lines, samples)."""
+    values = np.asarray(values, np.float32)
+    if stats.mu.shape[0] != values.shape[-1]:
+        raise ValueError(
+            f"stats fitted for {stats.mu.shape[0]} bands, cube has {values.shape[-1]}"
+        )
+    d = mahalanobis_sq(values.reshape(-1, values.shape[-1]), stats.mu, stats.chol_lower)
+    return d.reshape(values.shape[:2]).astype(np.float32)
+
+
+def max_score(scores) -> float:
+    """cube.py:174-176."""
+    s = np.asarray(scores, np.float32)
+    return float(s.max()) if s.size else 0.0
+
+
+def normalize_scores(scores) -> np.ndarray:
+    """rx.py:100-105 — divide by f32(max); unchanged when max <= 0."""
+    s = np.asarray(scores, np.float32)
+    m = max_score(s)
+    if m <= 0.0:
+        return s
+    return s / np.float32(m)
+
+
+def threshold_scores(norm_scores, threshold: float) -> np.ndarray:
+    """rx.py:108-112 — strict ``>`` compare in f32 (numpy 2 / NEP 50 semantics)."""
+    if not 0.0 <= threshold <= 1.0:
+        raise ValueError(f"threshold {threshold} outside [0, 1]")
+    return np.asarray(norm_scores, np.float32) > np.float32(threshold)
+
+
+def transmit_domain(values, max_score_: float) -> np.ndarray:
+    """rx.py:115-124 — sqrt(v / max) in f64, zeros when max <= 0."""
+    v = np.asarray(values, dtype=np.float64)
+    if max_score_ <= 0.0:
+        return np.zeros_like(v)
+    return np.sqrt(np.clip(v / max_score_, 0.0, None))
+
+
+# --------------------------------------------------------------------------- R-TOPK (new)
+def topk_count(n: int, fraction_per_mille: int = 1) -> int:
+    """k = ceil(n * 0.001) computed in integers (SURVEY.md §8(a) R-TOPK)."""
+    return (n * fraction_per_mille + 999) // 1000
+
+
+def topk_threshold(scores, k: int | None = None) -> float:
+    """The (k+1)-th largest f32 score; -inf when k >= N (everything selected)."""
+    s = np.asarray(scores, np.float32).ravel()
+    n = s.size
+    if k is None:
+        k = topk_count(n)
+    if k >= n:
+        return float("-inf")
+    return float(np.partition(s, n - k - 1)[n - k - 1])
+
+
+def topk_mask(scores, k: int | None = None) -> np.ndarray:
+    """R-TOPK: mask = delta > delta_(k+1) (strict, like rx.py:112)."""
+    s = np.asarray(scores, np.float32)
+    t = topk_threshold(s, k)
+    if t == float("-inf"):
+        return np.ones(s.shape, bool)
+    return s > np.float32(t)
+
+
+# --------------------------------------------------------------------------- R-GLOBAL / R-STREAM (new)
+def moments(values, shift) -> tuple[float, np.ndarray, np.ndarray]:
+    """Shifted f64 moments (n, sum(x-c), sum((x-c)(x-c)^T)) of one block."""
+    px = np.asarray(values, np.float32).reshape(-1, np.asarray(shift).shape[0])
+    d = px.astype(np.float64) - np.asarray(shift, np.float64)
+    return float(px.shape[0]), d.sum(axis=0), d.T @ d
+
+
+def combine_moments(parts):
+    """Sum of per-shard moments sharing one shift (the NCCL all-reduce payload)."""
+    n = sum(p[0] for p in parts)
+    s = sum(p[1] for p in parts)
+    q = sum(p[2] for p in parts)
+    return n, s, q
+
+
+def finalize_moments(n, s, q, shift, bands=None) -> Stats:
+    """mu = c + s/n; sigma = (Q - s s^T / n) / (n - 1), symmetrised; then rx.py:68-86."""
+    shift = np.asarray(shift, np.float64)
+    bands = shift.shape[0] if bands is None else bands
+    if n <= bands:
+        raise ValueError(f"insufficient samples: {n} pixels for {bands} bands")
+    mu = shift + s / n
+    cov = (q - np.outer(s, s) / n) / (n - 1)
+    cov = (cov + cov.T) / 2.0
+    return factor_covariance(mu, cov)
+
+
+class StreamingStats:
+    """R-STREAM: exponential-forgetting background, score each chunk after folding it in.
+
+    State (n, s, Q) in f64 around a fixed shift c = f64 mean of chunk 0.
+    Update per chunk: n <- lam*n + m, s <- lam*s + sum(x-c), Q <- lam*Q + sum((x-c)(x-c)^T).
+    For chunk 0 this is exactly compute_stats(chunk 0) up to rounding.
+    """
+
+    def __init__(self, bands: int, forget: float = 0.99):
+        self.bands = bands
+        self.forget = forget
+        self.shift = None
+        self.n = 0.0
+        self.s = np.zeros(bands)
+        self.q = np.zeros((bands, bands))
+
+    def update(self, values) -> Stats:
+        px = np.asarray(values, np.float32).reshape(-1, self.bands)
+        if not np.isfinite(px).all():
+            raise ValueError("invalid data: cube contains non-finite values")
+        if self.shift is None:
+            self.shift = px.astype(np.float64).mean(axis=0)
+        m, s, q = moments(px, self.shift)
+        lam = self.forget
+        self.n = lam * self.n + m
+        self.s = lam * self.s + s
+        self.q = lam * self.q + q
+        return finalize_moments(self.n, self.s, self.q, self.shift, self.bands)
+
+
+# --------------------------------------------------------------------------- whole path
+def detect(raw, dark, coeff, gains, k: int | None = None):
+    """raw -> radiance -> stats -> f32 scores -> top-0.1% mask (one global background)."""
+    rad = apply_calibration(raw, dark, coeff, gains)
+    stats = compute_stats(rad)
+    scores = rx_scores(rad, stats)
+    mask = topk_mask(scores, k)
+    return stats, scores, mask
