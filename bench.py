@@ -1,0 +1,365 @@
+"""Throughput of the fused calibrate + RX hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c4|c1|c3|c5] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Default workload = BASELINE config 4 ("multi-strip batch"): 64 independent
+strips of 16384 lines x 900 samples x 70 bands of 12-bit raw counts, each
+with its own seeded mixture (seed 4000+i) and its own background; strips are
+dealt round-robin to ranks (no collective).  One step = every strip of this
+rank through raw -> shift -> fused calibrate+moments -> batched Cholesky /
+inverse -> fused calibrate+score -> top-0.1% radix select -> mask.  Inputs
+are generated on the device (bit-identical to oracle/synth.py) and resident
+in HBM before timing; the inputs (132 GB at N=1) exceed L2 many times over.
+
+`value` = pixels of all ranks / max-over-ranks device time of K steps.
+`e2e`   = the same path through the public API `detect()` on HOST numpy
+          cubes (H2D of raw + D2H of scores, mask and stats inside the
+          timed region), over a bounded number of strips per step.
+`--impl reference` times the CPU oracle port (oracle/skyrx_oracle.py, the
+reference's numpy/LAPACK path) on a bounded sample on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(lines=2048, samples=900, bands=70, components=5, seed=1, strips=1),
+    "c3": dict(lines=8192, samples=1024, bands=270, components=8, seed=3, strips=1),
+    "c4": dict(lines=16384, samples=900, bands=70, components=5, seed=4000, strips=64),
+    "c5": dict(lines=131072, samples=2048, bands=128, components=5, seed=5, strips=1),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--strips", type=int, default=None, help="override strip count (testing)")
+    ap.add_argument("--lines", type=int, default=None, help="override lines per strip (testing)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-strips", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def bytes_per_pixel(bands: int) -> int:
+    # 2B raw read (moments) + 2B raw read (score) + 4 (f32 delta) + 1 (mask)
+    return 4 * bands + 5
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/skyrx_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    from oracle import skyrx_oracle as O
+    from oracle import synth as osynth
+
+    lines = args.lines or cfg["lines"]
+    sample_lines = min(lines, 512 if cfg["bands"] <= 128 else 96)
+    t = osynth.make_tables(cfg["seed"], cfg["samples"], cfg["bands"], cfg["components"])
+    raw = osynth.generate_lines(t, 0, sample_lines)
+    gains = np.ones(sample_lines)
+    for _ in range(max(args.warmup, 1)):
+        O.detect(raw, t.dark, t.coeff, gains)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.detect(raw, t.dark, t.coeff, gains)
+        times.append(time.perf_counter() - t0)
+    px = sample_lines * cfg["samples"]
+    sec = float(np.mean(times))
+    value = px / sec
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "calibrated+RX-scored pixels/sec", "value": value,
+        "unit": "pixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle/synth.py, seeded)",
+        "config": config_key(args, cfg, world),
+        "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample_lines} lines x {cfg['samples']} samples of strip 0 "
+                                   f"(seed {cfg['seed']}), full oracle detect path "
+                                   "(numpy/OpenBLAS/LAPACK, all host threads)"},
+        "e2e": {"value": value, "unit": "pixels/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_key(args, cfg, world):
+    lines = args.lines or cfg["lines"]
+    strips = args.strips or cfg["strips"]
+    return {"workload": {"c1": "single strip 2048x900x70", "c3": "high-band cube 8192x1024x270",
+                         "c4": "multi-strip batch 64 x (16384x900x70)",
+                         "c5": "global mosaic 131072x2048x128"}[args.config]
+            + ("" if (args.lines is None and args.strips is None) else " (resized)"),
+            "config": args.config, "lines": lines, "samples": cfg["samples"],
+            "bands": cfg["bands"], "strips": strips, "parallelism": f"strips/dp{world}",
+            "l2": "inputs larger than L2 (no flush needed)"
+            if strips * lines * cfg["samples"] * cfg["bands"] * 2 > 4 * 126e6 else
+            "L2 flushed between steps"}
+
+
+# ----------------------------------------------------------------------------- b200 arm
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2602_13509_b200 as P
+    from paper_2602_13509_b200 import _dev
+    from paper_2602_13509_b200.synth import Scene
+
+    lines = args.lines or cfg["lines"]
+    S, B = cfg["samples"], cfg["bands"]
+    nstrips = args.strips or cfg["strips"]
+    mine = list(range(rank, nstrips, world))
+    npix = lines * S
+    scenes = [Scene(cfg["seed"] + i if nstrips > 1 else cfg["seed"], S, B, cfg["components"])
+              for i in mine]
+    raws = [sc.generate(0, lines) for sc in scenes]
+    tabs = [(_dev.to_device(sc.dark), _dev.to_device(sc.coeff)) for sc in scenes]
+    gains = _dev.to_device(np.ones(lines, np.float32))
+    plan = P.DetectPlan(lines, S, B, batch=len(mine))
+    stream = torch.cuda.current_stream()
+    flush = None
+    if len(mine) * npix * B * 2 <= 4 * 126e6:
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    ev = {"gram": [], "score": []}
+
+    def step(instrument=False):
+        if flush is not None:
+            flush.zero_()
+        for j in range(len(mine)):
+            raw = raws[j]
+            d, c = tabs[j]
+            if instrument:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            plan.run(j, raw, d, c, gains)
+            if instrument:
+                b.record(stream)
+                ev["gram"].append((a, b))
+        plan.finalize()
+        for j in range(len(mine)):
+            d, c = tabs[j]
+            if instrument:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            plan.score(j, raws[j], d, c, gains)
+            if instrument:
+                b.record(stream)
+                ev["score"].append((a, b))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    plan.ds.check(0, npix)
+    launches0 = plan.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            step(instrument=True)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    launches = (plan.launches - launches0) // args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_px = nstrips * npix * args.steps
+    value = total_px / (ms / 1e3)
+
+    # dominant kernel and its roofline (events bracket each launch on `stream`)
+    gram_ms = np.mean([a.elapsed_time(b) for a, b in ev["gram"]])
+    score_ms = np.mean([a.elapsed_time(b) for a, b in ev["score"]])
+    peak, peak_kind = load_peaks()
+    if gram_ms >= score_ms:
+        dom, dom_ms, dom_bytes = "stats (shift+gram_kernel+reduce)", gram_ms, npix * 2 * B
+    else:
+        dom, dom_ms, dom_bytes = ("score (score_kernel+topk+mask)", score_ms,
+                                  npix * (2 * B + 4 + 1) + 3 * 4 * npix)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(dom.split()[0])
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "calibrated+RX-scored pixels/sec", "value": value, "unit": "pixels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (fp64 stats accumulation, fp64 factorisation)",
+        "data": "synthetic (seeded device generator, bit-identical to oracle/synth.py)",
+        "config": config_key(args, cfg, world),
+        "hbm_fraction_whole_path": value / world * bytes_per_pixel(B) / (peak * 1e9),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
+                     "stats_ms_per_strip": gram_ms, "score_ms_per_strip": score_ms},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = measure_e2e(args, P, cfg, lines, scenes[: max(1, args.e2e_strips)])
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, raws[0], scenes[0], lines)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(args, P, cfg, lines, scenes):
+    """Public API on host numpy cubes: H2D raw, D2H scores+mask+stats, per strip."""
+    import torch
+
+    S, B = cfg["samples"], cfg["bands"]
+    hosts = []
+    for sc in scenes:
+        raw = sc.generate(0, lines).cpu().pin_memory().numpy()
+        hosts.append((P.RawCube(raw, np.linspace(400, 1000, B), gains=np.ones(lines, np.float32)),
+                      P.CalibrationTables(sc.dark, sc.coeff)))
+    plan = P.DetectPlan(lines, S, B)
+    for cube, tab in hosts[:1]:
+        P.detect(cube, tab, plan=plan)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps = max(1, min(args.steps, 3))
+    for _ in range(steps):
+        for cube, tab in hosts:
+            det = P.detect(cube, tab, plan=plan)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    px = lines * S * len(hosts) * steps
+    h2d = lines * S * B * 2 * len(hosts)
+    d2h = lines * S * (4 + 1) * len(hosts)
+    return {"value": px / sec, "unit": "pixels/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "strips_per_step": len(hosts),
+            "api": "paper_2602_13509_b200.detect(RawCube[numpy], CalibrationTables)",
+            "last_threshold": det.threshold}
+
+
+def cpu_baseline(cfg, raw_dev, scene, lines):
+    from oracle import skyrx_oracle as O
+
+    sample = min(lines, 512 if cfg["bands"] <= 128 else 96)
+    raw = raw_dev[:sample].cpu().numpy()
+    gains = np.ones(sample)
+    O.detect(raw, scene.dark, scene.coeff, gains)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        O.detect(raw, scene.dark, scene.coeff, gains)
+        reps += 1
+        if time.perf_counter() - t0 > 10.0 or reps >= 20:
+            break
+    sec = (time.perf_counter() - t0) / reps
+    return {"value": sample * cfg["samples"] / sec, "unit": "pixels/s", "cores": os.cpu_count(),
+            "kind": "port", "sample": f"{sample} lines x {cfg['samples']} samples of strip 0, "
+                                      f"oracle detect (numpy/OpenBLAS/LAPACK), {reps} reps"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * skyrx_b200.h — C ABI of the B200 (sm_100a) calibrate + RX hot path.
+ *
+ * Drop-in boundary for the reference package `skyrx` (arXiv 2602.13509,
+ * /root/reference/pkg/src/skyrx).  The reference is Python; its only native
+ * slot on this path is `skyrx._accel` (numba, _accel.py:19-31 / 109-131).  A
+ * maintainer binds this library with ctypes exactly as INTEGRATION.md shows;
+ * paper_2602_13509_b200/_lib.py is that binding.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless its name ends in _host;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - cubes are C-order (lines, samples, bands), bands innermost (BIP,
+ *     cube.py:80-105); pixel n = line * samples + sample;
+ *   - every call is asynchronous on `stream`, re-entrant and thread-safe (no
+ *     global scratch: callers pass workspaces), and returns an int status;
+ *     skyrx_last_error() gives the calling thread's last message;
+ *   - results are deterministic: no floating-point atomics anywhere.
+ */
+#ifndef SKYRX_B200_H_
+#define SKYRX_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* status codes (host return values and per-matrix device status words) */
+#define SKYRX_OK 0
+#define SKYRX_ERR_ARG 1          /* bad argument; message in skyrx_last_error()  */
+#define SKYRX_ERR_CUDA 2         /* CUDA runtime error                           */
+#define SKYRX_ERR_INSUFFICIENT 3 /* rx.py:51-52 "insufficient samples"          */
+#define SKYRX_ERR_NONFINITE 4    /* rx.py:53-54 "non-finite values"             */
+#define SKYRX_ERR_NOT_PD 5       /* rx.py:79-80 "not positive definite ..."     */
+
+/* pixel source kinds */
+#define SKYRX_IN_RAW_U16 0 /* uint16 raw counts + (dark, coeff, gain) calibration */
+#define SKYRX_IN_F32 1     /* float32 radiance (RadianceCube.values)             */
+#define SKYRX_IN_F64 2     /* float64 pixels (only skyrx_mahalanobis_sq)         */
+
+const char* skyrx_version(void);
+const char* skyrx_last_error(void);
+int skyrx_device_check(void); /* 0 if a sm_100 device is visible */
+
+/* ---------------------------------------------------------------- K1 calibration
+ * Replaces calibrate.py:90-102 (apply_calibration: keep == NULL, factor == 1)
+ * and calibrate.py:135-176 (calibrate_bin_rgb).  out[l,s,o] = sum over j<factor,
+ * left to right in f32, of max(0, f32(raw[l,s,keep[o*factor+j]]) - dark) * coeff
+ * / gain[l]; each op IEEE round-to-nearest (bit-exact vs the reference).
+ * rgb (nullable) receives out[..., rgb_idx[c]] for c < 3 (calibrate.py:129-132).
+ */
+int skyrx_calibrate(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                    const float* dark, const float* coeff, const float* gain,
+                    const int32_t* keep, int32_t kept, int32_t factor,
+                    float* out, const int32_t* rgb_idx_host, float* rgb, void* stream);
+
+/* Same band selection / binning / RGB on an f32 radiance cube:
+ * discard_oob_bands (calibrate.py:105-114), bin_bands (calibrate.py:117-126),
+ * extract_rgb (calibrate.py:129-132). */
+int skyrx_bin_radiance(const float* in, int64_t lines, int32_t samples, int32_t bands,
+                       const int32_t* keep, int32_t kept, int32_t factor, float* out,
+                       const int32_t* rgb_idx_host, float* rgb, void* stream);
+
+/* ---------------------------------------------------------------- K2 background moments
+ * Moments block layout (float64): [n, s[B], Q[B*B]] with shift c:
+ *   s = sum(x - c), Q = sum((x - c)(x - c)^T)  (Q stored full, symmetric).
+ * This is the payload all-reduced across GPUs (SURVEY §8 R-GLOBAL) and folded
+ * by forgetting (R-STREAM).  Equivalent to rx.py:56-66's two passes up to FP64
+ * rounding once finalized.
+ */
+size_t skyrx_moments_len(int32_t bands); /* 1 + B + B*B doubles */
+
+/* shift c[b] = f32(mean of a strided sample of <= 4096 pixels), stored as f64 */
+int skyrx_stats_shift(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
+                      int32_t bands, const float* dark, const float* coeff, const float* gain,
+                      double* shift, void* stream);
+
+int skyrx_stats_workspace(int64_t lines, int32_t samples, int32_t bands, size_t* bytes);
+
+/* Accumulate moments of all pixels of the cube (fused calibration for RAW).
+ * precise = 0: f32 products, f32 runs of <= 192 products promoted to f64
+ *              (fast path; SURVEY §7 precision budget);
+ * precise = 1: f64 products and sums throughout (reference-grade, for the
+ *              drop-in compute_stats and the reference's 1e-9 suites).
+ * flags[0] |= 1 if any calibrated value is non-finite (rx.py:53-54). */
+int skyrx_stats_accumulate(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
+                           int32_t bands, const float* dark, const float* coeff,
+                           const float* gain, const double* shift, int32_t precise,
+                           double* moments, int32_t* flags, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* state = forget * state + chunk (R-STREAM exponential forgetting) */
+int skyrx_moments_fold(double* state, const double* chunk, int32_t bands, double forget,
+                       void* stream);
+
+/* ---------------------------------------------------------------- K3 factorisation
+ * Replaces rx.py:56-86 finalisation: mu, unbiased symmetric sigma, ridge
+ * ladder eps in (0,1e-10,...,1e-6)*trace/B (rx.py:23, 68-80), Cholesky,
+ * sigma_inv = cho_solve(L, I) symmetrised (rx.py:82-83), plus the f32 whitening
+ * matrix W = L^-1 (padded to ld_w columns) and mu split into f32 hi/lo for K4.
+ * Batched over `batch` independent matrices (strips): array i starts at
+ * i * (its per-matrix size).  status[i] = SKYRX_OK / ERR_INSUFFICIENT /
+ * ERR_NONFINITE / ERR_NOT_PD.  flags may be NULL.
+ */
+int skyrx_stats_finalize(const double* moments, const double* shift, const int32_t* flags,
+                         int32_t bands, int32_t batch, double* mu, double* sigma,
+                         double* chol, double* sigma_inv, double* whiten64, float* whiten,
+                         int32_t ld_w, float* mu_hilo, double* ridge, int32_t* status,
+                         void* stream);
+
+/* W = L^-1 (f64 B*B workspace), its f32 transposed padded copy (ld_w*ld_w)
+ * and mu hi/lo, from caller-supplied CubeStats (rx_scores(cube, stats)). */
+int skyrx_whiten_prepare(const double* chol, const double* mu, int32_t bands, double* whiten64,
+                         float* whiten, int32_t ld_w, float* mu_hilo, void* stream);
+
+/* ---------------------------------------------------------------- K4 RX scores
+ * Replaces rx.py:89-97 + _accel.py:75-90 for a whole cube: delta = ||W (x - mu)||^2
+ * with x calibrated on the fly (kind RAW) or read (kind F32); f32 out (L,S).
+ * max_bits (nullable, device uint32, pre-zeroed) receives atomicMax of the
+ * order-preserving key of every score (ScoreMap.max_score, cube.py:174-176);
+ * keys: f2ord(x) = bits ^ (sign ? 0xffffffff : 0x80000000).
+ */
+int skyrx_score(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
+                int32_t bands, const float* dark, const float* coeff, const float* gain,
+                const float* mu_hilo, const float* whiten, int32_t ld_w, float* scores,
+                uint32_t* max_bits, void* stream);
+
+/* The kernel slot itself: _accel.mahalanobis_sq(pixels, mu, chol_lower)
+ * (_accel.py:109-131) with FP64 arithmetic; pixels f32 or f64 (kind F32/F64).
+ * whiten64 is a f64 workspace of B*B + BP*BP doubles, BP = 8*ceil(B/8). */
+int skyrx_mahalanobis_sq(int32_t kind, const void* pixels, int64_t n, int32_t bands,
+                         const double* mu, const double* chol, double* whiten64,
+                         double* out, void* stream);
+
+/* ---------------------------------------------------------------- K5 normalise / threshold / top-k
+ * rx.py:100-105: out = v / f32(max) unless max <= 0 (then a copy);
+ * rx.py:108-112: mask = v > t in f32.  max_bits from skyrx_score or skyrx_max. */
+int skyrx_max(const float* v, int64_t n, uint32_t* max_bits, void* stream);
+int skyrx_normalize(const float* v, int64_t n, const uint32_t* max_bits, float* out,
+                    void* stream);
+int skyrx_threshold(const float* v, int64_t n, float t, uint8_t* mask, void* stream);
+/* rx.py:115-124: out = sqrt(max(f64(v) / max_score, 0)), zeros if max_score <= 0 */
+int skyrx_transmit_domain(const float* v, int64_t n, double max_score, double* out,
+                          void* stream);
+
+/* R-TOPK: thr = the (k+1)-th largest value (-inf if k >= n) by a
+ * 3-digit radix select; mask = v > thr.  workspace from skyrx_topk_workspace. */
+size_t skyrx_topk_workspace(void);
+int skyrx_topk_threshold(const float* v, int64_t n, int64_t k, float* thr, void* workspace,
+                         void* stream);
+int skyrx_mask_gt(const float* v, int64_t n, const float* thr, uint8_t* mask, void* stream);
+
+/* ---------------------------------------------------------------- synthetic sensor (bench/test inputs)
+ * Bit-identical to oracle/synth.py generate_lines(): raw counts for lines
+ * [line0, line0 + nlines) of the seeded scene.  Tables as in SceneTables. */
+int skyrx_synth_raw(uint32_t seedkey, uint32_t cellkey, int32_t samples, int32_t bands,
+                    int32_t components, const uint32_t* cw24, const float* mean,
+                    const float* factor, const float* sd, const float* aspec,
+                    const float* asd, const float* xbar, const float* dark,
+                    const float* coeff, int64_t line0, int64_t nlines, uint16_t* out,
+                    void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKYRX_B200_H_ */

@@ -1,0 +1,164 @@
+// K1 — radiometric calibration (+ optional band discard / binning / RGB).
+//
+// Reference semantics: calibrate.py:90-102 (apply_calibration) and
+// calibrate.py:135-176 (calibrate_bin_rgb).  Bit-exact: every op is a
+// separately rounded f32 intrinsic and binned bands are summed left to right
+// (the order the reference's band-major boolean-indexed block produces; see
+// oracle/skyrx_oracle.py:sequential_sum_f32).
+//
+// HBM-bound elementwise map: 2 B read + 4 B write per element; the plain path
+// moves 16 B of raw per thread per iteration (uint4) with float4 table loads.
+#include "common.cuh"
+
+namespace skyrx {
+
+// plain apply_calibration, 8 elements (one uint4 of raw) per step
+__global__ void __launch_bounds__(256) calibrate_vec8_kernel(
+    const uint4* __restrict__ raw, int64_t n8, int64_t sb8, const float4* __restrict__ dark,
+    const float4* __restrict__ coeff, const float* __restrict__ gain, float4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t line = i / sb8;
+    const int64_t t = i - line * sb8;  // index of the 8-group inside the line
+    const uint4 r = __ldcs(raw + i);   // streamed once
+    const float g = __ldg(gain + line);
+    const float4 d0 = __ldg(dark + 2 * t), d1 = __ldg(dark + 2 * t + 1);
+    const float4 c0 = __ldg(coeff + 2 * t), c1 = __ldg(coeff + 2 * t + 1);
+    float4 o0, o1;
+    o0.x = calib((float)(r.x & 0xffffu), d0.x, c0.x, g);
+    o0.y = calib((float)(r.x >> 16), d0.y, c0.y, g);
+    o0.z = calib((float)(r.y & 0xffffu), d0.z, c0.z, g);
+    o0.w = calib((float)(r.y >> 16), d0.w, c0.w, g);
+    o1.x = calib((float)(r.z & 0xffffu), d1.x, c1.x, g);
+    o1.y = calib((float)(r.z >> 16), d1.y, c1.y, g);
+    o1.z = calib((float)(r.w & 0xffffu), d1.z, c1.z, g);
+    o1.w = calib((float)(r.w >> 16), d1.w, c1.w, g);
+    __stcs(out + 2 * i, o0);
+    __stcs(out + 2 * i + 1, o1);
+  }
+}
+
+__global__ void __launch_bounds__(256) calibrate_scalar_kernel(
+    const uint16_t* __restrict__ raw, int64_t n, int64_t sb, const float* __restrict__ dark,
+    const float* __restrict__ coeff, const float* __restrict__ gain, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t line = i / sb;
+    const int64_t t = i - line * sb;
+    out[i] = calib((float)raw[i], __ldg(dark + t), __ldg(coeff + t), __ldg(gain + line));
+  }
+}
+
+struct Rgb3 {
+  int c[3];
+};
+
+// general path: one thread per output (line, sample, out_band); RAW calibrates,
+// F32 re-bins an existing radiance cube
+template <int KIND>
+__global__ void __launch_bounds__(256) calibrate_bin_kernel(
+    const void* __restrict__ src, int64_t lines, int32_t samples, int32_t bands,
+    const float* __restrict__ dark, const float* __restrict__ coeff,
+    const float* __restrict__ gain, const int32_t* __restrict__ keep, int32_t nout,
+    int32_t factor, float* __restrict__ out, Rgb3 rgb_idx, float* __restrict__ rgb) {
+  const int64_t total = lines * (int64_t)samples * nout;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = i / nout;
+    const int32_t o = (int32_t)(i - pix * nout);
+    const int64_t line = pix / samples;
+    const int32_t s = (int32_t)(pix - line * samples);
+    const float g = (KIND == SKYRX_IN_RAW_U16) ? __ldg(gain + line) : 1.0f;
+    float acc = 0.0f;
+    for (int j = 0; j < factor; ++j) {
+      const int b = keep ? __ldg(keep + o * factor + j) : o * factor + j;
+      float x;
+      if constexpr (KIND == SKYRX_IN_RAW_U16) {
+        const int64_t tb = (int64_t)s * bands + b;
+        x = calib((float)reinterpret_cast<const uint16_t*>(src)[pix * bands + b],
+                  __ldg(dark + tb), __ldg(coeff + tb), g);
+      } else {
+        x = reinterpret_cast<const float*>(src)[pix * bands + b];
+      }
+      acc = (j == 0) ? x : __fadd_rn(acc, x);
+    }
+    out[i] = acc;
+    if (rgb) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (rgb_idx.c[c] == o) rgb[pix * 3 + c] = acc;
+    }
+  }
+}
+
+static int grid_for(int64_t work, int threads) {
+  int64_t blocks = ceil_div<int64_t>(work, threads);
+  const int64_t cap = (int64_t)kSMs * 16;
+  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_calibrate(const uint16_t* raw, int64_t lines, int32_t samples,
+                               int32_t bands, const float* dark, const float* coeff,
+                               const float* gain, const int32_t* keep, int32_t kept,
+                               int32_t factor, float* out, const int32_t* rgb_idx_host,
+                               float* rgb, void* stream) {
+  SKYRX_REQUIRE(lines >= 0 && samples >= 0 && bands >= 0, "negative cube shape");
+  SKYRX_REQUIRE(factor >= 1, "band count %d not divisible by factor %d", kept, factor);
+  if (keep == nullptr) kept = bands;
+  SKYRX_REQUIRE(kept % factor == 0, "band count %d not divisible by factor %d", kept, factor);
+  const int64_t pixels = lines * (int64_t)samples;
+  const int32_t nout = kept / factor;
+  cudaStream_t st = as_stream(stream);
+  if (pixels == 0 || nout == 0) return SKYRX_OK;
+  const bool plain = keep == nullptr && factor == 1 && rgb == nullptr;
+  if (plain) {
+    const int64_t n = pixels * bands;
+    const int64_t sb = (int64_t)samples * bands;
+    const bool aligned = (sb % 8 == 0) && ((uintptr_t)raw % 16 == 0) &&
+                         ((uintptr_t)out % 16 == 0) && ((uintptr_t)dark % 16 == 0) &&
+                         ((uintptr_t)coeff % 16 == 0);
+    if (aligned) {
+      calibrate_vec8_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(
+          (const uint4*)raw, n / 8, sb / 8, (const float4*)dark, (const float4*)coeff, gain,
+          (float4*)out);
+    } else {
+      calibrate_scalar_kernel<<<grid_for(n, 256), 256, 0, st>>>(raw, n, sb, dark, coeff, gain,
+                                                                 out);
+    }
+  } else {
+    Rgb3 r{{-1, -1, -1}};
+    if (rgb && rgb_idx_host)
+      for (int c = 0; c < 3; ++c) r.c[c] = rgb_idx_host[c];
+    const int64_t total = pixels * nout;
+    calibrate_bin_kernel<SKYRX_IN_RAW_U16><<<grid_for(total, 256), 256, 0, st>>>(
+        raw, lines, samples, bands, dark, coeff, gain, keep, nout, factor, out, r, rgb);
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_calibrate");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_bin_radiance(const float* in, int64_t lines, int32_t samples,
+                                  int32_t bands, const int32_t* keep, int32_t kept,
+                                  int32_t factor, float* out, const int32_t* rgb_idx_host,
+                                  float* rgb, void* stream) {
+  SKYRX_REQUIRE(lines >= 0 && samples >= 0 && bands >= 0, "negative cube shape");
+  if (keep == nullptr) kept = bands;
+  SKYRX_REQUIRE(factor >= 1 && kept % factor == 0, "band count %d not divisible by factor %d",
+                kept, factor);
+  const int64_t pixels = lines * (int64_t)samples;
+  const int32_t nout = kept / factor;
+  if (pixels == 0 || nout == 0) return SKYRX_OK;
+  Rgb3 r{{-1, -1, -1}};
+  if (rgb && rgb_idx_host)
+    for (int c = 0; c < 3; ++c) r.c[c] = rgb_idx_host[c];
+  calibrate_bin_kernel<SKYRX_IN_F32><<<grid_for(pixels * nout, 256), 256, 0,
+                                       as_stream(stream)>>>(in, lines, samples, bands, nullptr,
+                                                            nullptr, nullptr, keep, nout,
+                                                            factor, out, r, rgb);
+  SKYRX_CHECK_LAUNCH("skyrx_bin_radiance");
+  return SKYRX_OK;
+}

@@ -1,0 +1,100 @@
+// Shared device helpers for the skyrx B200 hot path (sm_100a).
+//
+// Numerics contract: calibration is reproduced bit for
+// bit, so every f32 op on that path is an explicitly rounded intrinsic
+// (__fsub_rn/__fmul_rn/__fdiv_rn): no FMA contraction, no fast-math, and
+// subnormals are kept (a 1e-40 gain must still overflow to inf,
+// test_pipeline.py:84-102).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <cstdarg>
+
+#include "../../include/skyrx_b200.h"
+
+namespace skyrx {
+
+constexpr int kSMs = 148;
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+#define SKYRX_CHECK_LAUNCH(what)                                         \
+  do {                                                                    \
+    cudaError_t _e = cudaGetLastError();                                  \
+    if (_e != cudaSuccess) return ::skyrx::cuda_status(_e, what);         \
+  } while (0)
+
+#define SKYRX_REQUIRE(cond, ...)                                          \
+  do {                                                                    \
+    if (!(cond)) {                                                        \
+      ::skyrx::set_error(__VA_ARGS__);                                    \
+      return SKYRX_ERR_ARG;                                               \
+    }                                                                     \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ math
+// calibrate.py:98-101: out = max(0, f32(raw) - dark) * coeff / gain, each op RN.
+__device__ __forceinline__ float calib(float raw, float dark, float coeff, float gain) {
+  float t = __fsub_rn(raw, dark);
+  t = fmaxf(t, 0.0f);
+  t = __fmul_rn(t, coeff);
+  return __fdiv_rn(t, gain);
+}
+
+__device__ __forceinline__ bool finite_f(float x) { return isfinite(x); }
+
+template <typename T>
+__host__ __device__ __forceinline__ T ceil_div(T a, T b) { return (a + b - 1) / b; }
+
+// order-preserving float <-> uint32 map (total order, -0 < +0 collapsed)
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// 16-byte vectors for shared-memory operand loads
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+__device__ __forceinline__ void unpack(const float4& v, float* o) {
+  o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+}
+__device__ __forceinline__ void unpack(const double2& v, double* o) { o[0] = v.x, o[1] = v.y; }
+
+// load 8 consecutive T from 16-B aligned shared memory
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, T* o) {
+  using V = typename Vec16<T>::type;
+  constexpr int VN = Vec16<T>::n;
+#pragma unroll
+  for (int q = 0; q < 8; q += VN) unpack(*reinterpret_cast<const V*>(p + q), o + q);
+}
+
+// Warp reductions
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace skyrx

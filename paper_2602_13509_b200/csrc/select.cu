@@ -1,0 +1,225 @@
+// K5 — score maximum, normalisation, threshold masks and the top-0.1% select.
+//
+// rx.py:100-105 normalize_scores (f32 division by f32(max)), rx.py:108-112
+// threshold_scores (strict > in f32), cube.py:174-176 max_score, and the new
+// R-TOPK row: mask = delta > delta_(k+1), k = ceil(N/1000).
+// The select is an exact 3-digit (11/11/10-bit) radix select over
+// order-preserving u32 keys: integer histogram atomics only, so the threshold
+// is exact and deterministic.  HBM-bound: each digit re-reads the scores
+// (4 B/px); the mask pass reads 4 B and writes 1 B per pixel.
+#include "common.cuh"
+
+namespace skyrx {
+
+// workspace layout (uint32 words)
+constexpr int kHistBins = 2048;
+struct TopkState {
+  uint32_t prefix;   // key bits selected so far
+  uint32_t pad;
+  uint64_t rank;     // 1-based rank (from the top) still to find inside the prefix
+  uint32_t all;      // 1 -> k >= n: select everything
+};
+
+__global__ void max_kernel(const float* __restrict__ v, int64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, f2ord(v[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+__global__ void normalize_kernel(const float* __restrict__ v, int64_t n,
+                                 const uint32_t* __restrict__ max_key, float* __restrict__ out) {
+  const float m = ord2f(*max_key);
+  const bool scale = m > 0.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = scale ? __fdiv_rn(v[i], m) : v[i];
+}
+
+__global__ void threshold_kernel(const float* __restrict__ v, int64_t n, float t,
+                                 uint8_t* __restrict__ mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mask[i] = v[i] > t;
+}
+
+__global__ void transmit_kernel(const float* __restrict__ v, int64_t n, double m,
+                                double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = (double)v[i] / m;  // rx.py:124 sqrt(clip(v / max, 0))
+    out[i] = m > 0.0 ? sqrt(r > 0.0 ? r : 0.0) : 0.0;
+  }
+}
+
+__global__ void mask_gt_kernel(const float* __restrict__ v, int64_t n,
+                               const float* __restrict__ thr, uint8_t* __restrict__ mask) {
+  const float t = *thr;
+  const int64_t n4 = n / 4;
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  uint32_t* m4 = reinterpret_cast<uint32_t*>(mask);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 x = v4[i];
+    m4[i] = (uint32_t)(x.x > t) | ((uint32_t)(x.y > t) << 8) | ((uint32_t)(x.z > t) << 16) |
+            ((uint32_t)(x.w > t) << 24);
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mask[i] = v[i] > t;
+}
+
+__global__ void mask_gt_scalar_kernel(const float* __restrict__ v, int64_t n,
+                                      const float* __restrict__ thr, uint8_t* __restrict__ mask) {
+  const float t = *thr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mask[i] = v[i] > t;
+}
+
+__device__ __forceinline__ void digit_params(int digit, int& shift, int& bits) {
+  // digit 0: bits 31..21, digit 1: 20..10, digit 2: 9..0
+  if (digit == 0) shift = 21, bits = 11;
+  else if (digit == 1) shift = 10, bits = 11;
+  else shift = 0, bits = 10;
+}
+
+__global__ void topk_init_kernel(int64_t n, int64_t k, TopkState* st, uint32_t* hist) {
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) {
+    st->prefix = 0;
+    st->rank = (uint64_t)k + 1;
+    st->all = (k >= n) ? 1u : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(512) topk_hist_kernel(const float* __restrict__ v, int64_t n,
+                                                        int digit,
+                                                        const TopkState* __restrict__ st,
+                                                        uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kHistBins];
+  if (st->all) return;
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  int shift, bits;
+  digit_params(digit, shift, bits);
+  const int hi_shift = shift + bits;  // bits above this digit must equal the prefix
+  const uint32_t prefix = st->prefix;
+  const uint32_t mask = (1u << bits) - 1u;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = f2ord(v[i]);
+    const bool match = (hi_shift >= 32) ? true : ((key >> hi_shift) == prefix);
+    if (match) atomicAdd(&sh[(key >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// one CTA: walk bins from the top, pick the bin holding the target rank
+__global__ void topk_pick_kernel(int digit, TopkState* st, uint32_t* hist, float* thr) {
+  __shared__ uint32_t cnt[kHistBins];
+  if (st->all) {
+    if (threadIdx.x == 0 && digit == 2) *thr = -INFINITY;
+    return;
+  }
+  int shift, bits;
+  digit_params(digit, shift, bits);
+  const int nb = 1 << bits;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = hist[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t rank = st->rank;
+    uint64_t cum = 0;
+    int b = nb - 1;
+    for (; b > 0; --b) {
+      if (cum + cnt[b] >= rank) break;
+      cum += cnt[b];
+    }
+    st->rank = rank - cum;
+    st->prefix = (st->prefix << bits) | (uint32_t)b;
+    if (digit == 2) *thr = ord2f(st->prefix);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0;
+}
+
+static int grid_n(int64_t n, int threads, int per_sm) {
+  int64_t b = ceil_div<int64_t>(n, threads);
+  const int64_t cap = (int64_t)kSMs * per_sm;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_max(const float* v, int64_t n, uint32_t* max_bits, void* stream) {
+  if (n <= 0) return SKYRX_OK;
+  max_kernel<<<grid_n(n, 256, 8), 256, 0, as_stream(stream)>>>(v, n, max_bits);
+  SKYRX_CHECK_LAUNCH("skyrx_max");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_normalize(const float* v, int64_t n, const uint32_t* max_bits, float* out,
+                               void* stream) {
+  if (n <= 0) return SKYRX_OK;
+  normalize_kernel<<<grid_n(n, 256, 8), 256, 0, as_stream(stream)>>>(v, n, max_bits, out);
+  SKYRX_CHECK_LAUNCH("skyrx_normalize");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_threshold(const float* v, int64_t n, float t, uint8_t* mask,
+                               void* stream) {
+  if (n <= 0) return SKYRX_OK;
+  threshold_kernel<<<grid_n(n, 256, 8), 256, 0, as_stream(stream)>>>(v, n, t, mask);
+  SKYRX_CHECK_LAUNCH("skyrx_threshold");
+  return SKYRX_OK;
+}
+
+extern "C" size_t skyrx_topk_workspace(void) {
+  return sizeof(TopkState) + 16 + kHistBins * sizeof(uint32_t);
+}
+
+extern "C" int skyrx_topk_threshold(const float* v, int64_t n, int64_t k, float* thr,
+                                    void* workspace, void* stream) {
+  SKYRX_REQUIRE(n >= 0 && k >= 0, "bad top-k arguments n=%lld k=%lld", (long long)n,
+                (long long)k);
+  SKYRX_REQUIRE(((uintptr_t)workspace % 16) == 0, "top-k workspace must be 16-B aligned");
+  cudaStream_t st = as_stream(stream);
+  TopkState* state = reinterpret_cast<TopkState*>(workspace);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(workspace) + 32);
+  topk_init_kernel<<<1, 256, 0, st>>>(n, k, state, hist);
+  for (int digit = 0; digit < 3; ++digit) {
+    if (n > 0) topk_hist_kernel<<<grid_n(n, 512, 4), 512, 0, st>>>(v, n, digit, state, hist);
+    topk_pick_kernel<<<1, 256, 0, st>>>(digit, state, hist, thr);
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_topk_threshold");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_mask_gt(const float* v, int64_t n, const float* thr, uint8_t* mask,
+                             void* stream) {
+  if (n <= 0) return SKYRX_OK;
+  const bool aligned = ((uintptr_t)v % 16 == 0) && ((uintptr_t)mask % 4 == 0);
+  if (aligned) {
+    mask_gt_kernel<<<grid_n(n / 4 + 1, 256, 8), 256, 0, as_stream(stream)>>>(v, n, thr, mask);
+  } else {
+    mask_gt_scalar_kernel<<<grid_n(n, 256, 8), 256, 0, as_stream(stream)>>>(v, n, thr, mask);
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_mask_gt");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_transmit_domain(const float* v, int64_t n, double max_score, double* out,
+                                     void* stream) {
+  if (n <= 0) return SKYRX_OK;
+  transmit_kernel<<<grid_n(n, 256, 8), 256, 0, as_stream(stream)>>>(v, n, max_score, out);
+  SKYRX_CHECK_LAUNCH("skyrx_transmit_domain");
+  return SKYRX_OK;
+}

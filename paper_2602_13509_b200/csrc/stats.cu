@@ -1,0 +1,553 @@
+// K2 background moments and K3 batched factorisation.
+//
+// Reference: rx.py:42-86 (compute_stats).  The reference makes two passes
+// (f64 mean, then f64 dgemm of centred pixels).  Here one pass accumulates
+// shifted moments s = sum(x-c), Q = sum((x-c)(x-c)^T) around a per-band shift
+// c close to the mean (skyrx_stats_shift), so the raw cube is read once:
+//   mu = c + s/n,  sigma = (Q - s s^T / n) / (n - 1)      (identical algebra).
+//
+// Precision plan (measured in numpy emulation on the c1 generator, kappa ~6e3,
+// DESIGN.md §numerics): FP32 products and FP32 running sums of at most ~200
+// products per accumulator, promoted to FP64 registers, FP64 across threads
+// and CTAs in a fixed order (no float atomics -> bit-reproducible).
+//
+// Gram layout: B padded to BP = 8*nt; the lower triangle of nt x nt 8x8
+// tiles is distributed over threads (tile, pixel-group); each thread keeps an
+// 8x8 FP32 + 8x8 FP64 register accumulator and reads its two 8-band slices of
+// every pixel of its group from the shared-memory tile (4 LDS.128 / 64 FFMA).
+#include "common.cuh"
+#include "tile_loader.cuh"
+
+namespace skyrx {
+
+constexpr int kGramThreads = 256;
+constexpr int kGramTileP = 64;       // pixels per shared-memory tile
+constexpr int kFlushProducts = 192;  // FP32 products per accumulator before FP64 promotion
+
+struct GramGeom {
+  int bp, nt, ntiles, parts, groups, tiles_per_part, ld, grid;
+  int64_t ptiles;
+};
+
+static GramGeom gram_geom(int64_t npix, int bands, size_t tsize = 4) {
+  GramGeom g;
+  g.bp = ((bands + 7) / 8) * 8;
+  g.nt = g.bp / 8;
+  g.ntiles = g.nt * (g.nt + 1) / 2;
+  if (g.ntiles <= kGramThreads) {
+    g.parts = 1;
+    g.groups = kGramThreads / g.ntiles;
+    g.tiles_per_part = g.ntiles;
+  } else {
+    g.parts = ceil_div(g.ntiles, kGramThreads);
+    g.groups = 1;
+    g.tiles_per_part = kGramThreads;
+  }
+  g.ld = g.bp + (int)(16 / tsize);
+  g.ptiles = ceil_div<int64_t>(npix, kGramTileP);
+  int64_t grid = g.ptiles < kSMs ? g.ptiles : kSMs;
+  g.grid = (int)(grid < 1 ? 1 : grid);
+  return g;
+}
+
+static size_t gram_smem(const GramGeom& g, size_t tsize) {
+  return (size_t)kGramTileP * g.ld * tsize + (size_t)g.bp * sizeof(double) +
+         (size_t)(g.groups > 1 ? g.tiles_per_part * 64 : 0) * sizeof(double) +
+         (size_t)g.bp * sizeof(float) + 2 * kGramTileP * sizeof(int32_t);
+}
+
+// workspace: per-CTA partials [grid][ntiles*64] + [grid][bp] doubles
+static size_t gram_ws(const GramGeom& g) {
+  return ((size_t)g.grid * g.ntiles * 64 + (size_t)g.grid * g.bp) * sizeof(double);
+}
+
+__device__ __forceinline__ void tri_decode(int t, int& I, int& J) {
+  int i = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  I = i;
+  J = t - i * (i + 1) / 2;
+}
+
+template <int KIND, typename T>
+__global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
+    CubeRef cube, const double* __restrict__ shift, GramGeom geo, double* __restrict__ part_q,
+    double* __restrict__ part_s, int32_t* __restrict__ flags) {
+  constexpr bool kFast = sizeof(T) == 4;  // f32 products, FP64 promotion; else all-f64
+  extern __shared__ __align__(16) unsigned char smem[];
+  T* d = reinterpret_cast<T*>(smem);
+  double* c64 = reinterpret_cast<double*>(d + kGramTileP * geo.ld);
+  double* red = c64 + geo.bp;
+  float* c_f = reinterpret_cast<float*>(red + (geo.groups > 1 ? geo.tiles_per_part * 64 : 0));
+  int32_t* s_line = reinterpret_cast<int32_t*>(c_f + geo.bp);
+  int32_t* s_samp = s_line + kGramTileP;
+
+  const int B = cube.bands;
+  const int tid = threadIdx.x;
+  for (int b = tid; b < geo.bp; b += kGramThreads) {
+    const double c = b < B ? shift[b] : 0.0;
+    c64[b] = c;
+    c_f[b] = (float)c;  // shift is f32-representable (skyrx_stats_shift)
+  }
+
+  const int part = blockIdx.y;
+  const int tiles_here = min(geo.tiles_per_part, geo.ntiles - part * geo.tiles_per_part);
+  const int group = tid / tiles_here;
+  const int tl = tid - group * tiles_here;
+  const bool active = group < geo.groups;
+  int I = 0, J = 0;
+  if (active) tri_decode(part * geo.tiles_per_part + tl, I, J);
+  const bool do_s = (part == 0) && tid < geo.bp;
+
+  T acc[8][8];
+  double acc64[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = T(0), acc64[i][j] = 0.0;
+  double s64 = 0.0;
+  int since_flush = 0;
+  bool finite_ok = true;
+  const int per_thread = ceil_div(kGramTileP, geo.groups);
+
+  for (int64_t t = blockIdx.x; t < geo.ptiles; t += gridDim.x) {
+    __syncthreads();
+    finite_ok &= load_tile<KIND, T>(cube, t * kGramTileP, kGramTileP, geo.ld, geo.bp, c_f,
+                                    nullptr, c64, d, s_line, s_samp);
+    __syncthreads();
+    if (do_s) {  // band sums over the tile, then FP64 across tiles
+      T cs = T(0);
+      for (int p = 0; p < kGramTileP; ++p) cs += d[p * geo.ld + tid];
+      s64 += (double)cs;
+    }
+    if (active) {
+      if (kFast && since_flush + per_thread > kFlushProducts) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc64[i][j] += (double)acc[i][j], acc[i][j] = T(0);
+        since_flush = 0;
+      }
+      const T* rowI = d + 8 * I;
+      const T* rowJ = d + 8 * J;
+      for (int p = group; p < kGramTileP; p += geo.groups) {
+        T av[8], bv[8];
+        load8(rowI + p * geo.ld, av);
+        load8(rowJ + p * geo.ld, bv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      since_flush += per_thread;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc64[i][j] += (double)acc[i][j];
+
+  // combine pixel groups in a fixed order, then one partial per CTA
+  double* pq = part_q + (size_t)blockIdx.x * geo.ntiles * 64 +
+               (size_t)(part * geo.tiles_per_part) * 64;
+  if (geo.groups > 1) {
+    __syncthreads();
+    for (int g = 0; g < geo.groups; ++g) {
+      if (active && group == g) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            double* r = red + tl * 64 + i * 8 + j;
+            *r = (g == 0) ? acc64[i][j] : *r + acc64[i][j];
+          }
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < tiles_here * 64; e += kGramThreads) pq[e] = red[e];
+  } else if (active) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pq[tl * 64 + i * 8 + j] = acc64[i][j];
+  }
+  if (do_s) part_s[(size_t)blockIdx.x * geo.bp + tid] = s64;
+  if (!finite_ok) atomicOr(flags, 1);
+}
+
+// moments[0] = n, moments[1..B] = s, moments[1+B ..] = Q (full, symmetric)
+__global__ void gram_reduce_kernel(const double* __restrict__ part_q,
+                                   const double* __restrict__ part_s, GramGeom geo, int bands,
+                                   double n, double* __restrict__ moments) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nq = geo.ntiles * 64;
+  double* s_out = moments + 1;
+  double* q_out = moments + 1 + bands;
+  if (e < nq) {
+    double v = 0.0;
+    for (int c = 0; c < geo.grid; ++c) v += part_q[(size_t)c * nq + e];
+    const int t = e >> 6, r = (e >> 3) & 7, cc = e & 7;
+    int I, J;
+    tri_decode(t, I, J);
+    const int row = 8 * I + r, col = 8 * J + cc;
+    if (row < bands && col < bands && (I != J || r >= cc)) {
+      q_out[(size_t)row * bands + col] = v;
+      q_out[(size_t)col * bands + row] = v;
+    }
+  } else if (e < nq + bands) {
+    const int b = e - nq;
+    double v = 0.0;
+    for (int c = 0; c < geo.grid; ++c) v += part_s[(size_t)c * geo.bp + b];
+    s_out[b] = v;
+  } else if (e == nq + bands) {
+    moments[0] = n;
+  }
+}
+
+// shift: f32-rounded f64 mean of a strided sample of <= 4096 pixels
+template <int KIND>
+__global__ void shift_kernel(CubeRef cube, double* __restrict__ shift) {
+  const int64_t n = cube.npix;
+  const int64_t step = n > 4096 ? n / 4096 : 1;
+  const int64_t m = n > 0 ? (n + step - 1) / step : 0;
+  const int B = cube.bands;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t pix = i * step;
+      const int64_t gi = pix * B + b;
+      float x;
+      if constexpr (KIND == SKYRX_IN_RAW_U16) {
+        const int64_t line = pix / cube.samples;
+        const int64_t tb = (pix - line * cube.samples) * B + b;
+        x = calib((float)reinterpret_cast<const uint16_t*>(cube.pixels)[gi], cube.dark[tb],
+                  cube.coeff[tb], cube.gain[line]);
+      } else {
+        x = reinterpret_cast<const float*>(cube.pixels)[gi];
+      }
+      acc += (double)x;
+    }
+    shift[b] = m > 0 ? (double)(float)(acc / (double)m) : 0.0;
+  }
+}
+
+__global__ void fold_kernel(double* __restrict__ state, const double* __restrict__ chunk,
+                            int64_t len, double forget) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < len) state[i] = forget * state[i] + chunk[i];
+}
+
+// ------------------------------------------------------------------ K3
+constexpr int kFinThreads = 512;
+constexpr int kSmemCholMaxB = 160;
+
+__device__ __forceinline__ double block_sum_fixed(double v, double* scratch) {
+  // deterministic: warp tree then serial over warps
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += scratch[i];
+    scratch[32] = r;
+  }
+  __syncthreads();
+  r = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(
+    const double* __restrict__ moments_all, const double* __restrict__ shift_all,
+    const int32_t* __restrict__ flags_all, int bands, double* __restrict__ mu_all,
+    double* __restrict__ sigma_all, double* __restrict__ chol_all,
+    double* __restrict__ inv_all, double* __restrict__ w64_all, float* __restrict__ wf_all,
+    int ld_w, float* __restrict__ mhl_all, double* __restrict__ ridge_all,
+    int32_t* __restrict__ status_all) {
+  extern __shared__ __align__(16) double fsm[];
+  __shared__ double scratch[40];
+  __shared__ int s_fail;
+  const int B = bands;
+  const size_t BB = (size_t)B * B;
+  const int m = blockIdx.x;
+  const double* mom = moments_all + (size_t)m * (1 + B + BB);
+  const double* shift = shift_all + (size_t)m * B;
+  double* mu = mu_all + (size_t)m * B;
+  double* sigma = sigma_all + (size_t)m * BB;
+  double* chol = chol_all + (size_t)m * BB;
+  double* inv = inv_all + (size_t)m * BB;
+  double* w64 = w64_all + (size_t)m * BB;
+  float* wf = wf_all + (size_t)m * ld_w * ld_w;
+  float* mhl = mhl_all + (size_t)m * 2 * B;
+  const int tid = threadIdx.x;
+  const int NT = blockDim.x;
+
+  const double n = mom[0];
+  const double* s = mom + 1;
+  const double* q = mom + 1 + B;
+  int status = SKYRX_OK;
+  if (flags_all && (flags_all[m] & 1)) status = SKYRX_ERR_NONFINITE;
+  if (!(n > (double)B)) status = SKYRX_ERR_INSUFFICIENT;  // rx.py:51 checks size first
+  if (status != SKYRX_OK) {
+    if (tid == 0) {
+      status_all[m] = status;
+      ridge_all[m] = 0.0;
+    }
+    return;
+  }
+  // mu, sigma (rx.py:59, 65-66)
+  for (int b = tid; b < B; b += NT) {
+    const double mb = shift[b] + s[b] / n;
+    mu[b] = mb;
+    const float hi = (float)mb;
+    mhl[b] = hi;
+    mhl[B + b] = (float)(mb - (double)hi);
+  }
+  for (size_t e = tid; e < BB; e += NT) {
+    const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
+    const double vij = (q[(size_t)i * B + j] - s[i] * s[j] / n) / (n - 1.0);
+    const double vji = (q[(size_t)j * B + i] - s[j] * s[i] / n) / (n - 1.0);
+    sigma[e] = (vij + vji) / 2.0;
+  }
+  __syncthreads();
+  __threadfence_block();
+  double tr = 0.0;
+  for (int b = tid; b < B; b += NT) tr += sigma[(size_t)b * B + b];
+  const double trace = block_sum_fixed(tr, scratch);
+  const double scale = trace > 0.0 ? trace / B : 1.0;
+
+  double* A = (B <= kSmemCholMaxB) ? fsm : chol;  // working factor
+  const double eps_tab[6] = {0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6};
+  double ridge = 0.0;
+  bool ok = false;
+  for (int a = 0; a < 6 && !ok; ++a) {
+    ridge = eps_tab[a] * scale;
+    for (size_t e = tid; e < BB; e += NT) {
+      const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
+      A[e] = (j <= i) ? sigma[e] + (i == j ? ridge : 0.0) : 0.0;
+    }
+    if (tid == 0) s_fail = 0;
+    __syncthreads();
+    // right-looking Cholesky, lower triangle
+    for (int j = 0; j < B; ++j) {
+      const double ajj = A[(size_t)j * B + j];
+      if (!(ajj > 0.0)) {  // LAPACK potrf: non-positive or NaN pivot fails
+        if (tid == 0) s_fail = 1;
+        __syncthreads();
+        break;
+      }
+      const double ljj = sqrt(ajj);
+      __syncthreads();
+      if (tid == 0) A[(size_t)j * B + j] = ljj;
+      for (int i = j + 1 + tid; i < B; i += NT) A[(size_t)i * B + j] /= ljj;
+      __syncthreads();
+      const int r = B - j - 1;  // trailing order
+      const int cnt = r * (r + 1) / 2;
+      for (int e = tid; e < cnt; e += NT) {
+        int ii = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+        while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+        while (ii * (ii + 1) / 2 > e) --ii;
+        const int kk = e - ii * (ii + 1) / 2;
+        const int i = j + 1 + ii, k = j + 1 + kk;
+        A[(size_t)i * B + k] -= A[(size_t)i * B + j] * A[(size_t)k * B + j];
+      }
+      __syncthreads();
+    }
+    ok = (s_fail == 0);
+    __syncthreads();
+  }
+  if (!ok) {
+    if (tid == 0) {
+      status_all[m] = SKYRX_ERR_NOT_PD;
+      ridge_all[m] = ridge;
+    }
+    return;
+  }
+  if (A != chol)
+    for (size_t e = tid; e < BB; e += NT) chol[e] = A[e];
+  __syncthreads();
+  // W = L^-1, one column per thread (forward substitution on e_c)
+  for (int c = tid; c < B; c += NT) {
+    for (int i = 0; i < c; ++i) w64[(size_t)i * B + c] = 0.0;
+    for (int i = c; i < B; ++i) {
+      double a0 = (i == c) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int k = c;
+      for (; k + 3 < i; k += 4) {
+        a0 -= A[(size_t)i * B + k] * w64[(size_t)k * B + c];
+        a1 -= A[(size_t)i * B + k + 1] * w64[(size_t)(k + 1) * B + c];
+        a2 -= A[(size_t)i * B + k + 2] * w64[(size_t)(k + 2) * B + c];
+        a3 -= A[(size_t)i * B + k + 3] * w64[(size_t)(k + 3) * B + c];
+      }
+      for (; k < i; ++k) a0 -= A[(size_t)i * B + k] * w64[(size_t)k * B + c];
+      w64[(size_t)i * B + c] = ((a0 + a1) + (a2 + a3)) / A[(size_t)i * B + i];
+    }
+  }
+  __syncthreads();
+  __threadfence_block();
+  // sigma_inv = W^T W (= cho_solve(L, I)), exactly symmetric by construction
+  for (size_t e = tid; e < BB; e += NT) {
+    const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
+    if (j > i) continue;
+    double acc = 0.0;
+    for (int k = i; k < B; ++k) acc += w64[(size_t)k * B + i] * w64[(size_t)k * B + j];
+    inv[(size_t)i * B + j] = acc;
+    inv[(size_t)j * B + i] = acc;
+  }
+  // f32 whitening matrix, transposed (wf[k * ld_w + j] = W[j][k]) for K4
+  for (size_t e = tid; e < (size_t)ld_w * ld_w; e += NT) {
+    const int k = (int)(e / ld_w), j = (int)(e - (size_t)k * ld_w);
+    wf[e] = (j < B && k < B && k <= j) ? (float)w64[(size_t)j * B + k] : 0.0f;
+  }
+  if (tid == 0) {
+    status_all[m] = SKYRX_OK;
+    ridge_all[m] = ridge;
+  }
+}
+
+// W = L^-1 (f64, one column per thread), its f32 transposed padded copy and
+// mu hi/lo, for scoring with caller-supplied stats (rx_scores(cube, stats)).
+__global__ void whiten_prepare_kernel(const double* __restrict__ L, const double* __restrict__ mu,
+                                      int B, double* __restrict__ W, float* __restrict__ wf,
+                                      int ld_w, float* __restrict__ mhl) {
+  for (int c = threadIdx.x; c < B; c += blockDim.x) {
+    for (int i = 0; i < c; ++i) W[(size_t)i * B + c] = 0.0;
+    for (int i = c; i < B; ++i) {
+      double a = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) a -= L[(size_t)i * B + k] * W[(size_t)k * B + c];
+      W[(size_t)i * B + c] = a / L[(size_t)i * B + i];
+    }
+    const float hi = (float)mu[c];
+    mhl[c] = hi;
+    mhl[B + c] = (float)(mu[c] - (double)hi);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ld_w * ld_w; e += blockDim.x) {
+    const int k = e / ld_w, j = e - k * ld_w;
+    wf[e] = (j < B && k < B && k <= j) ? (float)W[(size_t)j * B + k] : 0.0f;
+  }
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_whiten_prepare(const double* chol, const double* mu, int32_t bands,
+                                    double* whiten64, float* whiten, int32_t ld_w,
+                                    float* mu_hilo, void* stream) {
+  SKYRX_REQUIRE(bands > 0 && bands <= 1024 && ld_w >= bands, "bad whiten arguments");
+  whiten_prepare_kernel<<<1, 512, 0, as_stream(stream)>>>(chol, mu, bands, whiten64, whiten,
+                                                          ld_w, mu_hilo);
+  SKYRX_CHECK_LAUNCH("skyrx_whiten_prepare");
+  return SKYRX_OK;
+}
+
+extern "C" size_t skyrx_moments_len(int32_t bands) {
+  return 1 + (size_t)bands + (size_t)bands * bands;
+}
+
+static CubeRef make_ref(const void* px, int64_t lines, int32_t samples, int32_t bands,
+                        const float* dark, const float* coeff, const float* gain) {
+  CubeRef c;
+  c.pixels = px;
+  c.dark = dark;
+  c.coeff = coeff;
+  c.gain = gain;
+  c.npix = lines * (int64_t)samples;
+  c.samples = samples;
+  c.bands = bands;
+  return c;
+}
+
+extern "C" int skyrx_stats_shift(int32_t kind, const void* pixels, int64_t lines,
+                                 int32_t samples, int32_t bands, const float* dark,
+                                 const float* coeff, const float* gain, double* shift,
+                                 void* stream) {
+  SKYRX_REQUIRE(bands > 0 && lines >= 0 && samples >= 0, "bad cube shape");
+  SKYRX_REQUIRE(kind == SKYRX_IN_RAW_U16 || kind == SKYRX_IN_F32, "bad pixel kind %d", kind);
+  CubeRef c = make_ref(pixels, lines, samples, bands, dark, coeff, gain);
+  cudaStream_t st = as_stream(stream);
+  if (kind == SKYRX_IN_RAW_U16)
+    shift_kernel<SKYRX_IN_RAW_U16><<<1, 256, 0, st>>>(c, shift);
+  else
+    shift_kernel<SKYRX_IN_F32><<<1, 256, 0, st>>>(c, shift);
+  SKYRX_CHECK_LAUNCH("skyrx_stats_shift");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_stats_workspace(int64_t lines, int32_t samples, int32_t bands,
+                                     size_t* bytes) {
+  SKYRX_REQUIRE(bands > 0 && bytes, "bad arguments");
+  *bytes = gram_ws(gram_geom(lines * (int64_t)samples, bands));  // grid independent of T
+  return SKYRX_OK;
+}
+
+template <int KIND, typename T>
+static void launch_gram(const CubeRef& c, const double* shift, const GramGeom& g, double* pq,
+                        double* ps, int32_t* flags, cudaStream_t st) {
+  const size_t sm = gram_smem(g, sizeof(T));
+  cudaFuncSetAttribute(gram_kernel<KIND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sm);
+  gram_kernel<KIND, T><<<dim3(g.grid, g.parts), kGramThreads, sm, st>>>(c, shift, g, pq, ps,
+                                                                        flags);
+}
+
+extern "C" int skyrx_stats_accumulate(int32_t kind, const void* pixels, int64_t lines,
+                                      int32_t samples, int32_t bands, const float* dark,
+                                      const float* coeff, const float* gain,
+                                      const double* shift, int32_t precise, double* moments,
+                                      int32_t* flags, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
+  SKYRX_REQUIRE(kind == SKYRX_IN_RAW_U16 || kind == SKYRX_IN_F32, "bad pixel kind %d", kind);
+  const int64_t npix = lines * (int64_t)samples;
+  const size_t ts = precise ? sizeof(double) : sizeof(float);
+  GramGeom g = gram_geom(npix, bands, ts);
+  SKYRX_REQUIRE(workspace_bytes >= gram_ws(g), "stats workspace too small (%zu < %zu)",
+                workspace_bytes, gram_ws(g));
+  CubeRef c = make_ref(pixels, lines, samples, bands, dark, coeff, gain);
+  double* part_q = reinterpret_cast<double*>(workspace);
+  double* part_s = part_q + (size_t)g.grid * g.ntiles * 64;
+  cudaStream_t st = as_stream(stream);
+  if (kind == SKYRX_IN_RAW_U16) {
+    if (precise) launch_gram<SKYRX_IN_RAW_U16, double>(c, shift, g, part_q, part_s, flags, st);
+    else launch_gram<SKYRX_IN_RAW_U16, float>(c, shift, g, part_q, part_s, flags, st);
+  } else {
+    if (precise) launch_gram<SKYRX_IN_F32, double>(c, shift, g, part_q, part_s, flags, st);
+    else launch_gram<SKYRX_IN_F32, float>(c, shift, g, part_q, part_s, flags, st);
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_stats_accumulate/gram");
+  const int work = g.ntiles * 64 + bands + 1;
+  gram_reduce_kernel<<<ceil_div(work, 256), 256, 0, st>>>(part_q, part_s, g, bands,
+                                                          (double)npix, moments);
+  SKYRX_CHECK_LAUNCH("skyrx_stats_accumulate/reduce");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_moments_fold(double* state, const double* chunk, int32_t bands,
+                                  double forget, void* stream) {
+  SKYRX_REQUIRE(bands > 0, "bad bands");
+  const int64_t len = (int64_t)skyrx_moments_len(bands);
+  fold_kernel<<<(int)ceil_div<int64_t>(len, 256), 256, 0, as_stream(stream)>>>(state, chunk,
+                                                                               len, forget);
+  SKYRX_CHECK_LAUNCH("skyrx_moments_fold");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
+                                    const int32_t* flags, int32_t bands, int32_t batch,
+                                    double* mu, double* sigma, double* chol, double* sigma_inv,
+                                    double* whiten64, float* whiten, int32_t ld_w,
+                                    float* mu_hilo, double* ridge, int32_t* status,
+                                    void* stream) {
+  SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
+  SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
+  SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
+  const size_t sm = bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double) : 0;
+  cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  finalize_kernel<<<batch, kFinThreads, sm, as_stream(stream)>>>(
+      moments, shift, flags, bands, mu, sigma, chol, sigma_inv, whiten64, whiten, ld_w, mu_hilo,
+      ridge, status);
+  SKYRX_CHECK_LAUNCH("skyrx_stats_finalize");
+  return SKYRX_OK;
+}

@@ -1,0 +1,385 @@
+"""Global RX detector on the B200 — drop-in for skyrx.rx.
+
+Reference: rx.py:26-124.  Public names, signatures, return types and error
+messages are the reference's; the work runs in CUDA kernels:
+
+    compute_stats   K2 moments (csrc/stats.cu gram_kernel) + K3 factorisation
+    rx_scores       K4 whitening product (csrc/score.cu)
+    normalize/threshold/transmit_domain/top-k   K5 (csrc/select.cu)
+
+Two arithmetic modes, both parity-tested:
+  * ``"precise"`` (default for the drop-in functions): FP64 products and
+    sums everywhere, so the reference's own suites pass at their tolerances
+    (1e-9 permutation / backend agreement, 1e-6 oracles).
+  * ``"fast"`` (``detect()``, bench.py): FP32 Gram blocks of <= 192 products
+    promoted to FP64, FP32 whitening — within BASELINE's 1e-5 (stats) and 1e-4
+    (scores) and several times faster.
+
+``detect()`` is the fused hot path the pipeline's calibrate+detect stages need
+(pipeline.py:167-175): raw -> moments -> factor -> scores -> top-0.1% mask
+without materialising radiance, device-resident end to end, one host sync.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .calibrate import _check_tables, _out_cls, _raw_device, line_gains, tables_of
+from .cube import ScoreMap
+
+RIDGE_EPSILONS = (1e-10, 1e-9, 1e-8, 1e-7, 1e-6)
+MODES = ("precise", "fast")
+
+_STATUS_MSG = {
+    _lib.ERR_NONFINITE: "invalid data: cube contains non-finite values",
+    _lib.ERR_NOT_PD: "covariance not positive definite even after ridging",
+}
+
+
+@dataclass(frozen=True)
+class CubeStats:
+    """rx.py:26-39: band means, covariance, its inverse, ridge and Cholesky factor."""
+
+    mu: np.ndarray
+    sigma: np.ndarray
+    sigma_inv: np.ndarray
+    ridge_used: float
+    chol_lower: np.ndarray
+    _device: object = field(default=None, compare=False, repr=False)
+
+
+def _bp(bands: int) -> int:
+    return ((bands + 7) // 8) * 8
+
+
+class DeviceStats:
+    """Device-resident fit of one or more backgrounds (batched over strips).
+
+    Arrays are (batch, ...) CUDA tensors; nothing is copied to the host until
+    :meth:`host` (which also raises the reference's ValueErrors).
+    """
+
+    def __init__(self, bands: int, batch: int = 1):
+        self.bands = bands
+        self.batch = batch
+        self.ld = _bp(bands)
+        f64, f32 = torch.float64, torch.float32
+        B = bands
+        self.shift = _dev.zeros((batch, B), f64)
+        self.moments = _dev.zeros((batch, int(_lib.load().skyrx_moments_len(B))), f64)
+        self.flags = _dev.zeros((batch,), torch.int32)
+        self.mu = _dev.empty((batch, B), f64)
+        self.sigma = _dev.empty((batch, B, B), f64)
+        self.chol = _dev.zeros((batch, B, B), f64)
+        self.sigma_inv = _dev.empty((batch, B, B), f64)
+        self.w64 = _dev.empty((batch, B, B), f64)
+        self.whiten = _dev.zeros((batch, self.ld, self.ld), f32)
+        self.mu_hilo = _dev.zeros((batch, 2 * B), f32)
+        self.ridge = _dev.zeros((batch,), f64)
+        self.status = _dev.zeros((batch,), torch.int32)
+
+    def finalize(self):
+        _lib.call("skyrx_stats_finalize", self.moments.data_ptr(), self.shift.data_ptr(),
+                  self.flags.data_ptr(), self.bands, self.batch, self.mu.data_ptr(),
+                  self.sigma.data_ptr(), self.chol.data_ptr(), self.sigma_inv.data_ptr(),
+                  self.w64.data_ptr(), self.whiten.data_ptr(), self.ld,
+                  self.mu_hilo.data_ptr(), self.ridge.data_ptr(), self.status.data_ptr(),
+                  _dev.stream_ptr())
+        return self
+
+    def check(self, i: int = 0, npix: int | None = None):
+        st = int(self.status[i].item())
+        if st == _lib.ERR_INSUFFICIENT:
+            n = npix if npix is not None else int(self.moments[i, 0].item())
+            raise ValueError(f"insufficient samples: {n} pixels for {self.bands} bands")
+        if st != _lib.OK:
+            raise ValueError(_STATUS_MSG.get(st, f"stats failed with status {st}"))
+
+    def host(self, i: int = 0, npix: int | None = None) -> CubeStats:
+        self.check(i, npix)
+        h = lambda t: _dev.to_host(t[i])  # noqa: E731
+        return CubeStats(mu=h(self.mu), sigma=h(self.sigma), sigma_inv=h(self.sigma_inv),
+                         ridge_used=float(self.ridge[i].item()), chol_lower=h(self.chol),
+                         _device=(self, i))
+
+
+def _radiance_device(cube) -> torch.Tensor:
+    return _dev.to_device(cube.values, torch.float32)
+
+
+def accumulate_moments(ds: DeviceStats, i: int, kind: int, pixels: torch.Tensor, lines: int,
+                       samples: int, tables=None, gains=None, *, precise: bool,
+                       shift: bool = True) -> None:
+    """K2 for one cube into slot i of ``ds`` (shift, moments, non-finite flag)."""
+    B = ds.bands
+    dark = coeff = None
+    if kind == _lib.IN_RAW_U16:
+        dark, coeff = tables
+    args = (pixels.data_ptr(), lines, samples, B, _dev.ptr(dark), _dev.ptr(coeff),
+            _dev.ptr(gains))
+    s = _dev.stream_ptr()
+    if shift:
+        _lib.call("skyrx_stats_shift", kind, *args, ds.shift[i].data_ptr(), s)
+    nbytes = _lib.C.c_size_t(0)
+    _lib.call("skyrx_stats_workspace", lines, samples, B, _lib.C.byref(nbytes))
+    ws = _dev.empty((max(int(nbytes.value), 8),), torch.uint8)
+    _lib.call("skyrx_stats_accumulate", kind, *args, ds.shift[i].data_ptr(), int(precise),
+              ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(), ws.data_ptr(),
+              int(nbytes.value), s)
+
+
+def compute_stats(cube, chunk: int = 65536, *, mode: str = "precise") -> CubeStats:
+    """rx.py:42-86: per-cube Gaussian fit (mean, unbiased covariance, inverse).
+
+    ``chunk`` is accepted for signature compatibility (results are
+    chunk-invariant, rx.py's own test_chunked_equals_unchunked)."""
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    bands = cube.bands
+    n = cube.lines * cube.samples
+    if n <= bands:
+        raise ValueError(f"insufficient samples: {n} pixels for {bands} bands")
+    ds = DeviceStats(bands)
+    px = _radiance_device(cube)
+    accumulate_moments(ds, 0, _lib.IN_F32, px, cube.lines, cube.samples,
+                       precise=(mode == "precise"))
+    ds.finalize()
+    return ds.host(0, n)
+
+
+def _device_whitening(stats: CubeStats, bands: int):
+    d = stats._device
+    if d is not None:
+        ds, i = d
+        return ds.whiten[i], ds.mu_hilo[i], ds.ld
+    ld = _bp(bands)
+    chol = _dev.to_device(np.asarray(stats.chol_lower, np.float64))
+    mu = _dev.to_device(np.asarray(stats.mu, np.float64))
+    w64 = _dev.empty((bands, bands), torch.float64)
+    wf = _dev.zeros((ld, ld), torch.float32)
+    mhl = _dev.empty((2 * bands,), torch.float32)
+    _lib.call("skyrx_whiten_prepare", chol.data_ptr(), mu.data_ptr(), bands, w64.data_ptr(),
+              wf.data_ptr(), ld, mhl.data_ptr(), _dev.stream_ptr())
+    return wf, mhl, ld
+
+
+def mahalanobis_sq_device(pixels: torch.Tensor, mu, chol) -> torch.Tensor:
+    """_accel.py:75-90 semantics on device: f64 delta per row of (N, B) pixels."""
+    n, b = pixels.shape
+    kind = _lib.IN_F64 if pixels.dtype == torch.float64 else _lib.IN_F32
+    if kind == _lib.IN_F32 and pixels.dtype != torch.float32:
+        pixels = pixels.to(torch.float32)
+    mu_d = _dev.to_device(mu, torch.float64)
+    ch_d = _dev.to_device(chol, torch.float64)
+    bp = _bp(b)
+    ws = _dev.empty((b * b + bp * bp,), torch.float64)
+    out = _dev.empty((n,), torch.float64)
+    _lib.call("skyrx_mahalanobis_sq", kind, pixels.data_ptr(), n, b, mu_d.data_ptr(),
+              ch_d.data_ptr(), ws.data_ptr(), out.data_ptr(), _dev.stream_ptr())
+    return out
+
+
+def rx_scores(cube, stats: CubeStats, *, mode: str = "precise") -> ScoreMap:
+    """rx.py:89-97: squared Mahalanobis distance of every pixel, f32 (lines, samples)."""
+    if stats.mu.shape[0] != cube.bands:
+        raise ValueError(
+            f"stats fitted for {stats.mu.shape[0]} bands, cube has {cube.bands}"
+        )
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    L, S, B = cube.lines, cube.samples, cube.bands
+    px = _radiance_device(cube)
+    if mode == "precise":
+        d = mahalanobis_sq_device(px.reshape(-1, B), stats.mu, stats.chol_lower)
+        out = d.to(torch.float32).reshape(L, S)
+    else:
+        wf, mhl, ld = _device_whitening(stats, B)
+        out = _dev.empty((L, S), torch.float32)
+        _lib.call("skyrx_score", _lib.IN_F32, px.data_ptr(), L, S, B, None, None, None,
+                  mhl.data_ptr(), wf.data_ptr(), ld, out.data_ptr(), None, _dev.stream_ptr())
+    cls = _out_cls(cube, "ScoreMap", ScoreMap)
+    return cls(_dev.like_input(cube.values, out))
+
+
+def _scores_device(scores) -> torch.Tensor:
+    v = scores.values if hasattr(scores, "values") else scores
+    return _dev.to_device(v, torch.float32)
+
+
+def score_max_key(v: torch.Tensor) -> torch.Tensor:
+    key = _dev.zeros((1,), torch.uint32)
+    _lib.call("skyrx_max", v.data_ptr(), v.numel(), key.data_ptr(), _dev.stream_ptr())
+    return key
+
+
+def key_to_float(key: torch.Tensor) -> float:
+    u = int(key.item())
+    b = (u & 0x7FFFFFFF) if (u & 0x80000000) else (~u & 0xFFFFFFFF)
+    return float(np.array([b], np.uint32).view(np.float32)[0])
+
+
+def normalize_scores(scores) -> ScoreMap:
+    """rx.py:100-105: divide by f32(max); an all-zero (max <= 0) map is returned as is."""
+    v = _scores_device(scores)
+    if v.numel() == 0:
+        return scores
+    key = score_max_key(v)
+    out = _dev.empty(tuple(v.shape), torch.float32)
+    _lib.call("skyrx_normalize", v.data_ptr(), v.numel(), key.data_ptr(), out.data_ptr(),
+              _dev.stream_ptr())
+    if key_to_float(key) <= 0.0:
+        return scores
+    cls = _out_cls(scores, "ScoreMap", ScoreMap)
+    return cls(_dev.like_input(scores.values, out))
+
+
+def threshold_scores(norm_scores, threshold: float):
+    """rx.py:108-112: mask = values > threshold, compared in f32 (NEP 50)."""
+    if not 0.0 <= threshold <= 1.0:
+        raise ValueError(f"threshold {threshold} outside [0, 1]")
+    v = _scores_device(norm_scores)
+    mask = _dev.empty(tuple(v.shape), torch.uint8)
+    _lib.call("skyrx_threshold", v.data_ptr(), v.numel(), float(np.float32(threshold)),
+              mask.data_ptr(), _dev.stream_ptr())
+    return _dev.like_input(norm_scores.values, mask.to(torch.bool))
+
+
+def transmit_domain(values, max_score: float):
+    """rx.py:115-124: sqrt(score / cube max) in f64; zeros when the max is 0."""
+    v = _dev.to_device(values, torch.float32)
+    out = _dev.empty(tuple(v.shape), torch.float64)
+    _lib.call("skyrx_transmit_domain", v.data_ptr(), v.numel(), float(max_score),
+              out.data_ptr(), _dev.stream_ptr())
+    return _dev.like_input(values, out)
+
+
+# --------------------------------------------------------------------------- R-TOPK
+def topk_count(n: int) -> int:
+    """k = ceil(0.001 * N) in integers (SURVEY.md §8(a) R-TOPK)."""
+    return (n + 999) // 1000
+
+
+def topk_threshold_device(v: torch.Tensor, k: int) -> torch.Tensor:
+    ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,), torch.int32)
+    thr = _dev.empty((1,), torch.float32)
+    _lib.call("skyrx_topk_threshold", v.data_ptr(), v.numel(), k, thr.data_ptr(),
+              ws.data_ptr(), _dev.stream_ptr())
+    return thr
+
+
+def topk_mask(scores, k: int | None = None):
+    """R-TOPK: mask = delta > delta_(k+1), the top ceil(0.1%) of raw f32 scores."""
+    v = _scores_device(scores)
+    k = topk_count(v.numel()) if k is None else int(k)
+    thr = topk_threshold_device(v, k)
+    mask = _dev.empty(tuple(v.shape), torch.uint8)
+    _lib.call("skyrx_mask_gt", v.data_ptr(), v.numel(), thr.data_ptr(), mask.data_ptr(),
+              _dev.stream_ptr())
+    src = scores.values if hasattr(scores, "values") else scores
+    return _dev.like_input(src, mask.to(torch.bool))
+
+
+# --------------------------------------------------------------------------- fused hot path
+@dataclass
+class Detection:
+    """Result of :func:`detect`: host numpy or device tensors (``device=True``)."""
+
+    stats: object       # CubeStats (host) or DeviceStats (device)
+    scores: object      # (L, S) f32
+    mask: object        # (L, S) bool (top 0.1%)
+    threshold: float    # delta_(k+1)
+    max_score: float
+
+
+class DetectPlan:
+    """Reusable device buffers for repeated detect() calls on one cube shape."""
+
+    def __init__(self, lines: int, samples: int, bands: int, batch: int = 1):
+        self.shape = (lines, samples, bands)
+        self.ds = DeviceStats(bands, batch)
+        nbytes = _lib.C.c_size_t(0)
+        _lib.call("skyrx_stats_workspace", lines, samples, bands, _lib.C.byref(nbytes))
+        self.ws_bytes = int(nbytes.value)
+        self.ws = _dev.empty((max(self.ws_bytes, 8),), torch.uint8)
+        self.scores = _dev.empty((batch, lines, samples), torch.float32)
+        self.mask = _dev.empty((batch, lines, samples), torch.uint8)
+        self.max_key = _dev.zeros((batch,), torch.uint32)
+        self.thr = _dev.empty((batch,), torch.float32)
+        self.topk_ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,),
+                                  torch.int32)
+        self.launches = 0
+
+    def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
+            precise: bool = False):
+        """Enqueue the whole path for cube i (no host synchronisation)."""
+        L, S, B = self.shape
+        ds = self.ds
+        s = _dev.stream_ptr()
+        args = (raw.data_ptr(), L, S, B, dark.data_ptr(), coeff.data_ptr(), gains.data_ptr())
+        ds.flags[i].zero_()
+        _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+        _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
+                  int(precise), ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
+                  self.ws.data_ptr(), self.ws_bytes, s)
+        self.launches += 3
+        return self
+
+    def finalize(self):
+        self.ds.finalize()
+        self.launches += 1
+        return self
+
+    def score(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None):
+        L, S, B = self.shape
+        ds = self.ds
+        s = _dev.stream_ptr()
+        n = L * S
+        k = topk_count(n) if k is None else int(k)
+        self.max_key[i].zero_()
+        sc = self.scores[i]
+        _lib.call("skyrx_score", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, dark.data_ptr(),
+                  coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
+                  ds.whiten[i].data_ptr(), ds.ld, sc.data_ptr(), self.max_key[i:i + 1].data_ptr(),
+                  s)
+        _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
+                  self.topk_ws.data_ptr(), s)
+        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),
+                  self.mask[i].data_ptr(), s)
+        self.launches += 1 + 7 + 1
+        return self
+
+
+def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
+           precise: bool = False, plan: DetectPlan | None = None) -> Detection:
+    """Fused calibrate + RX + top-0.1% mask for one raw cube (the hot path).
+
+    Equivalent to ``compute_stats(apply_calibration(raw))`` -> ``rx_scores`` ->
+    ``topk_mask`` (oracle ``detect``), without materialising radiance.
+    Raises the reference's ValueErrors (invalid tables, gains, insufficient,
+    non-finite, not positive definite).
+    """
+    tables = tables_of(tables)
+    _check_tables(raw, tables)
+    gains = line_gains(raw)
+    L, S, B = raw.lines, raw.samples, raw.bands
+    n = L * S
+    if n <= B:
+        raise ValueError(f"insufficient samples: {n} pixels for {B} bands")
+    dark, coeff = tables.device()
+    rv = _raw_device(raw)
+    gd = _dev.to_device(gains, torch.float32)
+    plan = plan or DetectPlan(L, S, B)
+    plan.run(0, rv, dark, coeff, gd, precise=precise).finalize().score(0, rv, dark, coeff, gd, k)
+    on_dev = _dev.is_device(raw.values) if device is None else device
+    ds = plan.ds
+    ds.check(0, n)
+    thr = float(plan.thr[0].item())
+    mx = key_to_float(plan.max_key[0])
+    if on_dev:
+        return Detection(ds, plan.scores[0], plan.mask[0].to(torch.bool), thr, mx)
+    return Detection(ds.host(0, n), _dev.to_host(plan.scores[0]),
+                     _dev.to_host(plan.mask[0]).astype(bool), thr, mx)

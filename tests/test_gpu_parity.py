@@ -1,0 +1,349 @@
+"""CUDA path vs the reference's golden outputs and the pinned CPU oracle.
+
+All tests need a B200 (`-m gpu`); they call the hand-written kernels through
+the C ABI (paper_2602_13509_b200._lib) and compare with:
+  * tests/golden/*.npz — produced by the real reference package;
+  * oracle/ — the CPU restatement pinned to those goldens (tests/test_oracle.py).
+Tolerances: calibration bit-exact; precise-mode stats/scores at the
+reference's own test tolerances; fast mode at BASELINE's 1e-5 (stats,
+normwise) and 1e-4 (scores, per pixel); masks bit-exact except pixels whose
+reference score lies within 1e-4 relative of the reference threshold.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import case_names
+from oracle import skyrx_oracle as O
+from oracle import synth as osynth
+
+pytestmark = pytest.mark.gpu
+
+STATS_RTOL_FAST = 1e-5      # BASELINE.json north_star: stats within 1e-5 relative
+SCORE_RTOL_FAST = 1e-4      # scores within 1e-4 relative
+MASK_BAND = 1e-4            # mask exemption band around the threshold
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2602_13509_b200 as P
+    from paper_2602_13509_b200 import build
+
+    build.build()
+    return P
+
+
+def raw_cube(P, values, gains=None, wl=None):
+    values = np.asarray(values, np.uint16)
+    if gains is None:
+        gains = np.ones(values.shape[0])
+    if wl is None:
+        wl = np.linspace(400, 1000, values.shape[2])
+    return P.RawCube(values, wl, P.cube.line_meta_for(gains))
+
+
+def rad_cube(P, values):
+    values = np.asarray(values, np.float32)
+    return P.RadianceCube(values, np.linspace(400, 1000, values.shape[2]),
+                          P.cube.line_meta_for([2.0] * values.shape[0]))
+
+
+def bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+def normwise(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
+
+
+# ----------------------------------------------------------------------------- generator
+class TestGenerator:
+    @pytest.mark.parametrize("args,line0,n", [((1, 900, 70, 5), 0, 40), ((3, 64, 270, 8), 500, 9),
+                                              ((5, 40, 128, 5), 131000, 12),
+                                              ((4007, 900, 70, 5), 16000, 16)])
+    def test_device_generator_bit_identical(self, P, args, line0, n):
+        from paper_2602_13509_b200.synth import Scene
+
+        dev = Scene(*args).generate(line0, n).cpu().numpy()
+        host = osynth.generate_lines(osynth.make_tables(*args), line0, n)
+        assert np.array_equal(dev, host)
+
+
+# ----------------------------------------------------------------------------- calibration
+class TestCalibration:
+    def test_random_tables_bit_exact(self, P, golden):
+        g = golden["calibrate"]
+        raw = raw_cube(P, g["rand/raw"], g["rand/gains"])
+        out = P.apply_calibration(raw, P.CalibrationTables(g["rand/dark"], g["rand/coeff"]))
+        assert np.array_equal(bits(out.values), bits(g["rand/out"]))
+
+    def test_synth_with_line_gains_bit_exact(self, P, golden):
+        g = golden["calibrate"]
+        t = osynth.make_tables(11, 96, 70)
+        out = P.apply_calibration(raw_cube(P, g["synth/raw"], g["synth/gains"]),
+                                  P.CalibrationTables(t.dark, t.coeff))
+        assert np.array_equal(bits(out.values), bits(g["synth/out"]))
+
+    def test_by_definition_and_clamp(self, P):
+        raw = raw_cube(P, np.full((1, 1, 24), 100), [4.0])
+        t = P.CalibrationTables(np.full((1, 24), 10.0), np.full((1, 24), 2.0))
+        assert (P.apply_calibration(raw, t).values == 45.0).all()
+        raw = raw_cube(P, np.full((1, 1, 24), 5))
+        t = P.CalibrationTables(np.full((1, 24), 10.0), np.ones((1, 24)))
+        assert (P.apply_calibration(raw, t).values == 0).all()
+
+    def test_unaligned_shapes(self, P, rng):
+        # odd S*B takes the scalar kernel; results must still be bit-exact
+        raw = rng.integers(0, 4096, (5, 7, 13)).astype(np.uint16)
+        dark = rng.uniform(0, 50, (7, 13)).astype(np.float32)
+        coeff = rng.uniform(0.5, 2, (7, 13)).astype(np.float32)
+        gains = rng.uniform(1, 8, 5)
+        out = P.apply_calibration(raw_cube(P, raw, gains), P.CalibrationTables(dark, coeff))
+        want = O.apply_calibration(raw, dark, coeff, gains)
+        assert np.array_equal(bits(out.values), bits(want))
+
+    def test_poisoned_gain_is_inf_then_nonfinite(self, P):
+        # test_pipeline.py:84-102: 1e-40 is subnormal in f32 and must not flush
+        raw = raw_cube(P, np.full((2, 2, 3), 500), [1.0, 1e-40])
+        t = P.CalibrationTables(np.zeros((2, 3)), np.ones((2, 3)))
+        out = P.apply_calibration(raw, t)
+        assert np.isinf(out.values[1]).all() and np.isfinite(out.values[0]).all()
+        with pytest.raises(ValueError, match="non-finite"):
+            P.compute_stats(out)
+        with pytest.raises(ValueError, match="non-finite"):
+            P.compute_stats(out, mode="fast")
+        with pytest.raises(ValueError, match="non-finite"):
+            P.detect(raw, t)
+
+    @pytest.mark.parametrize("name", ["b300", "b44", "b340f8"])
+    def test_fused_bin_rgb_bit_exact(self, P, golden, name):
+        g = golden["calibrate"]
+        raw = raw_cube(P, g[f"{name}/raw"], g[f"{name}/gains"], g[f"{name}/wl"])
+        cube, rgb = P.calibrate_bin_rgb(raw, P.CalibrationTables(g[f"{name}/dark"],
+                                                                 g[f"{name}/coeff"]),
+                                        factor=int(g[f"{name}/factor"]))
+        assert np.array_equal(bits(cube.values), bits(g[f"{name}/out"]))
+        assert np.array_equal(cube.wavelengths_nm, g[f"{name}/centers"])
+        assert np.array_equal(bits(rgb), bits(g[f"{name}/rgb"]))
+
+    def test_composed_ops_match_fused(self, P, golden):
+        g = golden["calibrate"]
+        raw = raw_cube(P, g["b300/raw"], g["b300/gains"], g["b300/wl"])
+        t = P.CalibrationTables(g["b300/dark"], g["b300/coeff"])
+        composed = P.bin_bands(P.discard_oob_bands(P.apply_calibration(raw, t)), 4)
+        assert composed.bands == 70
+        assert np.array_equal(bits(composed.values), bits(g["b300/out"]))
+        assert np.array_equal(bits(P.extract_rgb(composed)), bits(g["b300/rgb"]))
+
+    def test_bin_all_ones_and_sum_preserved(self, P, rng):
+        cube = rad_cube(P, np.ones((2, 3, 280), np.float32))
+        assert (P.bin_bands(cube, 4).values == 4.0).all()
+        vals = rng.integers(0, 256, (3, 4, 280)).astype(np.float32)
+        out = P.bin_bands(rad_cube(P, vals), 4)
+        assert np.sum(out.values, dtype=np.float64) == np.sum(vals, dtype=np.float64)
+
+    def test_device_tensors_stay_on_device(self, P, golden):
+        import torch
+
+        g = golden["calibrate"]
+        raw = P.RawCube(torch.from_numpy(g["rand/raw"]).cuda(), np.linspace(400, 1000, 24),
+                        gains=torch.tensor(g["rand/gains"], dtype=torch.float32).cuda())
+        out = P.apply_calibration(raw, P.CalibrationTables(g["rand/dark"], g["rand/coeff"]))
+        assert isinstance(out.values, torch.Tensor) and out.values.is_cuda
+        assert np.array_equal(bits(out.values.cpu().numpy()), bits(g["rand/out"]))
+
+
+# ----------------------------------------------------------------------------- statistics
+class TestStatsPrecise:
+    def test_every_golden_case(self, P, golden):
+        g = golden["stats"]
+        for name in case_names(g, "mu"):
+            st = P.compute_stats(rad_cube(P, g[f"{name}/values"]))
+            assert np.allclose(st.mu, g[f"{name}/mu"], rtol=1e-12, atol=1e-9), name
+            assert np.allclose(st.sigma, g[f"{name}/sigma"], rtol=1e-9, atol=1e-9), name
+            assert st.ridge_used == float(g[f"{name}/ridge"]), name
+            assert np.allclose(st.chol_lower, g[f"{name}/chol"], rtol=1e-8, atol=1e-9), name
+            assert normwise(st.sigma_inv, g[f"{name}/sigma_inv"]) < 1e-8, name
+
+    def test_every_golden_case_scores(self, P, golden):
+        g = golden["stats"]
+        for name in case_names(g, "mu"):
+            cube = rad_cube(P, g[f"{name}/values"])
+            sc = P.rx_scores(cube, P.compute_stats(cube)).values
+            want = g[f"{name}/scores"]
+            rel = np.abs(sc - want) / np.maximum(np.abs(want), 1e-12)
+            assert (rel < 1e-6).all(), (name, rel.max())
+
+    def test_degenerate(self, P):
+        cube = rad_cube(P, np.full((4, 4, 3), 9.0))
+        st = P.compute_stats(cube)
+        assert (st.sigma == 0).all() and st.ridge_used > 0
+        assert (P.rx_scores(cube, st).values == 0).all()
+        base = np.arange(16, dtype=np.float32)
+        cube = rad_cube(P, np.stack([base, 2 * base], axis=1).reshape(4, 4, 2))
+        st = P.compute_stats(cube)
+        assert st.ridge_used > 0 and np.isfinite(P.rx_scores(cube, st).values).all()
+
+    def test_errors(self, P, rng):
+        with pytest.raises(ValueError, match="insufficient"):
+            P.compute_stats(rad_cube(P, rng.random((1, 3, 4), dtype=np.float32)))
+        vals = np.ones((3, 3, 2), np.float32)
+        vals[1, 1, 0] = np.inf
+        with pytest.raises(ValueError, match="non-finite"):
+            P.compute_stats(rad_cube(P, vals))
+        a = rad_cube(P, rng.random((4, 4, 3), dtype=np.float32))
+        b = rad_cube(P, rng.random((4, 4, 5), dtype=np.float32))
+        with pytest.raises(ValueError, match="bands"):
+            P.rx_scores(b, P.compute_stats(a))
+
+    def test_permutation_invariance_rtol_1e9(self, P, rng):
+        # test_rx.py:144-158 at the reference's own tolerance (precise mode)
+        vals = rng.normal(10, 2, (6, 8, 3)).astype(np.float32)
+        s1 = P.rx_scores(rad_cube(P, vals), P.compute_stats(rad_cube(P, vals))).values.ravel()
+        perm = rng.permutation(48)
+        sh = vals.reshape(-1, 3)[perm].reshape(6, 8, 3)
+        s2 = P.rx_scores(rad_cube(P, sh), P.compute_stats(rad_cube(P, sh))).values.ravel()
+        assert np.allclose(s2, s1[perm], rtol=1e-9, atol=1e-9)
+
+    def test_large_band_counts(self, P):
+        # B = 270 / 300 exercise the multi-part Gram and the global-memory Cholesky
+        for b in (128, 270, 300):
+            t = osynth.make_tables(77, 48, b, 8)
+            raw = osynth.generate_lines(t, 0, 40)
+            rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(40))
+            want = O.compute_stats(rad)
+            st = P.compute_stats(rad_cube(P, rad))
+            assert normwise(st.sigma, want.sigma) < 1e-12, b
+            assert st.ridge_used == want.ridge_used
+            assert normwise(st.sigma_inv, want.sigma_inv) < 1e-6, b
+            sc = P.rx_scores(rad_cube(P, rad), st).values
+            ref = O.rx_scores(rad, want)
+            assert (np.abs(sc - ref) / ref).max() < 1e-5, b
+
+
+class TestAccelSlot:
+    def test_matches_reference_numba(self, P, golden):
+        from paper_2602_13509_b200 import _accel
+
+        a = golden["accel"]
+        d = _accel.mahalanobis_sq(a["px"], a["mu"], a["chol"])
+        assert d.dtype == np.float64
+        assert (np.abs(d - a["numba"]) / np.abs(a["numba"])).max() < 1e-9
+        d64 = _accel.mahalanobis_sq(a["px"].astype(np.float64), a["mu"], a["chol"])
+        assert (np.abs(d64 - a["numpy"]) / np.abs(a["numpy"])).max() < 1e-9
+
+
+class TestFastMode:
+    @pytest.mark.parametrize("name", ["synth70", "synth128", "normal", "acc0", "acc3"])
+    def test_stats_and_scores_within_baseline_tolerance(self, P, golden, name):
+        g = golden["stats"]
+        cube = rad_cube(P, g[f"{name}/values"])
+        st = P.compute_stats(cube, mode="fast")
+        assert normwise(st.mu, g[f"{name}/mu"]) < STATS_RTOL_FAST
+        assert normwise(st.sigma, g[f"{name}/sigma"]) < STATS_RTOL_FAST
+        assert normwise(st.sigma_inv, g[f"{name}/sigma_inv"]) < STATS_RTOL_FAST
+        assert st.ridge_used == float(g[f"{name}/ridge"])
+        sc = P.rx_scores(cube, st, mode="fast").values
+        want = g[f"{name}/scores"]
+        assert (np.abs(sc - want) / np.maximum(want, 1e-12)).max() < SCORE_RTOL_FAST
+
+
+# ----------------------------------------------------------------------------- normalise etc.
+class TestNormalize:
+    def test_golden(self, P, golden):
+        g = golden["normalize"]
+        n = P.normalize_scores(P.ScoreMap(g["rand/values"]))
+        assert np.array_equal(bits(n.values), bits(g["rand/norm"]))
+        assert np.array_equal(P.threshold_scores(n, 0.37), g["rand/mask037"])
+        n = P.normalize_scores(P.ScoreMap(g["small/values"]))
+        assert np.array_equal(P.threshold_scores(n, 1.0), g["small/mask1"])
+        assert np.array_equal(P.threshold_scores(n, 0.0), g["small/mask0"])
+        m = P.threshold_scores(P.ScoreMap(g["edge/values"]), float(g["edge/t"]))
+        assert np.array_equal(m, g["edge/mask"])
+
+    def test_zero_map_and_synth(self, P, golden):
+        z = P.ScoreMap(np.zeros((2, 2)))
+        assert (P.normalize_scores(z).values == 0).all()
+        g = golden["stats"]
+        n = P.normalize_scores(P.ScoreMap(g["synth70/scores"]))
+        assert np.array_equal(bits(n.values), bits(g["synth70/norm"]))
+        assert np.array_equal(P.threshold_scores(n, 0.11), g["synth70/mask_t"])
+
+    def test_transmit_domain(self, P, rng):
+        v = rng.random((7, 9)).astype(np.float32) * 20
+        got = P.transmit_domain(v, 17.5)
+        assert got.dtype == np.float64
+        assert np.array_equal(got, O.transmit_domain(v, 17.5))
+        assert (P.transmit_domain(v, 0.0) == 0).all()
+
+
+class TestTopK:
+    @pytest.mark.parametrize("n,k", [(10_000, None), (1_843_200, None), (5, 1), (1, None),
+                                     (1000, 999), (1000, 1000), (0, None)])
+    def test_matches_oracle(self, P, rng, n, k):
+        v = (rng.random(n) * rng.choice([1, 10, 1e4], n)).astype(np.float32)
+        got = P.topk_mask(v, k)
+        assert np.array_equal(got, O.topk_mask(v, k))
+
+    def test_ties(self, P):
+        v = np.array([1, 2, 2, 2, 0], np.float32)
+        assert np.array_equal(P.topk_mask(v), O.topk_mask(v))
+        v = np.full(5000, 3.0, np.float32)
+        assert not P.topk_mask(v).any()
+
+
+# ----------------------------------------------------------------------------- the fused path
+def check_detection(det, raw, t, gains=None):
+    gains = np.ones(raw.shape[0]) if gains is None else gains
+    want_stats, want_scores, want_mask = O.detect(raw, t.dark, t.coeff, gains)
+    st = det.stats
+    assert normwise(st.mu, want_stats.mu) < STATS_RTOL_FAST
+    assert normwise(st.sigma, want_stats.sigma) < STATS_RTOL_FAST
+    assert normwise(st.sigma_inv, want_stats.sigma_inv) < STATS_RTOL_FAST
+    assert st.ridge_used == want_stats.ridge_used
+    rel = np.abs(det.scores - want_scores) / np.maximum(want_scores, 1e-12)
+    assert rel.max() < SCORE_RTOL_FAST, rel.max()
+    thr = O.topk_threshold(want_scores)
+    differ = det.mask != want_mask
+    near = np.abs(want_scores - thr) <= MASK_BAND * abs(thr)
+    assert not (differ & ~near).any()
+    return rel.max(), differ.sum()
+
+
+class TestDetect:
+    @pytest.mark.parametrize("seed,L,S,B,K", [(21, 48, 64, 70, 5), (23, 30, 40, 128, 5),
+                                              (3, 40, 1024, 270, 8), (9, 17, 33, 5, 3)])
+    def test_small_cubes_vs_oracle(self, P, seed, L, S, B, K):
+        t = osynth.make_tables(seed, S, B, K)
+        raw = osynth.generate_lines(t, 0, L)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff))
+        check_detection(det, raw, t)
+
+    def test_line_gains(self, P):
+        t = osynth.make_tables(31, 64, 70)
+        raw = osynth.generate_lines(t, 0, 50)
+        gains = np.linspace(1.0, 8.0, 50)
+        det = P.detect(raw_cube(P, raw, gains), P.CalibrationTables(t.dark, t.coeff))
+        check_detection(det, raw, t, gains)
+
+    def test_deterministic(self, P):
+        t = osynth.make_tables(1, 900, 70)
+        raw = osynth.generate_lines(t, 0, 128)
+        cube = raw_cube(P, raw)
+        tab = P.CalibrationTables(t.dark, t.coeff)
+        a, b = P.detect(cube, tab), P.detect(cube, tab)
+        assert np.array_equal(bits(a.scores), bits(b.scores))
+        assert np.array_equal(a.stats.sigma, b.stats.sigma)
+        assert np.array_equal(a.mask, b.mask)
+
+    @pytest.mark.slow
+    def test_c1_full_size_vs_oracle(self, P):
+        c = osynth.CONFIGS["c1"]
+        t = osynth.make_tables(c["seed"], c["samples"], c["bands"], c["components"])
+        from paper_2602_13509_b200.synth import Scene
+
+        raw = Scene(c["seed"], c["samples"], c["bands"], c["components"]).generate(
+            0, c["lines"]).cpu().numpy()
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff))
+        worst, ndiff = check_detection(det, raw, t)
+        assert det.mask.sum() <= osynth.CONFIGS["c1"]["lines"] * 900 // 1000 + 1
