@@ -22,7 +22,7 @@ namespace skyrx {
 
 constexpr int kGramThreads = 256;
 constexpr int kGramTileP = 64;       // pixels per shared-memory tile
-constexpr int kFlushProducts = 192;  // FP32 products per accumulator before FP64 promotion
+constexpr int kFlushProducts = 64;   // FP32 products per accumulator before FP64 promotion
 
 struct GramGeom {
   int bp, nt, ntiles, parts, groups, tiles_per_part, ld, grid;
@@ -97,7 +97,9 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
   const bool active = group < geo.groups;
   int I = 0, J = 0;
   if (active) tri_decode(part * geo.tiles_per_part + tl, I, J);
+  // band sums: thread b owns bands b and b + 256 (bp <= 512 covers B <= 512)
   const bool do_s = (part == 0) && tid < geo.bp;
+  const bool do_s2 = (part == 0) && tid + kGramThreads < geo.bp;
 
   T acc[8][8];
   double acc64[8][8];
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = T(0), acc64[i][j] = 0.0;
-  double s64 = 0.0;
+  double s64 = 0.0, s64b = 0.0;
   int since_flush = 0;
   bool finite_ok = true;
   const int per_thread = ceil_div(kGramTileP, geo.groups);
@@ -119,6 +121,11 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
       T cs = T(0);
       for (int p = 0; p < kGramTileP; ++p) cs += d[p * geo.ld + tid];
       s64 += (double)cs;
+      if (do_s2) {
+        T cs2 = T(0);
+        for (int p = 0; p < kGramTileP; ++p) cs2 += d[p * geo.ld + tid + kGramThreads];
+        s64b += (double)cs2;
+      }
     }
     if (active) {
       if (kFast && since_flush + per_thread > kFlushProducts) {
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
       for (int j = 0; j < 8; ++j) pq[tl * 64 + i * 8 + j] = acc64[i][j];
   }
   if (do_s) part_s[(size_t)blockIdx.x * geo.bp + tid] = s64;
+  if (do_s2) part_s[(size_t)blockIdx.x * geo.bp + tid + kGramThreads] = s64b;
   if (!finite_ok) atomicOr(flags, 1);
 }
 
@@ -350,7 +358,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
         while (ii * (ii + 1) / 2 > e) --ii;
         const int kk = e - ii * (ii + 1) / 2;
         const int i = j + 1 + ii, k = j + 1 + kk;
-        A[(size_t)i * B + k] -= A[(size_t)i * B + j] * A[(size_t)k * B + j];
+        A[(size_t)i * B + k] = __dsub_rn(A[(size_t)i * B + k],
+                                        __dmul_rn(A[(size_t)i * B + j], A[(size_t)k * B + j]));
       }
       __syncthreads();
     }
@@ -498,7 +507,7 @@ extern "C" int skyrx_stats_accumulate(int32_t kind, const void* pixels, int64_t 
                                       const double* shift, int32_t precise, double* moments,
                                       int32_t* flags, void* workspace, size_t workspace_bytes,
                                       void* stream) {
-  SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
+  SKYRX_REQUIRE(bands > 0 && bands <= 320, "bands %d outside [1, 320]", bands);
   SKYRX_REQUIRE(kind == SKYRX_IN_RAW_U16 || kind == SKYRX_IN_F32, "bad pixel kind %d", kind);
   const int64_t npix = lines * (int64_t)samples;
   const size_t ts = precise ? sizeof(double) : sizeof(float);
