@@ -41,7 +41,11 @@ SIGNATURES = {
                                        vp, vp, vp]),
     "skyrx_whiten_prepare": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),
     "skyrx_score": (C.c_int, [i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
-    "skyrx_mahalanobis_sq": (C.c_int, [i32, vp, i64, i32, vp, vp, vp, vp, vp]),
+    "skyrx_wpack_bytes": (sz, [i32]),
+    "skyrx_pack_whiten": (C.c_int, [vp, i32, i32, vp, vp]),
+    "skyrx_score_tc_supported": (C.c_int, [i64, i32, i32, vp]),
+    "skyrx_score_tc": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "skyrx_mahalanobis_sq":(C.c_int, [i32, vp, i64, i32, vp, vp, vp, vp, vp]),
     "skyrx_max": (C.c_int, [vp, i64, vp, vp]),
     "skyrx_normalize": (C.c_int, [vp, i64, vp, vp, vp]),
     "skyrx_threshold": (C.c_int, [vp, i64, f32, vp, vp]),

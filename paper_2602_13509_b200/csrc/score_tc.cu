@@ -1,0 +1,365 @@
+// K4-TC — fused calibrate + RX score on the 5th-gen tensor cores (tcgen05).
+//
+// delta(p) = sum_j z_pj^2,  z = D W^T,  D = x - mu (128 pixels x KP bands),
+// W = L^-1 (KP x KP, lower).  Precision: D and W are
+// split into f16 hi + lo (W per output row scaled by a power of two so lo
+// stays normal); z accumulates Dhi*Whi + Dhi*Wlo + Dlo*Whi in the f32 TMEM
+// accumulator (which truncates, tools/umma_probe.cu); emulated worst-case
+// score error 1.6e-6 against the f64 reference (tolerance 1e-4).
+//
+// Warp roles (persistent CTA, one per SM):
+//   warp 4  TMA producer : raw line segments of each tile -> smem ring (cp.async.bulk)
+//   warp 5  MMA issuer   : 3*KP/16 tcgen05.mma per tile into a double-buffered
+//                          TMEM accumulator (128 lanes = pixels, KP columns)
+//   warps 0-3 workers    : calibrate + centre + f16 split each pixel row into the
+//                          K-major A operand; then the epilogue of the previous
+//                          tile (tcgen05.ld row, unscale, sum of squares, store).
+// Calibration tables of the current sample block live in shared memory.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "umma.cuh"
+
+namespace skyrx {
+using namespace umma;
+
+constexpr int kTcThreads = 192;
+constexpr int kTcWorkers = 128;
+constexpr int kScoreRawStages = 3;
+constexpr int kScoreAStages = 2;
+constexpr int kScoreWmax = 32;
+
+struct ScoreTcParams {
+  const uint16_t* raw;
+  const float* dark;
+  const float* coeff;
+  const float* gain;
+  const float* mu_hilo;
+  const uint8_t* wpack;
+  float* scores;
+  uint32_t* max_key;
+  TileSched ts;
+  int64_t per_cta;
+  uint32_t raw_stage_bytes;
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__host__ __device__ constexpr uint32_t wpack_bytes_for(int kp) {
+  return 2u * kp * kp * 2u + kp * 4u;
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
+  constexpr int NP = KP;
+  constexpr uint32_t A_BYTES = 128u * KP * 2u;
+  constexpr uint32_t SBO_A = (KP / 8) * 128u;
+  constexpr uint32_t W_BYTES = NP * KP * 2u;
+  constexpr uint32_t SBO_B = (KP / 8) * 128u;
+  constexpr uint32_t TMEM_COLS = 2 * NP <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int B = p.ts.B;
+  uint8_t* raw_ring = sm;
+  uint8_t* a_ring = raw_ring + kScoreRawStages * p.raw_stage_bytes;
+  uint8_t* wsm = a_ring + kScoreAStages * 2 * A_BYTES;
+  float* colscale = reinterpret_cast<float*>(wsm + 2 * W_BYTES);
+  float* dark_s = colscale + NP;
+  float* coeff_s = dark_s + kScoreWmax * (B + 1);
+  float* mhi = coeff_s + kScoreWmax * (B + 1);
+  float* mlo = mhi + KP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(mlo + KP) + 7) & ~uintptr_t(7));
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + kScoreRawStages;
+  uint64_t* a_full = raw_empty + kScoreRawStages;
+  uint64_t* a_empty = a_full + kScoreAStages;
+  uint64_t* acc_full = a_empty + kScoreAStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* w_bar = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int64_t it0 = (int64_t)blockIdx.x * p.per_cta;
+  int64_t it1 = it0 + p.per_cta;
+  if (it1 > p.ts.items) it1 = p.ts.items;
+  const int n = it0 < it1 ? (int)(it1 - it0) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kScoreRawStages; ++s) mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers);
+    for (int s = 0; s < kScoreAStages; ++s) mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers);
+    mbar_init(w_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, TMEM_COLS);
+  for (int k = tid; k < KP; k += blockDim.x) {
+    mhi[k] = k < B ? p.mu_hilo[k] : 0.0f;
+    mlo[k] = k < B ? p.mu_hilo[B + k] : 0.0f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
+      const uint32_t wb = wpack_bytes_for(KP);
+      mbar_arrive_expect_tx(w_bar, wb);
+      bulk_g2s(wsm, p.wpack, wb, w_bar);
+      for (int t = 0; t < n; ++t) {
+        const int s = t % kScoreRawStages;
+        mbar_wait(&raw_empty[s], ((t / kScoreRawStages) & 1) ^ 1);
+        const TileInfo ti = tile_info(p.ts, it0 + t);
+        const uint32_t seg = (uint32_t)ti.w * B * 2u;
+        mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)ti.nlines);
+        uint8_t* dst = raw_ring + s * p.raw_stage_bytes;
+        for (int li = 0; li < ti.nlines; ++li) {
+          const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
+          bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+      mbar_wait(w_bar, 0);
+      constexpr uint32_t idesc = idesc_f16_f32(128, NP, 0, 0);
+      for (int t = 0; t < n; ++t) {
+        const int as = t % kScoreAStages;
+        const int acs = t & 1;
+        mbar_wait(&a_full[as], (t / kScoreAStages) & 1);
+        mbar_wait(&acc_empty[acs], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint8_t* abase = a_ring + as * 2 * A_BYTES;
+        const uint32_t d = tmem + acs * NP;
+#pragma unroll
+        for (int ks = 0; ks < KP / 16; ++ks) {
+          const uint64_t ahi = smem_desc(abase + ks * 256, 128, SBO_A);
+          const uint64_t alo = smem_desc(abase + A_BYTES + ks * 256, 128, SBO_A);
+          const uint64_t bhi = smem_desc(wsm + ks * 256, 128, SBO_B);
+          const uint64_t blo = smem_desc(wsm + W_BYTES + ks * 256, 128, SBO_B);
+          mma_f16(d, ahi, bhi, idesc, ks > 0);
+          mma_f16(d, ahi, blo, idesc, 1);
+          mma_f16(d, alo, bhi, idesc, 1);
+        }
+        mma_commit(&a_empty[as]);
+        mma_commit(&acc_full[acs]);
+      }
+    }
+  } else {  // ------------------------------------------------------------ workers
+    const int r = tid;  // pixel row of the tile
+    mbar_wait(w_bar, 0);
+    int cur_block = -1;
+    uint32_t local_max = 0;
+    auto epilogue = [&](int t, const TileInfo& ti) {
+      const int acs = t & 1;
+      mbar_wait(&acc_full[acs], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + acs * NP;
+      float sum = 0.0f;
+#pragma unroll
+      for (int c = 0; c < NP / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float z = __uint_as_float(v[q]) * colscale[c * 16 + q];
+          sum = fmaf(z, z, sum);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[acs]);
+      if (r < ti.rows) {
+        const int li = r / ti.w;
+        const int j = r - li * ti.w;
+        p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + j] = sum;
+        local_max = max(local_max, f2ord(sum));
+      }
+    };
+    TileInfo prev{};
+    for (int t = 0; t < n; ++t) {
+      const TileInfo ti = tile_info(p.ts, it0 + t);
+      if (ti.block != cur_block) {
+        named_sync(1, kTcWorkers);
+        for (int e = r; e < ti.w * B; e += kTcWorkers) {
+          const int j = e / B, b = e - j * B;
+          const int64_t g = (int64_t)(ti.s0 + j) * B + b;
+          dark_s[j * (B + 1) + b] = __ldg(p.dark + g);
+          coeff_s[j * (B + 1) + b] = __ldg(p.coeff + g);
+        }
+        named_sync(1, kTcWorkers);
+        cur_block = ti.block;
+      }
+      const int s = t % kScoreRawStages;
+      const int as = t % kScoreAStages;
+      mbar_wait(&raw_full[s], (t / kScoreRawStages) & 1);
+      mbar_wait(&a_empty[as], ((t / kScoreAStages) & 1) ^ 1);
+      uint8_t* ahi = a_ring + as * 2 * A_BYTES;
+      uint8_t* alo = ahi + A_BYTES;
+      const uint32_t row_off = (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
+      const bool valid = r < ti.rows;
+      int li = 0, j = 0;
+      float g = 1.0f;
+      const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
+      if (valid) {
+        li = r / ti.w;
+        j = r - li * ti.w;
+        g = __ldg(p.gain + ti.line0 + li);
+      }
+      const float* dk = dark_s + j * (B + 1);
+      const float* ck = coeff_s + j * (B + 1);
+#pragma unroll 2
+      for (int c = 0; c < KP / 8; ++c) {
+        float dv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int k = c * 8 + q;
+          float v = 0.0f;
+          if (valid && k < B) {
+            float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dk[k]), 0.0f), ck[k]);
+            if (g != 1.0f) x = __fdiv_rn(x, g);
+            v = __fsub_rn(__fsub_rn(x, mhi[k]), mlo[k]);
+          }
+          dv[q] = v;
+        }
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __half2 h = __floats2half2_rn(dv[2 * q], dv[2 * q + 1]);
+          const float2 hf = __half22float2(h);
+          const __half2 l = __floats2half2_rn(dv[2 * q] - hf.x, dv[2 * q + 1] - hf.y);
+          hw[q] = *reinterpret_cast<const uint32_t*>(&h);
+          lw[q] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+        *reinterpret_cast<uint4*>(ahi + row_off + c * 128) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(alo + row_off + c * 128) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&a_full[as]);
+      mbar_arrive(&raw_empty[s]);
+      if (t > 0) epilogue(t - 1, prev);
+      prev = ti;
+    }
+    if (n > 0) epilogue(n - 1, prev);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+    if ((tid & 31) == 0 && local_max && p.max_key) atomicMax(p.max_key, local_max);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// W (f64, row-major B x B, lower) -> f16 hi/lo K-major B operand + column scales
+template <int KP>
+__global__ void pack_whiten_kernel(const double* __restrict__ w64, int B, uint8_t* __restrict__ out) {
+  constexpr uint32_t SBO_B = (KP / 8) * 128u;
+  constexpr uint32_t W_BYTES = KP * KP * 2u;
+  const double* W = w64 + (size_t)blockIdx.x * B * B;
+  uint8_t* o = out + (size_t)blockIdx.x * wpack_bytes_for(KP);
+  float* colscale = reinterpret_cast<float*>(o + 2 * W_BYTES);
+  for (int jn = threadIdx.x; jn < KP; jn += blockDim.x) {
+    double mx = 0.0;
+    if (jn < B)
+      for (int k = 0; k < B; ++k) mx = fmax(mx, fabs(W[(size_t)jn * B + k]));
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);        // mx in [2^(e-1), 2^e)
+    const double sc = ldexp(1.0, 14 - e);  // max scaled value in [2^13, 2^14)
+    colscale[jn] = (float)ldexp(1.0, e - 14);
+    for (int k = 0; k < KP; ++k) {
+      const double v = (jn < B && k < B && k <= jn) ? W[(size_t)jn * B + k] * sc : 0.0;
+      const __half h = __double2half(v);
+      const __half l = __double2half(v - (double)__half2float(h));
+      const uint32_t off = (jn >> 3) * SBO_B + (k >> 3) * 128u + (jn & 7) * 16u + (k & 7) * 2u;
+      *reinterpret_cast<__half*>(o + off) = h;
+      *reinterpret_cast<__half*>(o + W_BYTES + off) = l;
+    }
+  }
+}
+
+static int kp_for(int B) { return ((B + 15) / 16) * 16; }
+
+template <int KP>
+static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
+  p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
+  const size_t A_BYTES = 128u * KP * 2u;
+  const size_t smem = kScoreRawStages * (size_t)p.raw_stage_bytes + kScoreAStages * 2 * A_BYTES +
+                      wpack_bytes_for(KP) + 2 * (size_t)kScoreWmax * (p.ts.B + 1) * 4 +
+                      2 * KP * 4 + 16 * 8 + 64;
+  int grid = kSMs;
+  if (p.ts.items < grid) grid = (int)p.ts.items;
+  if (grid < 1) return SKYRX_OK;
+  p.per_cta = (p.ts.items + grid - 1) / grid;
+  cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
+  SKYRX_CHECK_LAUNCH("score_tc_kernel");
+  return SKYRX_OK;
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" size_t skyrx_wpack_bytes(int32_t bands) {
+  return wpack_bytes_for(kp_for(bands));
+}
+
+extern "C" int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t batch,
+                                 void* wpack, void* stream) {
+  SKYRX_REQUIRE(bands > 0 && bands <= 96 && batch >= 1, "pack_whiten supports 1 <= B <= 96");
+  cudaStream_t st = as_stream(stream);
+  switch (kp_for(bands)) {
+#define SKYRX_KP(k) \
+  case k:           \
+    pack_whiten_kernel<k><<<batch, 128, 0, st>>>(whiten64, bands, (uint8_t*)wpack); break;
+    SKYRX_KP(16) SKYRX_KP(32) SKYRX_KP(48) SKYRX_KP(64) SKYRX_KP(80) SKYRX_KP(96)
+#undef SKYRX_KP
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_pack_whiten");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t bands,
+                                        const void* raw) {
+  TileSched ts;
+  if (bands < 1 || bands > 96) return 0;
+  if (((uintptr_t)raw & 15) != 0) return 0;
+  return tc_sched(lines, samples, bands, kScoreWmax, ts) ? 1 : 0;
+}
+
+extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                              const float* dark, const float* coeff, const float* gain,
+                              const float* mu_hilo, const void* wpack, float* scores,
+                              uint32_t* max_key, void* stream) {
+  SKYRX_REQUIRE(skyrx_score_tc_supported(lines, samples, bands, raw),
+                "tensor-core score path unsupported for this shape/alignment");
+  ScoreTcParams p{};
+  p.raw = raw;
+  p.dark = dark;
+  p.coeff = coeff;
+  p.gain = gain;
+  p.mu_hilo = mu_hilo;
+  p.wpack = (const uint8_t*)wpack;
+  p.scores = scores;
+  p.max_key = max_key;
+  tc_sched(lines, samples, bands, kScoreWmax, p.ts);
+  if (lines * (int64_t)samples == 0) return SKYRX_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (kp_for(bands)) {
+    case 16: return launch_score_tc<16>(p, st);
+    case 32: return launch_score_tc<32>(p, st);
+    case 48: return launch_score_tc<48>(p, st);
+    case 64: return launch_score_tc<64>(p, st);
+    case 80: return launch_score_tc<80>(p, st);
+    case 96: return launch_score_tc<96>(p, st);
+  }
+  set_error("unsupported band count %d", bands);
+  return SKYRX_ERR_ARG;
+}

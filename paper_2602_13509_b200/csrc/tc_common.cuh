@@ -1,0 +1,67 @@
+// Tile schedule shared by the tensor-core kernels (K2 moments, K4 scores).
+//
+// A tile is up to 128 pixel rows = R lines x W samples of one "sample block"
+// [s0, s0 + W): every line segment of a tile is contiguous in the BIP cube, so
+// the producer fetches a tile with R 1-D bulk copies (cp.async.bulk, TMA
+// engine) and the calibration tables of the block (dark, coeff: W x B f32)
+// stay resident in shared memory while the CTA walks down the lines.
+// S = 900 uses W = 32 (R = 4): 28 full blocks + one 4-sample block that packs
+// 32 lines per tile, so rows are >= 97% occupied.
+#pragma once
+#include "common.cuh"
+
+namespace skyrx {
+
+struct TileSched {
+  int32_t S, B, W, nb, wl;    // samples, bands, block width, #blocks, last block width
+  int32_t R, rl;              // lines per tile in full / last block
+  int64_t L, ng, ngl, items;  // lines, tiles per full / last block, total tiles
+};
+
+inline bool tc_sched(int64_t L, int32_t S, int32_t B, int32_t Wmax, TileSched& t) {
+  t.S = S;
+  t.B = B;
+  t.L = L;
+  t.W = S < Wmax ? S : Wmax;
+  t.nb = (S + t.W - 1) / t.W;
+  t.wl = S - (t.nb - 1) * t.W;
+  t.R = 128 / t.W;
+  t.rl = 128 / t.wl;
+  if (t.rl > 128) t.rl = 128;
+  t.ng = (L + t.R - 1) / t.R;
+  t.ngl = (L + t.rl - 1) / t.rl;
+  t.items = (int64_t)(t.nb - 1) * t.ng + t.ngl;
+  // every bulk copy (line segment) must be 16-B sized and aligned
+  const bool ok = ((int64_t)S * B) % 8 == 0 && ((int64_t)t.W * B) % 8 == 0 &&
+                  ((int64_t)t.wl * B) % 8 == 0;
+  return ok;
+}
+
+struct TileInfo {
+  int32_t block, s0, w, r, rows;  // rows = r * w (<= 128)
+  int64_t line0, nlines;
+};
+
+__host__ __device__ __forceinline__ TileInfo tile_info(const TileSched& t, int64_t item) {
+  TileInfo ti;
+  const int64_t full = (int64_t)(t.nb - 1) * t.ng;
+  int64_t g;
+  if (item < full) {
+    ti.block = (int32_t)(item / t.ng);
+    g = item - (int64_t)ti.block * t.ng;
+    ti.w = t.W;
+    ti.r = t.R;
+  } else {
+    ti.block = t.nb - 1;
+    g = item - full;
+    ti.w = t.wl;
+    ti.r = t.rl;
+  }
+  ti.s0 = ti.block * t.W;
+  ti.line0 = g * ti.r;
+  ti.nlines = t.L - ti.line0 < ti.r ? t.L - ti.line0 : ti.r;
+  ti.rows = (int32_t)(ti.nlines * ti.w);
+  return ti;
+}
+
+}  // namespace skyrx

@@ -22,6 +22,7 @@ without materialising radiance, device-resident end to end, one host sync.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -312,6 +313,10 @@ class DetectPlan:
         self.topk_ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,),
                                   torch.int32)
         self.launches = 0
+        lib = _lib.load()
+        self.tc = (bands <= 96 and os.environ.get("SKYRX_B200_TC", "1") != "0")
+        self.wpack_bytes = int(lib.skyrx_wpack_bytes(bands)) if self.tc else 0
+        self.wpack = (_dev.empty((batch, self.wpack_bytes), torch.uint8) if self.tc else None)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
             precise: bool = False):
@@ -331,6 +336,10 @@ class DetectPlan:
     def finalize(self):
         self.ds.finalize()
         self.launches += 1
+        if self.tc:
+            _lib.call("skyrx_pack_whiten", self.ds.w64.data_ptr(), self.ds.bands, self.ds.batch,
+                      self.wpack.data_ptr(), _dev.stream_ptr())
+            self.launches += 1
         return self
 
     def score(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None):
@@ -341,10 +350,15 @@ class DetectPlan:
         k = topk_count(n) if k is None else int(k)
         self.max_key[i].zero_()
         sc = self.scores[i]
-        _lib.call("skyrx_score", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, dark.data_ptr(),
-                  coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
-                  ds.whiten[i].data_ptr(), ds.ld, sc.data_ptr(), self.max_key[i:i + 1].data_ptr(),
-                  s)
+        if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
+            _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
+                      coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
+                      self.wpack[i].data_ptr(), sc.data_ptr(), self.max_key[i:i + 1].data_ptr(), s)
+        else:
+            _lib.call("skyrx_score", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, dark.data_ptr(),
+                      coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
+                      ds.whiten[i].data_ptr(), ds.ld, sc.data_ptr(),
+                      self.max_key[i:i + 1].data_ptr(), s)
         _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
                   self.topk_ws.data_ptr(), s)
         _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),

@@ -326,6 +326,29 @@ class TestDetect:
         det = P.detect(raw_cube(P, raw, gains), P.CalibrationTables(t.dark, t.coeff))
         check_detection(det, raw, t, gains)
 
+    @pytest.mark.parametrize("S,B", [(900, 70), (64, 70), (96, 48), (40, 16), (100, 96)])
+    def test_tensor_core_score_matches_oracle_and_ffma(self, P, S, B):
+        import torch
+
+        from paper_2602_13509_b200 import _lib
+
+        t = osynth.make_tables(41, S, B, 5)
+        L = 70
+        raw = osynth.generate_lines(t, 0, L)
+        lib = _lib.load()
+        rv = torch.from_numpy(raw).cuda()
+        assert lib.skyrx_score_tc_supported(L, S, B, rv.data_ptr()) == 1
+        tab = P.CalibrationTables(t.dark, t.coeff)
+        plan_tc = P.DetectPlan(L, S, B)
+        assert plan_tc.tc
+        det_tc = P.detect(raw_cube(P, raw), tab, plan=plan_tc)
+        plan_ff = P.DetectPlan(L, S, B)
+        plan_ff.tc = False
+        det_ff = P.detect(raw_cube(P, raw), tab, plan=plan_ff)
+        check_detection(det_tc, raw, t)
+        rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
+        assert rel.max() < 2e-5, rel.max()
+
     def test_deterministic(self, P):
         t = osynth.make_tables(1, 900, 70)
         raw = osynth.generate_lines(t, 0, 128)
