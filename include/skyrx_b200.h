@@ -37,6 +37,7 @@ extern "C" {
 #define SKYRX_ERR_INSUFFICIENT 3 /* rx.py:51-52 "insufficient samples"          */
 #define SKYRX_ERR_NONFINITE 4    /* rx.py:53-54 "non-finite values"             */
 #define SKYRX_ERR_NOT_PD 5       /* rx.py:79-80 "not positive definite ..."     */
+#define SKYRX_ERR_RANGE 6        /* tensor-core quantiser overflow: recompute    */
 
 /* pixel source kinds */
 #define SKYRX_IN_RAW_U16 0 /* uint16 raw counts + (dark, coeff, gain) calibration */
@@ -93,6 +94,21 @@ int skyrx_stats_accumulate(int32_t kind, const void* pixels, int64_t lines, int3
                            const float* gain, const double* shift, int32_t precise,
                            double* moments, int32_t* flags, void* workspace,
                            size_t workspace_bytes, void* stream);
+
+/* Tensor-core (tcgen05 kind::i8) moments for RAW cubes with B <= 79: values
+ * quantised to 21-bit fixed point around the sample shift (skyrx_quant_shift
+ * gives c_b and 2^e_b), three int8 digits, exact int32 digit Gram.  Writes
+ * the same [n, s, Q] moments block; flags |= 2 if a value fell outside the
+ * quantiser range (caller then recomputes with skyrx_stats_accumulate). */
+int skyrx_stats_tc_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
+size_t skyrx_stats_tc_workspace(int32_t bands);
+int skyrx_quant_shift(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
+                      int32_t bands, const float* dark, const float* coeff, const float* gain,
+                      double* shift, float* qinv, void* stream);
+int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                   const float* dark, const float* coeff, const float* gain, const double* shift,
+                   const float* qinv, double* moments, int32_t* flags, void* workspace,
+                   size_t workspace_bytes, void* stream);
 
 /* state = forget * state + chunk (R-STREAM exponential forgetting) */
 int skyrx_moments_fold(double* state, const double* chunk, int32_t bands, double forget,

@@ -18,7 +18,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libskyrx_b200.so"
 
-OK, ERR_ARG, ERR_CUDA, ERR_INSUFFICIENT, ERR_NONFINITE, ERR_NOT_PD = range(6)
+OK, ERR_ARG, ERR_CUDA, ERR_INSUFFICIENT, ERR_NONFINITE, ERR_NOT_PD, ERR_RANGE = range(7)
 IN_RAW_U16, IN_F32, IN_F64 = 0, 1, 2
 
 vp, i32, i64, u32, f32, f64, sz = (C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_float,
@@ -36,7 +36,11 @@ SIGNATURES = {
     "skyrx_stats_workspace": (C.c_int, [i64, i32, i32, C.POINTER(sz)]),
     "skyrx_stats_accumulate": (C.c_int, [i32, vp, i64, i32, i32, vp, vp, vp, vp, i32, vp, vp,
                                          vp, sz, vp]),
-    "skyrx_moments_fold": (C.c_int, [vp, vp, i32, f64, vp]),
+    "skyrx_stats_tc_supported": (C.c_int, [i64, i32, i32, vp]),
+    "skyrx_stats_tc_workspace": (sz, [i32]),
+    "skyrx_quant_shift": (C.c_int, [i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "skyrx_stats_tc": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "skyrx_moments_fold":(C.c_int, [vp, vp, i32, f64, vp]),
     "skyrx_stats_finalize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp,
                                        vp, vp, vp]),
     "skyrx_whiten_prepare": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),

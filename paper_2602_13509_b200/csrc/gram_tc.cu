@@ -1,0 +1,414 @@
+// K2-TC — fused calibrate + background moments on the tensor cores, exact in int32.
+//
+// Reference: rx.py:56-66 (f64 mean, then f64 Gram of centred pixels).  Here
+// every calibrated value is centred by the sample shift c_b and quantised to a
+// fixed point D = rint((x - c_b) / q_b) with |D| < 2^20 (q_b a power of two
+// from 8x the largest sampled deviation).  D is split into three balanced
+// base-128 digits D = D2*2^14 + D1*2^7 + D0 (each in [-64, 64)) and the Gram
+// of the digits is accumulated EXACTLY in int32 by tcgen05.mma kind::i8
+// (|digit products| <= 2^12, so 2^19 pixels fit before any overflow):
+//     G = sum_a 2^14a Pa,a + sum_{a>b} 2^7(a+b) (Pa,b + Pa,b^T),  Pa,b = Da^T Db
+// One constant band (index B, digit D0 = 1 on valid pixels) makes the same
+// products carry n and sum(D).  The only approximation left is the
+// quantisation (noise ~q/sqrt(12) per element, averaged over the cube): the
+// emulated worst score error on the c1 generator is 8.5e-7.
+// Values outside the quantiser range set flags |= 2 and the host recomputes
+// that cube with the FFMA kernel (never happens on the BASELINE generators).
+//
+// Operands are MN-major (bands contiguous) so each pixel row writes 16-byte
+// chunks: smem address of (digit a, band b, pixel p) =
+//     (p/8)*LBO + (a*NG + b/16)*128 + (p%8)*16 + b%16,  LBO = 3*NG*128.
+// Per 32-pixel K step three MMAs cover the six products:
+//     A = D2 (M=128), B = [D0|D1|D2] (N = 3*BPg) -> P20 P21 P22
+//     A = D1,         B = [D0|D1]    (N = 2*BPg) -> P10 P11
+//     A = D0,         B = D0         (N =   BPg) -> P00          (6*BPg <= 480 TMEM cols)
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "umma.cuh"
+
+namespace skyrx {
+using namespace umma;
+
+constexpr int kGtThreads = 320;  // 8 worker warps (2 per pixel row) + TMA + MMA
+constexpr int kGtWorkers = 256;
+constexpr int kGtRawStages = 3;
+constexpr int kGtOpStages = 2;
+constexpr int kGtWmax = 32;
+constexpr int kGtFlushTiles = 3072;  // 3072*128 px * 2^12 < 2^31
+
+struct GramTcParams {
+  const uint16_t* raw;
+  const float* dark;
+  const float* coeff;
+  const float* gain;
+  const double* shift;   // c_b (f32-representable)
+  const float* qinv;     // 2^e_b
+  double* part;          // per CTA: Y[BPg*BPg] then X[BPg*BPg], column-major [j][i]
+  int32_t* flags;
+  TileSched ts;
+  int64_t per_cta;
+  uint32_t raw_stage_bytes;
+};
+
+template <int BPG>
+__global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) {
+  constexpr int NG = BPG / 16;
+  constexpr uint32_t LBO = 3u * NG * 128u;
+  // 16 pixel groups (128 px) + pad for the M=128 A reads past the last group
+  constexpr uint32_t OP_BYTES = 16u * LBO + 1024u;
+  constexpr uint32_t N2 = 3 * BPG, N1 = 2 * BPG, N0 = BPG;
+  static_assert(6 * BPG <= 512, "TMEM holds six BPG-wide products");
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int B = p.ts.B;
+  uint8_t* raw_ring = sm;
+  uint8_t* op_ring = raw_ring + kGtRawStages * p.raw_stage_bytes;
+  float* dark_s = reinterpret_cast<float*>(op_ring + kGtOpStages * OP_BYTES);
+  float* coeff_s = dark_s + kGtWmax * (B + 1);
+  float* cs = coeff_s + kGtWmax * (B + 1);
+  float* qs = cs + BPG;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(qs + BPG) + 7) & ~uintptr_t(7));
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + kGtRawStages;
+  uint64_t* op_full = raw_empty + kGtRawStages;
+  uint64_t* op_empty = op_full + kGtOpStages;
+  uint64_t* acc_full = op_empty + kGtOpStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int64_t it0 = (int64_t)blockIdx.x * p.per_cta;
+  int64_t it1 = it0 + p.per_cta;
+  if (it1 > p.ts.items) it1 = p.ts.items;
+  const int n = it0 < it1 ? (int)(it1 - it0) : 0;
+  const int nflush = (n + kGtFlushTiles - 1) / kGtFlushTiles;
+
+  if (tid == 0) {
+    for (int s = 0; s < kGtRawStages; ++s) mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kGtWorkers);
+    for (int s = 0; s < kGtOpStages; ++s) mbar_init(&op_full[s], kGtWorkers), mbar_init(&op_empty[s], 1);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kGtWorkers);
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  for (int b = tid; b < BPG; b += blockDim.x) {
+    cs[b] = b < B ? (float)p.shift[b] : 0.0f;
+    qs[b] = b < B ? p.qinv[b] : 0.0f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
+      for (int t = 0; t < n; ++t) {
+        const int s = t % kGtRawStages;
+        mbar_wait(&raw_empty[s], ((t / kGtRawStages) & 1) ^ 1);
+        const TileInfo ti = tile_info(p.ts, it0 + t);
+        const uint32_t seg = (uint32_t)ti.w * B * 2u;
+        mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)ti.nlines);
+        uint8_t* dst = raw_ring + s * p.raw_stage_bytes;
+        for (int li = 0; li < ti.nlines; ++li) {
+          const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
+          bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+      constexpr uint32_t id2 = idesc_s8_s32(128, N2, 1, 1);
+      constexpr uint32_t id1 = idesc_s8_s32(128, N1, 1, 1);
+      constexpr uint32_t id0 = idesc_s8_s32(128, N0, 1, 1);
+      for (int t = 0; t < n; ++t) {
+        const int os = t % kGtOpStages;
+        const bool first = (t % kGtFlushTiles) == 0;
+        if (first && t > 0) mbar_wait(acc_empty, ((t / kGtFlushTiles) - 1) & 1);
+        mbar_wait(&op_full[os], (t / kGtOpStages) & 1);
+        tc_fence_after();
+        const uint8_t* base = op_ring + os * OP_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {  // 4 x 32 pixels
+          const uint8_t* kb = base + ks * 4 * LBO;
+          const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+          const uint64_t b = smem_desc(kb, LBO, 128);
+          mma_i8(tmem + 0, smem_desc(kb + 2 * NG * 128, LBO, 128), b, id2, acc);
+          mma_i8(tmem + N2, smem_desc(kb + NG * 128, LBO, 128), b, id1, acc);
+          mma_i8(tmem + N2 + N1, smem_desc(kb, LBO, 128), b, id0, acc);
+        }
+        mma_commit(&op_empty[os]);
+        if ((t % kGtFlushTiles) == kGtFlushTiles - 1 || t == n - 1) mma_commit(acc_full);
+      }
+    }
+  } else {  // ------------------------------------------------------------ workers
+    const int r = tid & 127;          // pixel row
+    const int h = tid >> 7;           // which band groups this thread packs
+    constexpr int G0 = (NG + 1) / 2;  // groups [0, G0) for h = 0, [G0, NG) for h = 1
+    const int g_lo = h ? G0 : 0, g_hi = h ? NG : G0;
+    int cur_block = -1;
+    bool range_ok = true, finite_ok = true;
+    int flushes = 0;
+    auto flush = [&]() {
+      mbar_wait(acc_full, flushes & 1);
+      tc_fence_after();
+      // warp w reads TMEM lanes 32*(w%4).., columns split by h
+      const int lane_row = 32 * (warp & 3) + (tid & 31);  // band row i
+      const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+      double* Y = p.part + (size_t)blockIdx.x * 2 * BPG * BPG;
+      double* X = Y + BPG * BPG;
+      for (int jc = h; jc < NG; jc += 2) {
+        uint32_t p20[16], p21[16], p22[16], p10[16], p11[16], p00[16];
+        tmem_ld16(tl + 0 * BPG + jc * 16, p20);
+        tmem_ld16(tl + 1 * BPG + jc * 16, p21);
+        tmem_ld16(tl + 2 * BPG + jc * 16, p22);
+        tmem_ld16(tl + N2 + 0 * BPG + jc * 16, p10);
+        tmem_ld16(tl + N2 + 1 * BPG + jc * 16, p11);
+        tmem_ld16(tl + N2 + N1 + jc * 16, p00);
+        tmem_ld_wait();
+        if (lane_row < BPG) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int j = jc * 16 + q;
+            const double y = 268435456.0 * (double)(int32_t)p22[q] +
+                             16384.0 * (double)(int32_t)p11[q] + (double)(int32_t)p00[q];
+            const double x = 2097152.0 * (double)(int32_t)p21[q] +
+                             16384.0 * (double)(int32_t)p20[q] + 128.0 * (double)(int32_t)p10[q];
+            const size_t o = (size_t)j * BPG + lane_row;
+            if (flushes == 0) {
+              Y[o] = y;
+              X[o] = x;
+            } else {
+              Y[o] += y;
+              X[o] += x;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      ++flushes;
+    };
+    for (int t = 0; t < n; ++t) {
+      const TileInfo ti = tile_info(p.ts, it0 + t);
+      if (ti.block != cur_block) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
+        for (int e = tid; e < ti.w * B; e += kGtWorkers) {
+          const int j = e / B, b = e - j * B;
+          const int64_t g = (int64_t)(ti.s0 + j) * B + b;
+          dark_s[j * (B + 1) + b] = __ldg(p.dark + g);
+          coeff_s[j * (B + 1) + b] = __ldg(p.coeff + g);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
+        cur_block = ti.block;
+      }
+      const int s = t % kGtRawStages;
+      const int os = t % kGtOpStages;
+      mbar_wait(&raw_full[s], (t / kGtRawStages) & 1);
+      mbar_wait(&op_empty[os], ((t / kGtOpStages) & 1) ^ 1);
+      const bool valid = r < ti.rows;
+      int j = 0;
+      float g = 1.0f;
+      if (valid) {
+        const int li = r / ti.w;
+        j = r - li * ti.w;
+        g = __ldg(p.gain + ti.line0 + li);
+      }
+      const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
+      const float* dk = dark_s + j * (B + 1);
+      const float* ck = coeff_s + j * (B + 1);
+      uint8_t* ob = op_ring + os * OP_BYTES + (uint32_t)(r >> 3) * LBO + (uint32_t)(r & 7) * 16u;
+      for (int gi = g_lo; gi < g_hi; ++gi) {
+        uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int k = gi * 16 + q4 * 4 + q;
+            int D = 0;
+            if (valid && k < B) {
+              float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dk[k]), 0.0f), ck[k]);
+              if (g != 1.0f) x = __fdiv_rn(x, g);
+              finite_ok &= isfinite(x);
+              const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);
+              range_ok &= fabsf(tq) < 1048575.0f;
+              D = __float2int_rn(tq);
+            } else if (valid && k == B) {
+              D = 1;  // constant band: carries n and sum(D)
+            }
+            const int d0 = ((D + 64) & 127) - 64;
+            const int t1 = (D - d0) >> 7;
+            const int d1 = ((t1 + 64) & 127) - 64;
+            const int d2 = (t1 - d1) >> 7;
+            a0 |= (uint32_t)(d0 & 255) << (8 * q);
+            a1 |= (uint32_t)(d1 & 255) << (8 * q);
+            a2 |= (uint32_t)(d2 & 255) << (8 * q);
+          }
+          w0[q4] = a0, w1[q4] = a1, w2[q4] = a2;
+        }
+        *reinterpret_cast<uint4*>(ob + (0 * NG + gi) * 128) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(ob + (1 * NG + gi) * 128) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4*>(ob + (2 * NG + gi) * 128) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&op_full[os]);
+      mbar_arrive(&raw_empty[s]);
+      if ((t % kGtFlushTiles) == kGtFlushTiles - 1 && t != n - 1) flush();
+    }
+    if (n > 0) flush();
+    if (!range_ok) atomicOr(p.flags, 2);
+    if (!finite_ok) atomicOr(p.flags, 1);
+  }
+  (void)nflush;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc(tmem, 512);
+}
+
+// Gram (units) = sum over CTAs of Y + X + X^T, then scale to moments [n, s, Q]
+template <int BPG>
+__global__ void gram_tc_reduce_kernel(const double* __restrict__ part, int nparts, int B,
+                                      const float* __restrict__ qinv, double* __restrict__ moments) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // e = i * BPG + j
+  if (e >= BPG * BPG) return;
+  const int i = e / BPG, j = e - i * BPG;
+  if (i > B || j > B || j > i) return;  // lower triangle incl. the constant band B
+  double v = 0.0;
+  for (int c = 0; c < nparts; ++c) {
+    const double* Y = part + (size_t)c * 2 * BPG * BPG;
+    const double* X = Y + BPG * BPG;
+    v += Y[(size_t)j * BPG + i] + X[(size_t)j * BPG + i] + X[(size_t)i * BPG + j];
+  }
+  double* s_out = moments + 1;
+  double* q_out = moments + 1 + B;
+  const double qi = i < B ? 1.0 / (double)qinv[i] : 1.0;
+  const double qj = j < B ? 1.0 / (double)qinv[j] : 1.0;
+  if (i == B && j == B) {
+    moments[0] = v;                       // pixel count (exact)
+  } else if (i == B) {
+    s_out[j] = v * qj;                    // sum over pixels of (x_j - c_j), quantised
+  } else {
+    q_out[(size_t)i * B + j] = v * qi * qj;
+    q_out[(size_t)j * B + i] = v * qi * qj;
+  }
+}
+
+// c_b = f32(mean of a strided sample), q_b from 8x the largest sampled deviation
+template <int KIND>
+__global__ void quant_shift_kernel(const void* pixels, int64_t npix, int32_t samples, int32_t B,
+                                   const float* dark, const float* coeff, const float* gain,
+                                   double* shift, float* qinv) {
+  const int64_t step = npix > 4096 ? npix / 4096 : 1;
+  const int64_t m = npix > 0 ? (npix + step - 1) / step : 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    auto val = [&](int64_t i) {
+      const int64_t pix = i * step;
+      const int64_t gi = pix * B + b;
+      if constexpr (KIND == SKYRX_IN_RAW_U16) {
+        const int64_t line = pix / samples;
+        const int64_t tb = (pix - line * samples) * B + b;
+        return calib((float)reinterpret_cast<const uint16_t*>(pixels)[gi], dark[tb], coeff[tb],
+                     gain[line]);
+      } else {
+        return reinterpret_cast<const float*>(pixels)[gi];
+      }
+    };
+    double acc = 0.0;
+    for (int64_t i = 0; i < m; ++i) acc += (double)val(i);
+    const float c = m > 0 ? (float)(acc / (double)m) : 0.0f;
+    float amax = 0.0f;
+    for (int64_t i = 0; i < m; ++i) amax = fmaxf(amax, fabsf(__fsub_rn(val(i), c)));
+    const float bound = fmaxf(8.0f * amax, 1e-30f);
+    int e = 0;
+    frexpf(bound, &e);                 // bound < 2^e
+    int ex = 20 - e;                   // |D| <= bound * 2^ex < 2^20
+    ex = ex > 120 ? 120 : (ex < -120 ? -120 : ex);
+    shift[b] = (double)c;
+    qinv[b] = ldexpf(1.0f, ex);
+  }
+}
+
+static int bpg_for(int B) { return ((B + 1 + 15) / 16) * 16; }
+
+template <int BPG>
+static int launch_gram_tc(GramTcParams p, double* moments, cudaStream_t st) {
+  p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
+  constexpr uint32_t LBO = 3u * (BPG / 16) * 128u;
+  const size_t smem = kGtRawStages * (size_t)p.raw_stage_bytes + kGtOpStages * (16u * LBO + 1024u) +
+                      2 * (size_t)kGtWmax * (p.ts.B + 1) * 4 + 2 * BPG * 4 + 16 * 8 + 64;
+  int grid = kSMs;
+  if (p.ts.items < grid) grid = (int)p.ts.items;
+  if (grid < 1) grid = 1;
+  p.per_cta = (p.ts.items + grid - 1) / grid;
+  cudaFuncSetAttribute(gram_tc_kernel<BPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_tc_kernel<BPG><<<grid, kGtThreads, smem, st>>>(p);
+  SKYRX_CHECK_LAUNCH("gram_tc_kernel");
+  gram_tc_reduce_kernel<BPG><<<ceil_div(BPG * BPG, 256), 256, 0, st>>>(p.part, grid, p.ts.B, p.qinv,
+                                                                        moments);
+  SKYRX_CHECK_LAUNCH("gram_tc_reduce_kernel");
+  return SKYRX_OK;
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_stats_tc_supported(int64_t lines, int32_t samples, int32_t bands,
+                                        const void* raw) {
+  TileSched ts;
+  if (bands < 1 || bands > 79) return 0;
+  if (((uintptr_t)raw & 15) != 0) return 0;
+  return tc_sched(lines, samples, bands, kGtWmax, ts) ? 1 : 0;
+}
+
+extern "C" size_t skyrx_stats_tc_workspace(int32_t bands) {
+  const size_t bpg = (size_t)bpg_for(bands);
+  return (size_t)kSMs * 2 * bpg * bpg * sizeof(double) + 256 * sizeof(float);
+}
+
+extern "C" int skyrx_quant_shift(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
+                                 int32_t bands, const float* dark, const float* coeff,
+                                 const float* gain, double* shift, float* qinv, void* stream) {
+  SKYRX_REQUIRE(bands > 0 && lines >= 0 && samples >= 0, "bad cube shape");
+  const int64_t npix = lines * (int64_t)samples;
+  if (kind == SKYRX_IN_RAW_U16)
+    quant_shift_kernel<SKYRX_IN_RAW_U16><<<1, 128, 0, as_stream(stream)>>>(
+        pixels, npix, samples, bands, dark, coeff, gain, shift, qinv);
+  else
+    quant_shift_kernel<SKYRX_IN_F32><<<1, 128, 0, as_stream(stream)>>>(
+        pixels, npix, samples, bands, dark, coeff, gain, shift, qinv);
+  SKYRX_CHECK_LAUNCH("skyrx_quant_shift");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                              const float* dark, const float* coeff, const float* gain,
+                              const double* shift, const float* qinv, double* moments,
+                              int32_t* flags, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  SKYRX_REQUIRE(skyrx_stats_tc_supported(lines, samples, bands, raw),
+                "tensor-core moments path unsupported for this shape/alignment");
+  SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_tc_workspace(bands), "workspace too small");
+  GramTcParams p{};
+  p.raw = raw;
+  p.dark = dark;
+  p.coeff = coeff;
+  p.gain = gain;
+  p.shift = shift;
+  p.qinv = qinv;
+  p.part = reinterpret_cast<double*>(workspace);
+  p.flags = flags;
+  tc_sched(lines, samples, bands, kGtWmax, p.ts);
+  cudaStream_t st = as_stream(stream);
+  switch (bpg_for(bands)) {
+    case 16: return launch_gram_tc<16>(p, moments, st);
+    case 32: return launch_gram_tc<32>(p, moments, st);
+    case 48: return launch_gram_tc<48>(p, moments, st);
+    case 64: return launch_gram_tc<64>(p, moments, st);
+    case 80: return launch_gram_tc<80>(p, moments, st);
+  }
+  set_error("unsupported band count %d", bands);
+  return SKYRX_ERR_ARG;
+}

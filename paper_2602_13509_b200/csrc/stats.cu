@@ -22,7 +22,7 @@ namespace skyrx {
 
 constexpr int kGramThreads = 256;
 constexpr int kGramTileP = 64;       // pixels per shared-memory tile
-constexpr int kFlushProducts = 64;   // FP32 products per accumulator before FP64 promotion
+constexpr int kFlushProducts = 16;  // FP32 products per accumulator before FP64 promotion
 
 struct GramGeom {
   int bp, nt, ntiles, parts, groups, tiles_per_part, ld, grid;
@@ -128,13 +128,6 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
       }
     }
     if (active) {
-      if (kFast && since_flush + per_thread > kFlushProducts) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc64[i][j] += (double)acc[i][j], acc[i][j] = T(0);
-        since_flush = 0;
-      }
       const T* rowI = d + 8 * I;
       const T* rowJ = d + 8 * J;
       for (int p = group; p < kGramTileP; p += geo.groups) {
@@ -145,8 +138,14 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
         for (int i = 0; i < 8; ++i)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        if (kFast && ++since_flush == kFlushProducts) {  // promote short f32 runs to f64
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc64[i][j] += (double)acc[i][j], acc[i][j] = T(0);
+          since_flush = 0;
+        }
       }
-      since_flush += per_thread;
     }
   }
 #pragma unroll
@@ -295,6 +294,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   const double* s = mom + 1;
   const double* q = mom + 1 + B;
   int status = SKYRX_OK;
+  if (flags_all && (flags_all[m] & 2)) status = SKYRX_ERR_RANGE;
   if (flags_all && (flags_all[m] & 1)) status = SKYRX_ERR_NONFINITE;
   if (!(n > (double)B)) status = SKYRX_ERR_INSUFFICIENT;  // rx.py:51 checks size first
   if (status != SKYRX_OK) {

@@ -314,24 +314,52 @@ class DetectPlan:
                                   torch.int32)
         self.launches = 0
         lib = _lib.load()
-        self.tc = (bands <= 96 and os.environ.get("SKYRX_B200_TC", "1") != "0")
+        use_tc = os.environ.get("SKYRX_B200_TC", "1") != "0"
+        self.tc = bands <= 96 and use_tc              # tensor-core score kernel
+        self.tc_stats = bands <= 79 and use_tc        # tensor-core moments kernel
         self.wpack_bytes = int(lib.skyrx_wpack_bytes(bands)) if self.tc else 0
         self.wpack = (_dev.empty((batch, self.wpack_bytes), torch.uint8) if self.tc else None)
+        self.qinv = _dev.zeros((batch, bands), torch.float32)
+        self.tc_ws_bytes = int(lib.skyrx_stats_tc_workspace(bands)) if self.tc_stats else 0
+        self.tc_ws = _dev.empty((max(self.tc_ws_bytes, 8),), torch.uint8)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
-            precise: bool = False):
-        """Enqueue the whole path for cube i (no host synchronisation)."""
+            precise: bool = False, force_ffma: bool = False):
+        """Enqueue the moments of cube i (no host synchronisation)."""
         L, S, B = self.shape
         ds = self.ds
         s = _dev.stream_ptr()
         args = (raw.data_ptr(), L, S, B, dark.data_ptr(), coeff.data_ptr(), gains.data_ptr())
         ds.flags[i].zero_()
-        _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
-        _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
-                  int(precise), ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
-                  self.ws.data_ptr(), self.ws_bytes, s)
+        lib = _lib.load()
+        if (self.tc_stats and not precise and not force_ffma
+                and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
+            _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
+                      self.qinv[i].data_ptr(), s)
+            _lib.call("skyrx_stats_tc", *args, ds.shift[i].data_ptr(), self.qinv[i].data_ptr(),
+                      ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
+                      self.tc_ws.data_ptr(), self.tc_ws_bytes, s)
+        else:
+            _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
+                      int(precise), ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
+                      self.ws.data_ptr(), self.ws_bytes, s)
         self.launches += 3
         return self
+
+    def recover_range(self, cubes) -> list[int]:
+        """Redo (synchronously) any cube whose tensor-core quantiser overflowed.
+
+        ``cubes[i] = (raw, dark, coeff, gains)``.  Returns the recomputed slots."""
+        st = self.ds.status.cpu().numpy()
+        redo = [i for i in range(self.ds.batch) if st[i] == _lib.ERR_RANGE]
+        if redo:
+            for i in redo:
+                self.run(i, *cubes[i], force_ffma=True)
+            self.finalize()
+            for i in redo:
+                self.score(i, *cubes[i])
+        return redo
 
     def finalize(self):
         self.ds.finalize()
@@ -388,6 +416,7 @@ def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
     gd = _dev.to_device(gains, torch.float32)
     plan = plan or DetectPlan(L, S, B)
     plan.run(0, rv, dark, coeff, gd, precise=precise).finalize().score(0, rv, dark, coeff, gd, k)
+    plan.recover_range({0: (rv, dark, coeff, gd)})
     on_dev = _dev.is_device(raw.values) if device is None else device
     ds = plan.ds
     ds.check(0, n)

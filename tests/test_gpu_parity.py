@@ -349,6 +349,42 @@ class TestDetect:
         rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
         assert rel.max() < 2e-5, rel.max()
 
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 40), (64, 70, 33), (96, 48, 50), (40, 15, 64),
+                                       (128, 79, 20)])
+    def test_tensor_core_moments(self, P, S, B, L):
+        import torch
+
+        from paper_2602_13509_b200 import _lib
+
+        t = osynth.make_tables(43, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        rv = torch.from_numpy(raw).cuda()
+        assert _lib.load().skyrx_stats_tc_supported(L, S, B, rv.data_ptr()) == 1
+        plan = P.DetectPlan(L, S, B)
+        assert plan.tc_stats
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        check_detection(det, raw, t)
+        rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
+        ref = O.compute_stats(rad)
+        assert normwise(det.stats.sigma, ref.sigma) < 1e-7
+        assert normwise(det.stats.mu, ref.mu) < 1e-9
+
+    def test_tensor_core_moments_range_fallback(self, P, rng):
+        # a flat cube with one far outlier outside the shift sample overflows the
+        # int8 quantiser; detect() must notice and recompute with the FFMA kernel
+        L, S, B = 60, 64, 70
+        raw = (1000 + rng.integers(-3, 4, (L, S, B))).astype(np.uint16)
+        raw[3, 5] = 4000
+        dark = np.full((S, B), 100.0, np.float32)
+        coeff = np.ones((S, B), np.float32)
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(dark, coeff), plan=plan)
+        ref = O.compute_stats(O.apply_calibration(raw, dark, coeff, np.ones(L)))
+        assert normwise(det.stats.sigma, ref.sigma) < 1e-6
+        want = O.rx_scores(O.apply_calibration(raw, dark, coeff, np.ones(L)), ref)
+        assert (np.abs(det.scores - want) / np.maximum(want, 1e-12)).max() < 1e-4
+        assert det.mask[3, 5]
+
     def test_deterministic(self, P):
         t = osynth.make_tables(1, 900, 70)
         raw = osynth.generate_lines(t, 0, 128)
