@@ -146,7 +146,7 @@ int skyrx_score(int32_t kind, const void* pixels, int64_t lines, int32_t samples
                 const float* mu_hilo, const float* whiten, int32_t ld_w, float* scores,
                 uint32_t* max_bits, void* stream);
 
-/* Tensor-core (tcgen05) variant of skyrx_score for RAW cubes with B <= 96:
+/* Tensor-core (tcgen05) variant of skyrx_score for RAW cubes with B <= 80:
  * f16 hi/lo split of (x - mu) and of W, f32 TMEM accumulation, sum of squares
  * in the epilogue.  wpack = skyrx_pack_whiten(whiten64) (skyrx_wpack_bytes(B)
  * bytes per matrix).  skyrx_score_tc_supported() says whether the shape and

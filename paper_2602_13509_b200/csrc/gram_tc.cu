@@ -2,11 +2,11 @@
 //
 // Reference: rx.py:56-66 (f64 mean, then f64 Gram of centred pixels).  Here
 // every calibrated value is centred by the sample shift c_b and quantised to a
-// fixed point D = rint((x - c_b) / q_b) with |D| < 2^20 (q_b a power of two
-// from 8x the largest sampled deviation).  D is split into three balanced
-// base-128 digits D = D2*2^14 + D1*2^7 + D0 (each in [-64, 64)) and the Gram
-// of the digits is accumulated EXACTLY in int32 by tcgen05.mma kind::i8
-// (|digit products| <= 2^12, so 2^19 pixels fit before any overflow):
+// fixed point D = rint((x - c_b) / q_b) with |D| < 2^21 - 2^15 (q_b a power of
+// two from 4x the largest sampled deviation).  D is split into three digits
+// D = D2*2^14 + D1*2^7 + D0 (D0, D1 in [-64, 64), D2 in [-127, 127]) and the
+// Gram of the digits is accumulated EXACTLY in int32 by tcgen05.mma kind::i8
+// (|digit products| <= 2^14; TMEM is drained every 2^17 pixels):
 //     G = sum_a 2^14a Pa,a + sum_{a>b} 2^7(a+b) (Pa,b + Pa,b^T),  Pa,b = Da^T Db
 // One constant band (index B, digit D0 = 1 on valid pixels) makes the same
 // products carry n and sum(D).  The only approximation left is the
@@ -34,7 +34,7 @@ constexpr int kGtWorkers = 256;
 constexpr int kGtRawStages = 3;
 constexpr int kGtOpStages = 2;
 constexpr int kGtWmax = 32;
-constexpr int kGtFlushTiles = 3072;  // 3072*128 px * 2^12 < 2^31
+constexpr int kGtFlushTiles = 1023;  // 1023 tiles * 128 px * 2^14 < 2^31
 
 struct GramTcParams {
   const uint16_t* raw;
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
               if (g != 1.0f) x = __fdiv_rn(x, g);
               finite_ok &= isfinite(x);
               const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);
-              range_ok &= fabsf(tq) < 1048575.0f;
+              range_ok &= fabsf(tq) < 2064384.0f;  // keeps D2 within int8
               D = __float2int_rn(tq);
             } else if (valid && k == B) {
               D = 1;  // constant band: carries n and sum(D)
@@ -320,10 +320,10 @@ __global__ void quant_shift_kernel(const void* pixels, int64_t npix, int32_t sam
     const float c = m > 0 ? (float)(acc / (double)m) : 0.0f;
     float amax = 0.0f;
     for (int64_t i = 0; i < m; ++i) amax = fmaxf(amax, fabsf(__fsub_rn(val(i), c)));
-    const float bound = fmaxf(8.0f * amax, 1e-30f);
+    const float bound = fmaxf(4.2f * amax, 1e-30f);
     int e = 0;
     frexpf(bound, &e);                 // bound < 2^e
-    int ex = 20 - e;                   // |D| <= bound * 2^ex < 2^20
+    int ex = 21 - e;                   // |x - c| <= 4 amax  =>  |D| < 2^21 * 4/4.2
     ex = ex > 120 ? 120 : (ex < -120 ? -120 : ex);
     shift[b] = (double)c;
     qinv[b] = ldexpf(1.0f, ex);

@@ -313,7 +313,7 @@ extern "C" size_t skyrx_wpack_bytes(int32_t bands) {
 
 extern "C" int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t batch,
                                  void* wpack, void* stream) {
-  SKYRX_REQUIRE(bands > 0 && bands <= 96 && batch >= 1, "pack_whiten supports 1 <= B <= 96");
+  SKYRX_REQUIRE(bands > 0 && bands <= 80 && batch >= 1, "pack_whiten supports 1 <= B <= 80");
   cudaStream_t st = as_stream(stream);
   switch (kp_for(bands)) {
 #define SKYRX_KP(k) \
@@ -329,7 +329,7 @@ extern "C" int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t 
 extern "C" int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t bands,
                                         const void* raw) {
   TileSched ts;
-  if (bands < 1 || bands > 96) return 0;
+  if (bands < 1 || bands > 80) return 0;  // KP = 96 would need > 227 KB of shared memory
   if (((uintptr_t)raw & 15) != 0) return 0;
   return tc_sched(lines, samples, bands, kScoreWmax, ts) ? 1 : 0;
 }

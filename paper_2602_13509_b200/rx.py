@@ -315,7 +315,7 @@ class DetectPlan:
         self.launches = 0
         lib = _lib.load()
         use_tc = os.environ.get("SKYRX_B200_TC", "1") != "0"
-        self.tc = bands <= 96 and use_tc              # tensor-core score kernel
+        self.tc = bands <= 80 and use_tc              # tensor-core score kernel
         self.tc_stats = bands <= 79 and use_tc        # tensor-core moments kernel
         self.wpack_bytes = int(lib.skyrx_wpack_bytes(bands)) if self.tc else 0
         self.wpack = (_dev.empty((batch, self.wpack_bytes), torch.uint8) if self.tc else None)
