@@ -2,7 +2,8 @@
 //
 // Reference: rx.py:56-66 (f64 mean, then f64 Gram of centred pixels).  Here
 // every calibrated value is centred by the sample shift c_b and quantised to a
-// fixed point D = rint((x - c_b) / q_b) with |D| < 2^21 - 2^15 (q_b a power of
+// fixed point D = floor((x - c_b) / q_b + u) with a deterministic per-element
+// dither u in [0, 1) (unbiased even for lattice-valued data), |D| < 2^21 - 2^15 (q_b a power of
 // two from 4x the largest sampled deviation).  D is split into three digits
 // D = D2*2^14 + D1*2^7 + D0 (D0, D1 in [-64, 64), D2 in [-127, 127]) and the
 // Gram of the digits is accumulated EXACTLY in int32 by tcgen05.mma kind::i8
@@ -78,8 +79,10 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int64_t it0 = (int64_t)blockIdx.x * p.per_cta;
-  int64_t it1 = it0 + p.per_cta;
+  // balanced contiguous item ranges: every CTA owns >= 1 tile (grid <= items),
+  // so every per-CTA partial below is written
+  const int64_t it0 = (int64_t)blockIdx.x * p.ts.items / gridDim.x;
+  int64_t it1 = (int64_t)(blockIdx.x + 1) * p.ts.items / gridDim.x;
   if (it1 > p.ts.items) it1 = p.ts.items;
   const int n = it0 < it1 ? (int)(it1 - it0) : 0;
   const int nflush = (n + kGtFlushTiles - 1) / kGtFlushTiles;
@@ -209,10 +212,13 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       const bool valid = r < ti.rows;
       int j = 0;
       float g = 1.0f;
+      uint32_t pixkey = 0;
       if (valid) {
         const int li = r / ti.w;
         j = r - li * ti.w;
         g = __ldg(p.gain + ti.line0 + li);
+        const uint64_t pix = (uint64_t)(ti.line0 + li) * (uint64_t)p.ts.S + (uint64_t)(ti.s0 + j);
+        pixkey = (uint32_t)(pix * 0x9E3779B97F4A7C15ull >> 32) * 0x85EBCA6Bu;
       }
       const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
       const float* dk = dark_s + j * (B + 1);
@@ -232,8 +238,13 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
               if (g != 1.0f) x = __fdiv_rn(x, g);
               finite_ok &= isfinite(x);
               const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);
-              range_ok &= fabsf(tq) < 2064384.0f;  // keeps D2 within int8
-              D = __float2int_rn(tq);
+              range_ok &= fabsf(tq) < 2064383.0f;  // keeps D2 within int8
+              // deterministic dithered rounding: E[D] = tq for any input lattice
+              uint32_t hq = pixkey ^ ((uint32_t)k * 0x9E3779B9u);
+              hq ^= hq >> 15;
+              hq *= 0x2C1B3C6Du;
+              hq ^= hq >> 12;
+              D = __float2int_rd(tq + (float)(hq >> 8) * 0x1p-24f);
             } else if (valid && k == B) {
               D = 1;  // constant band: carries n and sum(D)
             }

@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int64_t it0 = (int64_t)blockIdx.x * p.per_cta;
-  int64_t it1 = it0 + p.per_cta;
+  const int64_t it0 = (int64_t)blockIdx.x * p.ts.items / gridDim.x;
+  int64_t it1 = (int64_t)(blockIdx.x + 1) * p.ts.items / gridDim.x;
   if (it1 > p.ts.items) it1 = p.ts.items;
   const int n = it0 < it1 ? (int)(it1 - it0) : 0;
 

@@ -34,6 +34,7 @@ from .cube import ScoreMap
 
 RIDGE_EPSILONS = (1e-10, 1e-9, 1e-8, 1e-7, 1e-6)
 MODES = ("precise", "fast")
+TC_MIN_PIXELS = 1 << 18   # below this detect() fits the background in f64
 
 _STATUS_MSG = {
     _lib.ERR_NONFINITE: "invalid data: cube contains non-finite values",
@@ -332,7 +333,11 @@ class DetectPlan:
         args = (raw.data_ptr(), L, S, B, dark.data_ptr(), coeff.data_ptr(), gains.data_ptr())
         ds.flags[i].zero_()
         lib = _lib.load()
-        if (self.tc_stats and not precise and not force_ffma
+        # small cubes take the f64 kernel (cheap there; the int8 quantiser's noise
+        # averages out only over many pixels); a quantiser overflow is redone in f64
+        small = L * S < TC_MIN_PIXELS
+        precise = precise or small or force_ffma
+        if (self.tc_stats and not precise
                 and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
             _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
                       self.qinv[i].data_ptr(), s)
