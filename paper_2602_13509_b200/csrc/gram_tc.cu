@@ -244,7 +244,10 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
               hq ^= hq >> 15;
               hq *= 0x2C1B3C6Du;
               hq ^= hq >> 12;
-              D = __float2int_rd(tq + (float)(hq >> 8) * 0x1p-24f);
+              // round up with probability frac(tq): u >= 1 - frac is exact in f32
+              const float fl = floorf(tq);
+              const float u = (float)(hq >> 8) * 0x1p-24f;
+              D = (int)fl + (u >= 1.0f - (tq - fl) ? 1 : 0);
             } else if (valid && k == B) {
               D = 1;  // constant band: carries n and sum(D)
             }

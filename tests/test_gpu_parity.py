@@ -371,8 +371,9 @@ class TestDetect:
         check_detection(det, raw, t)
         rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
         ref = O.compute_stats(rad)
+        # quantiser noise only (dithered, unbiased): far below the 1e-5 contract
         assert normwise(det.stats.sigma, ref.sigma) < 1e-6
-        assert normwise(det.stats.mu, ref.mu) < 1e-8
+        assert normwise(det.stats.mu, ref.mu) < 1e-7
 
     def test_tensor_core_moments_range_fallback(self, P, rng):
         # a flat cube with one far outlier outside the shift sample overflows the
