@@ -314,26 +314,46 @@ template <int KIND>
 __global__ void quant_shift_kernel(const void* pixels, int64_t npix, int32_t samples, int32_t B,
                                    const float* dark, const float* coeff, const float* gain,
                                    double* shift, float* qinv) {
+  // one CTA per band (grid = B), 256 threads over the sample, fixed-order reductions
+  __shared__ double part[8];
+  __shared__ float partf[8];
+  __shared__ float c_sh;
   const int64_t step = npix > 4096 ? npix / 4096 : 1;
   const int64_t m = npix > 0 ? (npix + step - 1) / step : 0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    auto val = [&](int64_t i) {
-      const int64_t pix = i * step;
-      const int64_t gi = pix * B + b;
-      if constexpr (KIND == SKYRX_IN_RAW_U16) {
-        const int64_t line = pix / samples;
-        const int64_t tb = (pix - line * samples) * B + b;
-        return calib((float)reinterpret_cast<const uint16_t*>(pixels)[gi], dark[tb], coeff[tb],
-                     gain[line]);
-      } else {
-        return reinterpret_cast<const float*>(pixels)[gi];
-      }
-    };
-    double acc = 0.0;
-    for (int64_t i = 0; i < m; ++i) acc += (double)val(i);
-    const float c = m > 0 ? (float)(acc / (double)m) : 0.0f;
-    float amax = 0.0f;
-    for (int64_t i = 0; i < m; ++i) amax = fmaxf(amax, fabsf(__fsub_rn(val(i), c)));
+  const int b = blockIdx.x;
+  auto val = [&](int64_t i) {
+    const int64_t pix = i * step;
+    const int64_t gi = pix * B + b;
+    if constexpr (KIND == SKYRX_IN_RAW_U16) {
+      const int64_t line = pix / samples;
+      const int64_t tb = (pix - line * samples) * B + b;
+      return calib((float)reinterpret_cast<const uint16_t*>(pixels)[gi], dark[tb], coeff[tb],
+                   gain[line]);
+    } else {
+      return reinterpret_cast<const float*>(pixels)[gi];
+    }
+  };
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) acc += (double)val(i);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += part[w];
+    c_sh = m > 0 ? (float)(s / (double)m) : 0.0f;
+  }
+  __syncthreads();
+  const float c = c_sh;
+  float amax = 0.0f;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
+    amax = fmaxf(amax, fabsf(__fsub_rn(val(i), c)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if ((threadIdx.x & 31) == 0) partf[threadIdx.x >> 5] = amax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 8; ++w) amax = fmaxf(amax, partf[w]);
     const float bound = fmaxf(4.2f * amax, 1e-30f);
     int e = 0;
     frexpf(bound, &e);                 // bound < 2^e
@@ -388,10 +408,10 @@ extern "C" int skyrx_quant_shift(int32_t kind, const void* pixels, int64_t lines
   SKYRX_REQUIRE(bands > 0 && lines >= 0 && samples >= 0, "bad cube shape");
   const int64_t npix = lines * (int64_t)samples;
   if (kind == SKYRX_IN_RAW_U16)
-    quant_shift_kernel<SKYRX_IN_RAW_U16><<<1, 128, 0, as_stream(stream)>>>(
+    quant_shift_kernel<SKYRX_IN_RAW_U16><<<bands, 256, 0, as_stream(stream)>>>(
         pixels, npix, samples, bands, dark, coeff, gain, shift, qinv);
   else
-    quant_shift_kernel<SKYRX_IN_F32><<<1, 128, 0, as_stream(stream)>>>(
+    quant_shift_kernel<SKYRX_IN_F32><<<bands, 256, 0, as_stream(stream)>>>(
         pixels, npix, samples, bands, dark, coeff, gain, shift, qinv);
   SKYRX_CHECK_LAUNCH("skyrx_quant_shift");
   return SKYRX_OK;

@@ -5,15 +5,17 @@
 // split into f16 hi + lo (W per output row scaled by a power of two so lo
 // stays normal); z accumulates Dhi*Whi + Dhi*Wlo + Dlo*Whi in the f32 TMEM
 // accumulator (which truncates, tools/umma_probe.cu); emulated worst-case
-// score error 1.6e-6 against the f64 reference (tolerance 1e-4).
+// score error 1.6e-6 against the f64 reference (tolerance 1e-4), measured
+// 1.4e-6 on B200 (tools/debug_score.py).
 //
-// Warp roles (persistent CTA, one per SM):
-//   warp 4  TMA producer : raw line segments of each tile -> smem ring (cp.async.bulk)
-//   warp 5  MMA issuer   : 3*KP/16 tcgen05.mma per tile into a double-buffered
+// Warp roles (persistent CTA, one per SM, 320 threads):
+//   warp 8  TMA producer : raw line segments of each tile -> smem ring (cp.async.bulk)
+//   warp 9  MMA issuer   : 3*KP/16 tcgen05.mma per tile into a double-buffered
 //                          TMEM accumulator (128 lanes = pixels, KP columns)
-//   warps 0-3 workers    : calibrate + centre + f16 split each pixel row into the
-//                          K-major A operand; then the epilogue of the previous
-//                          tile (tcgen05.ld row, unscale, sum of squares, store).
+//   warps 0-7 workers    : two threads per pixel row (each half of the bands):
+//                          calibrate + centre + f16 split into the K-major A
+//                          operand, then the epilogue of the previous tile
+//                          (tcgen05.ld, unscale, sum of squares, store).
 // Calibration tables of the current sample block live in shared memory.
 #include <cuda_fp16.h>
 
@@ -24,8 +26,8 @@
 namespace skyrx {
 using namespace umma;
 
-constexpr int kTcThreads = 192;
-constexpr int kTcWorkers = 128;
+constexpr int kTcThreads = 320;
+constexpr int kTcWorkers = 256;
 constexpr int kScoreRawStages = 3;
 constexpr int kScoreAStages = 2;
 constexpr int kScoreWmax = 32;
@@ -40,7 +42,6 @@ struct ScoreTcParams {
   float* scores;
   uint32_t* max_key;
   TileSched ts;
-  int64_t per_cta;
   uint32_t raw_stage_bytes;
 };
 
@@ -52,9 +53,44 @@ __host__ __device__ constexpr uint32_t wpack_bytes_for(int kp) {
   return 2u * kp * kp * 2u + kp * 4u;
 }
 
+// 8 centred values of one pixel row -> f16 hi/lo chunks
+template <bool FULL, bool DIV>
+__device__ __forceinline__ void centre8(const uint16_t* rp, const float2* tab, const float2* mu,
+                                        int k0, int B, float ginv, float* dv) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int k = k0 + q;
+    float v = 0.0f;
+    if (FULL || k < B) {
+      const float2 dc = tab[k];
+      float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dc.x), 0.0f), dc.y);
+      if (DIV) x = __fmul_rn(x, ginv);  // fast path: 1 ulp of the exact division
+      const float2 m = mu[k];
+      v = __fsub_rn(__fsub_rn(x, m.x), m.y);
+    }
+    dv[q] = v;
+  }
+}
+
+__device__ __forceinline__ void store_split8(const float* dv, uint8_t* hi, uint8_t* lo) {
+  uint32_t hw[4], lw[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const __half2 h = __floats2half2_rn(dv[2 * q], dv[2 * q + 1]);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(dv[2 * q] - hf.x, dv[2 * q + 1] - hf.y);
+    hw[q] = *reinterpret_cast<const uint32_t*>(&h);
+    lw[q] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+  *reinterpret_cast<uint4*>(hi) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+  *reinterpret_cast<uint4*>(lo) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
   constexpr int NP = KP;
+  constexpr int NCH = KP / 8;            // 8-band chunks per row
+  constexpr int CH0 = (NCH + 1) / 2;     // chunks [0, CH0) for h = 0
   constexpr uint32_t A_BYTES = 128u * KP * 2u;
   constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
@@ -66,12 +102,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   uint8_t* a_ring = raw_ring + kScoreRawStages * p.raw_stage_bytes;
   uint8_t* wsm = a_ring + kScoreAStages * 2 * A_BYTES;
   float* colscale = reinterpret_cast<float*>(wsm + 2 * W_BYTES);
-  float* dark_s = colscale + NP;
-  float* coeff_s = dark_s + kScoreWmax * (B + 1);
-  float* mhi = coeff_s + kScoreWmax * (B + 1);
-  float* mlo = mhi + KP;
+  float2* tab = reinterpret_cast<float2*>(colscale + NP);   // [Wmax][B+1] {dark, coeff}
+  float2* mu = tab + kScoreWmax * (B + 1);                 // [KP] {hi, lo}
+  float* red = reinterpret_cast<float*>(mu + KP);          // [2][128] partial sums
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(mlo + KP) + 7) & ~uintptr_t(7));
+      (reinterpret_cast<uintptr_t>(red + 256) + 7) & ~uintptr_t(7));
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + kScoreRawStages;
   uint64_t* a_full = raw_empty + kScoreRawStages;
@@ -84,28 +119,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int64_t it0 = (int64_t)blockIdx.x * p.ts.items / gridDim.x;
-  int64_t it1 = (int64_t)(blockIdx.x + 1) * p.ts.items / gridDim.x;
-  if (it1 > p.ts.items) it1 = p.ts.items;
-  const int n = it0 < it1 ? (int)(it1 - it0) : 0;
+  const int64_t it1 = (int64_t)(blockIdx.x + 1) * p.ts.items / gridDim.x;
+  const int n = (int)(it1 - it0);
 
   if (tid == 0) {
-    for (int s = 0; s < kScoreRawStages; ++s) mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers);
-    for (int s = 0; s < kScoreAStages; ++s) mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
+    for (int s = 0; s < kScoreRawStages; ++s)
+      mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers);
+    for (int s = 0; s < kScoreAStages; ++s)
+      mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
     for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, TMEM_COLS);
-  for (int k = tid; k < KP; k += blockDim.x) {
-    mhi[k] = k < B ? p.mu_hilo[k] : 0.0f;
-    mlo[k] = k < B ? p.mu_hilo[B + k] : 0.0f;
-  }
+  if (warp == 9) tmem_alloc(tmem_slot, TMEM_COLS);
+  for (int k = tid; k < KP; k += blockDim.x)
+    mu[k] = k < B ? make_float2(p.mu_hilo[k], p.mu_hilo[B + k]) : make_float2(0.0f, 0.0f);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       const uint32_t wb = wpack_bytes_for(KP);
       mbar_arrive_expect_tx(w_bar, wb);
@@ -123,7 +157,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       mbar_wait(w_bar, 0);
       constexpr uint32_t idesc = idesc_f16_f32(128, NP, 0, 0);
@@ -150,7 +184,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       }
     }
   } else {  // ------------------------------------------------------------ workers
-    const int r = tid;  // pixel row of the tile
+    const int r = tid & 127;   // pixel row of the tile
+    const int h = tid >> 7;    // band half
+    const int c_lo = h ? CH0 : 0, c_hi = h ? NCH : CH0;
     mbar_wait(w_bar, 0);
     int cur_block = -1;
     uint32_t local_max = 0;
@@ -158,22 +194,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       const int acs = t & 1;
       mbar_wait(&acc_full[acs], (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + acs * NP;
+      const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + acs * NP;
       float sum = 0.0f;
 #pragma unroll
-      for (int c = 0; c < NP / 16; ++c) {
-        uint32_t v[16];
-        tmem_ld16(taddr + c * 16, v);
+      for (int c = 0; c < NCH; ++c) {
+        if (c < c_lo || c >= c_hi) continue;
+        uint32_t v[8];
+        tmem_ld8(taddr + c * 8, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float z = __uint_as_float(v[q]) * colscale[c * 16 + q];
+        for (int q = 0; q < 8; ++q) {
+          const float z = __uint_as_float(v[q]) * colscale[c * 8 + q];
           sum = fmaf(z, z, sum);
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[acs]);
-      if (r < ti.rows) {
+      float* rb = red + (t & 1) * 128;
+      if (h) rb[r] = sum;
+      named_sync(2, kTcWorkers);
+      if (!h && r < ti.rows) {
+        sum += rb[r];
         const int li = r / ti.w;
         const int j = r - li * ti.w;
         p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + j] = sum;
@@ -185,11 +226,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       const TileInfo ti = tile_info(p.ts, it0 + t);
       if (ti.block != cur_block) {
         named_sync(1, kTcWorkers);
-        for (int e = r; e < ti.w * B; e += kTcWorkers) {
+        for (int e = tid; e < ti.w * B; e += kTcWorkers) {
           const int j = e / B, b = e - j * B;
           const int64_t g = (int64_t)(ti.s0 + j) * B + b;
-          dark_s[j * (B + 1) + b] = __ldg(p.dark + g);
-          coeff_s[j * (B + 1) + b] = __ldg(p.coeff + g);
+          tab[j * (B + 1) + b] = make_float2(__ldg(p.dark + g), __ldg(p.coeff + g));
         }
         named_sync(1, kTcWorkers);
         cur_block = ti.block;
@@ -198,45 +238,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       const int as = t % kScoreAStages;
       mbar_wait(&raw_full[s], (t / kScoreRawStages) & 1);
       mbar_wait(&a_empty[as], ((t / kScoreAStages) & 1) ^ 1);
-      uint8_t* ahi = a_ring + as * 2 * A_BYTES;
+      uint8_t* ahi = a_ring + as * 2 * A_BYTES + (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
       uint8_t* alo = ahi + A_BYTES;
-      const uint32_t row_off = (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
-      const bool valid = r < ti.rows;
-      int li = 0, j = 0;
-      float g = 1.0f;
-      const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
-      if (valid) {
-        li = r / ti.w;
-        j = r - li * ti.w;
-        g = __ldg(p.gain + ti.line0 + li);
-      }
-      const float* dk = dark_s + j * (B + 1);
-      const float* ck = coeff_s + j * (B + 1);
-#pragma unroll 2
-      for (int c = 0; c < KP / 8; ++c) {
-        float dv[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int k = c * 8 + q;
-          float v = 0.0f;
-          if (valid && k < B) {
-            float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dk[k]), 0.0f), ck[k]);
-            if (g != 1.0f) x = __fdiv_rn(x, g);
-            v = __fsub_rn(__fsub_rn(x, mhi[k]), mlo[k]);
+      if (r < ti.rows) {
+        const int li = r / ti.w;
+        const int j = r - li * ti.w;
+        const float g = __ldg(p.gain + ti.line0 + li);
+        const float ginv = 1.0f / g;
+        const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
+        const float2* tk = tab + j * (B + 1);
+        for (int c = c_lo; c < c_hi; ++c) {
+          float dv[8];
+          const bool full = c * 8 + 8 <= B;
+          if (g == 1.0f) {
+            if (full) centre8<true, false>(rp, tk, mu, c * 8, B, ginv, dv);
+            else centre8<false, false>(rp, tk, mu, c * 8, B, ginv, dv);
+          } else {
+            if (full) centre8<true, true>(rp, tk, mu, c * 8, B, ginv, dv);
+            else centre8<false, true>(rp, tk, mu, c * 8, B, ginv, dv);
           }
-          dv[q] = v;
+          store_split8(dv, ahi + c * 128, alo + c * 128);
         }
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const __half2 h = __floats2half2_rn(dv[2 * q], dv[2 * q + 1]);
-          const float2 hf = __half22float2(h);
-          const __half2 l = __floats2half2_rn(dv[2 * q] - hf.x, dv[2 * q + 1] - hf.y);
-          hw[q] = *reinterpret_cast<const uint32_t*>(&h);
-          lw[q] = *reinterpret_cast<const uint32_t*>(&l);
+      } else {
+        for (int c = c_lo; c < c_hi; ++c) {
+          *reinterpret_cast<uint4*>(ahi + c * 128) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(alo + c * 128) = make_uint4(0, 0, 0, 0);
         }
-        *reinterpret_cast<uint4*>(ahi + row_off + c * 128) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(alo + row_off + c * 128) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
       fence_async_smem();
       mbar_arrive(&a_full[as]);
@@ -253,7 +280,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 9) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 // W (f64, row-major B x B, lower) -> f16 hi/lo K-major B operand + column scales
@@ -269,15 +296,15 @@ __global__ void pack_whiten_kernel(const double* __restrict__ w64, int B, uint8_
     if (jn < B)
       for (int k = 0; k < B; ++k) mx = fmax(mx, fabs(W[(size_t)jn * B + k]));
     int e = 0;
-    if (mx > 0.0) frexp(mx, &e);        // mx in [2^(e-1), 2^e)
+    if (mx > 0.0) frexp(mx, &e);           // mx in [2^(e-1), 2^e)
     const double sc = ldexp(1.0, 14 - e);  // max scaled value in [2^13, 2^14)
     colscale[jn] = (float)ldexp(1.0, e - 14);
     for (int k = 0; k < KP; ++k) {
       const double v = (jn < B && k < B && k <= jn) ? W[(size_t)jn * B + k] * sc : 0.0;
-      const __half h = __double2half(v);
-      const __half l = __double2half(v - (double)__half2float(h));
+      const __half hh = __double2half(v);
+      const __half l = __double2half(v - (double)__half2float(hh));
       const uint32_t off = (jn >> 3) * SBO_B + (k >> 3) * 128u + (jn & 7) * 16u + (k & 7) * 2u;
-      *reinterpret_cast<__half*>(o + off) = h;
+      *reinterpret_cast<__half*>(o + off) = hh;
       *reinterpret_cast<__half*>(o + W_BYTES + off) = l;
     }
   }
@@ -290,12 +317,11 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
   const size_t A_BYTES = 128u * KP * 2u;
   const size_t smem = kScoreRawStages * (size_t)p.raw_stage_bytes + kScoreAStages * 2 * A_BYTES +
-                      wpack_bytes_for(KP) + 2 * (size_t)kScoreWmax * (p.ts.B + 1) * 4 +
-                      2 * KP * 4 + 16 * 8 + 64;
+                      wpack_bytes_for(KP) + (size_t)kScoreWmax * (p.ts.B + 1) * 8 + KP * 8 +
+                      256 * 4 + 16 * 8 + 64;
   int grid = kSMs;
   if (p.ts.items < grid) grid = (int)p.ts.items;
   if (grid < 1) return SKYRX_OK;
-  p.per_cta = (p.ts.items + grid - 1) / grid;
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
@@ -319,7 +345,7 @@ extern "C" int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t 
 #define SKYRX_KP(k) \
   case k:           \
     pack_whiten_kernel<k><<<batch, 128, 0, st>>>(whiten64, bands, (uint8_t*)wpack); break;
-    SKYRX_KP(16) SKYRX_KP(32) SKYRX_KP(48) SKYRX_KP(64) SKYRX_KP(80) SKYRX_KP(96)
+    SKYRX_KP(16) SKYRX_KP(32) SKYRX_KP(48) SKYRX_KP(64) SKYRX_KP(80)
 #undef SKYRX_KP
   }
   SKYRX_CHECK_LAUNCH("skyrx_pack_whiten");
@@ -358,7 +384,6 @@ extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t sample
     case 48: return launch_score_tc<48>(p, st);
     case 64: return launch_score_tc<64>(p, st);
     case 80: return launch_score_tc<80>(p, st);
-    case 96: return launch_score_tc<96>(p, st);
   }
   set_error("unsupported band count %d", bands);
   return SKYRX_ERR_ARG;

@@ -212,29 +212,37 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part_q,
 }
 
 // shift: f32-rounded f64 mean of a strided sample of <= 4096 pixels
+// one CTA per band, 256 threads over the sample, fixed-order tree reduction
 template <int KIND>
-__global__ void shift_kernel(CubeRef cube, double* __restrict__ shift) {
+__global__ void __launch_bounds__(256) shift_kernel(CubeRef cube, double* __restrict__ shift) {
+  __shared__ double part[8];
   const int64_t n = cube.npix;
   const int64_t step = n > 4096 ? n / 4096 : 1;
   const int64_t m = n > 0 ? (n + step - 1) / step : 0;
   const int B = cube.bands;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    double acc = 0.0;
-    for (int64_t i = 0; i < m; ++i) {
-      const int64_t pix = i * step;
-      const int64_t gi = pix * B + b;
-      float x;
-      if constexpr (KIND == SKYRX_IN_RAW_U16) {
-        const int64_t line = pix / cube.samples;
-        const int64_t tb = (pix - line * cube.samples) * B + b;
-        x = calib((float)reinterpret_cast<const uint16_t*>(cube.pixels)[gi], cube.dark[tb],
-                  cube.coeff[tb], cube.gain[line]);
-      } else {
-        x = reinterpret_cast<const float*>(cube.pixels)[gi];
-      }
-      acc += (double)x;
+  const int b = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t pix = i * step;
+    const int64_t gi = pix * B + b;
+    float x;
+    if constexpr (KIND == SKYRX_IN_RAW_U16) {
+      const int64_t line = pix / cube.samples;
+      const int64_t tb = (pix - line * cube.samples) * B + b;
+      x = calib((float)reinterpret_cast<const uint16_t*>(cube.pixels)[gi], cube.dark[tb],
+                cube.coeff[tb], cube.gain[line]);
+    } else {
+      x = reinterpret_cast<const float*>(cube.pixels)[gi];
     }
-    shift[b] = m > 0 ? (double)(float)(acc / (double)m) : 0.0;
+    acc += (double)x;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += part[w];
+    shift[b] = m > 0 ? (double)(float)(s / (double)m) : 0.0;
   }
 }
 
@@ -477,9 +485,9 @@ extern "C" int skyrx_stats_shift(int32_t kind, const void* pixels, int64_t lines
   CubeRef c = make_ref(pixels, lines, samples, bands, dark, coeff, gain);
   cudaStream_t st = as_stream(stream);
   if (kind == SKYRX_IN_RAW_U16)
-    shift_kernel<SKYRX_IN_RAW_U16><<<1, 256, 0, st>>>(c, shift);
+    shift_kernel<SKYRX_IN_RAW_U16><<<bands, 256, 0, st>>>(c, shift);
   else
-    shift_kernel<SKYRX_IN_F32><<<1, 256, 0, st>>>(c, shift);
+    shift_kernel<SKYRX_IN_F32><<<bands, 256, 0, st>>>(c, shift);
   SKYRX_CHECK_LAUNCH("skyrx_stats_shift");
   return SKYRX_OK;
 }
