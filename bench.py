@@ -225,7 +225,7 @@ def main():
             if instrument:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-            plan.run(j, raw, d, c, gains)
+            plan.run(j, raw, d, c, gains, gain_const=1.0)
             if instrument:
                 b.record(stream)
                 ev["gram"].append((a, b))

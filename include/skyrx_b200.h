@@ -110,6 +110,18 @@ int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
                    const float* qinv, double* moments, int32_t* flags, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* Raw-byte tensor-core moments (RAW cubes, one constant line gain, B <= 128,
+ * samples*bands*2 % 16 == 0): exact integer byte Grams per sample column
+ * (tcgen05 kind::i8, TMA-fed), calibration applied per sample in f64.  Same
+ * [n, s, Q] moments about `shift`; flags |= 4 if any value would clamp at 0
+ * (caller recomputes with another path). */
+int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
+size_t skyrx_stats_raw_workspace(int32_t bands);
+int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                    const float* dark, const float* coeff, double gain, const double* shift,
+                    double* moments, int32_t* flags, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* state = forget * state + chunk (R-STREAM exponential forgetting) */
 int skyrx_moments_fold(double* state, const double* chunk, int32_t bands, double forget,
                        void* stream);

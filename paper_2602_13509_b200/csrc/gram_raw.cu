@@ -1,0 +1,425 @@
+// K2-RAW — background moments straight from the raw uint16 bytes on the tensor cores.
+//
+// For one sample column s the calibrated pixel is x = C_s (r - d_s) with
+// C_s = diag(coeff[s,:]) / gain and d_s = dark[s,:] (calibrate.py:98-101,
+// valid whenever no value clamps at 0 and the gain is one constant).  So
+//     sum_l x x^T = C_s (G_s - d_s m_s^T - m_s d_s^T + L d_s d_s^T) C_s,
+//     G_s = sum_l r r^T,  m_s = sum_l r
+// and G_s is an exact integer Gram of 12..16-bit counts.  Reading a line's
+// bands as their 2B little-endian bytes, G_s = 65536 HH + 256 (HL + LH) + LL
+// comes from ONE byte Gram D = sum_l b b^T (b = the 2B bytes), which the
+// tensor cores compute exactly (tcgen05.mma kind::i8, unsigned, s32 TMEM
+// accumulators; 255^2 * 32768 lines < 2^31).  TMA loads each tile's bytes
+// ([16-byte chunk][line][16 B] boxes of a 3-D tensor map) directly in the
+// canonical MN-major UMMA layout, so no thread touches the data on its way to
+// the tensor core.  The CUDA cores only scan each tile for m_s and for the
+// per-band minimum (a value below dark would clamp: the cube is then redone by
+// the generic path, flags |= 4).  Everything after the integer Gram is f64;
+// the result is the exact Gram up to f64 rounding (~1e-13 after centring).
+//
+// Work unit = (sample s, line range of <= 32768 lines); units are dealt to
+// CTAs in balanced contiguous ranges so the summation order is fixed.
+// Roles: warps 0-3 scan + epilogue, warp 4 TMA producer, warp 5 MMA issuer.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace skyrx {
+using namespace umma;
+
+constexpr int kGrThreads = 192;
+constexpr int kGrWorkers = 128;
+constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
+constexpr int kGrStages = 4;
+constexpr int64_t kGrMaxUnitLines = 32768;
+
+struct GramRawParams {
+  const float* dark;
+  const float* coeff;
+  double ginv;
+  double* part;       // per CTA: Sxx[B*B], Sx[B], n
+  int32_t* flags;
+  int64_t L;
+  int32_t S, B;
+  int64_t split_lines;  // lines per unit
+  int32_t nsplit;
+  int64_t units;
+};
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// idesc for kind::i8 with unsigned 8-bit operands, MN-major A and B, S32 accumulators
+__host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (1u << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 GramRawParams p) {
+  constexpr int NW = 16 * NCH;                    // window bytes = MMA N
+  constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
+  constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
+  constexpr uint32_t SBO = kGrLb * 16u;           // chunk stride in the stage
+  constexpr uint32_t PAD = TWO_M ? (16 - NCH) * SBO : 0;
+  constexpr int G = kGrWorkers / NCH;             // scan line groups
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int B = p.B;
+  uint8_t* stages = sm;
+  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE + PAD);
+  double* sacc = qacc + B * B;
+  uint32_t* smin = reinterpret_cast<uint32_t*>(sacc + B);  // [G][NCH][4] packed u16 mins
+  uint32_t* ssum = smin + G * NCH * 4;                       // [G][NCH][8]
+  uint32_t* minv = ssum + G * NCH * 8;                       // [NCH*8]
+  uint32_t* sumv = minv + NCH * 8;                           // [NCH*8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(sumv + NCH * 8) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars;
+  uint64_t* empty = full + kGrStages;
+  uint64_t* acc_full = empty + kGrStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
+  const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < kGrStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], kGrWorkers + 1);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kGrWorkers);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  for (int e = tid; e < B * B + B; e += blockDim.x) qacc[e] = 0.0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto unit_geom = [&](int64_t u, int& s, int64_t& l0, int64_t& nl) {
+    s = (int)(u % p.S);
+    const int64_t sp = u / p.S;
+    l0 = sp * p.split_lines;
+    nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
+  };
+
+  if (warp == 4) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
+      int t = 0;
+      for (int64_t u = u0; u < u1; ++u) {
+        int s;
+        int64_t l0, nl;
+        unit_geom(u, s, l0, nl);
+        const int c0 = (int)(((int64_t)s * B * 2) >> 4);
+        const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
+        for (int k = 0; k < ntile; ++k, ++t) {
+          const int st = t % kGrStages;
+          mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], STAGE);
+          tma_load_3d(stages + st * STAGE, &tmap, 0, (int)(l0 + (int64_t)k * kGrLb), c0, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+      constexpr uint32_t id = idesc_u8_s32(128, NW);
+      int t = 0, unit = 0;
+      for (int64_t u = u0; u < u1; ++u, ++unit) {
+        int s;
+        int64_t l0, nl;
+        unit_geom(u, s, l0, nl);
+        const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
+        if (unit > 0) mbar_wait(acc_empty, (unit - 1) & 1);
+        tc_fence_after();
+        for (int k = 0; k < ntile; ++k, ++t) {
+          const int st = t % kGrStages;
+          mbar_wait(&full[st], (t / kGrStages) & 1);
+          tc_fence_after();
+          const uint8_t* base = stages + st * STAGE;
+#pragma unroll
+          for (int ks = 0; ks < kGrLb / 32; ++ks) {
+            const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+            const uint8_t* kb = base + ks * 512;  // 32 lines = 4 groups of 8 x 16 B
+            const uint64_t bdesc = smem_desc(kb, 128, SBO);
+            mma_i8(tmem, smem_desc(kb, 128, SBO), bdesc, id, acc);
+            if (TWO_M) mma_i8(tmem + NW, smem_desc(kb + 8 * SBO, 128, SBO), bdesc, id, acc);
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(acc_full);
+      }
+    }
+  } else {  // ------------------------------------------------------------ scan + epilogue
+    const int c = tid % NCH, g = tid / NCH;
+    const bool scanner = g < G;
+    int t = 0, unit = 0;
+    for (int64_t u = u0; u < u1; ++u, ++unit) {
+      int s;
+      int64_t l0, nl;
+      unit_geom(u, s, l0, nl);
+      const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
+      uint32_t mn[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+      uint32_t sm8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int k = 0; k < ntile; ++k, ++t) {
+        const int st = t % kGrStages;
+        mbar_wait(&full[st], (t / kGrStages) & 1);
+        if (scanner) {
+          const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
+          const uint4* row = reinterpret_cast<const uint4*>(stages + st * STAGE + c * SBO);
+          for (int l = g; l < valid; l += G) {
+            const uint4 v = row[l];
+            mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
+            mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
+            sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
+            sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+          }
+        }
+        mbar_arrive(&empty[st]);
+      }
+      // per-unit reduction of the scans (fixed order over line groups)
+      if (scanner) {
+        for (int q = 0; q < 4; ++q) smin[(g * NCH + c) * 4 + q] = mn[q];
+        for (int q = 0; q < 8; ++q) ssum[(g * NCH + c) * 8 + q] = sm8[q];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
+      if (tid < NCH * 8) {
+        const int cc = tid >> 3, q = tid & 7;
+        uint32_t mv = 0xffffu, sv = 0;
+        for (int gg = 0; gg < G; ++gg) {
+          const uint32_t w = smin[(gg * NCH + cc) * 4 + (q >> 1)];
+          mv = min(mv, (q & 1) ? (w >> 16) : (w & 0xffffu));
+          sv += ssum[(gg * NCH + cc) * 8 + q];
+        }
+        minv[tid] = mv;
+        sumv[tid] = sv;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
+      // ---- epilogue: byte Gram (TMEM) -> calibrated sum x x^T of this sample
+      mbar_wait(acc_full, unit & 1);
+      tc_fence_after();
+      const int off = (int)(((int64_t)s * B * 2) & 15);
+      const double Lu = (double)nl;
+      const float* drow = p.dark + (int64_t)s * B;
+      const float* crow = p.coeff + (int64_t)s * B;
+      bool clamp = false;
+#pragma unroll
+      for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
+        if (part == 1 && 128 + 32 * warp >= off + 2 * B) continue;  // warp-uniform
+        const int m = 128 * part + tid;
+        const int rel = m - off;
+        const bool lo_row = rel >= 0 && rel < 2 * B && (rel & 1) == 0;
+        const int b = rel >> 1;
+        double Cb = 0.0, db = 0.0, Sb = 0.0;
+        if (lo_row) {
+          Cb = (double)crow[b] * p.ginv;
+          db = (double)drow[b];
+          Sb = (double)sumv[(off >> 1) + b];
+          clamp |= (float)minv[(off >> 1) + b] < drow[b];
+        }
+        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(part * NW);
+        for (int cc = 0; cc < NCH; ++cc) {
+          uint32_t v[16];
+          tmem_ld16(taddr + cc * 16, v);
+          tmem_ld_wait();
+          uint32_t pv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, v[q], 1);
+          if (lo_row) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int reln = cc * 16 + 2 * i - off;
+              if (reln < 0 || reln >= 2 * B) continue;
+              const int b2 = reln >> 1;
+              if (b2 > b) continue;  // lower triangle; mirrored in the reduction
+              // own row = lo byte of band b, partner row = hi byte of band b
+              const double gv = 65536.0 * (double)pv[2 * i + 1] +
+                                256.0 * ((double)pv[2 * i] + (double)v[2 * i + 1]) +
+                                (double)v[2 * i];
+              const double C2 = (double)crow[b2] * p.ginv;
+              const double d2 = (double)drow[b2];
+              const double S2 = (double)sumv[(off >> 1) + b2];
+              const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
+              qacc[b * B + b2] += Cb * C2 * xx;
+            }
+          }
+        }
+        if (lo_row) sacc[b] += Cb * (Sb - Lu * db);
+      }
+      if (clamp) atomicOr(p.flags, 4);
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+    // per-CTA partial: Sxx (lower triangle), Sx, n
+    asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
+    double* out = p.part + (size_t)blockIdx.x * (B * B + B + 1);
+    for (int e = tid; e < B * B + B; e += kGrWorkers) out[e] = qacc[e];
+    if (tid == 0) {
+      double n = 0.0;
+      for (int64_t u = u0; u < u1; ++u) {
+        int s;
+        int64_t l0, nl;
+        unit_geom(u, s, l0, nl);
+        n += (double)nl;
+      }
+      out[B * B + B] = n;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem, 512);
+}
+
+// moments about the shift c: s = Sx - n c, Q = Sxx - c Sx^T - Sx c^T + n c c^T
+__global__ void gram_raw_reduce_kernel(const double* __restrict__ part, int nparts, int B,
+                                       const double* __restrict__ shift,
+                                       double* __restrict__ moments) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = B * B + B + 1;
+  double* s_out = moments + 1;
+  double* q_out = moments + 1 + B;
+  double n = 0.0;
+  for (int c = 0; c < nparts; ++c) n += part[(size_t)c * stride + B * B + B];
+  if (e < B * B) {
+    const int i = e / B, j = e - i * B;
+    if (j > i) return;
+    double xx = 0.0, si = 0.0, sj = 0.0;
+    for (int c = 0; c < nparts; ++c) {
+      const double* pp = part + (size_t)c * stride;
+      xx += pp[i * B + j];
+      si += pp[B * B + i];
+      sj += pp[B * B + j];
+    }
+    const double ci = shift[i], cj = shift[j];
+    const double q = xx - ci * sj - si * cj + n * ci * cj;
+    q_out[(size_t)i * B + j] = q;
+    q_out[(size_t)j * B + i] = q;
+  } else if (e < B * B + B) {
+    const int i = e - B * B;
+    double si = 0.0;
+    for (int c = 0; c < nparts; ++c) si += part[(size_t)c * stride + B * B + i];
+    s_out[i] = si - n * shift[i];
+  } else if (e == B * B + B) {
+    moments[0] = n;
+  }
+}
+
+static int nch_for(int B) {
+  // widest window over all samples: start offset in its 16-B chunk + 2B bytes
+  int maxoff = 0;
+  for (int s = 0; s < 8; ++s) maxoff = maxoff > ((s * B * 2) & 15) ? maxoff : ((s * B * 2) & 15);
+  return (maxoff + 2 * B + 15) / 16;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int NCH>
+static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* moments,
+                           const double* shift, cudaStream_t st) {
+  constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
+  constexpr uint32_t PAD = NCH > 8 ? (16 - NCH) * kGrLb * 16u : 0;
+  constexpr int G = kGrWorkers / NCH;
+  const size_t smem = kGrStages * (size_t)STAGE + PAD + ((size_t)p.B * p.B + p.B) * 8 +
+                      (size_t)G * NCH * 12 * 4 + NCH * 8 * 8 + 16 * 8 + 1024;
+  int grid = kSMs;
+  if (p.units < grid) grid = (int)p.units;
+  cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, p);
+  SKYRX_CHECK_LAUNCH("gram_raw_kernel");
+  const int work = p.B * p.B + p.B + 1;
+  gram_raw_reduce_kernel<<<ceil_div(work, 256), 256, 0, st>>>(p.part, grid, p.B, shift, moments);
+  SKYRX_CHECK_LAUNCH("gram_raw_reduce_kernel");
+  return SKYRX_OK;
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t bands,
+                                         const void* raw) {
+  if (bands < 1 || lines < 1 || samples < 1) return 0;
+  if (((uintptr_t)raw & 15) != 0) return 0;
+  if (((int64_t)samples * bands * 2) % 16 != 0) return 0;  // TMA line stride
+  if (nch_for(bands) > 16) return 0;                        // window <= 256 bytes (B <= 128)
+  if (lines > ((int64_t)1 << 31) - 1) return 0;
+  return tensor_map_encoder() != nullptr ? 1 : 0;
+}
+
+extern "C" size_t skyrx_stats_raw_workspace(int32_t bands) {
+  return (size_t)kSMs * ((size_t)bands * bands + bands + 1) * sizeof(double);
+}
+
+extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                               const float* dark, const float* coeff, double gain,
+                               const double* shift, double* moments, int32_t* flags,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  SKYRX_REQUIRE(skyrx_stats_raw_supported(lines, samples, bands, raw),
+                "raw-byte tensor-core moments unsupported for this shape/alignment");
+  SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
+  SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_raw_workspace(bands), "workspace too small");
+  const int nch = nch_for(bands);
+  // 3-D byte view: (16 bytes of a chunk, line, chunk within line)
+  const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;
+  cuuint64_t dims[3] = {16, (cuuint64_t)lines, line_bytes / 16};
+  cuuint64_t strides[2] = {line_bytes, 16};  // bytes, for dims 1 and 2
+  cuuint32_t box[3] = {16, (cuuint32_t)kGrLb, (cuuint32_t)nch};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap map;
+  CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)raw, dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  GramRawParams p{};
+  p.dark = dark;
+  p.coeff = coeff;
+  p.ginv = 1.0 / gain;
+  p.part = reinterpret_cast<double*>(workspace);
+  p.flags = flags;
+  p.L = lines;
+  p.S = samples;
+  p.B = bands;
+  p.nsplit = (int)((lines + kGrMaxUnitLines - 1) / kGrMaxUnitLines);
+  // also split so that there are at least ~2 units per SM
+  while ((int64_t)samples * p.nsplit < 2 * kSMs && lines / (p.nsplit + 1) >= 4 * kGrLb) ++p.nsplit;
+  p.split_lines = (lines + p.nsplit - 1) / p.nsplit;
+  p.split_lines = ((p.split_lines + kGrLb - 1) / kGrLb) * kGrLb;
+  p.nsplit = (int)((lines + p.split_lines - 1) / p.split_lines);
+  p.units = (int64_t)samples * p.nsplit;
+  cudaStream_t st = as_stream(stream);
+  switch (nch) {
+#define SKYRX_NCH(k) \
+  case k:            \
+    return launch_gram_raw<k>(map, p, moments, shift, st);
+    SKYRX_NCH(1) SKYRX_NCH(2) SKYRX_NCH(3) SKYRX_NCH(4) SKYRX_NCH(5) SKYRX_NCH(6) SKYRX_NCH(7)
+    SKYRX_NCH(8) SKYRX_NCH(9) SKYRX_NCH(10) SKYRX_NCH(11) SKYRX_NCH(12) SKYRX_NCH(13)
+    SKYRX_NCH(14) SKYRX_NCH(15) SKYRX_NCH(16)
+#undef SKYRX_NCH
+  }
+  set_error("unsupported band count %d", bands);
+  return SKYRX_ERR_ARG;
+}

@@ -323,9 +323,12 @@ class DetectPlan:
         self.qinv = _dev.zeros((batch, bands), torch.float32)
         self.tc_ws_bytes = int(lib.skyrx_stats_tc_workspace(bands)) if self.tc_stats else 0
         self.tc_ws = _dev.empty((max(self.tc_ws_bytes, 8),), torch.uint8)
+        self.raw_stats = bands <= 128 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
+        self.raw_ws_bytes = int(lib.skyrx_stats_raw_workspace(bands)) if self.raw_stats else 0
+        self.raw_ws = _dev.empty((max(self.raw_ws_bytes, 8),), torch.uint8)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
-            precise: bool = False, force_ffma: bool = False):
+            precise: bool = False, force_ffma: bool = False, gain_const: float | None = None):
         """Enqueue the moments of cube i (no host synchronisation)."""
         L, S, B = self.shape
         ds = self.ds
@@ -337,7 +340,15 @@ class DetectPlan:
         # averages out only over many pixels); a quantiser overflow is redone in f64
         small = L * S < TC_MIN_PIXELS
         precise = precise or small or force_ffma
-        if (self.tc_stats and not precise
+        if (self.raw_stats and not precise and gain_const is not None
+                and lib.skyrx_stats_raw_supported(L, S, B, raw.data_ptr())):
+            # exact integer byte Grams on the tensor cores (constant line gain)
+            _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            _lib.call("skyrx_stats_raw", raw.data_ptr(), L, S, B, dark.data_ptr(),
+                      coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
+                      ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
+                      self.raw_ws.data_ptr(), self.raw_ws_bytes, s)
+        elif (self.tc_stats and not precise
                 and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
             _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
                       self.qinv[i].data_ptr(), s)
@@ -400,6 +411,20 @@ class DetectPlan:
         return self
 
 
+def constant_gain(gains, tables) -> float | None:
+    """The common line gain if every line shares it (and calibration cannot
+    overflow f32), else None — the raw-byte moments path needs one gain."""
+    g = gains.detach().cpu().numpy() if isinstance(gains, torch.Tensor) else np.asarray(gains)
+    if g.size == 0 or not (g == g.flat[0]).all():
+        return None
+    g0 = float(np.float32(g.flat[0]))
+    if not g0 > 0.0:
+        return None
+    if not np.isfinite(np.float32(65535.0) * np.float32(tables.coeff.max()) / np.float32(g0)):
+        return None
+    return g0
+
+
 def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
            precise: bool = False, plan: DetectPlan | None = None) -> Detection:
     """Fused calibrate + RX + top-0.1% mask for one raw cube (the hot path).
@@ -420,7 +445,9 @@ def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
     rv = _raw_device(raw)
     gd = _dev.to_device(gains, torch.float32)
     plan = plan or DetectPlan(L, S, B)
-    plan.run(0, rv, dark, coeff, gd, precise=precise).finalize().score(0, rv, dark, coeff, gd, k)
+    gain_const = constant_gain(gains, tables)
+    plan.run(0, rv, dark, coeff, gd, precise=precise, gain_const=gain_const)
+    plan.finalize().score(0, rv, dark, coeff, gd, k)
     plan.recover_range({0: (rv, dark, coeff, gd)})
     on_dev = _dev.is_device(raw.values) if device is None else device
     ds = plan.ds

@@ -353,9 +353,11 @@ class TestDetect:
         rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
         assert rel.max() < 2e-5, rel.max()
 
-    @pytest.mark.parametrize("S,B,L", [(900, 70, 300), (64, 70, 4100), (96, 48, 2800),
-                                       (40, 15, 6600), (128, 79, 2100)])
-    def test_tensor_core_moments(self, P, S, B, L):
+    @pytest.mark.parametrize("S,B,L,gain", [(900, 70, 300, 1.0), (64, 70, 4100, 2.5),
+                                            (96, 48, 2800, 1.0), (40, 16, 6600, 1.0),
+                                            (1024, 128, 260, 1.0), (128, 79, 2100, 0.75)])
+    def test_raw_byte_moments(self, P, S, B, L, gain):
+        """Constant line gain: exact integer byte Grams on the tensor cores."""
         from paper_2602_13509_b200 import _lib
         from paper_2602_13509_b200.rx import TC_MIN_PIXELS
         from paper_2602_13509_b200.synth import Scene
@@ -364,35 +366,65 @@ class TestDetect:
         rv = Scene(43, S, B, 5).generate(0, L)
         raw = rv.cpu().numpy()
         t = osynth.make_tables(43, S, B, 5)
-        assert _lib.load().skyrx_stats_tc_supported(L, S, B, rv.data_ptr()) == 1
+        assert _lib.load().skyrx_stats_raw_supported(L, S, B, rv.data_ptr()) == 1
+        gains = np.full(L, gain)
+        det = P.detect(raw_cube(P, raw, gains), P.CalibrationTables(t.dark, t.coeff))
+        check_detection(det, raw, t, gains)
+        ref = O.compute_stats(O.apply_calibration(raw, t.dark, t.coeff, gains))
+        # exact integer Gram: only f32-vs-exact calibration rounding and f64 sums remain
+        assert normwise(det.stats.sigma, ref.sigma) < 1e-9
+        assert normwise(det.stats.mu, ref.mu) < 1e-10
+
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 300), (96, 48, 2800), (128, 79, 2100)])
+    def test_quantised_moments_varying_gains(self, P, S, B, L):
+        """Varying line gains: dithered int8-digit Gram on the tensor cores."""
+        from paper_2602_13509_b200.synth import Scene
+
+        raw = Scene(44, S, B, 5).generate(0, L).cpu().numpy()
+        t = osynth.make_tables(44, S, B, 5)
+        gains = 1.0 + 0.5 * np.sin(np.arange(L) / 17.0) ** 2
         plan = P.DetectPlan(L, S, B)
         assert plan.tc_stats
-        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
-        check_detection(det, raw, t)
-        rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
-        ref = O.compute_stats(rad)
+        det = P.detect(raw_cube(P, raw, gains), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        check_detection(det, raw, t, gains)
+        ref = O.compute_stats(O.apply_calibration(raw, t.dark, t.coeff, gains))
         # quantiser noise only (dithered, unbiased): far below the 1e-5 contract
         assert normwise(det.stats.sigma, ref.sigma) < 1e-6
         assert normwise(det.stats.mu, ref.mu) < 1e-7
 
-    def test_tensor_core_moments_range_fallback(self, P, rng):
-        # a flat cube with one far outlier outside the shift sample overflows the
-        # int8 quantiser; detect() must notice and recompute in f64
+    def test_quantiser_range_fallback(self, P, rng):
+        # varying gains + a flat cube with one far outlier outside the shift sample
+        # overflow the int8 quantiser; detect() must notice and redo the fit in f64
         L, S, B = 300, 900, 70
         raw = (1000 + rng.integers(-3, 4, (L, S, B))).astype(np.uint16)
         assert (1 * S + 100) % ((L * S) // 4096) != 0   # not a sampled pixel
         raw[1, 100] = 4000
         dark = np.full((S, B), 100.0, np.float32)
         coeff = np.ones((S, B), np.float32)
-        plan = P.DetectPlan(L, S, B)
-        det = P.detect(raw_cube(P, raw), P.CalibrationTables(dark, coeff), plan=plan)
-        rad = O.apply_calibration(raw, dark, coeff, np.ones(L))
+        gains = np.ones(L)
+        gains[7] = 2.0
+        det = P.detect(raw_cube(P, raw, gains), P.CalibrationTables(dark, coeff))
+        rad = O.apply_calibration(raw, dark, coeff, gains)
         ref = O.compute_stats(rad)
         assert normwise(det.stats.sigma, ref.sigma) < 1e-12
         assert normwise(det.stats.mu, ref.mu) < 1e-12
         want = O.rx_scores(rad, ref)
         assert (np.abs(det.scores - want) / np.maximum(want, 1e-12)).max() < 1e-4
         assert det.mask[1, 100]
+
+    def test_raw_path_clamp_fallback(self, P):
+        # a value below its dark level clamps to 0 (calibrate.py:99): the raw-byte
+        # algebra no longer holds, so detect() must redo the fit in f64
+        L, S, B = 300, 900, 70
+        t = osynth.make_tables(45, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        raw[5, 17, 3] = 20      # dark ~ 100 -> clamps
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff))
+        rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
+        assert rad[5, 17, 3] == 0.0
+        ref = O.compute_stats(rad)
+        assert normwise(det.stats.sigma, ref.sigma) < 1e-12
+        check_detection(det, raw, t)
 
     def test_deterministic(self, P):
         t = osynth.make_tables(1, 900, 70)
