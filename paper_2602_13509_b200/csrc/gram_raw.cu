@@ -18,7 +18,7 @@
 // the result is the exact Gram up to f64 rounding (~1e-13 after centring).
 //
 // Work unit = (sample s, line range of <= 32768 lines); units are dealt to
-// CTAs in balanced contiguous ranges so the summation order is fixed.
+// CTAs round-robin (static), so the summation order is fixed.
 // Roles: warps 0-3 scan + epilogue, warp 4 TMA producer, warp 5 MMA issuer.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -91,8 +91,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int64_t u0 = (int64_t)blockIdx.x * p.units / gridDim.x;
-  const int64_t u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+  // round-robin units: at any moment the CTAs work on neighbouring samples of
+  // the same lines, so the 16-B chunks two windows share are fetched once (L2)
+  const int64_t u0 = blockIdx.x;
+  const int64_t u1 = p.units;
+  const int64_t ustep = gridDim.x;
 
   if (tid == 0) {
     for (int s = 0; s < kGrStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], kGrWorkers + 1);
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   if (warp == 4) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       int t = 0;
-      for (int64_t u = u0; u < u1; ++u) {
+      for (int64_t u = u0; u < u1; u += ustep) {
         int s;
         int64_t l0, nl;
         unit_geom(u, s, l0, nl);
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       constexpr uint32_t id = idesc_u8_s32(128, NW);
       int t = 0, unit = 0;
-      for (int64_t u = u0; u < u1; ++u, ++unit) {
+      for (int64_t u = u0; u < u1; u += ustep, ++unit) {
         int s;
         int64_t l0, nl;
         unit_geom(u, s, l0, nl);
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     const int c = tid % NCH, g = tid / NCH;
     const bool scanner = g < G;
     int t = 0, unit = 0;
-    for (int64_t u = u0; u < u1; ++u, ++unit) {
+    for (int64_t u = u0; u < u1; u += ustep, ++unit) {
       int s;
       int64_t l0, nl;
       unit_geom(u, s, l0, nl);
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     for (int e = tid; e < B * B + B; e += kGrWorkers) out[e] = qacc[e];
     if (tid == 0) {
       double n = 0.0;
-      for (int64_t u = u0; u < u1; ++u) {
+      for (int64_t u = u0; u < u1; u += ustep) {
         int s;
         int64_t l0, nl;
         unit_geom(u, s, l0, nl);

@@ -53,25 +53,6 @@ __host__ __device__ constexpr uint32_t wpack_bytes_for(int kp) {
   return 2u * kp * kp * 2u + kp * 4u;
 }
 
-// 8 centred values of one pixel row -> f16 hi/lo chunks
-template <bool FULL, bool DIV>
-__device__ __forceinline__ void centre8(const uint16_t* rp, const float2* tab, const float2* mu,
-                                        int k0, int B, float ginv, float* dv) {
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int k = k0 + q;
-    float v = 0.0f;
-    if (FULL || k < B) {
-      const float2 dc = tab[k];
-      float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dc.x), 0.0f), dc.y);
-      if (DIV) x = __fmul_rn(x, ginv);  // fast path: 1 ulp of the exact division
-      const float2 m = mu[k];
-      v = __fsub_rn(__fsub_rn(x, m.x), m.y);
-    }
-    dv[q] = v;
-  }
-}
-
 __device__ __forceinline__ void store_split8(const float* dv, uint8_t* hi, uint8_t* lo) {
   uint32_t hw[4], lw[4];
 #pragma unroll
@@ -186,10 +167,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   } else {  // ------------------------------------------------------------ workers
     const int r = tid & 127;   // pixel row of the tile
     const int h = tid >> 7;    // band half
-    const int c_lo = h ? CH0 : 0, c_hi = h ? NCH : CH0;
+    constexpr int CHT = CH0;   // chunks per thread (h = 1 may own one fewer)
+    const int c_lo = h ? CH0 : 0;
+    const int nmine = h ? NCH - CH0 : CH0;
     mbar_wait(w_bar, 0);
-    int cur_block = -1;
+    // calibration of this thread's row, kept in registers: a tile row always maps
+    // to the same sample of the current block, so these change only with the block.
+    //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
+    float tco[CHT * 8], toff[CHT * 8], tmu[CHT * 8];
+    int cur_block = -1, cur_w = -1;
     uint32_t local_max = 0;
+    auto load_row_tables = [&](const TileInfo& ti) {
+      const int j = r % ti.w;
+      const int64_t srow = (int64_t)(ti.s0 + j) * B;
+#pragma unroll
+      for (int cc = 0; cc < CHT; ++cc)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int k = 8 * (c_lo + cc) + q;
+          float co = 0.0f, of = 0.0f, mm = 0.0f;
+          if (cc < nmine && k < B) {
+            const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
+            co = __ldg(p.coeff + srow + k);
+            of = (float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
+            mm = (float)(-mu_k);
+          }
+          tco[cc * 8 + q] = co;
+          toff[cc * 8 + q] = of;
+          tmu[cc * 8 + q] = mm;
+        }
+    };
     auto epilogue = [&](int t, const TileInfo& ti) {
       const int acs = t & 1;
       mbar_wait(&acc_full[acs], (t >> 1) & 1);
@@ -197,8 +204,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + acs * NP;
       float sum = 0.0f;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        if (c < c_lo || c >= c_hi) continue;
+      for (int cc = 0; cc < CHT; ++cc) {
+        if (cc >= nmine) continue;  // warp-uniform
+        const int c = c_lo + cc;
         uint32_t v[8];
         tmem_ld8(taddr + c * 8, v);
         tmem_ld_wait();
@@ -224,15 +232,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     TileInfo prev{};
     for (int t = 0; t < n; ++t) {
       const TileInfo ti = tile_info(p.ts, it0 + t);
-      if (ti.block != cur_block) {
-        named_sync(1, kTcWorkers);
-        for (int e = tid; e < ti.w * B; e += kTcWorkers) {
-          const int j = e / B, b = e - j * B;
-          const int64_t g = (int64_t)(ti.s0 + j) * B + b;
-          tab[j * (B + 1) + b] = make_float2(__ldg(p.dark + g), __ldg(p.coeff + g));
-        }
-        named_sync(1, kTcWorkers);
+      if (ti.block != cur_block || ti.w != cur_w) {
+        load_row_tables(ti);
         cur_block = ti.block;
+        cur_w = ti.w;
       }
       const int s = t % kScoreRawStages;
       const int as = t % kScoreAStages;
@@ -242,25 +245,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       uint8_t* alo = ahi + A_BYTES;
       if (r < ti.rows) {
         const int li = r / ti.w;
-        const int j = r - li * ti.w;
         const float g = __ldg(p.gain + ti.line0 + li);
-        const float ginv = 1.0f / g;
-        const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
-        const float2* tk = tab + j * (B + 1);
-        for (int c = c_lo; c < c_hi; ++c) {
-          float dv[8];
-          const bool full = c * 8 + 8 <= B;
-          if (g == 1.0f) {
-            if (full) centre8<true, false>(rp, tk, mu, c * 8, B, ginv, dv);
-            else centre8<false, false>(rp, tk, mu, c * 8, B, ginv, dv);
+        const uint8_t* rrow = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2;
+#pragma unroll
+        for (int cc = 0; cc < CHT; ++cc) {
+          if (cc >= nmine) continue;
+          const int c = c_lo + cc;
+          float rf[8];
+          if ((B & 1) == 0) {  // 4-byte aligned rows: two counts per LDS.32
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(rrow + 16 * c + 4 * q);
+              // exact u16 -> f32 without the conversion pipe: 2^23 + r - 2^23
+              rf[2 * q] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
+              rf[2 * q + 1] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
+            }
           } else {
-            if (full) centre8<true, true>(rp, tk, mu, c * 8, B, ginv, dv);
-            else centre8<false, true>(rp, tk, mu, c * 8, B, ginv, dv);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              rf[q] = (float)reinterpret_cast<const uint16_t*>(rrow)[8 * c + q];
+          }
+          float dv[8];
+          if (g == 1.0f) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dv[q] = fmaxf(fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]), tmu[cc * 8 + q]);
+          } else {  // per-line gain: x = max(r c - dark c, 0) / g
+            const float gi = 1.0f / g;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float xc = fmaf(rf[q], tco[cc * 8 + q], -(toff[cc * 8 + q] + tmu[cc * 8 + q]));
+              dv[q] = fmaf(fmaxf(xc, 0.0f), gi, tmu[cc * 8 + q]);
+            }
           }
           store_split8(dv, ahi + c * 128, alo + c * 128);
         }
       } else {
-        for (int c = c_lo; c < c_hi; ++c) {
+#pragma unroll
+        for (int cc = 0; cc < CHT; ++cc) {
+          if (cc >= nmine) continue;
+          const int c = c_lo + cc;
           *reinterpret_cast<uint4*>(ahi + c * 128) = make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(alo + c * 128) = make_uint4(0, 0, 0, 0);
         }
