@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
   constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
   constexpr uint32_t SBO = kGrLb * 16u;           // chunk stride in the stage
-  constexpr uint32_t PAD = TWO_M ? (16 - NCH) * SBO : 0;
+  // M=128 A reads cover 8 (or 16) chunks from the window start: pad past the last stage
+  constexpr uint32_t PAD = ((TWO_M ? 16 : 8) - NCH) * SBO;
   constexpr int G = kGrWorkers / NCH;             // scan line groups
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
@@ -342,7 +343,7 @@ template <int NCH>
 static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* moments,
                            const double* shift, cudaStream_t st) {
   constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
-  constexpr uint32_t PAD = NCH > 8 ? (16 - NCH) * kGrLb * 16u : 0;
+  constexpr uint32_t PAD = ((NCH > 8 ? 16 : 8) - NCH) * kGrLb * 16u;
   constexpr int G = kGrWorkers / NCH;
   const size_t smem = kGrStages * (size_t)STAGE + PAD + ((size_t)p.B * p.B + p.B) * 8 +
                       (size_t)G * NCH * 12 * 4 + NCH * 8 * 8 + 16 * 8 + 1024;

@@ -16,7 +16,7 @@
 //                          calibrate + centre + f16 split into the K-major A
 //                          operand, then the epilogue of the previous tile
 //                          (tcgen05.ld, unscale, sum of squares, store).
-// Calibration tables of the current sample block live in shared memory.
+// Each worker keeps its row's per-sample calibration constants in registers.
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, TMEM_COLS);
+  // mu[k].x = f32(-mu_k): clamp floor of the centred value, read as a warp broadcast
   for (int k = tid; k < KP; k += blockDim.x)
-    mu[k] = k < B ? make_float2(p.mu_hilo[k], p.mu_hilo[B + k]) : make_float2(0.0f, 0.0f);
+    mu[k] = k < B ? make_float2((float)(-((double)p.mu_hilo[k] + (double)p.mu_hilo[B + k])), 0.0f)
+                  : make_float2(0.0f, 0.0f);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     // calibration of this thread's row, kept in registers: a tile row always maps
     // to the same sample of the current block, so these change only with the block.
     //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
-    float tco[CHT * 8], toff[CHT * 8], tmu[CHT * 8];
+    float tco[CHT * 8], toff[CHT * 8];
     int cur_block = -1, cur_w = -1;
     uint32_t local_max = 0;
     auto load_row_tables = [&](const TileInfo& ti) {
@@ -185,16 +187,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int k = 8 * (c_lo + cc) + q;
-          float co = 0.0f, of = 0.0f, mm = 0.0f;
+          float co = 0.0f, of = 0.0f;
           if (cc < nmine && k < B) {
             const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
             co = __ldg(p.coeff + srow + k);
             of = (float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
-            mm = (float)(-mu_k);
           }
           tco[cc * 8 + q] = co;
           toff[cc * 8 + q] = of;
-          tmu[cc * 8 + q] = mm;
         }
     };
     auto epilogue = [&](int t, const TileInfo& ti) {
@@ -266,16 +266,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
               rf[q] = (float)reinterpret_cast<const uint16_t*>(rrow)[8 * c + q];
           }
           float dv[8];
+          const float2* nm = mu + 8 * c;
           if (g == 1.0f) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              dv[q] = fmaxf(fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]), tmu[cc * 8 + q]);
+              dv[q] = fmaxf(fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]), nm[q].x);
           } else {  // per-line gain: x = max(r c - dark c, 0) / g
             const float gi = 1.0f / g;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const float xc = fmaf(rf[q], tco[cc * 8 + q], -(toff[cc * 8 + q] + tmu[cc * 8 + q]));
-              dv[q] = fmaf(fmaxf(xc, 0.0f), gi, tmu[cc * 8 + q]);
+              const float xc = fmaf(rf[q], tco[cc * 8 + q], -(toff[cc * 8 + q] + nm[q].x));
+              dv[q] = fmaf(fmaxf(xc, 0.0f), gi, nm[q].x);
             }
           }
           store_split8(dv, ahi + c * 128, alo + c * 128);
