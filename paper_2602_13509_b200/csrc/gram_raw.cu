@@ -10,8 +10,8 @@
 // comes from ONE byte Gram D = sum_l b b^T (b = the 2B bytes), which the
 // tensor cores compute exactly (tcgen05.mma kind::i8, unsigned, s32 TMEM
 // accumulators; 255^2 * 32768 lines < 2^31).  TMA loads each tile's bytes
-// ([16-byte chunk][line][16 B] boxes of a 3-D tensor map) directly in the
-// canonical MN-major UMMA layout, so no thread touches the data on its way to
+// (128-byte x 128-line boxes, 128B-swizzled by the TMA engine) directly in the
+// canonical MN-major SWIZZLE_128B UMMA layout, so no thread touches the data on its way to
 // the tensor core.  The CUDA cores only scan each tile for m_s and for the
 // per-band minimum (a value below dark would clamp: the cube is then redone by
 // the generic path, flags |= 4).  Everything after the integer Gram is f64;
@@ -32,7 +32,9 @@ using namespace umma;
 constexpr int kGrThreads = 192;
 constexpr int kGrWorkers = 128;
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
-constexpr int kGrStages = 4;
+// TMA ring depth: 4 stages, 2 for the widest windows (B > ~96) to fit the f64 accumulator
+template <int NCH>
+__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : 4; }
 constexpr int64_t kGrMaxUnitLines = 32768;
 
 struct GramRawParams {
@@ -48,12 +50,12 @@ struct GramRawParams {
   int64_t units;
 };
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, uint64_t* bar) {
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -66,17 +68,19 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
 template <int NCH>
 __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  GramRawParams p) {
+  constexpr int kGrStages = gr_stages<NCH>();
   constexpr int NW = 16 * NCH;                    // window bytes = MMA N
   constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
-  constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
-  constexpr uint32_t SBO = kGrLb * 16u;           // chunk stride in the stage
-  // M=128 A reads cover 8 (or 16) chunks from the window start: pad past the last stage
-  constexpr uint32_t PAD = ((TWO_M ? 16 : 8) - NCH) * SBO;
+  // a tile = NATOM boxes of [128 window bytes][Lb lines], 128B-swizzled by TMA:
+  // the canonical MN-major SWIZZLE_128B UMMA layout (LBO = atom stride, SBO = 8 lines)
+  constexpr int NATOM = TWO_M ? 2 : 1;
+  constexpr uint32_t ATOM = kGrLb * 128u;
+  constexpr uint32_t STAGE = NATOM * ATOM;
   constexpr int G = kGrWorkers / NCH;             // scan line groups
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
   uint8_t* stages = sm;
-  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE + PAD);
+  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE);
   double* sacc = qacc + B * B;
   uint32_t* smin = reinterpret_cast<uint32_t*>(sacc + B);  // [G][NCH][4] packed u16 mins
   uint32_t* ssum = smin + G * NCH * 4;                       // [G][NCH][8]
@@ -131,7 +135,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           const int st = t % kGrStages;
           mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], STAGE);
-          tma_load_3d(stages + st * STAGE, &tmap, 0, (int)(l0 + (int64_t)k * kGrLb), c0, &full[st]);
+#pragma unroll
+          for (int a = 0; a < NATOM; ++a)
+            tma_load_2d(stages + st * STAGE + a * ATOM, &tmap, 16 * c0 + 128 * a,
+                        (int)(l0 + (int64_t)k * kGrLb), &full[st]);
         }
       }
     }
@@ -154,10 +161,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #pragma unroll
           for (int ks = 0; ks < kGrLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-            const uint8_t* kb = base + ks * 512;  // 32 lines = 4 groups of 8 x 16 B
-            const uint64_t bdesc = smem_desc(kb, 128, SBO);
-            mma_i8(tmem, smem_desc(kb, 128, SBO), bdesc, id, acc);
-            if (TWO_M) mma_i8(tmem + NW, smem_desc(kb + 8 * SBO, 128, SBO), bdesc, id, acc);
+            const uint8_t* kb = base + ks * 4096;  // 32 lines = 4 swizzle atoms of 8 x 128 B
+            const uint64_t bdesc = smem_desc_sw128(kb, ATOM, 1024);
+            mma_i8(tmem, smem_desc_sw128(kb, ATOM, 1024), bdesc, id, acc);
+            if (TWO_M) mma_i8(tmem + NW, smem_desc_sw128(kb + ATOM, ATOM, 1024), bdesc, id, acc);
           }
           mma_commit(&empty[st]);
         }
@@ -180,9 +187,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         mbar_wait(&full[st], (t / kGrStages) & 1);
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
-          const uint4* row = reinterpret_cast<const uint4*>(stages + st * STAGE + c * SBO);
+          const uint8_t* atom = stages + st * STAGE + (c >> 3) * ATOM;
           for (int l = g; l < valid; l += G) {
-            const uint4 v = row[l];
+            // 128B swizzle: 16-B chunk c of line l sits at chunk c ^ (l & 7)
+            const uint4 v = *reinterpret_cast<const uint4*>(atom + l * 128 + (((c & 7) ^ (l & 7)) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
             sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
@@ -342,10 +350,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <int NCH>
 static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* moments,
                            const double* shift, cudaStream_t st) {
-  constexpr uint32_t STAGE = (uint32_t)NCH * kGrLb * 16u;
-  constexpr uint32_t PAD = ((NCH > 8 ? 16 : 8) - NCH) * kGrLb * 16u;
+  constexpr uint32_t STAGE = (NCH > 8 ? 2u : 1u) * kGrLb * 128u;
   constexpr int G = kGrWorkers / NCH;
-  const size_t smem = kGrStages * (size_t)STAGE + PAD + ((size_t)p.B * p.B + p.B) * 8 +
+  constexpr int kGrStages = gr_stages<NCH>();
+  const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
                       (size_t)G * NCH * 12 * 4 + NCH * 8 * 8 + 16 * 8 + 1024;
   int grid = kSMs;
   if (p.units < grid) grid = (int)p.units;
@@ -386,16 +394,16 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
   SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_raw_workspace(bands), "workspace too small");
   const int nch = nch_for(bands);
-  // 3-D byte view: (16 bytes of a chunk, line, chunk within line)
+  // 2-D byte view (byte within line, line); boxes of 128 bytes x Lb lines, swizzled
   const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;
-  cuuint64_t dims[3] = {16, (cuuint64_t)lines, line_bytes / 16};
-  cuuint64_t strides[2] = {line_bytes, 16};  // bytes, for dims 1 and 2
-  cuuint32_t box[3] = {16, (cuuint32_t)kGrLb, (cuuint32_t)nch};
-  cuuint32_t estr[3] = {1, 1, 1};
+  cuuint64_t dims[2] = {line_bytes, (cuuint64_t)lines};
+  cuuint64_t strides[1] = {line_bytes};
+  cuuint32_t box[2] = {128, (cuuint32_t)kGrLb};
+  cuuint32_t estr[2] = {1, 1};
   CUtensorMap map;
-  CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)raw, dims, strides,
+  CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)raw, dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   GramRawParams p{};

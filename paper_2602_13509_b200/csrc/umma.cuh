@@ -94,6 +94,11 @@ __device__ __forceinline__ uint64_t smem_desc(const void* base, uint32_t lbo, ui
   return d;
 }
 
+// 128-byte swizzle atoms (TMA CU_TENSOR_MAP_SWIZZLE_128B), 1024-B aligned bases
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* base, uint32_t lbo, uint32_t sbo) {
+  return smem_desc(base, lbo, sbo) | ((uint64_t)2 << 61);
+}
+
 // instruction descriptor (cute UMMA::InstrDescriptor):
 // c_format [4,6), a_format [7,10), b_format [10,13), a_major 15, b_major 16,
 // n_dim=N>>3 [17,23), m_dim=M>>4 [24,29)
