@@ -161,7 +161,9 @@ int skyrx_score(int32_t kind, const void* pixels, int64_t lines, int32_t samples
 /* Tensor-core (tcgen05) variant of skyrx_score for RAW cubes with B <= 80:
  * f16 hi/lo split of (x - mu) and of W, f32 TMEM accumulation, sum of squares
  * in the epilogue.  wpack = skyrx_pack_whiten(whiten64) (skyrx_wpack_bytes(B)
- * bytes per matrix).  skyrx_score_tc_supported() says whether the shape and
+ * bytes per matrix).  flags (nullable) = the moments-pass flags word: when it
+ * reads 8 (raw-byte path ran, no value below dark) the clamp is skipped.
+ * skyrx_score_tc_supported() says whether the shape and
  * alignment allow it (every line segment of a tile must be a 16-B multiple). */
 size_t skyrx_wpack_bytes(int32_t bands);
 int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t batch, void* wpack,
@@ -169,8 +171,8 @@ int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t batch, void
 int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
 int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                    const float* dark, const float* coeff, const float* gain,
-                   const float* mu_hilo, const void* wpack, float* scores, uint32_t* max_key,
-                   void* stream);
+                   const float* mu_hilo, const void* wpack, const int32_t* flags,
+                   float* scores, uint32_t* max_key, void* stream);
 
 /* The kernel slot itself: _accel.mahalanobis_sq(pixels, mu, chol_lower)
  * (_accel.py:109-131) with FP64 arithmetic; pixels f32 or f64 (kind F32/F64).

@@ -77,10 +77,14 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   constexpr uint32_t ATOM = kGrLb * 128u;
   constexpr uint32_t STAGE = NATOM * ATOM;
   constexpr int G = kGrWorkers / NCH;             // scan line groups
+  // column sums m_s ride on the tensor core too: A x ones(N=16) into TMEM
+  constexpr uint32_t SUMC = (TWO_M ? 2 : 1) * NW;
+  constexpr bool ONES = SUMC + (TWO_M ? 32 : 16) <= 512;
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
   uint8_t* stages = sm;
-  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE);
+  uint8_t* ones = stages + kGrStages * STAGE;                 // 128 lines x 16 B of 1
+  double* qacc = reinterpret_cast<double*>(ones + kGrLb * 16);
   double* sacc = qacc + B * B;
   uint32_t* smin = reinterpret_cast<uint32_t*>(sacc + B);  // [G][NCH][4] packed u16 mins
   uint32_t* ssum = smin + G * NCH * 4;                       // [G][NCH][8]
@@ -109,7 +113,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, 512);
+  // bit 8: this cube's clamp check ran (bit 4 would report a value below dark)
+  if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 8);
   for (int e = tid; e < B * B + B; e += blockDim.x) qacc[e] = 0.0;
+  for (int e = tid; e < kGrLb * 4; e += blockDim.x) reinterpret_cast<uint32_t*>(ones)[e] = 0x01010101u;
+  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -145,6 +153,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   } else if (warp == 5) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       constexpr uint32_t id = idesc_u8_s32(128, NW);
+      constexpr uint32_t id1 = idesc_u8_s32(128, 16);
       int t = 0, unit = 0;
       for (int64_t u = u0; u < u1; u += ustep, ++unit) {
         int s;
@@ -165,6 +174,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             const uint64_t bdesc = smem_desc_sw128(kb, ATOM, 1024);
             mma_i8(tmem, smem_desc_sw128(kb, ATOM, 1024), bdesc, id, acc);
             if (TWO_M) mma_i8(tmem + NW, smem_desc_sw128(kb + ATOM, ATOM, 1024), bdesc, id, acc);
+            if (ONES) {
+              const uint64_t odesc = smem_desc(ones + ks * 512, 128, 128);
+              mma_i8(tmem + SUMC, smem_desc_sw128(kb, ATOM, 1024), odesc, id1, acc);
+              if (TWO_M) mma_i8(tmem + SUMC + 16, smem_desc_sw128(kb + ATOM, ATOM, 1024), odesc, id1, acc);
+            }
           }
           mma_commit(&empty[st]);
         }
@@ -188,13 +202,16 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           const uint8_t* atom = stages + st * STAGE + (c >> 3) * ATOM;
+#pragma unroll 4
           for (int l = g; l < valid; l += G) {
             // 128B swizzle: 16-B chunk c of line l sits at chunk c ^ (l & 7)
             const uint4 v = *reinterpret_cast<const uint4*>(atom + l * 128 + (((c & 7) ^ (l & 7)) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
-            sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
-            sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+            if (!ONES) {
+              sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
+              sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+            }
           }
         }
         mbar_arrive(&empty[st]);
@@ -214,13 +231,27 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           sv += ssum[(gg * NCH + cc) * 8 + q];
         }
         minv[tid] = mv;
-        sumv[tid] = sv;
+        if (!ONES) sumv[tid] = sv;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
       // ---- epilogue: byte Gram (TMEM) -> calibrated sum x x^T of this sample
       mbar_wait(acc_full, unit & 1);
       tc_fence_after();
       const int off = (int)(((int64_t)s * B * 2) & 15);
+      if (ONES) {  // band sums: 256 * (hi-byte row sum) + (lo-byte row sum)
+#pragma unroll
+        for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
+          if (part == 1 && 128 + 32 * warp >= off + 2 * B) continue;  // warp-uniform
+          uint32_t v[8];
+          tmem_ld8(tmem + ((uint32_t)(32 * warp) << 16) + SUMC + 16 * part, v);
+          tmem_ld_wait();
+          const uint32_t hi = __shfl_xor_sync(0xffffffffu, v[0], 1);
+          const int rel = 128 * part + tid - off;
+          if (rel >= 0 && rel < 2 * B && (rel & 1) == 0)
+            sumv[(off >> 1) + (rel >> 1)] = 256u * hi + v[0];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
+      }
       const double Lu = (double)nl;
       const float* drow = p.dark + (int64_t)s * B;
       const float* crow = p.coeff + (int64_t)s * B;
@@ -353,7 +384,7 @@ static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* mome
   constexpr uint32_t STAGE = (NCH > 8 ? 2u : 1u) * kGrLb * 128u;
   constexpr int G = kGrWorkers / NCH;
   constexpr int kGrStages = gr_stages<NCH>();
-  const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
+  const size_t smem = kGrStages * (size_t)STAGE + kGrLb * 16 + ((size_t)p.B * p.B + p.B) * 8 +
                       (size_t)G * NCH * 12 * 4 + NCH * 8 * 8 + 16 * 8 + 1024;
   int grid = kSMs;
   if (p.units < grid) grid = (int)p.units;

@@ -41,6 +41,7 @@ struct ScoreTcParams {
   const uint8_t* wpack;
   float* scores;
   uint32_t* max_key;
+  const int32_t* flags;  // moments-pass flags: (flags & 12) == 8 -> no value below dark
   TileSched ts;
   uint32_t raw_stage_bytes;
 };
@@ -173,6 +174,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     const int c_lo = h ? CH0 : 0;
     const int nmine = h ? NCH - CH0 : CH0;
     mbar_wait(w_bar, 0);
+    // the raw-byte moments pass proved min(raw) >= dark everywhere: skip the clamp
+    const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
+    const float wscale = colscale[0];  // one power-of-two scale for all of W
     // calibration of this thread's row, kept in registers: a tile row always maps
     // to the same sample of the current block, so these change only with the block.
     //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
@@ -212,10 +216,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         tmem_ld_wait();
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float z = __uint_as_float(v[q]) * colscale[c * 8 + q];
+          const float z = __uint_as_float(v[q]);
           sum = fmaf(z, z, sum);
         }
       }
+      sum *= wscale * wscale;
       tc_fence_before();
       mbar_arrive(&acc_empty[acs]);
       float* rb = red + (t & 1) * 128;
@@ -267,7 +272,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
           }
           float dv[8];
           const float2* nm = mu + 8 * c;
-          if (g == 1.0f) {
+          if (g == 1.0f && noclamp) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dv[q] = fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]);
+          } else if (g == 1.0f) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               dv[q] = fmaxf(fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]), nm[q].x);
@@ -316,13 +324,20 @@ __global__ void pack_whiten_kernel(const double* __restrict__ w64, int B, uint8_
   const double* W = w64 + (size_t)blockIdx.x * B * B;
   uint8_t* o = out + (size_t)blockIdx.x * wpack_bytes_for(KP);
   float* colscale = reinterpret_cast<float*>(o + 2 * W_BYTES);
+  // one power-of-two scale for the whole matrix (the epilogue then squares raw
+  // accumulators and multiplies once); tiny rows stay accurate in absolute terms,
+  // which is what delta = sum_j z_j^2 needs
+  __shared__ double smx[128];
+  double m0 = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)B * B; e += blockDim.x) m0 = fmax(m0, fabs(W[e]));
+  smx[threadIdx.x] = m0;
+  __syncthreads();
+  double mx = 0.0;
+  for (int i = 0; i < (int)blockDim.x; ++i) mx = fmax(mx, smx[i]);
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);           // mx in [2^(e-1), 2^e)
+  const double sc = ldexp(1.0, 14 - e);  // max scaled value in [2^13, 2^14)
   for (int jn = threadIdx.x; jn < KP; jn += blockDim.x) {
-    double mx = 0.0;
-    if (jn < B)
-      for (int k = 0; k < B; ++k) mx = fmax(mx, fabs(W[(size_t)jn * B + k]));
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);           // mx in [2^(e-1), 2^e)
-    const double sc = ldexp(1.0, 14 - e);  // max scaled value in [2^13, 2^14)
     colscale[jn] = (float)ldexp(1.0, e - 14);
     for (int k = 0; k < KP; ++k) {
       const double v = (jn < B && k < B && k <= jn) ? W[(size_t)jn * B + k] * sc : 0.0;
@@ -387,8 +402,8 @@ extern "C" int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t 
 
 extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                               const float* dark, const float* coeff, const float* gain,
-                              const float* mu_hilo, const void* wpack, float* scores,
-                              uint32_t* max_key, void* stream) {
+                              const float* mu_hilo, const void* wpack, const int32_t* flags,
+                              float* scores, uint32_t* max_key, void* stream) {
   SKYRX_REQUIRE(skyrx_score_tc_supported(lines, samples, bands, raw),
                 "tensor-core score path unsupported for this shape/alignment");
   ScoreTcParams p{};
@@ -400,6 +415,7 @@ extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t sample
   p.wpack = (const uint8_t*)wpack;
   p.scores = scores;
   p.max_key = max_key;
+  p.flags = flags;
   tc_sched(lines, samples, bands, kScoreWmax, p.ts);
   if (lines * (int64_t)samples == 0) return SKYRX_OK;
   cudaStream_t st = as_stream(stream);

@@ -397,7 +397,8 @@ class DetectPlan:
         if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
             _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
-                      self.wpack[i].data_ptr(), sc.data_ptr(), self.max_key[i:i + 1].data_ptr(), s)
+                      self.wpack[i].data_ptr(), ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
+                      self.max_key[i:i + 1].data_ptr(), s)
         else:
             _lib.call("skyrx_score", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
