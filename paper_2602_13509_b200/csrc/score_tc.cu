@@ -68,11 +68,54 @@ __device__ __forceinline__ void store_split8(const float* dv, uint8_t* hi, uint8
   *reinterpret_cast<uint4*>(lo) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
 }
 
+// One pixel row's share (CHT 8-band chunks) of the A operand.
+//   MODE 0: gain 1, no value below dark  d = fma(r, c, -(dark c + mu))
+//   MODE 1: gain 1, clamp                d = max(fma(...), -mu)
+//   MODE 2: per-line gain g              d = max(r c - dark c, 0) / g - mu
+//   MODE 3: odd B (2-byte aligned rows), general formula
+template <int MODE, int CHT>
+__device__ __forceinline__ void transform_row(const uint8_t* rr, const float (&tco)[CHT * 8],
+                                              const float (&toff)[CHT * 8], const float2* nm,
+                                              float g, uint8_t* hi, uint8_t* lo) {
+  const float gi = 1.0f / g;
+#pragma unroll
+  for (int cc = 0; cc < CHT; ++cc) {
+    float rf[8];
+    if (MODE != 3) {  // 4-byte aligned rows: two counts per LDS.32
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(rr + 16 * cc + 4 * q);
+        // exact u16 -> f32 on the ALU pipes: (2^23 + r) - 2^23
+        rf[2 * q] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
+        rf[2 * q + 1] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rf[q] = (float)reinterpret_cast<const uint16_t*>(rr)[8 * cc + q];
+    }
+    float dv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float co = tco[cc * 8 + q], of = toff[cc * 8 + q];
+      if (MODE == 0) {
+        dv[q] = fmaf(rf[q], co, -of);
+      } else if (MODE == 1) {
+        dv[q] = fmaxf(fmaf(rf[q], co, -of), nm[8 * cc + q].x);
+      } else {
+        const float m = nm[8 * cc + q].x;
+        dv[q] = fmaf(fmaxf(fmaf(rf[q], co, -(of + m)), 0.0f), gi, m);
+      }
+    }
+    store_split8(dv, hi + cc * 128, lo + cc * 128);
+  }
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
-  constexpr int CH0 = (NCH + 1) / 2;     // chunks [0, CH0) for h = 0
+  static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
+  constexpr int CH0 = NCH / 2;           // chunks [0, CH0) for h = 0, [CH0, NCH) for h = 1
   constexpr uint32_t A_BYTES = 128u * KP * 2u;
   constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
@@ -170,9 +213,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   } else {  // ------------------------------------------------------------ workers
     const int r = tid & 127;   // pixel row of the tile
     const int h = tid >> 7;    // band half
-    constexpr int CHT = CH0;   // chunks per thread (h = 1 may own one fewer)
+    constexpr int CHT = CH0;   // chunks per thread
     const int c_lo = h ? CH0 : 0;
-    const int nmine = h ? NCH - CH0 : CH0;
     mbar_wait(w_bar, 0);
     // the raw-byte moments pass proved min(raw) >= dark everywhere: skip the clamp
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
@@ -192,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         for (int q = 0; q < 8; ++q) {
           const int k = 8 * (c_lo + cc) + q;
           float co = 0.0f, of = 0.0f;
-          if (cc < nmine && k < B) {
+          if (k < B) {
             const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
             co = __ldg(p.coeff + srow + k);
             of = (float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
@@ -209,7 +251,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       float sum = 0.0f;
 #pragma unroll
       for (int cc = 0; cc < CHT; ++cc) {
-        if (cc >= nmine) continue;  // warp-uniform
         const int c = c_lo + cc;
         uint32_t v[8];
         tmem_ld8(taddr + c * 8, v);
@@ -248,54 +289,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       mbar_wait(&a_empty[as], ((t / kScoreAStages) & 1) ^ 1);
       uint8_t* ahi = a_ring + as * 2 * A_BYTES + (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
       uint8_t* alo = ahi + A_BYTES;
+      uint8_t* hi0 = ahi + c_lo * 128;
+      uint8_t* lo0 = alo + c_lo * 128;
       if (r < ti.rows) {
         const int li = r / ti.w;
         const float g = __ldg(p.gain + ti.line0 + li);
-        const uint8_t* rrow = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2;
-#pragma unroll
-        for (int cc = 0; cc < CHT; ++cc) {
-          if (cc >= nmine) continue;
-          const int c = c_lo + cc;
-          float rf[8];
-          if ((B & 1) == 0) {  // 4-byte aligned rows: two counts per LDS.32
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t v = *reinterpret_cast<const uint32_t*>(rrow + 16 * c + 4 * q);
-              // exact u16 -> f32 without the conversion pipe: 2^23 + r - 2^23
-              rf[2 * q] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
-              rf[2 * q + 1] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              rf[q] = (float)reinterpret_cast<const uint16_t*>(rrow)[8 * c + q];
-          }
-          float dv[8];
-          const float2* nm = mu + 8 * c;
-          if (g == 1.0f && noclamp) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dv[q] = fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]);
-          } else if (g == 1.0f) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              dv[q] = fmaxf(fmaf(rf[q], tco[cc * 8 + q], -toff[cc * 8 + q]), nm[q].x);
-          } else {  // per-line gain: x = max(r c - dark c, 0) / g
-            const float gi = 1.0f / g;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float xc = fmaf(rf[q], tco[cc * 8 + q], -(toff[cc * 8 + q] + nm[q].x));
-              dv[q] = fmaf(fmaxf(xc, 0.0f), gi, nm[q].x);
-            }
-          }
-          store_split8(dv, ahi + c * 128, alo + c * 128);
-        }
+        const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
+        const float2* nm0 = mu + 8 * c_lo;
+        // one uniform mode per row, each a fully unrolled straight-line body
+        if (B & 1) transform_row<3, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
+        else if (g != 1.0f) transform_row<2, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
+        else if (!noclamp) transform_row<1, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
+        else transform_row<0, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
       } else {
 #pragma unroll
         for (int cc = 0; cc < CHT; ++cc) {
-          if (cc >= nmine) continue;
-          const int c = c_lo + cc;
-          *reinterpret_cast<uint4*>(ahi + c * 128) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(alo + c * 128) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(hi0 + cc * 128) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(lo0 + cc * 128) = make_uint4(0, 0, 0, 0);
         }
       }
       fence_async_smem();
