@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers);
     for (int s = 0; s < kScoreAStages; ++s)
       mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers);
+    // each accumulator is drained by one worker half (128 threads)
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers / 2);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
@@ -223,11 +224,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     // to the same sample of the current block, so these change only with the block.
     //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
     float tco[CHT * 8], toff[CHT * 8];
-    int cur_block = -1, cur_w = -1;
     uint32_t local_max = 0;
-    auto load_row_tables = [&](const TileInfo& ti) {
-      const int j = r % ti.w;
-      const int64_t srow = (int64_t)(ti.s0 + j) * B;
+    auto load_row_tables = [&](const TileInfo& tb) {
+      const int j = r % tb.w;
+      const int64_t srow = (int64_t)(tb.s0 + j) * B;
 #pragma unroll
       for (int cc = 0; cc < CHT; ++cc)
 #pragma unroll
@@ -243,45 +243,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
           toff[cc * 8 + q] = of;
         }
     };
-    auto epilogue = [&](int t, const TileInfo& ti) {
+    // epilogue of tile t by the worker half h == t & 1, full row each: no
+    // cross-half exchange, no block-wide barrier per tile
+    auto epilogue = [&](int t, float* out, bool valid) {
+      if (h != (t & 1)) return;  // warp-uniform
       const int acs = t & 1;
       mbar_wait(&acc_full[acs], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + acs * NP;
-      float sum = 0.0f;
+      float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
-      for (int cc = 0; cc < CHT; ++cc) {
-        const int c = c_lo + cc;
-        uint32_t v[8];
-        tmem_ld8(taddr + c * 8, v);
+      for (int c = 0; c < NCH; c += 2) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c * 8, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float z = __uint_as_float(v[q]);
-          sum = fmaf(z, z, sum);
+        for (int q = 0; q < 16; q += 2) {
+          s0 = fmaf(__uint_as_float(v[q]), __uint_as_float(v[q]), s0);
+          s1 = fmaf(__uint_as_float(v[q + 1]), __uint_as_float(v[q + 1]), s1);
         }
       }
-      sum *= wscale * wscale;
       tc_fence_before();
       mbar_arrive(&acc_empty[acs]);
-      float* rb = red + (t & 1) * 128;
-      if (h) rb[r] = sum;
-      named_sync(2, kTcWorkers);
-      if (!h && r < ti.rows) {
-        sum += rb[r];
-        const int li = r / ti.w;
-        const int j = r - li * ti.w;
-        p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + j] = sum;
+      if (valid) {
+        const float sum = (s0 + s1) * (wscale * wscale);
+        *out = sum;
         local_max = max(local_max, f2ord(sum));
       }
     };
-    TileInfo prev{};
+    // incremental walk over this CTA's contiguous tile range
+    TileInfo ti = tile_info(p.ts, it0);
+    int li = r / ti.w, jr = r - li * ti.w;
+    if (n > 0) load_row_tables(ti);
+    float* prev_out = nullptr;
+    bool prev_valid = false;
     for (int t = 0; t < n; ++t) {
-      const TileInfo ti = tile_info(p.ts, it0 + t);
-      if (ti.block != cur_block || ti.w != cur_w) {
-        load_row_tables(ti);
-        cur_block = ti.block;
-        cur_w = ti.w;
+      if (t > 0) {
+        const int ob = ti.block;
+        tile_advance(p.ts, ti);
+        if (ti.block != ob) {
+          li = r / ti.w;
+          jr = r - li * ti.w;
+          load_row_tables(ti);
+        }
       }
       const int s = t % kScoreRawStages;
       const int as = t % kScoreAStages;
@@ -291,8 +295,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       uint8_t* alo = ahi + A_BYTES;
       uint8_t* hi0 = ahi + c_lo * 128;
       uint8_t* lo0 = alo + c_lo * 128;
-      if (r < ti.rows) {
-        const int li = r / ti.w;
+      const bool valid = r < ti.rows;
+      float* out = p.scores + (ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + jr;
+      if (valid) {
         const float g = __ldg(p.gain + ti.line0 + li);
         const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
         const float2* nm0 = mu + 8 * c_lo;
@@ -311,10 +316,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       fence_async_smem();
       mbar_arrive(&a_full[as]);
       mbar_arrive(&raw_empty[s]);
-      if (t > 0) epilogue(t - 1, prev);
-      prev = ti;
+      if (t > 0) epilogue(t - 1, prev_out, prev_valid);
+      prev_out = out;
+      prev_valid = valid;
     }
-    if (n > 0) epilogue(n - 1, prev);
+    if (n > 0) epilogue(n - 1, prev_out, prev_valid);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));

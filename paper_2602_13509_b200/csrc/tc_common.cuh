@@ -64,4 +64,21 @@ __host__ __device__ __forceinline__ TileInfo tile_info(const TileSched& t, int64
   return ti;
 }
 
+// next tile in item order (same order as tile_info): down the lines of the
+// current block, then the next block — no divisions on the per-tile path
+__host__ __device__ __forceinline__ void tile_advance(const TileSched& t, TileInfo& ti) {
+  if (ti.line0 + ti.r < t.L) {
+    ti.line0 += ti.r;
+  } else {
+    ti.block += 1;
+    ti.s0 += t.W;
+    ti.line0 = 0;
+    const bool last = ti.block == t.nb - 1;
+    ti.w = last ? t.wl : t.W;
+    ti.r = last ? t.rl : t.R;
+  }
+  ti.nlines = t.L - ti.line0 < ti.r ? t.L - ti.line0 : ti.r;
+  ti.rows = (int32_t)(ti.nlines * ti.w);
+}
+
 }  // namespace skyrx
