@@ -26,12 +26,8 @@
 namespace skyrx {
 using namespace umma;
 
-// Worker layout: NCH/2 groups of 128 threads; thread (group g, row r) owns the
-// two 8-band chunks [2g, 2g+2) of pixel row r.  KP = 80 -> 5 groups, 20 worker
-// warps (+ TMA + MMA warps): enough resident warps to hide smem/TMEM latency.
-__host__ __device__ constexpr int tc_groups(int kp) { return kp / 16; }
-__host__ __device__ constexpr int tc_workers(int kp) { return 128 * tc_groups(kp); }
-__host__ __device__ constexpr int tc_threads(int kp) { return tc_workers(kp) + 64; }
+constexpr int kTcThreads = 320;
+constexpr int kTcWorkers = 256;
 constexpr int kScoreRawStages = 3;
 constexpr int kScoreAStages = 2;
 constexpr int kScoreWmax = 32;
@@ -115,13 +111,11 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float (&t
 }
 
 template <int KP>
-__global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcParams p) {
-  constexpr int kTcWorkers = tc_workers(KP);
-  constexpr int kTmaWarp = kTcWorkers / 32, kMmaWarp = kTmaWarp + 1;
+__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
   static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
-  constexpr int NGRP = tc_groups(KP);     // worker groups, 2 chunks each
+  constexpr int CH0 = NCH / 2;           // chunks [0, CH0) for h = 0, [CH0, NCH) for h = 1
   constexpr uint32_t A_BYTES = 128u * KP * 2u;
   constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
@@ -159,11 +153,11 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
     for (int s = 0; s < kScoreAStages; ++s)
       mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
     // each accumulator is drained by one worker half (128 threads)
-    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 128);
+    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers / 2);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 9) tmem_alloc(tmem_slot, TMEM_COLS);
   // mu[k].x = f32(-mu_k): clamp floor of the centred value, read as a warp broadcast
   for (int k = tid; k < KP; k += blockDim.x)
     mu[k] = k < B ? make_float2((float)(-((double)p.mu_hilo[k] + (double)p.mu_hilo[B + k])), 0.0f)
@@ -173,7 +167,7 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kTmaWarp) {
+  if (warp == 8) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       const uint32_t wb = wpack_bytes_for(KP);
       mbar_arrive_expect_tx(w_bar, wb);
@@ -191,7 +185,7 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == 9) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       mbar_wait(w_bar, 0);
       constexpr uint32_t idesc = idesc_f16_f32(128, NP, 0, 0);
@@ -219,9 +213,9 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
     }
   } else {  // ------------------------------------------------------------ workers
     const int r = tid & 127;   // pixel row of the tile
-    const int h = tid >> 7;    // worker group
-    constexpr int CHT = 2;     // chunks per thread
-    const int c_lo = 2 * h;
+    const int h = tid >> 7;    // band half
+    constexpr int CHT = CH0;   // chunks per thread
+    const int c_lo = h ? CH0 : 0;
     mbar_wait(w_bar, 0);
     // the raw-byte moments pass proved min(raw) >= dark everywhere: skip the clamp
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
@@ -252,7 +246,7 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
     // epilogue of tile t by the worker half h == t & 1, full row each: no
     // cross-half exchange, no block-wide barrier per tile
     auto epilogue = [&](int t, float* out, bool valid) {
-      if (h != t % NGRP) return;  // warp-uniform: groups take turns
+      if (h != (t & 1)) return;  // warp-uniform
       const int acs = t & 1;
       mbar_wait(&acc_full[acs], (t >> 1) & 1);
       tc_fence_after();
@@ -335,7 +329,7 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 9) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 // W (f64, row-major B x B, lower) -> f16 hi/lo K-major B operand + column scales
@@ -386,7 +380,7 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   if (grid < 1) return SKYRX_OK;
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  score_tc_kernel<KP><<<grid, tc_threads(KP), smem, st>>>(p);
+  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
   SKYRX_CHECK_LAUNCH("score_tc_kernel");
   return SKYRX_OK;
 }
