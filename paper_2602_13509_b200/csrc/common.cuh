@@ -18,6 +18,7 @@
 namespace skyrx {
 
 constexpr int kSMs = 148;
+constexpr size_t kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 
 // ------------------------------------------------------------------ errors
 void set_error(const char* fmt, ...);

@@ -26,11 +26,22 @@
 namespace skyrx {
 using namespace umma;
 
-constexpr int kTcThreads = 320;
-constexpr int kTcWorkers = 256;
-constexpr int kScoreRawStages = 3;
-constexpr int kScoreAStages = 2;
-constexpr int kScoreWmax = 32;
+// Worker layout: KP/16 groups of 128 threads; thread (group g, row r) owns the
+// two 8-band chunks [2g, 2g+2) of pixel row r.  KP = 80 -> 5 groups, 20 worker
+// warps (+ TMA + MMA warps): enough resident warps to hide smem/TMEM latency.
+#ifndef SKYRX_SCORE_GROUPS
+#define SKYRX_SCORE_GROUPS 2
+#endif
+__host__ __device__ constexpr int tc_groups(int kp) {
+  return (kp / 8) % SKYRX_SCORE_GROUPS == 0 ? SKYRX_SCORE_GROUPS : 2;
+}
+__host__ __device__ constexpr int tc_workers(int kp) { return 128 * tc_groups(kp); }
+__host__ __device__ constexpr int tc_threads(int kp) { return tc_workers(kp) + 64; }
+constexpr int kScoreRawStagesMax = 8;
+constexpr int kScoreAStages = 3;
+constexpr int kScoreAcc = 3;    // TMEM accumulators
+constexpr int kScoreLag = 2;    // the epilogue of tile t runs after the transform of tile t + kScoreLag
+constexpr int kScoreWmax = 128;
 
 struct ScoreTcParams {
   const uint16_t* raw;
@@ -44,6 +55,7 @@ struct ScoreTcParams {
   const int32_t* flags;  // moments-pass flags: (flags & 12) == 8 -> no value below dark
   TileSched ts;
   uint32_t raw_stage_bytes;
+  int nraw;   // raw ring depth (as many stages as shared memory allows, <= kScoreRawStagesMax)
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -54,13 +66,44 @@ __host__ __device__ constexpr uint32_t wpack_bytes_for(int kp) {
   return 2u * kp * kp * 2u + kp * 4u;
 }
 
-__device__ __forceinline__ void store_split8(const float* dv, uint8_t* hi, uint8_t* lo) {
+// packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes per instruction,
+// each lane rounded exactly like the scalar fmaf / __fadd_rn
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+// 8 centred values -> f16 hi (round to nearest) + f16 lo (the exact f32 residual, rounded)
+__device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint8_t* hi, uint8_t* lo) {
   uint32_t hw[4], lw[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const __half2 h = __floats2half2_rn(dv[2 * q], dv[2 * q + 1]);
-    const float2 hf = __half22float2(h);
-    const __half2 l = __floats2half2_rn(dv[2 * q] - hf.x, dv[2 * q + 1] - hf.y);
+    const __half2 h = __floats2half2_rn(dv[q].x, dv[q].y);
+    const float2 res = fsub2(dv[q], __half22float2(h));
+    const __half2 l = __floats2half2_rn(res.x, res.y);
     hw[q] = *reinterpret_cast<const uint32_t*>(&h);
     lw[q] = *reinterpret_cast<const uint32_t*>(&l);
   }
@@ -68,42 +111,49 @@ __device__ __forceinline__ void store_split8(const float* dv, uint8_t* hi, uint8
   *reinterpret_cast<uint4*>(lo) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
 }
 
-// One pixel row's share (CHT 8-band chunks) of the A operand.
-//   MODE 0: gain 1, no value below dark  d = fma(r, c, -(dark c + mu))
-//   MODE 1: gain 1, clamp                d = max(fma(...), -mu)
+// One pixel row's share (CHT 8-band chunks) of the A operand.  Per band pair
+// (tco = coeff, tnof = -(dark*coeff + mu) in registers, nm = -mu broadcast):
+//   MODE 0: gain 1, no value below dark  d = fma(r, c, nof)
+//   MODE 1: gain 1, clamp                d = max(fma(r, c, nof), -mu)
 //   MODE 2: per-line gain g              d = max(r c - dark c, 0) / g - mu
 //   MODE 3: odd B (2-byte aligned rows), general formula
 template <int MODE, int CHT>
-__device__ __forceinline__ void transform_row(const uint8_t* rr, const float (&tco)[CHT * 8],
-                                              const float (&toff)[CHT * 8], const float2* nm,
+__device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&tco)[CHT * 4],
+                                              const float2 (&tnof)[CHT * 4], const float2* nm,
                                               float g, uint8_t* hi, uint8_t* lo) {
   const float gi = 1.0f / g;
+  const float2 bias = make_float2(-8388608.0f, -8388608.0f);
 #pragma unroll
   for (int cc = 0; cc < CHT; ++cc) {
-    float rf[8];
+    float2 rf[4];
     if (MODE != 3) {  // 4-byte aligned rows: two counts per LDS.32
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t v = *reinterpret_cast<const uint32_t*>(rr + 16 * cc + 4 * q);
         // exact u16 -> f32 on the ALU pipes: (2^23 + r) - 2^23
-        rf[2 * q] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
-        rf[2 * q + 1] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
+        rf[q] = fadd2(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)),
+                                  __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632))),
+                      bias);
       }
     } else {
+      const uint16_t* r16 = reinterpret_cast<const uint16_t*>(rr) + 8 * cc;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) rf[q] = (float)reinterpret_cast<const uint16_t*>(rr)[8 * cc + q];
+      for (int q = 0; q < 4; ++q) rf[q] = make_float2((float)r16[2 * q], (float)r16[2 * q + 1]);
     }
-    float dv[8];
+    float2 dv[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float co = tco[cc * 8 + q], of = toff[cc * 8 + q];
+    for (int q = 0; q < 4; ++q) {
+      const float2 co = tco[cc * 4 + q], nof = tnof[cc * 4 + q];
       if (MODE == 0) {
-        dv[q] = fmaf(rf[q], co, -of);
+        dv[q] = ffma2(rf[q], co, nof);
       } else if (MODE == 1) {
-        dv[q] = fmaxf(fmaf(rf[q], co, -of), nm[8 * cc + q].x);
+        const float2 d = ffma2(rf[q], co, nof);
+        dv[q] = make_float2(fmaxf(d.x, nm[8 * cc + 2 * q].x), fmaxf(d.y, nm[8 * cc + 2 * q + 1].x));
       } else {
-        const float m = nm[8 * cc + q].x;
-        dv[q] = fmaf(fmaxf(fmaf(rf[q], co, -(of + m)), 0.0f), gi, m);
+        const float m0 = nm[8 * cc + 2 * q].x, m1 = nm[8 * cc + 2 * q + 1].x;
+        const float2 d = ffma2(rf[q], co, make_float2(nof.x - m0, nof.y - m1));
+        dv[q] = ffma2(make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f)), make_float2(gi, gi),
+                      make_float2(m0, m1));
       }
     }
     store_split8(dv, hi + cc * 128, lo + cc * 128);
@@ -111,53 +161,59 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float (&t
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
+__global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcParams p) {
+  constexpr int kTcWorkers = tc_workers(KP);
+  constexpr int kTmaWarp = kTcWorkers / 32, kMmaWarp = kTmaWarp + 1;
+  constexpr int NGRP = tc_groups(KP);     // worker groups, 2 chunks each
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
-  static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
-  constexpr int CH0 = NCH / 2;           // chunks [0, CH0) for h = 0, [CH0, NCH) for h = 1
+  static_assert(KP % 16 == 0, "KP is a multiple of 16: every group owns 2 chunks");
   constexpr uint32_t A_BYTES = 128u * KP * 2u;
   constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
   constexpr uint32_t SBO_B = (KP / 8) * 128u;
-  constexpr uint32_t TMEM_COLS = 2 * NP <= 128 ? 128 : 256;
+  constexpr uint32_t TMEM_COLS = kScoreAcc * NP <= 128 ? 128 : 256;
+  static_assert(kScoreAcc * NP <= 256, "accumulators fit 256 TMEM columns");
+  static_assert(kScoreAcc >= kScoreLag + 1, "epilogue lag needs lag + 1 accumulators");
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.ts.B;
   uint8_t* raw_ring = sm;
-  uint8_t* a_ring = raw_ring + kScoreRawStages * p.raw_stage_bytes;
+  const int NR = p.nraw;
+  uint8_t* a_ring = raw_ring + NR * p.raw_stage_bytes;
   uint8_t* wsm = a_ring + kScoreAStages * 2 * A_BYTES;
   float* colscale = reinterpret_cast<float*>(wsm + 2 * W_BYTES);
-  float2* tab = reinterpret_cast<float2*>(colscale + NP);   // [Wmax][B+1] {dark, coeff}
-  float2* mu = tab + kScoreWmax * (B + 1);                 // [KP] {hi, lo}
-  float* red = reinterpret_cast<float*>(mu + KP);          // [2][128] partial sums
+  float2* mu = reinterpret_cast<float2*>(colscale + NP);   // [KP] {-mu, 0}
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(red + 256) + 7) & ~uintptr_t(7));
+      (reinterpret_cast<uintptr_t>(mu + KP) + 7) & ~uintptr_t(7));
   uint64_t* raw_full = bars;
-  uint64_t* raw_empty = raw_full + kScoreRawStages;
-  uint64_t* a_full = raw_empty + kScoreRawStages;
+  uint64_t* raw_empty = raw_full + kScoreRawStagesMax;
+  uint64_t* a_full = raw_empty + kScoreRawStagesMax;
   uint64_t* a_empty = a_full + kScoreAStages;
   uint64_t* acc_full = a_empty + kScoreAStages;
-  uint64_t* acc_empty = acc_full + 2;
-  uint64_t* w_bar = acc_empty + 2;
+  uint64_t* acc_empty = acc_full + kScoreAcc;
+  uint64_t* w_bar = acc_empty + kScoreAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int64_t it0 = (int64_t)blockIdx.x * p.ts.items / gridDim.x;
-  const int64_t it1 = (int64_t)(blockIdx.x + 1) * p.ts.items / gridDim.x;
-  const int n = (int)(it1 - it0);
+  // round-robin tiles: the CTAs sweep the cube together, so at any moment they
+  // read neighbouring lines of one sample block (DRAM pages / TLB locality)
+  const int64_t it0 = blockIdx.x;
+  const int64_t istep = gridDim.x;
+  const int n = it0 < p.ts.items ? (int)((p.ts.items - 1 - it0) / istep + 1) : 0;
 
   if (tid == 0) {
-    for (int s = 0; s < kScoreRawStages; ++s)
-      mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers);
+    for (int s = 0; s < NR; ++s)
+      mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers / 32);
     for (int s = 0; s < kScoreAStages; ++s)
-      mbar_init(&a_full[s], kTcWorkers), mbar_init(&a_empty[s], 1);
+      mbar_init(&a_full[s], kTcWorkers / 32), mbar_init(&a_empty[s], 1);
     // each accumulator is drained by one worker half (128 threads)
-    for (int s = 0; s < 2; ++s) mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcWorkers / 2);
+    for (int s = 0; s < kScoreAcc; ++s)
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 4);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, TMEM_COLS);
   // mu[k].x = f32(-mu_k): clamp floor of the centred value, read as a warp broadcast
   for (int k = tid; k < KP; k += blockDim.x)
     mu[k] = k < B ? make_float2((float)(-((double)p.mu_hilo[k] + (double)p.mu_hilo[B + k])), 0.0f)
@@ -167,15 +223,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       const uint32_t wb = wpack_bytes_for(KP);
       mbar_arrive_expect_tx(w_bar, wb);
       bulk_g2s(wsm, p.wpack, wb, w_bar);
+      int s = 0;
+      uint32_t ph = 0;
+      TileInfo ti = tile_info(p.ts, it0);
+      int64_t g = ti.line0 / ti.r;
       for (int t = 0; t < n; ++t) {
-        const int s = t % kScoreRawStages;
-        mbar_wait(&raw_empty[s], ((t / kScoreRawStages) & 1) ^ 1);
-        const TileInfo ti = tile_info(p.ts, it0 + t);
+        if (t > 0) tile_step(p.ts, ti, g, istep);
+        mbar_wait(&raw_empty[s], ph ^ 1);
         const uint32_t seg = (uint32_t)ti.w * B * 2u;
         mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)ti.nlines);
         uint8_t* dst = raw_ring + s * p.raw_stage_bytes;
@@ -183,17 +242,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
           const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
           bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
         }
+        if (++s == NR) s = 0, ph ^= 1;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       mbar_wait(w_bar, 0);
       constexpr uint32_t idesc = idesc_f16_f32(128, NP, 0, 0);
+      int as = 0, acs = 0;
+      uint32_t aph = 0, cph = 0;
       for (int t = 0; t < n; ++t) {
-        const int as = t % kScoreAStages;
-        const int acs = t & 1;
-        mbar_wait(&a_full[as], (t / kScoreAStages) & 1);
-        mbar_wait(&acc_empty[acs], ((t >> 1) & 1) ^ 1);
+        mbar_wait(&a_full[as], aph);
+        mbar_wait(&acc_empty[acs], cph ^ 1);
         tc_fence_after();
         const uint8_t* abase = a_ring + as * 2 * A_BYTES;
         const uint32_t d = tmem + acs * NP;
@@ -209,13 +269,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         }
         mma_commit(&a_empty[as]);
         mma_commit(&acc_full[acs]);
+        if (++as == kScoreAStages) as = 0, aph ^= 1;
+        if (++acs == kScoreAcc) acs = 0, cph ^= 1;
       }
     }
   } else {  // ------------------------------------------------------------ workers
     const int r = tid & 127;   // pixel row of the tile
-    const int h = tid >> 7;    // band half
-    constexpr int CHT = CH0;   // chunks per thread
-    const int c_lo = h ? CH0 : 0;
+    const int h = tid >> 7;    // worker group
+    const int lane = tid & 31;
+    constexpr int CHT = NCH / NGRP;  // chunks per thread
+    const int c_lo = CHT * h;
     mbar_wait(w_bar, 0);
     // the raw-byte moments pass proved min(raw) >= dark everywhere: skip the clamp
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
@@ -223,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     // calibration of this thread's row, kept in registers: a tile row always maps
     // to the same sample of the current block, so these change only with the block.
     //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
-    float tco[CHT * 8], toff[CHT * 8];
+    float2 tco[CHT * 4], tnof[CHT * 4];
     uint32_t local_max = 0;
     auto load_row_tables = [&](const TileInfo& tb) {
       const int j = r % tb.w;
@@ -233,22 +296,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int k = 8 * (c_lo + cc) + q;
-          float co = 0.0f, of = 0.0f;
+          float co = 0.0f, nof = 0.0f;
           if (k < B) {
             const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
             co = __ldg(p.coeff + srow + k);
-            of = (float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
+            nof = -(float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
           }
-          tco[cc * 8 + q] = co;
-          toff[cc * 8 + q] = of;
+          float* c2 = reinterpret_cast<float*>(&tco[cc * 4 + q / 2]);
+          float* o2 = reinterpret_cast<float*>(&tnof[cc * 4 + q / 2]);
+          c2[q & 1] = co;
+          o2[q & 1] = nof;
         }
     };
     // epilogue of tile t by the worker half h == t & 1, full row each: no
     // cross-half exchange, no block-wide barrier per tile
     auto epilogue = [&](int t, float* out, bool valid) {
-      if (h != (t & 1)) return;  // warp-uniform
-      const int acs = t & 1;
-      mbar_wait(&acc_full[acs], (t >> 1) & 1);
+      if (h != t % NGRP) return;  // warp-uniform: groups take turns
+      const int acs = t % kScoreAcc;
+      mbar_wait(&acc_full[acs], (t / kScoreAcc) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + acs * NP;
       float s0 = 0.0f, s1 = 0.0f;
@@ -264,48 +329,52 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_empty[acs]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acs]);  // one arrival per warp
       if (valid) {
         const float sum = (s0 + s1) * (wscale * wscale);
         *out = sum;
         local_max = max(local_max, f2ord(sum));
       }
     };
-    // incremental walk over this CTA's contiguous tile range
+    // incremental walk over this CTA's round-robin tiles
     TileInfo ti = tile_info(p.ts, it0);
+    int64_t gt = ti.line0 / ti.r;
     int li = r / ti.w, jr = r - li * ti.w;
     if (n > 0) load_row_tables(ti);
-    float* prev_out = nullptr;
-    bool prev_valid = false;
+    // outputs of the tiles whose epilogue is still pending (ring of kScoreLag)
+    float* pend_out[kScoreLag];
+    bool pend_valid[kScoreLag];
+    int s = 0, as = 0;
+    uint32_t ph = 0, aph = 0;
     for (int t = 0; t < n; ++t) {
       if (t > 0) {
         const int ob = ti.block;
-        tile_advance(p.ts, ti);
+        tile_step(p.ts, ti, gt, istep);
         if (ti.block != ob) {
           li = r / ti.w;
           jr = r - li * ti.w;
           load_row_tables(ti);
         }
       }
-      const int s = t % kScoreRawStages;
-      const int as = t % kScoreAStages;
-      mbar_wait(&raw_full[s], (t / kScoreRawStages) & 1);
-      mbar_wait(&a_empty[as], ((t / kScoreAStages) & 1) ^ 1);
+      const bool valid = r < ti.rows;
+      // the line gain is fetched before the barrier waits so its latency hides behind them
+      const float g = (valid && p.gain) ? __ldg(p.gain + ti.line0 + li) : 1.0f;
+      mbar_wait(&raw_full[s], ph);
+      mbar_wait(&a_empty[as], aph ^ 1);
       uint8_t* ahi = a_ring + as * 2 * A_BYTES + (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
       uint8_t* alo = ahi + A_BYTES;
       uint8_t* hi0 = ahi + c_lo * 128;
       uint8_t* lo0 = alo + c_lo * 128;
-      const bool valid = r < ti.rows;
       float* out = p.scores + (ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + jr;
       if (valid) {
-        const float g = __ldg(p.gain + ti.line0 + li);
         const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
         const float2* nm0 = mu + 8 * c_lo;
         // one uniform mode per row, each a fully unrolled straight-line body
-        if (B & 1) transform_row<3, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
-        else if (g != 1.0f) transform_row<2, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
-        else if (!noclamp) transform_row<1, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
-        else transform_row<0, CHT>(rr, tco, toff, nm0, g, hi0, lo0);
+        if (B & 1) transform_row<3, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
+        else if (g != 1.0f) transform_row<2, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
+        else if (!noclamp) transform_row<1, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
+        else transform_row<0, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
       } else {
 #pragma unroll
         for (int cc = 0; cc < CHT; ++cc) {
@@ -314,13 +383,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
         }
       }
       fence_async_smem();
-      mbar_arrive(&a_full[as]);
-      mbar_arrive(&raw_empty[s]);
-      if (t > 0) epilogue(t - 1, prev_out, prev_valid);
-      prev_out = out;
-      prev_valid = valid;
+      __syncwarp();
+      if (lane == 0) {  // one arrival per warp
+        mbar_arrive(&a_full[as]);
+        mbar_arrive(&raw_empty[s]);
+      }
+      if (++s == NR) s = 0, ph ^= 1;
+      if (++as == kScoreAStages) as = 0, aph ^= 1;
+      // compile-time ring slots: t % kScoreLag via a small unrolled select
+#pragma unroll
+      for (int q = 0; q < kScoreLag; ++q)
+        if (q == t % kScoreLag) {
+          if (t >= kScoreLag) epilogue(t - kScoreLag, pend_out[q], pend_valid[q]);
+          pend_out[q] = out;
+          pend_valid[q] = valid;
+        }
     }
-    if (n > 0) epilogue(n - 1, prev_out, prev_valid);
+    for (int t = n - kScoreLag > 0 ? n - kScoreLag : 0; t < n; ++t) {
+#pragma unroll
+      for (int q = 0; q < kScoreLag; ++q)
+        if (q == t % kScoreLag) epilogue(t, pend_out[q], pend_valid[q]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
@@ -329,7 +412,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, TMEM_COLS);
 }
 
 // W (f64, row-major B x B, lower) -> f16 hi/lo K-major B operand + column scales
@@ -372,15 +455,23 @@ template <int KP>
 static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
   const size_t A_BYTES = 128u * KP * 2u;
-  const size_t smem = kScoreRawStages * (size_t)p.raw_stage_bytes + kScoreAStages * 2 * A_BYTES +
-                      wpack_bytes_for(KP) + (size_t)kScoreWmax * (p.ts.B + 1) * 8 + KP * 8 +
-                      256 * 4 + 16 * 8 + 64;
+  const size_t fixed = kScoreAStages * 2 * A_BYTES + wpack_bytes_for(KP) + KP * 8 +
+                       (2 * kScoreRawStagesMax + 2 * kScoreAStages + 5) * 8 + 16 + 64;
+  int nraw = (int)((kSmemMax - fixed) / p.raw_stage_bytes);
+  if (nraw > kScoreRawStagesMax) nraw = kScoreRawStagesMax;
+  if (const char* e = getenv("SKYRX_B200_SCORE_STAGES")) nraw = std::min(nraw, atoi(e));
+  if (nraw < 2) {
+    set_error("score_tc: shared memory too small for B = %d", p.ts.B);
+    return SKYRX_ERR_ARG;
+  }
+  p.nraw = nraw;
+  const size_t smem = fixed + (size_t)nraw * p.raw_stage_bytes;
   int grid = kSMs;
   if (p.ts.items < grid) grid = (int)p.ts.items;
   if (grid < 1) return SKYRX_OK;
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
+  score_tc_kernel<KP><<<grid, tc_threads(KP), smem, st>>>(p);
   SKYRX_CHECK_LAUNCH("score_tc_kernel");
   return SKYRX_OK;
 }

@@ -81,4 +81,24 @@ __host__ __device__ __forceinline__ void tile_advance(const TileSched& t, TileIn
   ti.rows = (int32_t)(ti.nlines * ti.w);
 }
 
+// jump `step` tiles ahead in item order (round-robin schedules); g is the
+// tile's index inside its block and is updated with it
+__host__ __device__ __forceinline__ void tile_step(const TileSched& t, TileInfo& ti, int64_t& g,
+                                                   int64_t step) {
+  g += step;
+  int64_t ngb = ti.block == t.nb - 1 ? t.ngl : t.ng;
+  while (g >= ngb && ti.block < t.nb - 1) {
+    g -= ngb;
+    ti.block += 1;
+    ngb = ti.block == t.nb - 1 ? t.ngl : t.ng;
+  }
+  const bool last = ti.block == t.nb - 1;
+  ti.s0 = ti.block * t.W;
+  ti.w = last ? t.wl : t.W;
+  ti.r = last ? t.rl : t.R;
+  ti.line0 = g * ti.r;
+  ti.nlines = t.L - ti.line0 < ti.r ? t.L - ti.line0 : ti.r;
+  ti.rows = (int32_t)(ti.nlines * ti.w);
+}
+
 }  // namespace skyrx

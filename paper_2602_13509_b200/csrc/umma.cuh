@@ -37,14 +37,27 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // until the phase flips (or the hint expires) instead of spinning through the
 // issue slots the worker warps need (ncu showed 36% of issued instructions in
 // hint-less spin loops of the single-lane producer / MMA threads).
+#ifndef SKYRX_MBAR_HINT
+#define SKYRX_MBAR_HINT 0x989680u
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SKYRX_MBAR_HINT
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
+      "r"(parity), "r"(SKYRX_MBAR_HINT)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ bulk copy (1-D TMA)
