@@ -214,7 +214,7 @@ def main():
     if len(mine) * npix * B * 2 <= 4 * 126e6:
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
-    ev = {"gram": [], "score": []}
+    ev = {"gram": [], "score": [], "kernel": []}
 
     def step(instrument=False):
         if flush is not None:
@@ -232,13 +232,16 @@ def main():
         plan.finalize()
         for j in range(len(mine)):
             d, c = tabs[j]
+            kev = None
             if instrument:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 a.record(stream)
-            plan.score(j, raws[j], d, c, gains)
+            plan.score(j, raws[j], d, c, gains, events=kev)
             if instrument:
                 b.record(stream)
                 ev["score"].append((a, b))
+                ev["kernel"].append(kev)
 
     for _ in range(args.warmup):
         step()
@@ -266,21 +269,21 @@ def main():
     total_px = nstrips * npix * args.steps
     value = total_px / (ms / 1e3)
 
-    # dominant kernel and its roofline (events bracket each launch on `stream`)
-    gram_ms = np.mean([a.elapsed_time(b) for a, b in ev["gram"]])
-    score_ms = np.mean([a.elapsed_time(b) for a, b in ev["score"]])
+    # dominant kernel and its roofline: CUDA events on `stream` around the
+    # fused calibrate+score kernel alone (its algorithmic bytes: 2B raw read +
+    # 4 B f32 delta write per pixel)
+    gram_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["gram"]]))
+    score_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["score"]]))
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["kernel"]]))
     peak, peak_kind = load_peaks()
-    if gram_ms >= score_ms:
-        dom, dom_ms, dom_bytes = "stats (shift+gram_kernel+reduce)", gram_ms, npix * 2 * B
-    else:
-        dom, dom_ms, dom_bytes = ("score (score_kernel+topk+mask)", score_ms,
-                                  npix * (2 * B + 4 + 1) + 3 * 4 * npix)
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    kname = "score_tc_kernel" if plan.tc else "score_kernel"
+    dom_bytes = npix * (2 * B + 4)
+    achieved = dom_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(dom.split()[0])
+            traffic = json.loads(tp.read_text()).get(kname)
         except Exception:
             traffic = None
 
@@ -292,11 +295,11 @@ def main():
         "data": "synthetic (seeded device generator, bit-identical to oracle/synth.py)",
         "config": config_key(args, cfg, world),
         "hbm_fraction_whole_path": value / world * bytes_per_pixel(B) / (peak * 1e9),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
-                     "stats_ms_per_strip": gram_ms, "score_ms_per_strip": score_ms},
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": kern_ms,
+                     "stats_ms_per_strip": gram_ms, "score_path_ms_per_strip": score_ms},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

@@ -459,7 +459,6 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
                        (2 * kScoreRawStagesMax + 2 * kScoreAStages + 5) * 8 + 16 + 64;
   int nraw = (int)((kSmemMax - fixed) / p.raw_stage_bytes);
   if (nraw > kScoreRawStagesMax) nraw = kScoreRawStagesMax;
-  if (const char* e = getenv("SKYRX_B200_SCORE_STAGES")) nraw = std::min(nraw, atoi(e));
   if (nraw < 2) {
     set_error("score_tc: shared memory too small for B = %d", p.ts.B);
     return SKYRX_ERR_ARG;

@@ -386,7 +386,10 @@ class DetectPlan:
             self.launches += 1
         return self
 
-    def score(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None):
+    def score(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
+              events=None):
+        """Enqueue scores, top-k threshold and mask of cube i.  ``events`` =
+        (start, end) CUDA events recorded around the score kernel alone."""
         L, S, B = self.shape
         ds = self.ds
         s = _dev.stream_ptr()
@@ -394,6 +397,8 @@ class DetectPlan:
         k = topk_count(n) if k is None else int(k)
         self.max_key[i].zero_()
         sc = self.scores[i]
+        if events is not None:
+            events[0].record()
         if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
             _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
@@ -404,6 +409,8 @@ class DetectPlan:
                       coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
                       ds.whiten[i].data_ptr(), ds.ld, sc.data_ptr(),
                       self.max_key[i:i + 1].data_ptr(), s)
+        if events is not None:
+            events[1].record()
         _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
                   self.topk_ws.data_ptr(), s)
         _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),
@@ -458,4 +465,4 @@ def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
     if on_dev:
         return Detection(ds, plan.scores[0], plan.mask[0].to(torch.bool), thr, mx)
     return Detection(ds.host(0, n), _dev.to_host(plan.scores[0]),
-                     _dev.to_host(plan.mask[0]).astype(bool), thr, mx)
+                     _dev.to_host(plan.mask[0]).view(bool), thr, mx)
