@@ -199,6 +199,18 @@ int skyrx_topk_threshold(const float* v, int64_t n, int64_t k, float* thr, void*
                          void* stream);
 int skyrx_mask_gt(const float* v, int64_t n, const float* thr, uint8_t* mask, void* stream);
 
+/* The same select split into its steps, for a threshold over values spread
+ * across ranks (R-GLOBAL): init with the GLOBAL n and k, then
+ * for digit 0..2: skyrx_topk_hist on the local values, SUM all-reduce of the
+ * skyrx_topk_hist_len() uint32 bins at skyrx_topk_histogram(workspace), and
+ * skyrx_topk_pick (identical on every rank, since the bins are identical).
+ * skyrx_topk_threshold == init + 3 x (hist + pick) on one rank. */
+int skyrx_topk_init(int64_t n_total, int64_t k, void* workspace, void* stream);
+int skyrx_topk_hist(const float* v, int64_t n, int32_t digit, void* workspace, void* stream);
+int skyrx_topk_pick(int32_t digit, void* workspace, float* thr, void* stream);
+uint32_t* skyrx_topk_histogram(void* workspace);
+int32_t skyrx_topk_hist_len(void);
+
 /* ---------------------------------------------------------------- synthetic sensor (bench/test inputs)
  * Bit-identical to oracle/synth.py generate_lines(): raw counts for lines
  * [line0, line0 + nlines) of the seeded scene.  Tables as in SceneTables. */

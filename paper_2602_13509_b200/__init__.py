@@ -34,6 +34,7 @@ from .rx import (
     topk_mask,
     transmit_domain,
 )
+from .stream import ChunkResult, StreamingRX
 
 __version__ = "0.1.0"
 
@@ -42,7 +43,7 @@ __all__ = [
     "band_nearest", "CalibrationTables", "apply_calibration", "bin_bands", "calibrate_bin_rgb",
     "discard_oob_bands", "extract_rgb", "CubeStats", "DetectPlan", "DeviceStats",
     "compute_stats", "detect", "normalize_scores", "rx_scores", "threshold_scores",
-    "topk_mask", "transmit_domain", "install", "__version__",
+    "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install", "__version__",
 ]
 
 

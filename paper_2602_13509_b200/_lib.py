@@ -60,6 +60,11 @@ SIGNATURES = {
     "skyrx_topk_workspace": (sz, []),
     "skyrx_topk_threshold": (C.c_int, [vp, i64, i64, vp, vp, vp]),
     "skyrx_mask_gt": (C.c_int, [vp, i64, vp, vp, vp]),
+    "skyrx_topk_init": (C.c_int, [i64, i64, vp, vp]),
+    "skyrx_topk_hist": (C.c_int, [vp, i64, i32, vp, vp]),
+    "skyrx_topk_pick": (C.c_int, [i32, vp, vp, vp]),
+    "skyrx_topk_histogram": (vp, [vp]),
+    "skyrx_topk_hist_len": (i32, []),
     "skyrx_synth_raw": (C.c_int, [u32, u32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                   i64, i64, vp, vp]),
 }

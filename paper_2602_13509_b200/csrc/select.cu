@@ -203,6 +203,41 @@ extern "C" int skyrx_topk_threshold(const float* v, int64_t n, int64_t k, float*
   return SKYRX_OK;
 }
 
+extern "C" int skyrx_topk_init(int64_t n_total, int64_t k, void* workspace, void* stream) {
+  SKYRX_REQUIRE(n_total >= 0 && k >= 0, "bad top-k arguments n=%lld k=%lld", (long long)n_total,
+                (long long)k);
+  SKYRX_REQUIRE(((uintptr_t)workspace % 16) == 0, "top-k workspace must be 16-B aligned");
+  topk_init_kernel<<<1, 256, 0, as_stream(stream)>>>(
+      n_total, k, reinterpret_cast<TopkState*>(workspace), skyrx_topk_histogram(workspace));
+  SKYRX_CHECK_LAUNCH("skyrx_topk_init");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_topk_hist(const float* v, int64_t n, int32_t digit, void* workspace,
+                               void* stream) {
+  SKYRX_REQUIRE(digit >= 0 && digit < 3 && n >= 0, "bad top-k digit %d / n %lld", digit,
+                (long long)n);
+  if (n == 0) return SKYRX_OK;
+  topk_hist_kernel<<<grid_n(n, 512, 4), 512, 0, as_stream(stream)>>>(
+      v, n, digit, reinterpret_cast<TopkState*>(workspace), skyrx_topk_histogram(workspace));
+  SKYRX_CHECK_LAUNCH("skyrx_topk_hist");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_topk_pick(int32_t digit, void* workspace, float* thr, void* stream) {
+  SKYRX_REQUIRE(digit >= 0 && digit < 3, "bad top-k digit %d", digit);
+  topk_pick_kernel<<<1, 256, 0, as_stream(stream)>>>(
+      digit, reinterpret_cast<TopkState*>(workspace), skyrx_topk_histogram(workspace), thr);
+  SKYRX_CHECK_LAUNCH("skyrx_topk_pick");
+  return SKYRX_OK;
+}
+
+extern "C" uint32_t* skyrx_topk_histogram(void* workspace) {
+  return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(workspace) + 32);
+}
+
+extern "C" int32_t skyrx_topk_hist_len(void) { return kHistBins; }
+
 extern "C" int skyrx_mask_gt(const float* v, int64_t n, const float* thr, uint8_t* mask,
                              void* stream) {
   if (n <= 0) return SKYRX_OK;

@@ -330,6 +330,15 @@ class DetectPlan:
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
             precise: bool = False, force_ffma: bool = False, gain_const: float | None = None):
         """Enqueue the moments of cube i (no host synchronisation)."""
+        return self._moments(i, raw, dark, coeff, gains, precise, force_ffma, gain_const, True)
+
+    def run_moments(self, i: int, raw: torch.Tensor, dark, coeff, gains, precise: bool = False,
+                    force_ffma: bool = False, gain_const: float | None = None):
+        """Moments of cube i about the shift already in ``ds.shift[i]`` (R-GLOBAL:
+        a shift common to every rank's block)."""
+        return self._moments(i, raw, dark, coeff, gains, precise, force_ffma, gain_const, False)
+
+    def _moments(self, i, raw, dark, coeff, gains, precise, force_ffma, gain_const, own_shift):
         L, S, B = self.shape
         ds = self.ds
         s = _dev.stream_ptr()
@@ -343,12 +352,13 @@ class DetectPlan:
         if (self.raw_stats and not precise and gain_const is not None
                 and lib.skyrx_stats_raw_supported(L, S, B, raw.data_ptr())):
             # exact integer byte Grams on the tensor cores (constant line gain)
-            _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            if own_shift:
+                _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
             _lib.call("skyrx_stats_raw", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.raw_ws.data_ptr(), self.raw_ws_bytes, s)
-        elif (self.tc_stats and not precise
+        elif (self.tc_stats and not precise and own_shift
                 and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
             _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
                       self.qinv[i].data_ptr(), s)
@@ -356,7 +366,8 @@ class DetectPlan:
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.tc_ws.data_ptr(), self.tc_ws_bytes, s)
         else:
-            _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            if own_shift:
+                _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
             _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
                       int(precise), ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.ws.data_ptr(), self.ws_bytes, s)
@@ -386,15 +397,33 @@ class DetectPlan:
             self.launches += 1
         return self
 
+    def topk_hist_view(self) -> torch.Tensor:
+        """The radix histogram inside the top-k workspace (int32 view, for all-reduce)."""
+        off = 32 // 4
+        return self.topk_ws[off:off + int(_lib.load().skyrx_topk_hist_len())]
+
     def score(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
               events=None):
         """Enqueue scores, top-k threshold and mask of cube i.  ``events`` =
         (start, end) CUDA events recorded around the score kernel alone."""
         L, S, B = self.shape
-        ds = self.ds
-        s = _dev.stream_ptr()
         n = L * S
         k = topk_count(n) if k is None else int(k)
+        self.score_only(i, raw, dark, coeff, gains, events)
+        s = _dev.stream_ptr()
+        sc = self.scores[i]
+        _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
+                  self.topk_ws.data_ptr(), s)
+        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),
+                  self.mask[i].data_ptr(), s)
+        self.launches += 7 + 1
+        return self
+
+    def score_only(self, i: int, raw: torch.Tensor, dark, coeff, gains, events=None):
+        """Scores of cube i and their max key (no threshold / mask)."""
+        L, S, B = self.shape
+        ds = self.ds
+        s = _dev.stream_ptr()
         self.max_key[i].zero_()
         sc = self.scores[i]
         if events is not None:
@@ -411,11 +440,7 @@ class DetectPlan:
                       self.max_key[i:i + 1].data_ptr(), s)
         if events is not None:
             events[1].record()
-        _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
-                  self.topk_ws.data_ptr(), s)
-        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),
-                  self.mask[i].data_ptr(), s)
-        self.launches += 1 + 7 + 1
+        self.launches += 1
         return self
 
 

@@ -1,0 +1,148 @@
+"""R-STREAM: line-by-line detection with an exponentially forgetting background.
+
+BASELINE config 2 (SURVEY.md §8(a) R-STREAM): 249-line chunks of the 900 x 70
+geometry (1 s at the paper's line rate), background updated
+per chunk with forgetting factor 0.99 and Sigma^-1 recomputed per chunk.  The
+reference has no streaming detector; the frozen definition (and its CPU
+restatement, oracle/skyrx_oracle.py StreamingStats) is:
+
+    state (n, s, Q) in f64 about a fixed shift c (set from chunk 0)
+    per chunk:  n <- lam n + m,  s <- lam s + sum(x - c),  Q <- lam Q + sum((x-c)(x-c)^T)
+    mu = c + s/n,  Sigma = (Q - s s^T / n) / (n - 1)  -> rx.py:68-86 factorisation
+    score the chunk with the stats that already include it; mask = top 0.1 %.
+
+Chunk 0 therefore reduces to compute_stats/rx_scores on chunk 0, which the
+reference pins.  Everything per chunk stays on the device: K2 moments of the
+chunk (f64, the chunk is small), the fold (skyrx_moments_fold), K3 finalize,
+K4 score and the top-k select.  From chunk 1 on the fixed chain is replayed
+from one CUDA graph, so a chunk costs one graph launch plus its copies.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .calibrate import line_gains, tables_of
+from .rx import CubeStats, DetectPlan, key_to_float, topk_count
+
+
+@dataclass
+class ChunkResult:
+    """Scores / mask of one chunk and the background they were scored against."""
+
+    index: int
+    scores: object       # (lines, samples) f32 (numpy for host input, tensor for device input)
+    mask: object         # (lines, samples) bool, top 0.1 % of the chunk
+    threshold: float     # delta_(k+1) of the chunk
+    max_score: float
+    stats: CubeStats | None = None   # host copy, only when update(..., with_stats=True)
+
+
+class StreamingRX:
+    """Per-chunk RX detector with an exponentially forgetting background.
+
+    ``update(raw_chunk)`` takes a RawCube-like object (``values`` u16 (L, S, B),
+    optional line gains) or a bare u16 array / CUDA tensor of one chunk and
+    returns its :class:`ChunkResult`.  Chunks must all have ``chunk_lines``
+    lines (the geometry of the captured graph).
+    """
+
+    def __init__(self, tables, chunk_lines: int = 249, forget: float = 0.99,
+                 k: int | None = None, use_graph: bool = True):
+        self.tables = tables_of(tables)
+        S, B = self.tables.samples, self.tables.bands
+        if not 0.0 < forget <= 1.0:
+            raise ValueError(f"forget factor {forget} outside (0, 1]")
+        self.shape = (chunk_lines, S, B)
+        self.forget = float(forget)
+        self.k = topk_count(chunk_lines * S) if k is None else int(k)
+        self.plan = DetectPlan(chunk_lines, S, B)
+        self.dark, self.coeff = self.tables.device()
+        self.raw = _dev.zeros(self.shape, torch.int16).view(torch.uint16)
+        self.gains = _dev.zeros((chunk_lines,), torch.float32) + 1.0
+        self.chunk_moments = _dev.zeros((int(_lib.load().skyrx_moments_len(B)),),
+                                        torch.float64)
+        self.use_graph = use_graph
+        self.graph = None
+        self.chunks = 0
+
+    # ------------------------------------------------------------------ device chain
+    def _enqueue(self, first: bool):
+        L, S, B = self.shape
+        plan, ds = self.plan, self.plan.ds
+        s = _dev.stream_ptr()
+        args = (self.raw.data_ptr(), L, S, B, self.dark.data_ptr(), self.coeff.data_ptr(),
+                self.gains.data_ptr())
+        ds.flags.zero_()
+        if first:
+            _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(), s)
+        # chunk moments in f64 (a chunk is 224 100 px: the f64 kernel costs ~30 us)
+        _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(), 1,
+                  self.chunk_moments.data_ptr(), ds.flags.data_ptr(), plan.ws.data_ptr(),
+                  plan.ws_bytes, s)
+        _lib.call("skyrx_moments_fold", ds.moments[0].data_ptr(), self.chunk_moments.data_ptr(),
+                  B, self.forget, s)
+        plan.finalize()
+        plan.score(0, self.raw, self.dark, self.coeff, self.gains, self.k)
+
+    def _run(self):
+        if self.chunks == 0:
+            self.plan.ds.moments.zero_()
+            self._enqueue(first=True)
+            return
+        if not self.use_graph:
+            self._enqueue(first=False)
+            return
+        if self.graph is None:
+            # capture the steady-state chain once (shift fixed, buffers static)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._enqueue(first=False)
+            torch.cuda.current_stream().wait_stream(side)
+            self.graph = g
+        self.graph.replay()
+
+    # ------------------------------------------------------------------ public API
+    def update(self, chunk, *, with_stats: bool = False) -> ChunkResult:
+        values = chunk if isinstance(chunk, (torch.Tensor, np.ndarray)) else chunk.values
+        L, S, B = self.shape
+        if tuple(values.shape) != self.shape:
+            raise ValueError(f"chunk shape {tuple(values.shape)} != stream geometry {self.shape}")
+        on_dev = _dev.is_device(values)
+        if isinstance(values, torch.Tensor):
+            self.raw.copy_(values.view(torch.uint16) if values.dtype != torch.uint16 else values,
+                           non_blocking=True)
+        else:
+            a = np.ascontiguousarray(np.asarray(values, np.uint16))
+            self.raw.copy_(torch.from_numpy(a.view(np.int16)).view(torch.uint16),
+                           non_blocking=True)
+        if getattr(chunk, "gains", None) is not None or len(getattr(chunk, "line_meta", ())):
+            g = line_gains(chunk)
+            g = g if isinstance(g, torch.Tensor) else torch.from_numpy(np.asarray(g, np.float32))
+            self.gains.copy_(g, non_blocking=True)
+        else:
+            self.gains.fill_(1.0)
+        self._run()
+        ds = self.plan.ds
+        ds.check(0, L * S)  # synchronises: raises the reference's errors
+        idx = self.chunks
+        self.chunks += 1
+        thr = float(self.plan.thr[0].item())
+        mx = key_to_float(self.plan.max_key[0])
+        stats = ds.host(0, L * S) if with_stats else None
+        if on_dev:
+            return ChunkResult(idx, self.plan.scores[0].clone(),
+                               self.plan.mask[0].to(torch.bool), thr, mx, stats)
+        return ChunkResult(idx, _dev.to_host(self.plan.scores[0]),
+                           _dev.to_host(self.plan.mask[0]).view(bool), thr, mx, stats)
+
+    def reset(self):
+        """Forget the background (the next chunk re-seeds the shift)."""
+        self.chunks = 0
+        self.graph = None
