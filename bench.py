@@ -38,6 +38,8 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
     "c1": dict(lines=2048, samples=900, bands=70, components=5, seed=1, strips=1),
+    "c2": dict(lines=249, samples=900, bands=70, components=5, seed=2, strips=1, chunks=60,
+               forget=0.99),
     "c3": dict(lines=8192, samples=1024, bands=270, components=8, seed=3, strips=1),
     "c4": dict(lines=16384, samples=900, bands=70, components=5, seed=4000, strips=64),
     "c5": dict(lines=131072, samples=2048, bands=128, components=5, seed=5, strips=1),
@@ -168,6 +170,7 @@ def config_key(args, cfg, world):
     lines = args.lines or cfg["lines"]
     strips = args.strips or cfg["strips"]
     return {"workload": {"c1": "single strip 2048x900x70", "c3": "high-band cube 8192x1024x270",
+                         "c2": "streaming 60 x 249-line chunks of 900x70, forgetting 0.99",
                          "c4": "multi-strip batch 64 x (16384x900x70)",
                          "c5": "global mosaic 131072x2048x128"}[args.config]
             + ("" if (args.lines is None and args.strips is None) else " (resized)"),
@@ -187,6 +190,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
+    if args.config == "c2":
+        return run_stream(args, cfg, rank, world, local)
+    if args.config == "c5":
+        return run_global(args, cfg, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -309,6 +316,149 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, raws[0], scenes[0], lines)
     if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- c2: streaming
+def run_stream(args, cfg, rank, world, local):
+    """BASELINE config 2: per-chunk latency and sustained throughput of StreamingRX.
+
+    Replicas only (streaming is single-GPU latency work); every
+    rank runs its own stream, rank 0 reports.  `value` = chunk pixels per
+    second with chunks resident in HBM (device events around K steps of the
+    whole 60-chunk stream); `e2e` = the same through update() on pinned host
+    chunks (H2D, graph replay, D2H of scores + mask, host sync per chunk)."""
+    import torch
+
+    torch.cuda.set_device(local)
+    import paper_2602_13509_b200 as P
+    from paper_2602_13509_b200.stream import StreamingRX
+    from paper_2602_13509_b200.synth import Scene
+
+    L, S, B, nch = cfg["lines"], cfg["samples"], cfg["bands"], cfg["chunks"]
+    sc = Scene(cfg["seed"] + rank, S, B, cfg["components"])
+    tabs = P.CalibrationTables(sc.dark, sc.coeff)
+    raw = sc.generate(0, L * nch)
+    chunks = [raw[i * L:(i + 1) * L] for i in range(nch)]
+    stream = torch.cuda.current_stream()
+
+    def one_pass(srx, src, lat=None):
+        for c in src:
+            if lat is not None:
+                t0 = time.perf_counter()
+            srx.update(c)
+            if lat is not None:
+                lat.append((time.perf_counter() - t0) * 1e3)
+
+    srx = StreamingRX(tabs, L, cfg["forget"])
+    for _ in range(args.warmup):
+        srx.reset()
+        one_pass(srx, chunks)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lat_dev = []
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            srx.reset()
+            one_pass(srx, chunks, lat_dev)
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    px = L * S * nch * args.steps
+    value = px / (ms / 1e3)
+    # e2e: pinned host chunks through the public update()
+    hosts = [c.cpu().pin_memory().numpy() for c in chunks]
+    srx_h = StreamingRX(tabs, L, cfg["forget"])
+    one_pass(srx_h, hosts[:3])
+    lat = []
+    srx_h.reset()
+    t0 = time.perf_counter()
+    one_pass(srx_h, hosts, lat)
+    sec = time.perf_counter() - t0
+    if rank != 0:
+        return
+    pct = lambda a, q: float(np.percentile(a, q))  # noqa: E731
+    line = {
+        "metric": "calibrated+RX-scored pixels/sec", "value": value, "unit": "pixels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 moments, fold and factorisation)",
+        "data": "synthetic (seeded device generator, bit-identical to oracle/synth.py)",
+        "config": config_key(args, cfg, world) | {"parallelism": f"replicas{world}"},
+        "latency_ms_per_chunk": {"device_resident": {"p50": pct(lat_dev, 50),
+                                                     "p99": pct(lat_dev, 99),
+                                                     "max": max(lat_dev)},
+                                 "host_e2e": {"p50": pct(lat, 50), "p99": pct(lat, 99),
+                                              "max": max(lat)},
+                                 "realtime_budget": 1000.0},
+        "gpu_launches": srx.plan.launches // max(1, (args.steps + args.warmup) * nch),
+        "clocks": clocks.summary(),
+        "e2e": {"value": L * S * nch / sec, "unit": "pixels/s",
+                "h2d_bytes_per_step": L * S * B * 2 * nch,
+                "d2h_bytes_per_step": L * S * 5 * nch,
+                "api": "paper_2602_13509_b200.StreamingRX.update(numpy chunk)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- c5: global mosaic
+def run_global(args, cfg, rank, world, local):
+    """BASELINE config 5: one background over line blocks, NCCL all-reduce of
+    FP64 moments + radix histograms (paper_2602_13509_b200/distributed.py).
+    Total work fixed (131072 lines split over the ranks): strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2602_13509_b200 as P
+    from paper_2602_13509_b200.distributed import GlobalRX
+    from paper_2602_13509_b200.synth import Scene
+
+    L = args.lines or cfg["lines"]
+    S, B = cfg["samples"], cfg["bands"]
+    per = L // world
+    sc = Scene(cfg["seed"], S, B, cfg["components"])
+    raw = sc.generate(rank * per, per)
+    tabs = P.CalibrationTables(sc.dark, sc.coeff)
+    g = GlobalRX(per, S, B, tabs, n_total=per * world * S)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        det = g.detect(raw)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            det = g.detect(raw)
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = per * world * S * args.steps / (ms / 1e3)
+    if rank == 0:
+        line = {
+            "metric": "calibrated+RX-scored pixels/sec", "value": value, "unit": "pixels/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (fp64 moments, all-reduce and factorisation)",
+            "data": "synthetic (seeded device generator, bit-identical to oracle/synth.py)",
+            "config": config_key(args, cfg, world) | {"parallelism": f"lineblocks/dp{world}"},
+            "hbm_fraction_whole_path": value / world * bytes_per_pixel(B)
+            / (load_peaks()[0] * 1e9),
+            "global_threshold": det.threshold, "global_max": det.max_score,
+            "gpu_launches": g.ops.plan.launches // max(1, args.steps + args.warmup),
+            "clocks": clocks.summary(),
+        }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
