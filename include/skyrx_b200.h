@@ -163,6 +163,7 @@ int skyrx_score(int32_t kind, const void* pixels, int64_t lines, int32_t samples
  * in the epilogue.  wpack = skyrx_pack_whiten(whiten64) (skyrx_wpack_bytes(B)
  * bytes per matrix).  flags (nullable) = the moments-pass flags word: when it
  * reads 8 (raw-byte path ran, no value below dark) the clamp is skipped.
+ * gain may be NULL: every line gain is 1 (the transform drops the division).
  * skyrx_score_tc_supported() says whether the shape and
  * alignment allow it (every line segment of a tile must be a 16-B multiple). */
 size_t skyrx_wpack_bytes(int32_t bands);

@@ -8,14 +8,14 @@
 // score error 1.6e-6 against the f64 reference (tolerance 1e-4), measured
 // 1.4e-6 on B200 (tools/debug_score.py).
 //
-// Warp roles (persistent CTA, one per SM, 320 threads):
-//   warp 8  TMA producer : raw line segments of each tile -> smem ring (cp.async.bulk)
-//   warp 9  MMA issuer   : 3*KP/16 tcgen05.mma per tile into a double-buffered
-//                          TMEM accumulator (128 lanes = pixels, KP columns)
-//   warps 0-7 workers    : two threads per pixel row (each half of the bands):
-//                          calibrate + centre + f16 split into the K-major A
-//                          operand, then the epilogue of the previous tile
-//                          (tcgen05.ld, unscale, sum of squares, store).
+// Warp roles (persistent CTA, one per SM, 448 threads):
+//   warp 12      TMA producer : raw line segments of each tile -> smem ring (cp.async.bulk)
+//   warp 13      MMA issuer   : 3*KP/16 tcgen05.mma per tile into a 3-deep TMEM
+//                               accumulator ring (128 lanes = pixels, KP columns)
+//   warps 0-7    transform    : two threads per pixel row (each half of the bands):
+//                               calibrate + centre + f16 split into the K-major A operand
+//   warps 8-11   epilogue     : tcgen05.ld, sum of squares (FFMA2), unscale, store, max
+// Tiles are 128 pixels (one line x 128 samples) dealt round-robin to the CTAs.
 // Each worker keeps its row's per-sample calibration constants in registers.
 #include <cuda_fp16.h>
 
@@ -26,21 +26,19 @@
 namespace skyrx {
 using namespace umma;
 
-// Worker layout: KP/16 groups of 128 threads; thread (group g, row r) owns the
-// two 8-band chunks [2g, 2g+2) of pixel row r.  KP = 80 -> 5 groups, 20 worker
-// warps (+ TMA + MMA warps): enough resident warps to hide smem/TMEM latency.
-#ifndef SKYRX_SCORE_GROUPS
-#define SKYRX_SCORE_GROUPS 2
-#endif
-__host__ __device__ constexpr int tc_groups(int kp) {
-  return (kp / 8) % SKYRX_SCORE_GROUPS == 0 ? SKYRX_SCORE_GROUPS : 2;
-}
-__host__ __device__ constexpr int tc_workers(int kp) { return 128 * tc_groups(kp); }
-__host__ __device__ constexpr int tc_threads(int kp) { return tc_workers(kp) + 64; }
+// Warp roles (persistent CTA, one per SM, 448 threads):
+//   warps 0-7   transform : two threads per pixel row (each half of the bands)
+//   warps 8-11  epilogue  : one thread per pixel row (TMEM lane quarter = warp % 4)
+//   warp 12     TMA producer, warp 13 MMA issuer (one elected lane each)
+constexpr int kTcTransform = 256;
+constexpr int kTcEpilogue = 128;
+constexpr int kTcThreads = kTcTransform + kTcEpilogue + 64;
+constexpr int kEpiWarp0 = kTcTransform / 32;           // 8
+constexpr int kTmaWarp = (kTcTransform + kTcEpilogue) / 32;  // 12
+constexpr int kMmaWarp = kTmaWarp + 1;                 // 13
 constexpr int kScoreRawStagesMax = 8;
-constexpr int kScoreAStages = 3;
-constexpr int kScoreAcc = 3;    // TMEM accumulators
-constexpr int kScoreLag = 2;    // the epilogue of tile t runs after the transform of tile t + kScoreLag
+constexpr int kScoreAStages = 2;
+constexpr int kScoreAcc = 3;    // TMEM accumulator ring
 constexpr int kScoreWmax = 128;
 
 struct ScoreTcParams {
@@ -160,21 +158,99 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
   }
 }
 
+// Transform warps: calibrate + centre + f16-split every tile of this CTA into
+// the A ring.  MODE is uniform over the launch (see transform_row).
+template <int KP, int MODE>
+__device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int64_t it0,
+                                               int64_t istep, uint8_t* raw_ring, uint8_t* a_ring,
+                                               const float2* mu, uint64_t* raw_full,
+                                               uint64_t* raw_empty, uint64_t* a_full,
+                                               uint64_t* a_empty) {
+  constexpr int NCH = KP / 8;
+  constexpr int CHT = NCH / 2;  // chunks per thread (row half)
+  constexpr uint32_t A_BYTES = 128u * KP * 2u;
+  constexpr uint32_t SBO_A = (KP / 8) * 128u;
+  const int tid = threadIdx.x;
+  const int r = tid & 127;  // pixel row of the tile
+  const int h = tid >> 7;   // band half
+  const int lane = tid & 31;
+  const int c_lo = CHT * h;
+  const int B = p.ts.B;
+  const int NR = p.nraw;
+  // this row's calibration in registers; a tile row maps to the same sample of
+  // the current block on every tile, so the tables change only with the block
+  float2 tco[CHT * 4], tnof[CHT * 4];
+  auto load_row_tables = [&](const TileInfo& tb) {
+    const int64_t srow = (int64_t)(tb.s0 + r % tb.w) * B;
+#pragma unroll
+    for (int cc = 0; cc < CHT; ++cc)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = 8 * (c_lo + cc) + q;
+        float co = 0.0f, nof = 0.0f;
+        if (k < B) {
+          const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
+          co = __ldg(p.coeff + srow + k);
+          nof = -(float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
+        }
+        float* c2 = reinterpret_cast<float*>(&tco[cc * 4 + q / 2]);
+        float* o2 = reinterpret_cast<float*>(&tnof[cc * 4 + q / 2]);
+        c2[q & 1] = co;
+        o2[q & 1] = nof;
+      }
+  };
+  TileInfo ti = tile_info(p.ts, it0);
+  int64_t gt = ti.line0 / ti.r;
+  if (n > 0) load_row_tables(ti);
+  const uint32_t arow = (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u + c_lo * 128u;
+  const float2* nm0 = mu + 8 * c_lo;
+  int s = 0, as = 0;
+  uint32_t ph = 0, aph = 0;
+  for (int t = 0; t < n; ++t) {
+    if (t > 0) {
+      const int ob = ti.block;
+      tile_step(p.ts, ti, gt, istep);
+      if (ti.block != ob) load_row_tables(ti);
+    }
+    const bool valid = r < ti.rows;
+    float g = 1.0f;
+    if (MODE >= 2 && valid && p.gain) g = __ldg(p.gain + ti.line0 + r / ti.w);
+    mbar_wait(&raw_full[s], ph);
+    mbar_wait(&a_empty[as], aph ^ 1);
+    uint8_t* hi0 = a_ring + as * 2 * A_BYTES + arow;
+    uint8_t* lo0 = hi0 + A_BYTES;
+    if (valid) {
+      const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
+      transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < CHT; ++cc) {
+        *reinterpret_cast<uint4*>(hi0 + cc * 128) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(lo0 + cc * 128) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {  // one arrival per warp
+      mbar_arrive(&a_full[as]);
+      mbar_arrive(&raw_empty[s]);
+    }
+    if (++s == NR) s = 0, ph ^= 1;
+    if (++as == kScoreAStages) as = 0, aph ^= 1;
+  }
+}
+
 template <int KP>
-__global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcParams p) {
-  constexpr int kTcWorkers = tc_workers(KP);
-  constexpr int kTmaWarp = kTcWorkers / 32, kMmaWarp = kTmaWarp + 1;
-  constexpr int NGRP = tc_groups(KP);     // worker groups, 2 chunks each
+__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
-  static_assert(KP % 16 == 0, "KP is a multiple of 16: every group owns 2 chunks");
+  static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
   constexpr uint32_t A_BYTES = 128u * KP * 2u;
   constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
   constexpr uint32_t SBO_B = (KP / 8) * 128u;
   constexpr uint32_t TMEM_COLS = kScoreAcc * NP <= 128 ? 128 : 256;
   static_assert(kScoreAcc * NP <= 256, "accumulators fit 256 TMEM columns");
-  static_assert(kScoreAcc >= kScoreLag + 1, "epilogue lag needs lag + 1 accumulators");
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.ts.B;
   uint8_t* raw_ring = sm;
@@ -204,12 +280,11 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
 
   if (tid == 0) {
     for (int s = 0; s < NR; ++s)
-      mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcWorkers / 32);
+      mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], kTcTransform / 32);
     for (int s = 0; s < kScoreAStages; ++s)
-      mbar_init(&a_full[s], kTcWorkers / 32), mbar_init(&a_empty[s], 1);
-    // each accumulator is drained by one worker half (128 threads)
+      mbar_init(&a_full[s], kTcTransform / 32), mbar_init(&a_empty[s], 1);
     for (int s = 0; s < kScoreAcc; ++s)
-      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], 4);
+      mbar_init(&acc_full[s], 1), mbar_init(&acc_empty[s], kTcEpilogue / 32);
     mbar_init(w_bar, 1);
     fence_mbar_init();
   }
@@ -273,141 +348,65 @@ __global__ void __launch_bounds__(tc_threads(KP), 1) score_tc_kernel(ScoreTcPara
         if (++acs == kScoreAcc) acs = 0, cph ^= 1;
       }
     }
-  } else {  // ------------------------------------------------------------ workers
-    const int r = tid & 127;   // pixel row of the tile
-    const int h = tid >> 7;    // worker group
+  } else if (warp >= kEpiWarp0) {  // ------------------------------------ epilogue
+    const int r = tid & 127;  // pixel row = TMEM lane
     const int lane = tid & 31;
-    constexpr int CHT = NCH / NGRP;  // chunks per thread
-    const int c_lo = CHT * h;
     mbar_wait(w_bar, 0);
-    // the raw-byte moments pass proved min(raw) >= dark everywhere: skip the clamp
-    const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
-    const float wscale = colscale[0];  // one power-of-two scale for all of W
-    // calibration of this thread's row, kept in registers: a tile row always maps
-    // to the same sample of the current block, so these change only with the block.
-    //   d = max(fma(r, coeff, -(dark*coeff + mu)), -mu)  ==  max(r - dark, 0)*coeff - mu
-    float2 tco[CHT * 4], tnof[CHT * 4];
+    const float ws2 = colscale[0] * colscale[0];  // one power-of-two scale for all of W
+    const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     uint32_t local_max = 0;
-    auto load_row_tables = [&](const TileInfo& tb) {
-      const int j = r % tb.w;
-      const int64_t srow = (int64_t)(tb.s0 + j) * B;
-#pragma unroll
-      for (int cc = 0; cc < CHT; ++cc)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int k = 8 * (c_lo + cc) + q;
-          float co = 0.0f, nof = 0.0f;
-          if (k < B) {
-            const double mu_k = (double)p.mu_hilo[k] + (double)p.mu_hilo[B + k];
-            co = __ldg(p.coeff + srow + k);
-            nof = -(float)((double)__ldg(p.dark + srow + k) * (double)co + mu_k);
-          }
-          float* c2 = reinterpret_cast<float*>(&tco[cc * 4 + q / 2]);
-          float* o2 = reinterpret_cast<float*>(&tnof[cc * 4 + q / 2]);
-          c2[q & 1] = co;
-          o2[q & 1] = nof;
-        }
-    };
-    // epilogue of tile t by the worker half h == t & 1, full row each: no
-    // cross-half exchange, no block-wide barrier per tile
-    auto epilogue = [&](int t, float* out, bool valid) {
-      if (h != t % NGRP) return;  // warp-uniform: groups take turns
-      const int acs = t % kScoreAcc;
-      mbar_wait(&acc_full[acs], (t / kScoreAcc) & 1);
+    TileInfo ti = tile_info(p.ts, it0);
+    int64_t gt = ti.line0 / ti.r;
+    int acs = 0;
+    uint32_t cph = 0;
+    for (int t = 0; t < n; ++t) {
+      if (t > 0) tile_step(p.ts, ti, gt, istep);
+      mbar_wait(&acc_full[acs], cph);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + acs * NP;
-      float s0 = 0.0f, s1 = 0.0f;
+      float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int c = 0; c < NCH; c += 2) {
         uint32_t v[16];
-        tmem_ld16(taddr + c * 8, v);
+        tmem_ld16(tbase + acs * NP + c * 8, v);
         tmem_ld_wait();
 #pragma unroll
         for (int q = 0; q < 16; q += 2) {
-          s0 = fmaf(__uint_as_float(v[q]), __uint_as_float(v[q]), s0);
-          s1 = fmaf(__uint_as_float(v[q + 1]), __uint_as_float(v[q + 1]), s1);
+          const float2 z = make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1]));
+          acc = ffma2(z, z, acc);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acs]);  // one arrival per warp
-      if (valid) {
-        const float sum = (s0 + s1) * (wscale * wscale);
-        *out = sum;
+      if (r < ti.rows) {
+        const int li = r / ti.w;
+        const float sum = (acc.x + acc.y) * ws2;
+        p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + (r - li * ti.w)] = sum;
         local_max = max(local_max, f2ord(sum));
       }
-    };
-    // incremental walk over this CTA's round-robin tiles
-    TileInfo ti = tile_info(p.ts, it0);
-    int64_t gt = ti.line0 / ti.r;
-    int li = r / ti.w, jr = r - li * ti.w;
-    if (n > 0) load_row_tables(ti);
-    // outputs of the tiles whose epilogue is still pending (ring of kScoreLag)
-    float* pend_out[kScoreLag];
-    bool pend_valid[kScoreLag];
-    int s = 0, as = 0;
-    uint32_t ph = 0, aph = 0;
-    for (int t = 0; t < n; ++t) {
-      if (t > 0) {
-        const int ob = ti.block;
-        tile_step(p.ts, ti, gt, istep);
-        if (ti.block != ob) {
-          li = r / ti.w;
-          jr = r - li * ti.w;
-          load_row_tables(ti);
-        }
-      }
-      const bool valid = r < ti.rows;
-      // the line gain is fetched before the barrier waits so its latency hides behind them
-      const float g = (valid && p.gain) ? __ldg(p.gain + ti.line0 + li) : 1.0f;
-      mbar_wait(&raw_full[s], ph);
-      mbar_wait(&a_empty[as], aph ^ 1);
-      uint8_t* ahi = a_ring + as * 2 * A_BYTES + (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u;
-      uint8_t* alo = ahi + A_BYTES;
-      uint8_t* hi0 = ahi + c_lo * 128;
-      uint8_t* lo0 = alo + c_lo * 128;
-      float* out = p.scores + (ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + jr;
-      if (valid) {
-        const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
-        const float2* nm0 = mu + 8 * c_lo;
-        // one uniform mode per row, each a fully unrolled straight-line body
-        if (B & 1) transform_row<3, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
-        else if (g != 1.0f) transform_row<2, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
-        else if (!noclamp) transform_row<1, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
-        else transform_row<0, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < CHT; ++cc) {
-          *reinterpret_cast<uint4*>(hi0 + cc * 128) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(lo0 + cc * 128) = make_uint4(0, 0, 0, 0);
-        }
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {  // one arrival per warp
-        mbar_arrive(&a_full[as]);
-        mbar_arrive(&raw_empty[s]);
-      }
-      if (++s == NR) s = 0, ph ^= 1;
-      if (++as == kScoreAStages) as = 0, aph ^= 1;
-      // compile-time ring slots: t % kScoreLag via a small unrolled select
-#pragma unroll
-      for (int q = 0; q < kScoreLag; ++q)
-        if (q == t % kScoreLag) {
-          if (t >= kScoreLag) epilogue(t - kScoreLag, pend_out[q], pend_valid[q]);
-          pend_out[q] = out;
-          pend_valid[q] = valid;
-        }
-    }
-    for (int t = n - kScoreLag > 0 ? n - kScoreLag : 0; t < n; ++t) {
-#pragma unroll
-      for (int q = 0; q < kScoreLag; ++q)
-        if (q == t % kScoreLag) epilogue(t, pend_out[q], pend_valid[q]);
+      if (++acs == kScoreAcc) acs = 0, cph ^= 1;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
-    if ((tid & 31) == 0 && local_max && p.max_key) atomicMax(p.max_key, local_max);
+    if (lane == 0 && local_max && p.max_key) atomicMax(p.max_key, local_max);
+  } else {  // ------------------------------------------------------------ transform
+    mbar_wait(w_bar, 0);
+    // one arithmetic mode for the whole launch (uniform branch):
+    //   odd B -> 3; per-line gains given -> 2; moments pass proved raw >= dark -> 0; else 1
+    const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
+    if (B & 1)
+      transform_loop<KP, 3>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+                            a_empty);
+    else if (p.gain != nullptr)
+      transform_loop<KP, 2>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+                            a_empty);
+    else if (noclamp)
+      transform_loop<KP, 0>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+                            a_empty);
+    else
+      transform_loop<KP, 1>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+                            a_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -470,7 +469,7 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   if (grid < 1) return SKYRX_OK;
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  score_tc_kernel<KP><<<grid, tc_threads(KP), smem, st>>>(p);
+  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
   SKYRX_CHECK_LAUNCH("score_tc_kernel");
   return SKYRX_OK;
 }

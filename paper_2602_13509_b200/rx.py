@@ -314,6 +314,9 @@ class DetectPlan:
         self.topk_ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,),
                                   torch.int32)
         self.launches = 0
+        # per slot: every line gain is exactly 1 (set by run(); lets the score
+        # kernel drop the per-line gain from its transform)
+        self.gain_one = [False] * batch
         lib = _lib.load()
         use_tc = os.environ.get("SKYRX_B200_TC", "1") != "0"
         self.tc = bands <= 80 and use_tc              # tensor-core score kernel
@@ -343,6 +346,7 @@ class DetectPlan:
         ds = self.ds
         s = _dev.stream_ptr()
         args = (raw.data_ptr(), L, S, B, dark.data_ptr(), coeff.data_ptr(), gains.data_ptr())
+        self.gain_one[i] = gain_const == 1.0
         ds.flags[i].zero_()
         lib = _lib.load()
         # small cubes take the f64 kernel (cheap there; the int8 quantiser's noise
@@ -430,7 +434,8 @@ class DetectPlan:
             events[0].record()
         if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
             _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
-                      coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
+                      coeff.data_ptr(), None if self.gain_one[i] else gains.data_ptr(),
+                      ds.mu_hilo[i].data_ptr(),
                       self.wpack[i].data_ptr(), ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
                       self.max_key[i:i + 1].data_ptr(), s)
         else:

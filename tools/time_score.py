@@ -27,7 +27,7 @@ print(json.dumps({os.environ.get('SKYRX_B200_SCORE_DEBUG', '0'): res}))
 from paper_2602_13509_b200 import _lib, _dev
 ds = plan.ds
 def tc_only():
-    _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(), g.data_ptr(),
+    _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(), None,
               ds.mu_hilo[0].data_ptr(), plan.wpack[0].data_ptr(), ds.flags[0:1].data_ptr(),
               plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(), _dev.stream_ptr())
 def topk_only():
