@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "umma.cuh"
 
 namespace skyrx {
@@ -49,15 +50,6 @@ struct GramRawParams {
   int32_t nsplit;
   int64_t units;
 };
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // idesc for kind::i8 with unsigned 8-bit operands, MN-major A and B, S32 accumulators
 __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
@@ -363,19 +355,6 @@ static int nch_for(int B) {
   int maxoff = 0;
   for (int s = 0; s < 8; ++s) maxoff = maxoff > ((s * B * 2) & 15) ? maxoff : ((s * B * 2) & 15);
   return (maxoff + 2 * B + 15) / 16;
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
 }
 
 template <int NCH>

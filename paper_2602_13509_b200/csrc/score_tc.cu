@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "tc_common.cuh"
+#include "tma.cuh"
 #include "umma.cuh"
 
 namespace skyrx {
@@ -52,7 +53,9 @@ struct ScoreTcParams {
   uint32_t* max_key;
   const int32_t* flags;  // moments-pass flags: (flags & 12) == 8 -> no value below dark
   TileSched ts;
+  CtaPlan plan;  // block-pinned schedule (tc_common.cuh)
   uint32_t raw_stage_bytes;
+  int map_last;  // 1: multi-line tiles (last, narrow block) come in ONE 2-D TMA (tmap)
   int nraw;   // raw ring depth (as many stages as shared memory allows, <= kScoreRawStagesMax)
 };
 
@@ -161,8 +164,8 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
 // Transform warps: calibrate + centre + f16-split every tile of this CTA into
 // the A ring.  MODE is uniform over the launch (see transform_row).
 template <int KP, int MODE>
-__device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int64_t it0,
-                                               int64_t istep, uint8_t* raw_ring, uint8_t* a_ring,
+__device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int blk, int64_t g0,
+                                               int64_t gstep, uint8_t* raw_ring, uint8_t* a_ring,
                                                const float2* mu, uint64_t* raw_full,
                                                uint64_t* raw_empty, uint64_t* a_full,
                                                uint64_t* a_empty) {
@@ -199,19 +202,14 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
         o2[q & 1] = nof;
       }
   };
-  TileInfo ti = tile_info(p.ts, it0);
-  int64_t gt = ti.line0 / ti.r;
-  if (n > 0) load_row_tables(ti);
+  TileInfo ti = tile_at(p.ts, blk, g0);
+  if (n > 0) load_row_tables(ti);  // the CTA never leaves this block
   const uint32_t arow = (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u + c_lo * 128u;
   const float2* nm0 = mu + 8 * c_lo;
   int s = 0, as = 0;
   uint32_t ph = 0, aph = 0;
   for (int t = 0; t < n; ++t) {
-    if (t > 0) {
-      const int ob = ti.block;
-      tile_step(p.ts, ti, gt, istep);
-      if (ti.block != ob) load_row_tables(ti);
-    }
+    if (t > 0) tile_next_in_block(p.ts, ti, gstep);
     const bool valid = r < ti.rows;
     float g = 1.0f;
     if (MODE >= 2 && valid && p.gain) g = __ldg(p.gain + ti.line0 + r / ti.w);
@@ -241,7 +239,8 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p) {
+__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
+    const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ScoreTcParams p) {
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
   static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
@@ -272,11 +271,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  // round-robin tiles: the CTAs sweep the cube together, so at any moment they
-  // read neighbouring lines of one sample block (DRAM pages / TLB locality)
-  const int64_t it0 = blockIdx.x;
-  const int64_t istep = gridDim.x;
-  const int n = it0 < p.ts.items ? (int)((p.ts.items - 1 - it0) / istep + 1) : 0;
+  // block-pinned schedule: this CTA walks line groups g0, g0 + gstep, ... of block blk
+  const int blk = p.plan.block[blockIdx.x];
+  const int64_t g0 = p.plan.rank[blockIdx.x];
+  const int64_t gstep = p.plan.count[blockIdx.x];
+  const int64_t ngb = block_groups(p.ts, blk);
+  const int n = g0 < ngb ? (int)((ngb - 1 - g0) / gstep + 1) : 0;
 
   if (tid == 0) {
     for (int s = 0; s < NR; ++s)
@@ -305,17 +305,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
       bulk_g2s(wsm, p.wpack, wb, w_bar);
       int s = 0;
       uint32_t ph = 0;
-      TileInfo ti = tile_info(p.ts, it0);
-      int64_t g = ti.line0 / ti.r;
+      TileInfo ti = tile_at(p.ts, blk, g0);
       for (int t = 0; t < n; ++t) {
-        if (t > 0) tile_step(p.ts, ti, g, istep);
+        if (t > 0) tile_next_in_block(p.ts, ti, gstep);
         mbar_wait(&raw_empty[s], ph ^ 1);
         const uint32_t seg = (uint32_t)ti.w * B * 2u;
-        mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)ti.nlines);
+        const bool by_map = ti.r > 1 && p.map_last;
+        // a tensor copy always lands the full box (lines past L are zero-filled)
+        mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)(by_map ? ti.r : ti.nlines));
         uint8_t* dst = raw_ring + s * p.raw_stage_bytes;
-        for (int li = 0; li < ti.nlines; ++li) {
-          const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
-          bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
+        if (by_map) {
+          // narrow block: nlines x seg bytes, one tensor copy (box = full tile)
+          tma_load_2d(dst, &tmap, (int)((int64_t)ti.s0 * B / 2), (int)ti.line0, &raw_full[s]);
+        } else {
+          for (int li = 0; li < ti.nlines; ++li) {
+            const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
+            bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
+          }
         }
         if (++s == NR) s = 0, ph ^= 1;
       }
@@ -355,12 +361,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     const float ws2 = colscale[0] * colscale[0];  // one power-of-two scale for all of W
     const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     uint32_t local_max = 0;
-    TileInfo ti = tile_info(p.ts, it0);
-    int64_t gt = ti.line0 / ti.r;
+    TileInfo ti = tile_at(p.ts, blk, g0);
     int acs = 0;
     uint32_t cph = 0;
     for (int t = 0; t < n; ++t) {
-      if (t > 0) tile_step(p.ts, ti, gt, istep);
+      if (t > 0) tile_next_in_block(p.ts, ti, gstep);
       mbar_wait(&acc_full[acs], cph);
       tc_fence_after();
       float2 acc = make_float2(0.0f, 0.0f);
@@ -396,16 +401,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(ScoreTcParams p
     //   odd B -> 3; per-line gains given -> 2; moments pass proved raw >= dark -> 0; else 1
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
     if (B & 1)
-      transform_loop<KP, 3>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 3>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else if (p.gain != nullptr)
-      transform_loop<KP, 2>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 2>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else if (noclamp)
-      transform_loop<KP, 0>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 0>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else
-      transform_loop<KP, 1>(p, n, it0, istep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 1>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
                             a_empty);
   }
   tc_fence_before();
@@ -464,12 +469,33 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   }
   p.nraw = nraw;
   const size_t smem = fixed + (size_t)nraw * p.raw_stage_bytes;
-  int grid = kSMs;
-  if (p.ts.items < grid) grid = (int)p.ts.items;
-  if (grid < 1) return SKYRX_OK;
+  if (p.ts.items < 1) return SKYRX_OK;
+  if (p.ts.nb > kMaxPlanCtas) {
+    set_error("score_tc: %d sample blocks exceed the schedule table", p.ts.nb);
+    return SKYRX_ERR_ARG;
+  }
+  const int grid = plan_ctas(p.ts, p.ts.items < kSMs ? (int)p.ts.items : kSMs, p.plan);
+  // the narrow last block packs rl lines per tile: fetch each tile with ONE 2-D
+  // TMA (u32 elements; box = wl*B/2 x rl) instead of rl tiny line copies
+  CUtensorMap map;
+  memset(&map, 0, sizeof(map));
+  p.map_last = 0;
+  const int64_t box0 = (int64_t)p.ts.wl * p.ts.B / 2;
+  if (p.ts.rl > 1 && box0 <= 256 && p.ts.rl <= 256 && tensor_map_encoder() != nullptr) {
+    const cuuint64_t line_bytes = (cuuint64_t)p.ts.S * p.ts.B * 2;
+    cuuint64_t dims[2] = {line_bytes / 4, (cuuint64_t)p.ts.L};
+    cuuint64_t strides[1] = {line_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)p.ts.rl};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tensor_map_encoder()(
+        &map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)p.raw, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    p.map_last = r == CUDA_SUCCESS ? 1 : 0;
+  }
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(p);
+  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(map, p);
   SKYRX_CHECK_LAUNCH("score_tc_kernel");
   return SKYRX_OK;
 }

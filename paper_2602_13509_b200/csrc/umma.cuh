@@ -60,6 +60,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Wait for a phase that is usually NOT imminent (e.g. an epilogue warp waiting for
+// the next accumulator): probe, then back off with __nanosleep so idle waiters do
+// not take issue slots from the warps doing the work.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity,
+                                                  uint32_t max_ns = 256) {
+  uint32_t ns = 32;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < max_ns ? 2 * ns : max_ns;
+  }
+}
+
 // ------------------------------------------------------------------ bulk copy (1-D TMA)
 // bytes and both addresses must be multiples of 16
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
