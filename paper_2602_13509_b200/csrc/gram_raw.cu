@@ -19,7 +19,12 @@
 //
 // Work unit = (sample s, line range of <= 32768 lines); units are dealt to
 // CTAs round-robin (static), so the summation order is fixed.
-// Roles: warps 0-3 scan + epilogue, warp 4 TMA producer, warp 5 MMA issuer.
+// Roles: warps 0-3 scan (per-band min for the clamp check and the column sums
+// m_s, CUDA cores), warps 4-7 epilogue (TMEM byte Gram -> f64, one unit behind
+// the tensor core thanks to a double-buffered accumulator), warp 8 TMA
+// producer, warp 9 MMA issuer.  Only the lower triangle of the byte Gram is
+// needed: windows wider than 128 bytes add one M=128 x N=(NW-128) MMA for the
+// bottom-right block instead of a second full-width one.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -30,8 +35,8 @@
 namespace skyrx {
 using namespace umma;
 
-constexpr int kGrThreads = 192;
-constexpr int kGrWorkers = 128;
+constexpr int kGrThreads = 320;
+constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
 // TMA ring depth: 4 stages, 2 for the widest windows (B > ~96) to fit the f64 accumulator
 template <int NCH>
@@ -57,38 +62,47 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// TMEM columns per accumulator buffer: full-width block + the bottom-right block
+template <int NCH>
+__host__ __device__ constexpr int gr_bufcols() {
+  return ((16 * NCH + (NCH > 8 ? 16 * NCH - 128 : 0)) + 31) / 32 * 32;
+}
+template <int NCH>
+__host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 512 ? 2 : 1; }
+
 template <int NCH>
 __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  GramRawParams p) {
   constexpr int kGrStages = gr_stages<NCH>();
   constexpr int NW = 16 * NCH;                    // window bytes = MMA N
   constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
+  constexpr int N2 = TWO_M ? NW - 128 : 0;        // ... only over columns 128..NW-1
   // a tile = NATOM boxes of [128 window bytes][Lb lines], 128B-swizzled by TMA:
   // the canonical MN-major SWIZZLE_128B UMMA layout (LBO = atom stride, SBO = 8 lines)
   constexpr int NATOM = TWO_M ? 2 : 1;
   constexpr uint32_t ATOM = kGrLb * 128u;
   constexpr uint32_t STAGE = NATOM * ATOM;
   constexpr int G = kGrWorkers / NCH;             // scan line groups
-  // column sums m_s ride on the tensor core too: A x ones(N=16) into TMEM
-  constexpr uint32_t SUMC = (TWO_M ? 2 : 1) * NW;
-  constexpr bool ONES = SUMC + (TWO_M ? 32 : 16) <= 512;
+  constexpr int BUFC = gr_bufcols<NCH>();
+  constexpr int NBUF = gr_nbuf<NCH>();
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
   uint8_t* stages = sm;
-  uint8_t* ones = stages + kGrStages * STAGE;                 // 128 lines x 16 B of 1
-  double* qacc = reinterpret_cast<double*>(ones + kGrLb * 16);
+  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE);
   double* sacc = qacc + B * B;
   uint32_t* smin = reinterpret_cast<uint32_t*>(sacc + B);  // [G][NCH][4] packed u16 mins
   uint32_t* ssum = smin + G * NCH * 4;                       // [G][NCH][8]
-  uint32_t* minv = ssum + G * NCH * 8;                       // [NCH*8]
-  uint32_t* sumv = minv + NCH * 8;                           // [NCH*8]
+  uint32_t* minv = ssum + G * NCH * 8;                       // [2][NCH*8]
+  uint32_t* sumv = minv + 2 * NCH * 8;                       // [2][NCH*8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(sumv + NCH * 8) + 7) & ~uintptr_t(7));
+      (reinterpret_cast<uintptr_t>(sumv + 2 * NCH * 8) + 7) & ~uintptr_t(7));
   uint64_t* full = bars;
   uint64_t* empty = full + kGrStages;
-  uint64_t* acc_full = empty + kGrStages;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_full = empty + kGrStages;   // [NBUF]
+  uint64_t* acc_empty = acc_full + 2;       // [NBUF]
+  uint64_t* scan_full = acc_empty + 2;      // [2] unit's min / sums published
+  uint64_t* scan_empty = scan_full + 2;     // [2] ... consumed by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(scan_empty + 2);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -100,16 +114,16 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 
   if (tid == 0) {
     for (int s = 0; s < kGrStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], kGrWorkers + 1);
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, kGrWorkers);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1), mbar_init(&acc_empty[b], kGrWorkers);
+      mbar_init(&scan_full[b], 1), mbar_init(&scan_empty[b], kGrWorkers);
+    }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   // bit 8: this cube's clamp check ran (bit 4 would report a value below dark)
   if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 8);
   for (int e = tid; e < B * B + B; e += blockDim.x) qacc[e] = 0.0;
-  for (int e = tid; e < kGrLb * 4; e += blockDim.x) reinterpret_cast<uint32_t*>(ones)[e] = 0x01010101u;
-  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -122,7 +136,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
   };
 
-  if (warp == 4) {
+  if (warp == 8) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       int t = 0;
       for (int64_t u = u0; u < u1; u += ustep) {
@@ -142,18 +156,21 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       constexpr uint32_t id = idesc_u8_s32(128, NW);
-      constexpr uint32_t id1 = idesc_u8_s32(128, 16);
+      constexpr uint32_t id2 = idesc_u8_s32(128, N2 > 0 ? N2 : 16);
       int t = 0, unit = 0;
       for (int64_t u = u0; u < u1; u += ustep, ++unit) {
         int s;
         int64_t l0, nl;
         unit_geom(u, s, l0, nl);
         const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
-        if (unit > 0) mbar_wait(acc_empty, (unit - 1) & 1);
+        const int buf = NBUF == 2 ? (unit & 1) : 0;
+        const int use = NBUF == 2 ? (unit >> 1) : unit;
+        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc_fence_after();
+        const uint32_t d = tmem + buf * BUFC;
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kGrStages;
           mbar_wait(&full[st], (t / kGrStages) & 1);
@@ -163,21 +180,17 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           for (int ks = 0; ks < kGrLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
             const uint8_t* kb = base + ks * 4096;  // 32 lines = 4 swizzle atoms of 8 x 128 B
-            const uint64_t bdesc = smem_desc_sw128(kb, ATOM, 1024);
-            mma_i8(tmem, smem_desc_sw128(kb, ATOM, 1024), bdesc, id, acc);
-            if (TWO_M) mma_i8(tmem + NW, smem_desc_sw128(kb + ATOM, ATOM, 1024), bdesc, id, acc);
-            if (ONES) {
-              const uint64_t odesc = smem_desc(ones + ks * 512, 128, 128);
-              mma_i8(tmem + SUMC, smem_desc_sw128(kb, ATOM, 1024), odesc, id1, acc);
-              if (TWO_M) mma_i8(tmem + SUMC + 16, smem_desc_sw128(kb + ATOM, ATOM, 1024), odesc, id1, acc);
-            }
+            mma_i8(d, smem_desc_sw128(kb, ATOM, 1024), smem_desc_sw128(kb, ATOM, 1024), id, acc);
+            if (TWO_M)  // rows 128..NW-1 x columns 128..NW-1 (the rest is the transpose)
+              mma_i8(d + NW, smem_desc_sw128(kb + ATOM, ATOM, 1024),
+                     smem_desc_sw128(kb + ATOM, ATOM, 1024), id2, acc);
           }
           mma_commit(&empty[st]);
         }
-        mma_commit(acc_full);
+        mma_commit(&acc_full[buf]);
       }
     }
-  } else {  // ------------------------------------------------------------ scan + epilogue
+  } else if (warp < 4) {  // ---------------------------------------------- scan
     const int c = tid % NCH, g = tid / NCH;
     const bool scanner = g < G;
     int t = 0, unit = 0;
@@ -200,19 +213,19 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             const uint4 v = *reinterpret_cast<const uint4*>(atom + l * 128 + (((c & 7) ^ (l & 7)) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
-            if (!ONES) {
-              sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
-              sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
-            }
+            sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
+            sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
           }
         }
         mbar_arrive(&empty[st]);
       }
-      // per-unit reduction of the scans (fixed order over line groups)
+      // per-unit reduction of the scans (fixed order over line groups) into buffer ub
       if (scanner) {
         for (int q = 0; q < 4; ++q) smin[(g * NCH + c) * 4 + q] = mn[q];
         for (int q = 0; q < 8; ++q) ssum[(g * NCH + c) * 8 + q] = sm8[q];
       }
+      const int ub = unit & 1;
+      mbar_wait(&scan_empty[ub], ((unit >> 1) & 1) ^ 1);
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
       if (tid < NCH * 8) {
         const int cc = tid >> 3, q = tid & 7;
@@ -222,36 +235,37 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           mv = min(mv, (q & 1) ? (w >> 16) : (w & 0xffffu));
           sv += ssum[(gg * NCH + cc) * 8 + q];
         }
-        minv[tid] = mv;
-        if (!ONES) sumv[tid] = sv;
+        minv[ub * NCH * 8 + tid] = mv;
+        sumv[ub * NCH * 8 + tid] = sv;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
-      // ---- epilogue: byte Gram (TMEM) -> calibrated sum x x^T of this sample
-      mbar_wait(acc_full, unit & 1);
+      if (tid == 0) mbar_arrive(&scan_full[ub]);
+    }
+  } else {  // ------------------------------------------------------------ epilogue (warps 4-7)
+    const int te = tid - kGrWorkers;  // TMEM lane = byte row of the Gram
+    const int we = warp & 3;
+    int unit = 0;
+    for (int64_t u = u0; u < u1; u += ustep, ++unit) {
+      int s;
+      int64_t l0, nl;
+      unit_geom(u, s, l0, nl);
+      const int buf = NBUF == 2 ? (unit & 1) : 0;
+      const int use = NBUF == 2 ? (unit >> 1) : unit;
+      const int ub = unit & 1;
+      mbar_wait(&scan_full[ub], (unit >> 1) & 1);
+      mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
+      const uint32_t* mnv = minv + ub * NCH * 8;
+      const uint32_t* smv = sumv + ub * NCH * 8;
       const int off = (int)(((int64_t)s * B * 2) & 15);
-      if (ONES) {  // band sums: 256 * (hi-byte row sum) + (lo-byte row sum)
-#pragma unroll
-        for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
-          if (part == 1 && 128 + 32 * warp >= off + 2 * B) continue;  // warp-uniform
-          uint32_t v[8];
-          tmem_ld8(tmem + ((uint32_t)(32 * warp) << 16) + SUMC + 16 * part, v);
-          tmem_ld_wait();
-          const uint32_t hi = __shfl_xor_sync(0xffffffffu, v[0], 1);
-          const int rel = 128 * part + tid - off;
-          if (rel >= 0 && rel < 2 * B && (rel & 1) == 0)
-            sumv[(off >> 1) + (rel >> 1)] = 256u * hi + v[0];
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
-      }
       const double Lu = (double)nl;
       const float* drow = p.dark + (int64_t)s * B;
       const float* crow = p.coeff + (int64_t)s * B;
       bool clamp = false;
 #pragma unroll
       for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
-        if (part == 1 && 128 + 32 * warp >= off + 2 * B) continue;  // warp-uniform
-        const int m = 128 * part + tid;
+        if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
+        const int m = 128 * part + te;
         const int rel = m - off;
         const bool lo_row = rel >= 0 && rel < 2 * B && (rel & 1) == 0;
         const int b = rel >> 1;
@@ -259,13 +273,15 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         if (lo_row) {
           Cb = (double)crow[b] * p.ginv;
           db = (double)drow[b];
-          Sb = (double)sumv[(off >> 1) + b];
-          clamp |= (float)minv[(off >> 1) + b] < drow[b];
+          Sb = (double)smv[(off >> 1) + b];
+          clamp |= (float)mnv[(off >> 1) + b] < drow[b];
         }
-        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(part * NW);
-        for (int cc = 0; cc < NCH; ++cc) {
+        // part 0: byte columns 0..NW-1 of the full-width block; part 1: columns 128..NW-1
+        const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? NW : 0);
+        const int cc0 = part ? 8 : 0;
+        for (int cc = cc0; cc < NCH; ++cc) {
           uint32_t v[16];
-          tmem_ld16(taddr + cc * 16, v);
+          tmem_ld16(taddr + (cc - cc0) * 16, v);
           tmem_ld_wait();
           uint32_t pv[16];
 #pragma unroll
@@ -276,16 +292,21 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
               const int reln = cc * 16 + 2 * i - off;
               if (reln < 0 || reln >= 2 * B) continue;
               const int b2 = reln >> 1;
-              if (b2 > b) continue;  // lower triangle; mirrored in the reduction
+              // lower triangle (b2 <= b) from this row; a part-0 row also owns the
+              // (b2 > b) entries whose columns lie past byte 128: their part-1 rows
+              // only see columns >= 128
+              const bool mine = b2 <= b || (part == 0 && TWO_M && cc >= 8);
+              if (!mine) continue;
               // own row = lo byte of band b, partner row = hi byte of band b
               const double gv = 65536.0 * (double)pv[2 * i + 1] +
                                 256.0 * ((double)pv[2 * i] + (double)v[2 * i + 1]) +
                                 (double)v[2 * i];
               const double C2 = (double)crow[b2] * p.ginv;
               const double d2 = (double)drow[b2];
-              const double S2 = (double)sumv[(off >> 1) + b2];
+              const double S2 = (double)smv[(off >> 1) + b2];
               const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
-              qacc[b * B + b2] += Cb * C2 * xx;
+              const int e = b2 <= b ? b * B + b2 : b2 * B + b;
+              qacc[e] += Cb * C2 * xx;
             }
           }
         }
@@ -293,10 +314,13 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
       if (clamp) atomicOr(p.flags, 4);
       tc_fence_before();
-      mbar_arrive(acc_empty);
+      mbar_arrive(&acc_empty[buf]);
+      mbar_arrive(&scan_empty[ub]);
     }
-    // per-CTA partial: Sxx (lower triangle), Sx, n
-    asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
+  }
+  // per-CTA partial: Sxx (lower triangle), Sx, n
+  __syncthreads();
+  if (tid < kGrWorkers) {
     double* out = p.part + (size_t)blockIdx.x * (B * B + B + 1);
     for (int e = tid; e < B * B + B; e += kGrWorkers) out[e] = qacc[e];
     if (tid == 0) {
@@ -313,7 +337,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc(tmem, 512);
+  if (warp == 9) tmem_dealloc(tmem, 512);
 }
 
 // moments about the shift c: s = Sx - n c, Q = Sxx - c Sx^T - Sx c^T + n c c^T
@@ -363,8 +387,8 @@ static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* mome
   constexpr uint32_t STAGE = (NCH > 8 ? 2u : 1u) * kGrLb * 128u;
   constexpr int G = kGrWorkers / NCH;
   constexpr int kGrStages = gr_stages<NCH>();
-  const size_t smem = kGrStages * (size_t)STAGE + kGrLb * 16 + ((size_t)p.B * p.B + p.B) * 8 +
-                      (size_t)G * NCH * 12 * 4 + NCH * 8 * 8 + 16 * 8 + 1024;
+  const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
+                      (size_t)G * NCH * 12 * 4 + NCH * 8 * 16 + 16 * 8 + 1024;
   int grid = kSMs;
   if (p.units < grid) grid = (int)p.units;
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -427,7 +451,8 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   p.B = bands;
   p.nsplit = (int)((lines + kGrMaxUnitLines - 1) / kGrMaxUnitLines);
   // also split so that there are at least ~2 units per SM
-  while ((int64_t)samples * p.nsplit < 2 * kSMs && lines / (p.nsplit + 1) >= 4 * kGrLb) ++p.nsplit;
+  // and into enough units (>= 8 per SM) that the static round-robin tail stays small
+  while ((int64_t)samples * p.nsplit < 8 * kSMs && lines / (p.nsplit + 1) >= 4 * kGrLb) ++p.nsplit;
   p.split_lines = (lines + p.nsplit - 1) / p.nsplit;
   p.split_lines = ((p.split_lines + kGrLb - 1) / kGrLb) * kGrLb;
   p.nsplit = (int)((lines + p.split_lines - 1) / p.split_lines);
