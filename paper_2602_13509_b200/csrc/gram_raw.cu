@@ -340,35 +340,46 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   if (warp == 9) tmem_dealloc(tmem, 512);
 }
 
+// Deterministic reduction of the per-CTA partials [Sxx | Sx | n]: a block owns 32
+// elements (one per lane); its 8 warps sum fixed, contiguous slices of the
+// partials in order, then warp 0 adds the 8 slice sums in order.
+__global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restrict__ part,
+                                                           int nparts, int stride,
+                                                           double* __restrict__ out) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const int per = (nparts + 7) / 8;
+  const int c0 = w * per, c1 = min(nparts, c0 + per);
+  double acc = 0.0;
+  if (e < stride)
+    for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && e < stride) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    out[e] = t;
+  }
+}
+
 // moments about the shift c: s = Sx - n c, Q = Sxx - c Sx^T - Sx c^T + n c c^T
-__global__ void gram_raw_reduce_kernel(const double* __restrict__ part, int nparts, int B,
+__global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
                                        const double* __restrict__ shift,
                                        double* __restrict__ moments) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  const int stride = B * B + B + 1;
-  double* s_out = moments + 1;
-  double* q_out = moments + 1 + B;
-  double n = 0.0;
-  for (int c = 0; c < nparts; ++c) n += part[(size_t)c * stride + B * B + B];
+  const double* sx = tot + B * B;
+  const double n = tot[B * B + B];
   if (e < B * B) {
     const int i = e / B, j = e - i * B;
     if (j > i) return;
-    double xx = 0.0, si = 0.0, sj = 0.0;
-    for (int c = 0; c < nparts; ++c) {
-      const double* pp = part + (size_t)c * stride;
-      xx += pp[i * B + j];
-      si += pp[B * B + i];
-      sj += pp[B * B + j];
-    }
     const double ci = shift[i], cj = shift[j];
-    const double q = xx - ci * sj - si * cj + n * ci * cj;
-    q_out[(size_t)i * B + j] = q;
-    q_out[(size_t)j * B + i] = q;
+    const double q = tot[i * B + j] - ci * sx[j] - sx[i] * cj + n * ci * cj;
+    moments[1 + B + (size_t)i * B + j] = q;
+    moments[1 + B + (size_t)j * B + i] = q;
   } else if (e < B * B + B) {
     const int i = e - B * B;
-    double si = 0.0;
-    for (int c = 0; c < nparts; ++c) si += part[(size_t)c * stride + B * B + i];
-    s_out[i] = si - n * shift[i];
+    moments[1 + i] = sx[i] - n * shift[i];
   } else if (e == B * B + B) {
     moments[0] = n;
   }
@@ -396,8 +407,11 @@ static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* mome
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
   const int work = p.B * p.B + p.B + 1;
-  gram_raw_reduce_kernel<<<ceil_div(work, 256), 256, 0, st>>>(p.part, grid, p.B, shift, moments);
-  SKYRX_CHECK_LAUNCH("gram_raw_reduce_kernel");
+  double* tot = p.part + (size_t)kSMs * work;  // after the per-CTA partials
+  gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(p.part, grid, work, tot);
+  SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
+  gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, p.B, shift, moments);
+  SKYRX_CHECK_LAUNCH("gram_raw_center_kernel");
   return SKYRX_OK;
 }
 
@@ -416,7 +430,7 @@ extern "C" int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t
 }
 
 extern "C" size_t skyrx_stats_raw_workspace(int32_t bands) {
-  return (size_t)kSMs * ((size_t)bands * bands + bands + 1) * sizeof(double);
+  return (size_t)(kSMs + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double);
 }
 
 extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
