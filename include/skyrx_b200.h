@@ -164,6 +164,9 @@ int skyrx_score(int32_t kind, const void* pixels, int64_t lines, int32_t samples
  * bytes per matrix).  flags (nullable) = the moments-pass flags word: when it
  * reads 8 (raw-byte path ran, no value below dark) the clamp is skipped.
  * gain may be NULL: every line gain is 1 (the transform drops the division).
+ * topk_hist0 (nullable) = skyrx_topk_histogram(ws) after skyrx_topk_init: the
+ * kernel adds the digit-0 histogram of its scores, so the select continues
+ * with skyrx_topk_pick(0) instead of a first skyrx_topk_hist pass.
  * skyrx_score_tc_supported() says whether the shape and
  * alignment allow it (every line segment of a tile must be a 16-B multiple). */
 size_t skyrx_wpack_bytes(int32_t bands);
@@ -173,7 +176,7 @@ int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t bands, cons
 int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                    const float* dark, const float* coeff, const float* gain,
                    const float* mu_hilo, const void* wpack, const int32_t* flags,
-                   float* scores, uint32_t* max_key, void* stream);
+                   float* scores, uint32_t* max_key, uint32_t* topk_hist0, void* stream);
 
 /* The kernel slot itself: _accel.mahalanobis_sq(pixels, mu, chol_lower)
  * (_accel.py:109-131) with FP64 arithmetic; pixels f32 or f64 (kind F32/F64).

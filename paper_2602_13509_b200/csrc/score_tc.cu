@@ -41,6 +41,7 @@ constexpr int kScoreRawStagesMax = 8;
 constexpr int kScoreAStages = 2;
 constexpr int kScoreAcc = 3;    // TMEM accumulator ring
 constexpr int kScoreWmax = 128;
+constexpr int kTopkBins = 2048;  // digit 0 of the top-k radix select (select.cu)
 
 struct ScoreTcParams {
   const uint16_t* raw;
@@ -51,6 +52,7 @@ struct ScoreTcParams {
   const uint8_t* wpack;
   float* scores;
   uint32_t* max_key;
+  uint32_t* hist0;       // nullable: + digit-0 (top 11 key bits) histogram of the scores
   const int32_t* flags;  // moments-pass flags: (flags & 12) == 8 -> no value below dark
   TileSched ts;
   CtaPlan plan;  // block-pinned schedule (tc_common.cuh)
@@ -258,8 +260,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
   uint8_t* wsm = a_ring + kScoreAStages * 2 * A_BYTES;
   float* colscale = reinterpret_cast<float*>(wsm + 2 * W_BYTES);
   float2* mu = reinterpret_cast<float2*>(colscale + NP);   // [KP] {-mu, 0}
+  uint32_t* shist = reinterpret_cast<uint32_t*>(mu + KP);  // [2048] digit-0 histogram
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(mu + KP) + 7) & ~uintptr_t(7));
+      (reinterpret_cast<uintptr_t>(shist + kTopkBins) + 7) & ~uintptr_t(7));
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + kScoreRawStagesMax;
   uint64_t* a_full = raw_empty + kScoreRawStagesMax;
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, TMEM_COLS);
   // mu[k].x = f32(-mu_k): clamp floor of the centred value, read as a warp broadcast
+  for (int i = tid; i < kTopkBins; i += blockDim.x) shist[i] = 0;
   for (int k = tid; k < KP; k += blockDim.x)
     mu[k] = k < B ? make_float2((float)(-((double)p.mu_hilo[k] + (double)p.mu_hilo[B + k])), 0.0f)
                   : make_float2(0.0f, 0.0f);
@@ -383,11 +387,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acs]);  // one arrival per warp
-      if (r < ti.rows) {
+      const bool valid = r < ti.rows;
+      uint32_t key = 0;
+      if (valid) {
         const int li = r / ti.w;
         const float sum = (acc.x + acc.y) * ws2;
         p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + (r - li * ti.w)] = sum;
-        local_max = max(local_max, f2ord(sum));
+        key = f2ord(sum);
+        local_max = max(local_max, key);
+      }
+      if (p.hist0) {  // warp-aggregated shared-memory histogram of the top 11 key bits
+        const uint32_t bin = valid ? key >> 21 : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+        if (valid && lane == __ffs(peers) - 1) atomicAdd(&shist[bin], __popc(peers));
       }
       if (++acs == kScoreAcc) acs = 0, cph ^= 1;
     }
@@ -417,6 +429,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
   __syncthreads();
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc(tmem, TMEM_COLS);
+  if (p.hist0)
+    for (int i = tid; i < kTopkBins; i += blockDim.x)
+      if (shist[i]) atomicAdd(&p.hist0[i], shist[i]);
 }
 
 // W (f64, row-major B x B, lower) -> f16 hi/lo K-major B operand + column scales
@@ -459,7 +474,7 @@ template <int KP>
 static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
   const size_t A_BYTES = 128u * KP * 2u;
-  const size_t fixed = kScoreAStages * 2 * A_BYTES + wpack_bytes_for(KP) + KP * 8 +
+  const size_t fixed = kScoreAStages * 2 * A_BYTES + wpack_bytes_for(KP) + KP * 8 + kTopkBins * 4 +
                        (2 * kScoreRawStagesMax + 2 * kScoreAStages + 5) * 8 + 16 + 64;
   int nraw = (int)((kSmemMax - fixed) / p.raw_stage_bytes);
   if (nraw > kScoreRawStagesMax) nraw = kScoreRawStagesMax;
@@ -534,7 +549,8 @@ extern "C" int skyrx_score_tc_supported(int64_t lines, int32_t samples, int32_t 
 extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                               const float* dark, const float* coeff, const float* gain,
                               const float* mu_hilo, const void* wpack, const int32_t* flags,
-                              float* scores, uint32_t* max_key, void* stream) {
+                              float* scores, uint32_t* max_key, uint32_t* topk_hist0,
+                              void* stream) {
   SKYRX_REQUIRE(skyrx_score_tc_supported(lines, samples, bands, raw),
                 "tensor-core score path unsupported for this shape/alignment");
   ScoreTcParams p{};
@@ -546,6 +562,7 @@ extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t sample
   p.wpack = (const uint8_t*)wpack;
   p.scores = scores;
   p.max_key = max_key;
+  p.hist0 = topk_hist0;
   p.flags = flags;
   tc_sched(lines, samples, bands, kScoreWmax, p.ts);
   if (lines * (int64_t)samples == 0) return SKYRX_OK;

@@ -120,9 +120,13 @@ __global__ void __launch_bounds__(512) topk_hist_kernel(const float* __restrict_
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// one CTA: walk bins from the top, pick the bin holding the target rank
-__global__ void topk_pick_kernel(int digit, TopkState* st, uint32_t* hist, float* thr) {
-  __shared__ uint32_t cnt[kHistBins];
+// one CTA of 256 threads: suffix counts over the bins from the top (each thread owns
+// 8 consecutive bins), pick the bin holding the target rank
+__global__ void __launch_bounds__(256) topk_pick_kernel(int digit, TopkState* st, uint32_t* hist,
+                                                        float* thr) {
+  __shared__ uint64_t wsum[8];
+  __shared__ int found_bin;
+  __shared__ uint64_t found_cum;
   if (st->all) {
     if (threadIdx.x == 0 && digit == 2) *thr = -INFINITY;
     return;
@@ -130,22 +134,44 @@ __global__ void topk_pick_kernel(int digit, TopkState* st, uint32_t* hist, float
   int shift, bits;
   digit_params(digit, shift, bits);
   const int nb = 1 << bits;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = hist[i];
+  const int per = nb / 256;           // 8 (11-bit digits) or 4 (10-bit)
+  const int t = threadIdx.x;
+  // thread t owns bins [nb - per*(t+1), nb - per*t): thread 0 holds the top bins
+  const int hi = nb - per * t;
+  uint32_t c[8];
+  uint64_t mine = 0;
+  for (int q = 0; q < per; ++q) c[q] = hist[hi - 1 - q], mine += c[q];
+  // exclusive prefix over threads (= count of all bins above this thread's bins)
+  uint64_t incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += v;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  if (t == 0) found_bin = 0, found_cum = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t rank = st->rank;
-    uint64_t cum = 0;
-    int b = nb - 1;
-    for (; b > 0; --b) {
-      if (cum + cnt[b] >= rank) break;
-      cum += cnt[b];
+  uint64_t before = incl - mine;
+  for (int w = 0; w < (t >> 5); ++w) before += wsum[w];
+  const uint64_t rank = st->rank;
+  if (before < rank && before + mine >= rank) {  // exactly one thread (rank <= total)
+    uint64_t cum = before;
+    int q = 0;
+    for (; q < per - 1; ++q) {
+      if (cum + c[q] >= rank) break;
+      cum += c[q];
     }
-    st->rank = rank - cum;
-    st->prefix = (st->prefix << bits) | (uint32_t)b;
+    found_bin = hi - 1 - q;
+    found_cum = cum;
+  }
+  __syncthreads();
+  if (t == 0) {
+    // rank beyond every bin (cannot happen with a consistent histogram): keep bin 0
+    st->rank = rank - found_cum;
+    st->prefix = (st->prefix << bits) | (uint32_t)found_bin;
     if (digit == 2) *thr = ord2f(st->prefix);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0;
+  for (int i = t; i < kHistBins; i += blockDim.x) hist[i] = 0;
 }
 
 static int grid_n(int64_t n, int threads, int per_sm) {

@@ -413,18 +413,27 @@ class DetectPlan:
         L, S, B = self.shape
         n = L * S
         k = topk_count(n) if k is None else int(k)
-        self.score_only(i, raw, dark, coeff, gains, events)
         s = _dev.stream_ptr()
+        ws = self.topk_ws.data_ptr()
+        # R-TOPK as init -> (digit-0 histogram fused into the score kernel) ->
+        # pick 0 -> hist 1 -> pick 1 -> hist 2 -> pick 2
+        _lib.call("skyrx_topk_init", n, k, ws, s)
+        fused = self.score_only(i, raw, dark, coeff, gains, events, topk_hist0=True)
         sc = self.scores[i]
-        _lib.call("skyrx_topk_threshold", sc.data_ptr(), n, k, self.thr[i:i + 1].data_ptr(),
-                  self.topk_ws.data_ptr(), s)
-        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, self.thr[i:i + 1].data_ptr(),
-                  self.mask[i].data_ptr(), s)
-        self.launches += 7 + 1
+        thr = self.thr[i:i + 1].data_ptr()
+        for digit in range(3):
+            if digit > 0 or not fused:
+                _lib.call("skyrx_topk_hist", sc.data_ptr(), n, digit, ws, s)
+            _lib.call("skyrx_topk_pick", digit, ws, thr, s)
+        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, thr, self.mask[i].data_ptr(), s)
+        self.launches += 1 + (5 if fused else 6) + 1
         return self
 
-    def score_only(self, i: int, raw: torch.Tensor, dark, coeff, gains, events=None):
-        """Scores of cube i and their max key (no threshold / mask)."""
+    def score_only(self, i: int, raw: torch.Tensor, dark, coeff, gains, events=None,
+                   topk_hist0: bool = False) -> bool:
+        """Scores of cube i and their max key (no threshold / mask).  With
+        ``topk_hist0`` the tensor-core kernel also adds the digit-0 top-k
+        histogram into the top-k workspace; returns whether it did."""
         L, S, B = self.shape
         ds = self.ds
         s = _dev.stream_ptr()
@@ -432,12 +441,16 @@ class DetectPlan:
         sc = self.scores[i]
         if events is not None:
             events[0].record()
+        fused = False
         if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
+            hist = (_lib.load().skyrx_topk_histogram(self.topk_ws.data_ptr())
+                    if topk_hist0 else None)
             _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), None if self.gain_one[i] else gains.data_ptr(),
                       ds.mu_hilo[i].data_ptr(),
                       self.wpack[i].data_ptr(), ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
-                      self.max_key[i:i + 1].data_ptr(), s)
+                      self.max_key[i:i + 1].data_ptr(), hist, s)
+            fused = topk_hist0
         else:
             _lib.call("skyrx_score", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), gains.data_ptr(), ds.mu_hilo[i].data_ptr(),
@@ -446,7 +459,7 @@ class DetectPlan:
         if events is not None:
             events[1].record()
         self.launches += 1
-        return self
+        return fused
 
 
 def constant_gain(gains, tables) -> float | None:

@@ -22,6 +22,7 @@ def t(fn, reps=5):
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
 res = {'stats_ms': t(lambda: plan.run(0, raw, d, c, g, gain_const=1.0)),
+       'select_ms': t(lambda: plan.score(0, raw, d, c, g)) - t(lambda: plan.score_only(0, raw, d, c, g, topk_hist0=True)),
        'score_path_ms': t(lambda: plan.score(0, raw, d, c, g))}
 print(json.dumps({os.environ.get('SKYRX_B200_SCORE_DEBUG', '0'): res}))
 from paper_2602_13509_b200 import _lib, _dev
@@ -29,7 +30,7 @@ ds = plan.ds
 def tc_only():
     _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(), None,
               ds.mu_hilo[0].data_ptr(), plan.wpack[0].data_ptr(), ds.flags[0:1].data_ptr(),
-              plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(), _dev.stream_ptr())
+              plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(), None, _dev.stream_ptr())
 def topk_only():
     n = L * S
     _lib.call("skyrx_topk_threshold", plan.scores[0].data_ptr(), n, (n + 999) // 1000,
