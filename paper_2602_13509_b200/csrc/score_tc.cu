@@ -39,7 +39,8 @@ constexpr int kTmaWarp = (kTcTransform + kTcEpilogue) / 32;  // 12
 constexpr int kMmaWarp = kTmaWarp + 1;                 // 13
 constexpr int kScoreRawStagesMax = 8;
 constexpr int kScoreAStages = 2;
-constexpr int kScoreAcc = 3;    // TMEM accumulator ring
+constexpr int kScoreAcc = 3;    // TMEM accumulator ring: columns [0, 3 KP)
+constexpr int kScoreABase = 256;  // A ring (f16 hi/lo, from the transform warps): [256, 256 + 2 KP)
 constexpr int kScoreWmax = 128;
 constexpr int kTopkBins = 2048;  // digit 0 of the top-k radix select (select.cu)
 
@@ -99,8 +100,9 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return r;
 }
 
-// 8 centred values -> f16 hi (round to nearest) + f16 lo (the exact f32 residual, rounded)
-__device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint8_t* hi, uint8_t* lo) {
+// 8 centred values -> f16 hi (round to nearest) + f16 lo (the exact f32 residual,
+// rounded), written to this thread's TMEM lane: 4 columns of hi, 4 of lo
+__device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint32_t thi, uint32_t tlo) {
   uint32_t hw[4], lw[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -110,8 +112,8 @@ __device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint8_t* hi,
     hw[q] = *reinterpret_cast<const uint32_t*>(&h);
     lw[q] = *reinterpret_cast<const uint32_t*>(&l);
   }
-  *reinterpret_cast<uint4*>(hi) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-  *reinterpret_cast<uint4*>(lo) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  tmem_st4(thi, hw[0], hw[1], hw[2], hw[3]);
+  tmem_st4(tlo, lw[0], lw[1], lw[2], lw[3]);
 }
 
 // One pixel row's share (CHT 8-band chunks) of the A operand.  Per band pair
@@ -123,7 +125,7 @@ __device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint8_t* hi,
 template <int MODE, int CHT>
 __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&tco)[CHT * 4],
                                               const float2 (&tnof)[CHT * 4], const float2* nm,
-                                              float g, uint8_t* hi, uint8_t* lo) {
+                                              float g, uint32_t thi, uint32_t tlo) {
   const float gi = 1.0f / g;
   const float2 bias = make_float2(-8388608.0f, -8388608.0f);
 #pragma unroll
@@ -159,7 +161,7 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
                       make_float2(m0, m1));
       }
     }
-    store_split8(dv, hi + cc * 128, lo + cc * 128);
+    store_split8(dv, thi + cc * 4, tlo + cc * 4);
   }
 }
 
@@ -167,14 +169,12 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
 // the A ring.  MODE is uniform over the launch (see transform_row).
 template <int KP, int MODE>
 __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int blk, int64_t g0,
-                                               int64_t gstep, uint8_t* raw_ring, uint8_t* a_ring,
+                                               int64_t gstep, uint8_t* raw_ring, uint32_t tmem,
                                                const float2* mu, uint64_t* raw_full,
                                                uint64_t* raw_empty, uint64_t* a_full,
                                                uint64_t* a_empty) {
   constexpr int NCH = KP / 8;
   constexpr int CHT = NCH / 2;  // chunks per thread (row half)
-  constexpr uint32_t A_BYTES = 128u * KP * 2u;
-  constexpr uint32_t SBO_A = (KP / 8) * 128u;
   const int tid = threadIdx.x;
   const int r = tid & 127;  // pixel row of the tile
   const int h = tid >> 7;   // band half
@@ -206,30 +206,29 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
   };
   TileInfo ti = tile_at(p.ts, blk, g0);
   if (n > 0) load_row_tables(ti);  // the CTA never leaves this block
-  const uint32_t arow = (uint32_t)(r >> 3) * SBO_A + (uint32_t)(r & 7) * 16u + c_lo * 128u;
+  // A stage `as` lives in TMEM columns [kScoreABase + as*KP, + KP): hi in the first
+  // KP/2 (two f16 per column), lo in the next KP/2; this thread's lane = its row
+  const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase + 4 * c_lo;
   const float2* nm0 = mu + 8 * c_lo;
   int s = 0, as = 0;
   uint32_t ph = 0, aph = 0;
   for (int t = 0; t < n; ++t) {
     if (t > 0) tile_next_in_block(p.ts, ti, gstep);
-    const bool valid = r < ti.rows;
+    // rows past the tile's end transform stale ring bytes (finite u16 counts): the
+    // TMEM stores are warp-collective, and the epilogue drops those rows
     float g = 1.0f;
-    if (MODE >= 2 && valid && p.gain) g = __ldg(p.gain + ti.line0 + r / ti.w);
+    if (MODE >= 2 && p.gain) {
+      const int64_t line = ti.line0 + r / ti.w;
+      g = __ldg(p.gain + (line < p.ts.L ? line : p.ts.L - 1));
+    }
     mbar_wait(&raw_full[s], ph);
     mbar_wait(&a_empty[as], aph ^ 1);
-    uint8_t* hi0 = a_ring + as * 2 * A_BYTES + arow;
-    uint8_t* lo0 = hi0 + A_BYTES;
-    if (valid) {
-      const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
-      transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, hi0, lo0);
-    } else {
-#pragma unroll
-      for (int cc = 0; cc < CHT; ++cc) {
-        *reinterpret_cast<uint4*>(hi0 + cc * 128) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(lo0 + cc * 128) = make_uint4(0, 0, 0, 0);
-      }
-    }
-    fence_async_smem();
+    tc_fence_after();
+    const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
+    const uint32_t thi = tl + as * KP;
+    transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, thi, thi + KP / 2);
+    tmem_st_wait();
+    tc_fence_before();
     __syncwarp();
     if (lane == 0) {  // one arrival per warp
       mbar_arrive(&a_full[as]);
@@ -246,18 +245,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
   static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
-  constexpr uint32_t A_BYTES = 128u * KP * 2u;
-  constexpr uint32_t SBO_A = (KP / 8) * 128u;
   constexpr uint32_t W_BYTES = NP * KP * 2u;
   constexpr uint32_t SBO_B = (KP / 8) * 128u;
-  constexpr uint32_t TMEM_COLS = kScoreAcc * NP <= 128 ? 128 : 256;
-  static_assert(kScoreAcc * NP <= 256, "accumulators fit 256 TMEM columns");
+  constexpr uint32_t TMEM_COLS = 512;
+  static_assert(kScoreAcc * NP <= kScoreABase, "accumulators below the A ring");
+  static_assert(kScoreABase + kScoreAStages * KP <= 512, "A ring fits TMEM");
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.ts.B;
   uint8_t* raw_ring = sm;
   const int NR = p.nraw;
-  uint8_t* a_ring = raw_ring + NR * p.raw_stage_bytes;
-  uint8_t* wsm = a_ring + kScoreAStages * 2 * A_BYTES;
+  uint8_t* wsm = raw_ring + NR * p.raw_stage_bytes;
   float* colscale = reinterpret_cast<float*>(wsm + 2 * W_BYTES);
   float2* mu = reinterpret_cast<float2*>(colscale + NP);   // [KP] {-mu, 0}
   uint32_t* shist = reinterpret_cast<uint32_t*>(mu + KP);  // [2048] digit-0 histogram
@@ -340,17 +337,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
         mbar_wait(&a_full[as], aph);
         mbar_wait(&acc_empty[acs], cph ^ 1);
         tc_fence_after();
-        const uint8_t* abase = a_ring + as * 2 * A_BYTES;
+        const uint32_t abase = tmem + kScoreABase + as * KP;  // A from TMEM
         const uint32_t d = tmem + acs * NP;
 #pragma unroll
         for (int ks = 0; ks < KP / 16; ++ks) {
-          const uint64_t ahi = smem_desc(abase + ks * 256, 128, SBO_A);
-          const uint64_t alo = smem_desc(abase + A_BYTES + ks * 256, 128, SBO_A);
+          const uint32_t ahi = abase + ks * 8;
+          const uint32_t alo = abase + KP / 2 + ks * 8;
           const uint64_t bhi = smem_desc(wsm + ks * 256, 128, SBO_B);
           const uint64_t blo = smem_desc(wsm + W_BYTES + ks * 256, 128, SBO_B);
-          mma_f16(d, ahi, bhi, idesc, ks > 0);
-          mma_f16(d, ahi, blo, idesc, 1);
-          mma_f16(d, alo, bhi, idesc, 1);
+          mma_f16_ts(d, ahi, bhi, idesc, ks > 0);
+          mma_f16_ts(d, ahi, blo, idesc, 1);
+          mma_f16_ts(d, alo, bhi, idesc, 1);
         }
         mma_commit(&a_empty[as]);
         mma_commit(&acc_full[acs]);
@@ -413,16 +410,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
     //   odd B -> 3; per-line gains given -> 2; moments pass proved raw >= dark -> 0; else 1
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
     if (B & 1)
-      transform_loop<KP, 3>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 3>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else if (p.gain != nullptr)
-      transform_loop<KP, 2>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 2>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else if (noclamp)
-      transform_loop<KP, 0>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 0>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
                             a_empty);
     else
-      transform_loop<KP, 1>(p, n, blk, g0, gstep, raw_ring, a_ring, mu, raw_full, raw_empty, a_full,
+      transform_loop<KP, 1>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
                             a_empty);
   }
   tc_fence_before();
@@ -473,8 +470,7 @@ static int kp_for(int B) { return ((B + 15) / 16) * 16; }
 template <int KP>
 static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
-  const size_t A_BYTES = 128u * KP * 2u;
-  const size_t fixed = kScoreAStages * 2 * A_BYTES + wpack_bytes_for(KP) + KP * 8 + kTopkBins * 4 +
+  const size_t fixed = wpack_bytes_for(KP) + KP * 8 + kTopkBins * 4 +
                        (2 * kScoreRawStagesMax + 2 * kScoreAStages + 5) * 8 + 16 + 64;
   int nraw = (int)((kSmemMax - fixed) / p.raw_stage_bytes);
   if (nraw > kScoreRawStagesMax) nraw = kScoreRawStagesMax;

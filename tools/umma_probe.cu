@@ -137,6 +137,99 @@ int test_f16_kmajor() {
   return maxerr < 1e-2;
 }
 
+// A from TMEM (tcgen05.st by the 128 threads, 2 f16 per 32-bit column, even k
+// in the low half) x B K-major in smem: the layout the score kernel relies on
+__global__ void ts_kernel(const uint32_t* __restrict__ apack, const uint8_t* __restrict__ bbytes,
+                          int nb, int K, int N, uint32_t idesc, uint32_t* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t taddr_s;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sm[i] = bbytes[i];
+  fence_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if ((threadIdx.x >> 5) == 0) tmem_alloc(&taddr_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = taddr_s;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, r = threadIdx.x;
+  const uint32_t lanebase = tbase + ((uint32_t)(32 * w) << 16);
+  // A occupies columns [256, 256 + K/2)
+  for (int c = 0; c < K / 2; c += 4)
+    tmem_st4(lanebase + 256 + c, apack[r * (K / 2) + c], apack[r * (K / 2) + c + 1],
+             apack[r * (K / 2) + c + 2], apack[r * (K / 2) + c + 3]);
+  tmem_st_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t SBO = (K / 8) * 128;
+    for (int ks = 0; ks < K / 16; ++ks)
+      mma_f16_ts(tbase, tbase + 256 + ks * 8, smem_desc(sm + ks * 256, 128, SBO), idesc, ks > 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < N; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(lanebase + c, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) out[r * N + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc(tbase, 512);
+}
+
+int test_f16_a_in_tmem() {
+  const int M = 128, N = 80, K = 80;
+  std::vector<float> A(M * K), B(N * K);
+  srand(3);
+  for (auto& v : A) v = (float)((rand() % 2001) - 1000) / 64.0f;
+  for (auto& v : B) v = (float)((rand() % 2001) - 1000) / 128.0f;
+  std::vector<uint32_t> apack(M * K / 2);
+  for (int r = 0; r < M; ++r)
+    for (int k = 0; k < K; k += 2)
+      apack[r * (K / 2) + k / 2] = (uint32_t)h16(A[r * K + k]) | ((uint32_t)h16(A[r * K + k + 1]) << 16);
+  const uint32_t LBO = 128, SBO = (K / 8) * 128;
+  std::vector<uint8_t> bytes(N * K * 2, 0);
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k) {
+      uint16_t h = h16(B[n * K + k]);
+      uint32_t off = (n / 8) * SBO + (k / 8) * LBO + (n % 8) * 16 + (k % 8) * 2;
+      bytes[off] = h & 0xff;
+      bytes[off + 1] = h >> 8;
+    }
+  uint32_t *da, *dout;
+  uint8_t* db;
+  CK(cudaMalloc(&da, apack.size() * 4));
+  CK(cudaMalloc(&db, bytes.size()));
+  CK(cudaMalloc(&dout, M * N * 4));
+  CK(cudaMemcpy(da, apack.data(), apack.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db, bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
+  CK(cudaFuncSetAttribute(ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000));
+  ts_kernel<<<1, 128, bytes.size()>>>(da, db, (int)bytes.size(), K, N, idesc_f16_f32(M, N, 0, 0),
+                                      dout);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<uint32_t> out(M * N);
+  CK(cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost));
+  double maxerr = 0;
+  for (int r = 0; r < M; ++r)
+    for (int n = 0; n < N; ++n) {
+      double ref = 0;
+      for (int k = 0; k < K; ++k) ref += (double)A[r * K + k] * B[n * K + k];
+      float got;
+      memcpy(&got, &out[r * N + n], 4);
+      maxerr = fmax(maxerr, fabs(got - ref));
+    }
+  printf("f16 A-in-TMEM 128x80x80: max abs err %.3g %s\n", maxerr, maxerr < 1e-2 ? "OK" : "FAIL");
+  return maxerr < 1e-2;
+}
+
 int test_i8_mnmajor() {
   // Gram-shaped: A = D^T (M = bands, MN-major), B = D^T (N = bands), K = pixels
   const int M = 128, N = 80, K = 128, MV = 80;
@@ -226,6 +319,7 @@ void test_rounding() {
 int main() {
   int ok = test_f16_kmajor();
   ok &= test_i8_mnmajor();
+  ok &= test_f16_a_in_tmem();
   test_rounding();
   printf(ok ? "PROBE OK\n" : "PROBE FAIL\n");
   return ok ? 0 : 1;
