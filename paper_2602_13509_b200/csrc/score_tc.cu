@@ -330,7 +330,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
   } else if (warp == kMmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       mbar_wait(w_bar, 0);
-      constexpr uint32_t idesc = idesc_f16_f32(128, NP, 0, 0);
       int as = 0, acs = 0;
       uint32_t aph = 0, cph = 0;
       for (int t = 0; t < n; ++t) {
@@ -339,15 +338,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
         tc_fence_after();
         const uint32_t abase = tmem + kScoreABase + as * KP;  // A from TMEM
         const uint32_t d = tmem + acs * NP;
+        // W = L^-1 is lower triangular: k-step ks (k in [16ks, 16ks+16)) only feeds
+        // outputs j >= 16ks, so its MMAs cover N = KP - 16ks columns from column 16ks
+        // (40 % fewer tensor cycles at KP = 80); k-step 0 spans every column and
+        // initialises the accumulator.
 #pragma unroll
         for (int ks = 0; ks < KP / 16; ++ks) {
           const uint32_t ahi = abase + ks * 8;
           const uint32_t alo = abase + KP / 2 + ks * 8;
-          const uint64_t bhi = smem_desc(wsm + ks * 256, 128, SBO_B);
-          const uint64_t blo = smem_desc(wsm + W_BYTES + ks * 256, 128, SBO_B);
-          mma_f16_ts(d, ahi, bhi, idesc, ks > 0);
-          mma_f16_ts(d, ahi, blo, idesc, 1);
-          mma_f16_ts(d, alo, bhi, idesc, 1);
+          const uint32_t off_b = (uint32_t)(2 * ks) * SBO_B + ks * 256;  // rows j >= 16ks
+          const uint64_t bhi = smem_desc(wsm + off_b, 128, SBO_B);
+          const uint64_t blo = smem_desc(wsm + W_BYTES + off_b, 128, SBO_B);
+          const uint32_t idk = idesc_f16_f32(128, NP - 16 * ks, 0, 0);
+          const uint32_t dk = d + 16 * ks;
+          mma_f16_ts(dk, ahi, bhi, idk, ks > 0);
+          mma_f16_ts(dk, ahi, blo, idk, 1);
+          mma_f16_ts(dk, alo, bhi, idk, 1);
         }
         mma_commit(&a_empty[as]);
         mma_commit(&acc_full[acs]);
