@@ -27,16 +27,19 @@
 namespace skyrx {
 using namespace umma;
 
-// Warp roles (persistent CTA, one per SM, 448 threads):
-//   warps 0-7   transform : two threads per pixel row (each half of the bands)
-//   warps 8-11  epilogue  : one thread per pixel row (TMEM lane quarter = warp % 4)
-//   warp 12     TMA producer, warp 13 MMA issuer (one elected lane each)
-constexpr int kTcTransform = 256;
+// Warp roles (persistent CTA, one per SM):
+//   warps 0..4G-1  transform : G threads per pixel row, each owning a contiguous
+//                              run of the row's 8-band chunks (G = 3 for KP >= 48)
+//   next 4 warps   epilogue  : one thread per pixel row (TMEM lane quarter = warp % 4)
+//   last 2 warps   TMA producer, MMA issuer (one elected lane each)
+__host__ __device__ constexpr int sc_groups(int kp) { return kp >= 48 ? 3 : 2; }
+__host__ __device__ constexpr int sc_threads(int kp) { return 128 * sc_groups(kp) + 128 + 64; }
+// registers per thread such that the busiest SM sub-partition (ceil(warps / 4)
+// warps) fits its 16K-register file
+__host__ __device__ constexpr int sc_maxreg(int kp) {
+  return (16384 / (32 * ((sc_threads(kp) / 32 + 3) / 4))) / 8 * 8;
+}
 constexpr int kTcEpilogue = 128;
-constexpr int kTcThreads = kTcTransform + kTcEpilogue + 64;
-constexpr int kEpiWarp0 = kTcTransform / 32;           // 8
-constexpr int kTmaWarp = (kTcTransform + kTcEpilogue) / 32;  // 12
-constexpr int kMmaWarp = kTmaWarp + 1;                 // 13
 constexpr int kScoreRawStagesMax = 8;
 constexpr int kScoreAStages = 2;
 constexpr int kScoreAcc = 3;    // TMEM accumulator ring: columns [0, 3 KP)
@@ -125,11 +128,12 @@ __device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint32_t thi
 template <int MODE, int CHT>
 __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&tco)[CHT * 4],
                                               const float2 (&tnof)[CHT * 4], const float2* nm,
-                                              float g, uint32_t thi, uint32_t tlo) {
+                                              float g, uint32_t thi, uint32_t tlo, int cnt) {
   const float gi = 1.0f / g;
   const float2 bias = make_float2(-8388608.0f, -8388608.0f);
 #pragma unroll
   for (int cc = 0; cc < CHT; ++cc) {
+    if (cc >= cnt) break;  // warp-uniform
     float2 rf[4];
     if (MODE != 3) {  // 4-byte aligned rows: two counts per LDS.32
 #pragma unroll
@@ -167,20 +171,24 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
 
 // Transform warps: calibrate + centre + f16-split every tile of this CTA into
 // the A ring.  MODE is uniform over the launch (see transform_row).
-template <int KP, int MODE>
+template <int KP, int MODE, int CHT>
 __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int blk, int64_t g0,
                                                int64_t gstep, uint8_t* raw_ring, uint32_t tmem,
                                                const float2* mu, uint64_t* raw_full,
                                                uint64_t* raw_empty, uint64_t* a_full,
                                                uint64_t* a_empty) {
   constexpr int NCH = KP / 8;
-  constexpr int CHT = NCH / 2;  // chunks per thread (row half)
+  constexpr int NG = sc_groups(KP);  // CHT = chunks per thread (compile time)
   const int tid = threadIdx.x;
   const int r = tid & 127;  // pixel row of the tile
-  const int h = tid >> 7;   // band half
+  const int h = tid >> 7;   // band group
   const int lane = tid & 31;
-  const int c_lo = CHT * h;
   const int B = p.ts.B;
+  // real chunks only (8*c < B); the all-padding chunks of A are zeroed once
+  const int nchr = (B + 7) / 8;
+  const int cpg = (nchr + NG - 1) / NG;
+  const int c_lo = cpg * h;
+  const int cnt = min(cpg, nchr - c_lo);
   const int NR = p.nraw;
   // this row's calibration in registers; a tile row maps to the same sample of
   // the current block on every tile, so the tables change only with the block
@@ -209,6 +217,15 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
   // A stage `as` lives in TMEM columns [kScoreABase + as*KP, + KP): hi in the first
   // KP/2 (two f16 per column), lo in the next KP/2; this thread's lane = its row
   const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase + 4 * c_lo;
+  if (h == 0) {  // zero the all-padding chunks of both A stages (never rewritten)
+    const uint32_t tz = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase;
+    for (int st = 0; st < kScoreAStages; ++st)
+      for (int c = nchr; c < NCH; ++c) {
+        tmem_st4(tz + st * KP + 4 * c, 0u, 0u, 0u, 0u);
+        tmem_st4(tz + st * KP + KP / 2 + 4 * c, 0u, 0u, 0u, 0u);
+      }
+    tmem_st_wait();
+  }
   const float2* nm0 = mu + 8 * c_lo;
   int s = 0, as = 0;
   uint32_t ph = 0, aph = 0;
@@ -226,7 +243,7 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
     tc_fence_after();
     const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
     const uint32_t thi = tl + as * KP;
-    transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, thi, thi + KP / 2);
+    transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, thi, thi + KP / 2, cnt);
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
@@ -240,8 +257,12 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
 }
 
 template <int KP>
-__global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
+__global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ScoreTcParams p) {
+  constexpr int kTcTransform = 128 * sc_groups(KP);
+  constexpr int kEpiWarp0 = kTcTransform / 32;
+  constexpr int kTmaWarp = (kTcTransform + kTcEpilogue) / 32;
+  constexpr int kMmaWarp = kTmaWarp + 1;
   constexpr int NP = KP;
   constexpr int NCH = KP / 8;            // 8-band chunks per row
   static_assert(KP % 16 == 0, "KP is a multiple of 16: both row halves own NCH/2 chunks");
@@ -415,18 +436,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) score_tc_kernel(
     // one arithmetic mode for the whole launch (uniform branch):
     //   odd B -> 3; per-line gains given -> 2; moments pass proved raw >= dark -> 0; else 1
     const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
+    // chunks per thread: sized for B = KP; a smaller B runs fewer (cnt, runtime)
+    constexpr int NG = sc_groups(KP), NCH = KP / 8;
+    constexpr int CHT = (NCH + NG - 1) / NG;
     if (B & 1)
-      transform_loop<KP, 3>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
-                            a_empty);
+      transform_loop<KP, 3, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
+                                 a_full, a_empty);
     else if (p.gain != nullptr)
-      transform_loop<KP, 2>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
-                            a_empty);
+      transform_loop<KP, 2, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
+                                 a_full, a_empty);
     else if (noclamp)
-      transform_loop<KP, 0>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
-                            a_empty);
+      transform_loop<KP, 0, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
+                                 a_full, a_empty);
     else
-      transform_loop<KP, 1>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty, a_full,
-                            a_empty);
+      transform_loop<KP, 1, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
+                                 a_full, a_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -512,7 +536,7 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
   }
   cudaFuncSetAttribute(score_tc_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  score_tc_kernel<KP><<<grid, kTcThreads, smem, st>>>(map, p);
+  score_tc_kernel<KP><<<grid, sc_threads(KP), smem, st>>>(map, p);
   SKYRX_CHECK_LAUNCH("score_tc_kernel");
   return SKYRX_OK;
 }

@@ -353,6 +353,21 @@ class TestDetect:
         rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
         assert rel.max() < 2e-5, rel.max()
 
+    @pytest.mark.parametrize("L", [1, 33, 129])
+    def test_tensor_core_score_schedule_edges(self, P, L):
+        """Fewer tiles than sample blocks, and ragged narrow-block tiles (2-D TMA box
+        past the last line) against the FFMA kernel."""
+        S, B = 900, 70
+        t = osynth.make_tables(43, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        tab = P.CalibrationTables(t.dark, t.coeff)
+        det_tc = P.detect(raw_cube(P, raw), tab, plan=P.DetectPlan(L, S, B))
+        plan_ff = P.DetectPlan(L, S, B)
+        plan_ff.tc = False
+        det_ff = P.detect(raw_cube(P, raw), tab, plan=plan_ff)
+        rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
+        assert rel.max() < 2e-5, rel.max()
+
     @pytest.mark.parametrize("S,B,L,gain", [(900, 70, 300, 1.0), (64, 70, 4100, 2.5),
                                             (96, 48, 2800, 1.0), (40, 16, 6600, 1.0),
                                             (1024, 128, 260, 1.0), (128, 79, 2100, 0.75)])
