@@ -38,9 +38,10 @@ using namespace umma;
 constexpr int kGrThreads = 320;
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
-// TMA ring depth: 4 stages, 2 for the widest windows (B > ~96) to fit the f64 accumulator
+// TMA ring depth (stage = 128 lines x (128 + second-box) bytes) within the shared memory
+// left beside the f64 accumulator: 8 stages, 6 for windows > 160 B, 2 for > 192 B
 template <int NCH>
-__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : 4; }
+__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 6 : 8); }
 constexpr int64_t kGrMaxUnitLines = 32768;
 
 struct GramRawParams {
@@ -63,6 +64,11 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
 }
 
 // TMEM columns per accumulator buffer: full-width block + the bottom-right block
+// width of the second box (bytes 128.. of the window): 32, 64 or 128
+template <int NCH>
+__host__ __device__ constexpr uint32_t gr_w2b() {
+  return NCH <= 8 ? 0u : (16 * NCH - 128 <= 32 ? 32u : (16 * NCH - 128 <= 64 ? 64u : 128u));
+}
 template <int NCH>
 __host__ __device__ constexpr int gr_bufcols() {
   return ((16 * NCH + (NCH > 8 ? 16 * NCH - 128 : 0)) + 31) / 32 * 32;
@@ -72,16 +78,20 @@ __host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 51
 
 template <int NCH>
 __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 const __grid_constant__ CUtensorMap tmap1,
                                                                  GramRawParams p) {
   constexpr int kGrStages = gr_stages<NCH>();
   constexpr int NW = 16 * NCH;                    // window bytes = MMA N
   constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
   constexpr int N2 = TWO_M ? NW - 128 : 0;        // ... only over columns 128..NW-1
-  // a tile = NATOM boxes of [128 window bytes][Lb lines], 128B-swizzled by TMA:
-  // the canonical MN-major SWIZZLE_128B UMMA layout (LBO = atom stride, SBO = 8 lines)
-  constexpr int NATOM = TWO_M ? 2 : 1;
+  // a tile = a box of [128 window bytes][Lb lines], 128B-swizzled by TMA (the
+  // canonical MN-major SWIZZLE_128B UMMA layout, SBO = 8 lines), plus for wider
+  // windows a box of the W2B bytes past 128 in the matching 32/64/128B swizzle
   constexpr uint32_t ATOM = kGrLb * 128u;
-  constexpr uint32_t STAGE = NATOM * ATOM;
+  constexpr uint32_t W2B = gr_w2b<NCH>();
+  constexpr uint32_t ATOM1 = TWO_M ? kGrLb * W2B : 0u;
+  constexpr uint32_t STAGE = ATOM + ATOM1;
+  constexpr uint32_t LT1 = W2B == 32 ? 6u : (W2B == 64 ? 4u : 2u);
   constexpr int G = kGrWorkers / NCH;             // scan line groups
   constexpr int BUFC = gr_bufcols<NCH>();
   constexpr int NBUF = gr_nbuf<NCH>();
@@ -149,16 +159,17 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           const int st = t % kGrStages;
           mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], STAGE);
-#pragma unroll
-          for (int a = 0; a < NATOM; ++a)
-            tma_load_2d(stages + st * STAGE + a * ATOM, &tmap, 16 * c0 + 128 * a,
+          tma_load_2d(stages + st * STAGE, &tmap, 16 * c0, (int)(l0 + (int64_t)k * kGrLb),
+                      &full[st]);
+          if (TWO_M)
+            tma_load_2d(stages + st * STAGE + ATOM, &tmap1, 16 * c0 + 128,
                         (int)(l0 + (int64_t)k * kGrLb), &full[st]);
         }
       }
     }
   } else if (warp == 9) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
-      constexpr uint32_t id = idesc_u8_s32(128, NW);
+      constexpr uint32_t id = idesc_u8_s32(128, TWO_M ? 128 : NW);
       constexpr uint32_t id2 = idesc_u8_s32(128, N2 > 0 ? N2 : 16);
       int t = 0, unit = 0;
       for (int64_t u = u0; u < u1; u += ustep, ++unit) {
@@ -180,10 +191,17 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           for (int ks = 0; ks < kGrLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
             const uint8_t* kb = base + ks * 4096;  // 32 lines = 4 swizzle atoms of 8 x 128 B
-            mma_i8(d, smem_desc_sw128(kb, ATOM, 1024), smem_desc_sw128(kb, ATOM, 1024), id, acc);
-            if (TWO_M)  // rows 128..NW-1 x columns 128..NW-1 (the rest is the transpose)
-              mma_i8(d + NW, smem_desc_sw128(kb + ATOM, ATOM, 1024),
-                     smem_desc_sw128(kb + ATOM, ATOM, 1024), id2, acc);
+            const uint64_t d0 = smem_desc_sw128(kb, ATOM, 1024);
+            mma_i8(d, d0, d0, id, acc);
+            if (TWO_M) {
+              // bytes 128.. in their own (narrower) swizzle: columns 128..NW-1 of rows
+              // 0..127, and rows 128..NW-1 x columns 128..NW-1 (the rest is the
+              // transpose); the 128-row A of the second MMA re-reads its one atom
+              // (LBO 0): rows >= NW-128 are never used
+              const uint64_t d1 = smem_desc_swz(base + ATOM + ks * 32 * W2B, 0, 8 * W2B, LT1);
+              mma_i8(d + 128, d0, d1, id2, acc);
+              mma_i8(d + NW, d1, d1, id2, acc);
+            }
           }
           mma_commit(&empty[st]);
         }
@@ -206,11 +224,15 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         mbar_wait(&full[st], (t / kGrStages) & 1);
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
-          const uint8_t* atom = stages + st * STAGE + (c >> 3) * ATOM;
+          // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
+          const bool in1 = c >= 8;
+          const uint32_t wdt = in1 ? W2B : 128u;
+          const uint8_t* atom = stages + st * STAGE + (in1 ? ATOM : 0u);
+          const int q = c & 7;
 #pragma unroll 4
           for (int l = g; l < valid; l += G) {
-            // 128B swizzle: 16-B chunk c of line l sits at chunk c ^ (l & 7)
-            const uint4 v = *reinterpret_cast<const uint4*>(atom + l * 128 + (((c & 7) ^ (l & 7)) << 4));
+            const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
+            const uint4 v = *reinterpret_cast<const uint4*>(atom + l * wdt + ((q ^ sw) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
             sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
@@ -393,9 +415,25 @@ static int nch_for(int B) {
 }
 
 template <int NCH>
-static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* moments,
-                           const double* shift, cudaStream_t st) {
-  constexpr uint32_t STAGE = (NCH > 8 ? 2u : 1u) * kGrLb * 128u;
+static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawParams p,
+                           double* moments, const double* shift, cudaStream_t st) {
+  constexpr uint32_t W2B = gr_w2b<NCH>();
+  constexpr uint32_t STAGE = kGrLb * (128u + W2B);
+  CUtensorMap map1 = map;
+  if (W2B > 0) {  // the bytes past 128 of the window: narrower box, matching swizzle
+    const cuuint64_t line_bytes = (cuuint64_t)p.S * p.B * 2;
+    cuuint64_t dims[2] = {line_bytes, (cuuint64_t)p.L};
+    cuuint64_t strides[1] = {line_bytes};
+    cuuint32_t box[2] = {W2B, (cuuint32_t)kGrLb};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tensor_map_encoder()(
+        &map1, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)raw, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE,
+        W2B == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                  : (W2B == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
   constexpr int G = kGrWorkers / NCH;
   constexpr int kGrStages = gr_stages<NCH>();
   const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
@@ -404,7 +442,7 @@ static int launch_gram_raw(const CUtensorMap& map, GramRawParams p, double* mome
   if (p.units < grid) grid = (int)p.units;
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, p);
+  gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
   const int work = p.B * p.B + p.B + 1;
   double* tot = p.part + (size_t)kSMs * work;  // after the per-CTA partials
@@ -475,7 +513,7 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   switch (nch) {
 #define SKYRX_NCH(k) \
   case k:            \
-    return launch_gram_raw<k>(map, p, moments, shift, st);
+    return launch_gram_raw<k>(map, raw, p, moments, shift, st);
     SKYRX_NCH(1) SKYRX_NCH(2) SKYRX_NCH(3) SKYRX_NCH(4) SKYRX_NCH(5) SKYRX_NCH(6) SKYRX_NCH(7)
     SKYRX_NCH(8) SKYRX_NCH(9) SKYRX_NCH(10) SKYRX_NCH(11) SKYRX_NCH(12) SKYRX_NCH(13)
     SKYRX_NCH(14) SKYRX_NCH(15) SKYRX_NCH(16)

@@ -130,6 +130,11 @@ __device__ __forceinline__ uint64_t smem_desc(const void* base, uint32_t lbo, ui
   return d;
 }
 
+// any swizzle mode: layout 2 = 128B, 4 = 64B, 6 = 32B (cute UMMA::LayoutType)
+__device__ __forceinline__ uint64_t smem_desc_swz(const void* base, uint32_t lbo, uint32_t sbo,
+                                                  uint32_t layout) {
+  return smem_desc(base, lbo, sbo) | ((uint64_t)layout << 61);
+}
 // 128-byte swizzle atoms (TMA CU_TENSOR_MAP_SWIZZLE_128B), 1024-B aligned bases
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* base, uint32_t lbo, uint32_t sbo) {
   return smem_desc(base, lbo, sbo) | ((uint64_t)2 << 61);
