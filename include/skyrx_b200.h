@@ -178,6 +178,23 @@ int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
                    const float* mu_hilo, const void* wpack, const int32_t* flags,
                    float* scores, uint32_t* max_key, uint32_t* topk_hist0, void* stream);
 
+/* Exact-digit tensor-core score (raw-byte moments path ran, no clamp, one gain,
+ * B <= 128): per sample column s, z = V_s a + q_s with the integer deviations
+ * a = r - R_s (R_s = rint(dark + mu g / coeff)) split into two f16-exact digits
+ * and V_s = W diag(coeff_s / g) in f16 hi/lo.  skyrx_score_prep writes one
+ * record per sample (skyrx_score_rec_bytes(B) bytes each; batch backgrounds of
+ * samples records, background i from whiten64 + i*B*B and mu_hilo + i*2B with the
+ * SAME dark/coeff/gain).  Raw counts >= 4096 set flags |= 16 (the digit split
+ * assumes 12-bit data): the caller then rescores with skyrx_score_tc. */
+size_t skyrx_score_rec_bytes(int32_t bands);
+int skyrx_score_prep(const double* whiten64, const float* mu_hilo, int32_t samples,
+                     int32_t bands, const float* dark, const float* coeff, double gain,
+                     int32_t batch, void* records, void* stream);
+int skyrx_score_tcs_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
+int skyrx_score_tcs(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                    const void* records, int32_t* flags, float* scores, uint32_t* max_key,
+                    uint32_t* topk_hist0, void* stream);
+
 /* The kernel slot itself: _accel.mahalanobis_sq(pixels, mu, chol_lower)
  * (_accel.py:109-131) with FP64 arithmetic; pixels f32 or f64 (kind F32/F64).
  * whiten64 is a f64 workspace of B*B + BP*BP doubles, BP = 8*ceil(B/8). */

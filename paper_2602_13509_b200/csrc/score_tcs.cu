@@ -1,0 +1,560 @@
+// K4-TCS — fused calibrate + RX score with EXACT integer operands, one sample
+// column per work unit (tcgen05, A from TMEM).
+//
+// For sample s, gain g and no clamping (the moments pass proved raw >= dark):
+//     x - mu = (c_s / g) (r - R_s) + e_s,   R_s = rint(dark_s + mu g / c_s)  (integer counts)
+//     z = W (x - mu) = V_s a + q_s,          a = r - R_s,  V_s = W diag(c_s / g),  q_s = W e_s
+// so the tensor core only needs the INTEGER deviations a (exact for 12-bit raw):
+//     u = r + (4096 - R) in [0, 8192),  a = 64 h + l - 4096,  h = u >> 6, l = u & 63
+// with A_hi = 64 h - 4096 and A_lo = l built from u's bits by two LOP3 + HADD2 each
+// (f16-exact), and V_s split into f16 hi + lo: z = A_hi V_hi + A_hi V_lo + A_lo V_hi
+// + A_lo V_lo, f32 in TMEM.  Compared with K4-TC (score_tc.cu) the per-band work
+// drops from calibrate + centre + float split to a handful of integer ops, and the
+// per-row calibration tables shrink to one packed (4096 - R) word per band pair,
+// so B up to 128 fits (BASELINE config 5).  Per-sample V_s, q_s and R_s come from
+// skyrx_score_prep (one record per sample column, streamed in per unit).
+//
+// Work unit = (sample s, line range) dealt round-robin to persistent CTAs, like the
+// raw-byte moments kernel: at any moment the grid reads neighbouring samples of the
+// same lines.  Tiles are 128 lines of one sample: TMA 2-D box (16-B aligned window
+// of the line) into a raw ring; warps:
+//   0 .. 4G-1   transform  (G threads per line, each a run of 8-band chunks)
+//   next 4      epilogue   (tcgen05.ld, z = acc + q', sum of squares, store, max, hist)
+//   last 2      TMA producer, MMA issuer
+// Raw values >= 4096 (not 12-bit) set flags |= 16: the caller rescores with K4-TC.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
+
+namespace skyrx {
+using namespace umma;
+
+namespace tcs {
+
+constexpr int kLines = 128;       // lines per tile (= MMA M, TMEM lanes)
+constexpr int kRawMax = 6;        // raw ring depth (bounded by shared memory)
+constexpr int kAStages = 2;
+constexpr int kHist = 2048;
+constexpr int64_t kMaxUnitLines = 16384;
+
+__host__ __device__ constexpr int groups(int kp) { return kp >= 112 ? 4 : (kp >= 48 ? 3 : 2); }
+__host__ __device__ constexpr int threads(int kp) { return 128 * groups(kp) + 128 + 64; }
+__host__ __device__ constexpr int maxreg(int kp) {
+  return (16384 / (32 * ((threads(kp) / 32 + 3) / 4))) / 8 * 8;
+}
+__host__ __device__ constexpr int nacc(int kp) { return 2 * kp + 3 * kp <= 512 ? 3 : 2; }
+
+// per-sample record: V hi | V lo (KP x KP f16, K-major canonical layout) | T (KP u16:
+// 4096 - R, 0 for padding bands) | q' (KP f32, = q / inv_scale) | inv_scale (f32)
+__host__ __device__ constexpr uint32_t rec_vbytes(int kp) { return (uint32_t)kp * kp * 2u; }
+__host__ __device__ constexpr uint32_t rec_bytes(int kp) {
+  return ((2u * rec_vbytes(kp) + 2u * kp + 4u * kp + 4u) + 127u) & ~127u;
+}
+
+struct Params {
+  const uint8_t* rec;  // S records of rec_bytes(KP)
+  float* scores;
+  uint32_t* max_key;
+  uint32_t* hist0;
+  int32_t* flags;
+  int64_t L;
+  int32_t S, B;
+  int64_t split_lines;
+  int64_t units;
+  int32_t ne;          // u16 per line in the tile box (16-B multiple, odd # of 16-B chunks)
+  int32_t nraw;
+  uint32_t stage_bytes;
+};
+
+__device__ __forceinline__ void unit_geom(const Params& p, int64_t u, int& s, int64_t& l0,
+                                          int64_t& nl) {
+  s = (int)(u % p.S);
+  l0 = (u / p.S) * p.split_lines;
+  nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
+}
+
+// one band-chunk (8 bands = 4 packed words) -> A_hi / A_lo words
+__device__ __forceinline__ void digits4(const uint32_t (&w)[4], const uint32_t* t,
+                                        uint32_t (&hw)[4], uint32_t (&lw)[4], uint32_t& chk) {
+  const __half2 bias_hi = __floats2half2_rn(-36864.0f, -36864.0f);  // 32768 + 4096
+  const __half2 bias_lo = __floats2half2_rn(-1024.0f, -1024.0f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    chk |= w[i];
+    const uint32_t u = w[i] + t[i];  // two u16 lanes, no carry (w <= 4095, t <= 4096)
+    // f16 32768 + 64 h  (h = u >> 6 < 128: ulp of 32768 is 32)  and  f16 1024 + l
+    const uint32_t hb = ((u >> 5) & 0x00FE00FEu) | 0x78007800u;
+    const uint32_t lb = (u & 0x003F003Fu) | 0x64006400u;
+    __half2 hh = __hadd2(*reinterpret_cast<const __half2*>(&hb), bias_hi);
+    __half2 ll = __hadd2(*reinterpret_cast<const __half2*>(&lb), bias_lo);
+    hw[i] = *reinterpret_cast<uint32_t*>(&hh);
+    lw[i] = *reinterpret_cast<uint32_t*>(&ll);
+  }
+}
+
+// transform of one unit's tiles at window offset OFFW words (band 0 at word OFFW of
+// 16-B chunk 0); CHT = chunks per thread (compile time), cnt = this thread's count
+template <int KP, int CHT, int OFFW>
+__device__ __forceinline__ void transform_unit(const Params& p, int ntile, uint8_t* raw_ring,
+                                               uint32_t tl, const uint32_t* tt, int c_lo, int cnt,
+                                               uint64_t* raw_full, uint64_t* raw_empty,
+                                               uint64_t* a_full, uint64_t* a_empty, int& s,
+                                               uint32_t& ph, int& as, uint32_t& aph,
+                                               uint32_t& chk) {
+  const int r = threadIdx.x & 127;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rowb = (uint32_t)p.ne * 2u;
+  for (int k = 0; k < ntile; ++k) {
+    mbar_wait(&raw_full[s], ph);
+    mbar_wait(&a_empty[as], aph ^ 1);
+    tc_fence_after();
+    const uint4* row = reinterpret_cast<const uint4*>(raw_ring + s * p.stage_bytes + r * rowb);
+    uint4 cur = cnt > 0 ? row[c_lo] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int cc = 0; cc < CHT; ++cc) {
+      if (cc >= cnt) break;  // warp-uniform
+      const uint4 nxt = row[c_lo + cc + 1];
+      uint32_t w[4];
+      const uint32_t c4[8] = {cur.x, cur.y, cur.z, cur.w, nxt.x, nxt.y, nxt.z, nxt.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = c4[OFFW + i];
+      uint32_t hw[4], lw[4];
+      digits4(w, tt + 4 * cc, hw, lw, chk);
+      const uint32_t col = tl + as * KP + 4 * (c_lo + cc);
+      tmem_st4(col, hw[0], hw[1], hw[2], hw[3]);
+      tmem_st4(col + KP / 2, lw[0], lw[1], lw[2], lw[3]);
+      cur = nxt;
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&a_full[as]);
+      mbar_arrive(&raw_empty[s]);
+    }
+    if (++s == p.nraw) s = 0, ph ^= 1;
+    if (++as == kAStages) as = 0, aph ^= 1;
+  }
+}
+
+template <int KP>
+__global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                         const __grid_constant__ Params p) {
+  constexpr int NG = groups(KP);
+  constexpr int NT = 128 * NG;           // transform threads
+  constexpr int EPI0 = NT / 32, TMAW = EPI0 + 4, MMAW = TMAW + 1;
+  constexpr int NCH = KP / 8;
+  constexpr int CHT = (NCH + NG - 1) / NG;
+  constexpr int NACC = nacc(KP);
+  constexpr int ABASE = NACC * KP;       // A ring TMEM columns [ABASE, ABASE + 2 KP)
+  constexpr uint32_t VB = rec_vbytes(KP);
+  constexpr uint32_t RB = rec_bytes(KP);
+  constexpr uint32_t SBO_B = (KP / 8) * 128u;
+  static_assert(ABASE + kAStages * KP <= 512, "TMEM budget");
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* recs = sm;                              // [2][RB]
+  uint8_t* raw_ring = recs + 2 * RB;               // [nraw][stage_bytes]
+  uint32_t* shist = reinterpret_cast<uint32_t*>(raw_ring + p.nraw * p.stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(shist + kHist);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + kRawMax;
+  uint64_t* a_full = raw_empty + kRawMax;
+  uint64_t* a_empty = a_full + kAStages;
+  uint64_t* acc_full = a_empty + kAStages;
+  uint64_t* acc_empty = acc_full + 3;
+  uint64_t* rec_full = acc_empty + 3;
+  uint64_t* rec_empty = rec_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rec_empty + 2);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int B = p.B;
+  const int64_t u0 = blockIdx.x, ustep = gridDim.x;
+
+  if (tid == 0) {
+    for (int i = 0; i < p.nraw; ++i) mbar_init(&raw_full[i], 1), mbar_init(&raw_empty[i], NT / 32);
+    for (int i = 0; i < kAStages; ++i) mbar_init(&a_full[i], NT / 32), mbar_init(&a_empty[i], 1);
+    for (int i = 0; i < NACC; ++i) mbar_init(&acc_full[i], 1), mbar_init(&acc_empty[i], 4);
+    // a record is released by the MMA commit, the transform warps (T read) and the
+    // epilogue warps (unit's last tile done)
+    for (int i = 0; i < 2; ++i) mbar_init(&rec_full[i], 1), mbar_init(&rec_empty[i], 1 + NT / 32 + 4);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < kHist; i += blockDim.x) shist[i] = 0;
+  if (warp == MMAW) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == TMAW) {
+    if (lane == 0) {  // ------------------------------------------------- TMA producer
+      int s = 0, ui = 0;
+      uint32_t ph = 0;
+      for (int64_t u = u0; u < p.units; u += ustep, ++ui) {
+        int smp;
+        int64_t l0, nl;
+        unit_geom(p, u, smp, l0, nl);
+        const int rb = ui & 1;
+        mbar_wait(&rec_empty[rb], ((ui >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&rec_full[rb], RB);
+        bulk_g2s(recs + rb * RB, p.rec + (size_t)smp * RB, RB, &rec_full[rb]);
+        const int c0 = (int)((((int64_t)smp * B * 2) & ~(int64_t)15) >> 1);
+        const int ntile = (int)((nl + kLines - 1) / kLines);
+        for (int k = 0; k < ntile; ++k) {
+          mbar_wait(&raw_empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&raw_full[s], p.stage_bytes);
+          tma_load_2d(raw_ring + s * p.stage_bytes, &tmap, c0, (int)(l0 + (int64_t)k * kLines),
+                      &raw_full[s]);
+          if (++s == p.nraw) s = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == MMAW) {
+    if (lane == 0) {  // ------------------------------------------------- MMA issuer
+      int as = 0, acs = 0, ui = 0;
+      uint32_t aph = 0, cph = 0;
+      for (int64_t u = u0; u < p.units; u += ustep, ++ui) {
+        int smp;
+        int64_t l0, nl;
+        unit_geom(p, u, smp, l0, nl);
+        const int rb = ui & 1;
+        mbar_wait(&rec_full[rb], (ui >> 1) & 1);
+        const uint8_t* vh = recs + rb * RB;
+        const uint8_t* vl = vh + VB;
+        const int ntile = (int)((nl + kLines - 1) / kLines);
+        for (int k = 0; k < ntile; ++k) {
+          mbar_wait(&a_full[as], aph);
+          mbar_wait(&acc_empty[acs], cph ^ 1);
+          tc_fence_after();
+          const uint32_t abase = tmem + ABASE + as * KP;
+          const uint32_t d = tmem + acs * KP;
+          // V lower triangular: k-step ks feeds outputs j >= 16 ks only
+#pragma unroll
+          for (int ks = 0; ks < KP / 16; ++ks) {
+            const uint32_t ahi = abase + ks * 8, alo = abase + KP / 2 + ks * 8;
+            const uint32_t ob = (uint32_t)(2 * ks) * SBO_B + ks * 256;
+            const uint64_t bhi = smem_desc(vh + ob, 128, SBO_B);
+            const uint64_t blo = smem_desc(vl + ob, 128, SBO_B);
+            const uint32_t id = idesc_f16_f32(128, KP - 16 * ks, 0, 0);
+            const uint32_t dk = d + 16 * ks;
+            mma_f16_ts(dk, ahi, bhi, id, ks > 0);
+            mma_f16_ts(dk, ahi, blo, id, 1);
+            mma_f16_ts(dk, alo, bhi, id, 1);
+            mma_f16_ts(dk, alo, blo, id, 1);
+          }
+          mma_commit(&a_empty[as]);
+          mma_commit(&acc_full[acs]);
+          if (++as == kAStages) as = 0, aph ^= 1;
+          if (++acs == NACC) acs = 0, cph ^= 1;
+        }
+        mma_commit(&rec_empty[rb]);
+      }
+    }
+  } else if (warp >= EPI0) {  // --------------------------------------- epilogue
+    const int r = tid & 127;
+    const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint32_t local_max = 0;
+    int acs = 0, ui = 0;
+    uint32_t cph = 0;
+    for (int64_t u = u0; u < p.units; u += ustep, ++ui) {
+      int smp;
+      int64_t l0, nl;
+      unit_geom(p, u, smp, l0, nl);
+      const int rb = ui & 1;
+      mbar_wait(&rec_full[rb], (ui >> 1) & 1);
+      const float* qv = reinterpret_cast<const float*>(recs + rb * RB + 2 * VB + 2 * KP);
+      const float inv = qv[KP];
+      const float inv2 = inv * inv;
+      const int ntile = (int)((nl + kLines - 1) / kLines);
+      for (int k = 0; k < ntile; ++k) {
+        mbar_wait(&acc_full[acs], cph);
+        tc_fence_after();
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int c = 0; c < KP; c += 16) {
+          uint32_t v[16];
+          tmem_ld16(tb + acs * KP + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; q += 4) {
+            const float4 qq = *reinterpret_cast<const float4*>(qv + c + q);  // broadcast
+            const float2 z0 = fadd2(make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])),
+                                    make_float2(qq.x, qq.y));
+            const float2 z1 = fadd2(make_float2(__uint_as_float(v[q + 2]), __uint_as_float(v[q + 3])),
+                                    make_float2(qq.z, qq.w));
+            acc = ffma2(z0, z0, acc);
+            acc = ffma2(z1, z1, acc);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acs]);
+        const int64_t line = l0 + (int64_t)k * kLines + r;
+        const bool valid = line < l0 + nl;
+        uint32_t key = 0;
+        if (valid) {
+          const float sum = (acc.x + acc.y) * inv2;
+          p.scores[line * p.S + smp] = sum;
+          key = f2ord(sum);
+          local_max = max(local_max, key);
+        }
+        if (p.hist0) {
+          const uint32_t bin = valid ? key >> 21 : 0xFFFFFFFFu;
+          const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+          if (valid && lane == __ffs(peers) - 1) atomicAdd(&shist[bin], __popc(peers));
+        }
+        if (++acs == NACC) acs = 0, cph ^= 1;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rec_empty[rb]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+    if (lane == 0 && local_max && p.max_key) atomicMax(p.max_key, local_max);
+  } else {  // ------------------------------------------------------------ transform
+    const int g = tid >> 7;
+    const int nchr = (B + 7) / 8;
+    const int cpg = (nchr + NG - 1) / NG;
+    const int c_lo = cpg * g;
+    const int cnt = min(cpg, nchr - c_lo);
+    const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + ABASE;
+    if (g == 0) {  // all-padding chunks of both A stages: zero once, never rewritten
+      for (int st = 0; st < kAStages; ++st)
+        for (int c = nchr; c < NCH; ++c) {
+          tmem_st4(tl + st * KP + 4 * c, 0u, 0u, 0u, 0u);
+          tmem_st4(tl + st * KP + KP / 2 + 4 * c, 0u, 0u, 0u, 0u);
+        }
+      tmem_st_wait();
+    }
+    uint32_t chk = 0;
+    int s = 0, as = 0, ui = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int64_t u = u0; u < p.units; u += ustep, ++ui) {
+      int smp;
+      int64_t l0, nl;
+      unit_geom(p, u, smp, l0, nl);
+      const int rb = ui & 1;
+      mbar_wait(&rec_full[rb], (ui >> 1) & 1);
+      uint32_t tt[CHT * 4];
+      const uint32_t* tw = reinterpret_cast<const uint32_t*>(recs + rb * RB + 2 * VB);
+#pragma unroll
+      for (int i = 0; i < CHT * 4; ++i) tt[i] = i < cnt * 4 ? tw[4 * c_lo + i] : 0u;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&rec_empty[rb]);
+      const int ntile = (int)((nl + kLines - 1) / kLines);
+      const int offw = (int)((((int64_t)smp * B * 2) & 15) >> 2);
+      if (offw == 0)
+        transform_unit<KP, CHT, 0>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full, raw_empty,
+                                   a_full, a_empty, s, ph, as, aph, chk);
+      else if (offw == 1)
+        transform_unit<KP, CHT, 1>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full, raw_empty,
+                                   a_full, a_empty, s, ph, as, aph, chk);
+      else if (offw == 2)
+        transform_unit<KP, CHT, 2>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full, raw_empty,
+                                   a_full, a_empty, s, ph, as, aph, chk);
+      else
+        transform_unit<KP, CHT, 3>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full, raw_empty,
+                                   a_full, a_empty, s, ph, as, aph, chk);
+    }
+    // a raw count >= 4096 anywhere: the digit split is not exact -> caller rescores
+    if (__any_sync(0xffffffffu, (chk & 0xF000F000u) != 0) && lane == 0) atomicOr(p.flags, 16);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == MMAW) tmem_dealloc(tmem, 512);
+  if (p.hist0)
+    for (int i = tid; i < kHist; i += blockDim.x)
+      if (shist[i]) atomicAdd(&p.hist0[i], shist[i]);
+}
+
+// one CTA per (sample, background): V_s = W diag(c_s/g), R_s, q' = q / inv_scale
+template <int KP>
+__global__ void __launch_bounds__(128) tcs_pack_kernel(const double* __restrict__ w64,
+                                                       const float* __restrict__ mu_hilo, int B,
+                                                       int S, const float* __restrict__ dark,
+                                                       const float* __restrict__ coeff, double gain,
+                                                       uint8_t* __restrict__ out) {
+  constexpr uint32_t VB = rec_vbytes(KP);
+  constexpr uint32_t SBO_B = (KP / 8) * 128u;
+  const int s = blockIdx.x;
+  const int bg = blockIdx.y;
+  const double* W = w64 + (size_t)bg * B * B;
+  const float* mh = mu_hilo + (size_t)bg * 2 * B;
+  uint8_t* o = out + ((size_t)bg * S + s) * rec_bytes(KP);
+  __shared__ double cs[KP], es[KP], red[128];
+  // R = rint(dark + mu g / c), e = (c/g)(R - dark) - mu: x - mu = (c/g) a + e
+  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+    double c = 0.0, e = 0.0;
+    uint16_t t = 0;
+    if (k < B) {
+      const double mu = (double)mh[k] + (double)mh[B + k];
+      const double cg = (double)coeff[(size_t)s * B + k] / gain;
+      const double d = (double)dark[(size_t)s * B + k];
+      double R = rint(d + mu / cg);
+      R = R < 0.0 ? 0.0 : (R > 4095.0 ? 4095.0 : R);
+      c = cg;
+      e = cg * (R - d) - mu;
+      t = (uint16_t)(4096.0 - R);
+    }
+    cs[k] = c;
+    es[k] = e;
+    reinterpret_cast<uint16_t*>(o + 2 * VB)[k] = t;
+  }
+  __syncthreads();
+  // one power-of-two scale per sample: max |V| in [2^13, 2^14)
+  double m0 = 0.0;
+  for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+    const int j = e / B, k = e - j * B;
+    if (k <= j) m0 = fmax(m0, fabs(W[e] * cs[k]));
+  }
+  red[threadIdx.x] = m0;
+  __syncthreads();
+  double mx = 0.0;
+  for (int i = 0; i < 128; ++i) mx = fmax(mx, red[i]);
+  int ex = 0;
+  if (mx > 0.0) frexp(mx, &ex);
+  const double sc = ldexp(1.0, 14 - ex);
+  float* q = reinterpret_cast<float*>(o + 2 * VB + 2 * KP);
+  for (int j = threadIdx.x; j < KP; j += blockDim.x) {
+    double qj = 0.0;
+    for (int k = 0; k < KP; ++k) {
+      const double v = (j < B && k < B && k <= j) ? W[(size_t)j * B + k] * cs[k] * sc : 0.0;
+      if (j < B && k < B && k <= j) qj += W[(size_t)j * B + k] * es[k];
+      const __half hh = __double2half(v);
+      const __half l = __double2half(v - (double)__half2float(hh));
+      const uint32_t off = (j >> 3) * SBO_B + (k >> 3) * 128u + (j & 7) * 16u + (k & 7) * 2u;
+      *reinterpret_cast<__half*>(o + off) = hh;
+      *reinterpret_cast<__half*>(o + VB + off) = l;
+    }
+    q[j] = (float)(qj * sc);  // q' = q / inv_scale, added to the scaled accumulator
+  }
+  if (threadIdx.x == 0) q[KP] = (float)ldexp(1.0, ex - 14);
+}
+
+}  // namespace tcs
+
+static int tcs_kp(int B) { return ((B + 15) / 16) * 16; }
+
+// 16-B window of a sample (all samples): max offset + 2B, rounded to an ODD number of
+// 16-B chunks (conflict-free LDS.128 across lines)
+static int tcs_ne(int S, int B) {
+  int maxoff = 0;
+  for (int s = 0; s < 8 && s < S; ++s) maxoff = maxoff > ((s * B * 2) & 15) ? maxoff : ((s * B * 2) & 15);
+  int chunks = (maxoff + 2 * B + 15) / 16 + 1;  // + 1: the transform reads chunk c_lo + cnt
+  if ((chunks & 1) == 0) ++chunks;
+  return chunks * 8;
+}
+
+template <int KP>
+static int launch_tcs(const uint16_t* raw, tcs::Params p, cudaStream_t st) {
+  using namespace tcs;
+  p.ne = tcs_ne(p.S, p.B);
+  p.stage_bytes = (uint32_t)p.ne * 2u * kLines;
+  const size_t fixed = 2 * (size_t)rec_bytes(KP) + kHist * 4 + (2 * kRawMax + 12) * 8 + 64;
+  int nraw = (int)((kSmemMax - fixed) / p.stage_bytes);
+  if (nraw > kRawMax) nraw = kRawMax;
+  SKYRX_REQUIRE(nraw >= 2, "score_tcs: shared memory too small for B = %d", p.B);
+  p.nraw = nraw;
+  const size_t smem = fixed + (size_t)nraw * p.stage_bytes;
+  const cuuint64_t line_elems = (cuuint64_t)p.S * p.B;
+  cuuint64_t dims[2] = {line_elems, (cuuint64_t)p.L};
+  cuuint64_t strides[1] = {line_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)p.ne, (cuuint32_t)kLines};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap map;
+  const CUresult r = tensor_map_encoder()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)raw, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  // units: (sample, line range), >= 8 per SM when the cube allows
+  int64_t nsplit = (p.L + kMaxUnitLines - 1) / kMaxUnitLines;
+  while ((int64_t)p.S * nsplit < 8 * kSMs && p.L / (nsplit + 1) >= 4 * kLines) ++nsplit;
+  p.split_lines = (p.L + nsplit - 1) / nsplit;
+  p.split_lines = (p.split_lines + kLines - 1) / kLines * kLines;
+  nsplit = (p.L + p.split_lines - 1) / p.split_lines;
+  p.units = (int64_t)p.S * nsplit;
+  int grid = kSMs;
+  if (p.units < grid) grid = (int)p.units;
+  cudaFuncSetAttribute(score_tcs_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  score_tcs_kernel<KP><<<grid, threads(KP), smem, st>>>(map, p);
+  SKYRX_CHECK_LAUNCH("score_tcs_kernel");
+  return SKYRX_OK;
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" size_t skyrx_score_rec_bytes(int32_t bands) {
+  return (bands < 1 || bands > 128) ? 0 : tcs::rec_bytes(tcs_kp(bands));
+}
+
+extern "C" int skyrx_score_prep(const double* whiten64, const float* mu_hilo, int32_t samples,
+                                int32_t bands, const float* dark, const float* coeff, double gain,
+                                int32_t batch, void* records, void* stream) {
+  SKYRX_REQUIRE(bands >= 1 && bands <= 128 && samples >= 1 && batch >= 1,
+                "score_prep supports 1 <= B <= 128");
+  SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
+  cudaStream_t st = as_stream(stream);
+  const dim3 grid(samples, batch);
+  switch (tcs_kp(bands)) {
+#define SKYRX_KP(k)                                                                         \
+  case k:                                                                                   \
+    tcs::tcs_pack_kernel<k><<<grid, 128, 0, st>>>(whiten64, mu_hilo, bands, samples, dark,  \
+                                                  coeff, gain, (uint8_t*)records);          \
+    break;
+    SKYRX_KP(16) SKYRX_KP(32) SKYRX_KP(48) SKYRX_KP(64) SKYRX_KP(80) SKYRX_KP(96) SKYRX_KP(112)
+    SKYRX_KP(128)
+#undef SKYRX_KP
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_score_prep");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_score_tcs_supported(int64_t lines, int32_t samples, int32_t bands,
+                                         const void* raw) {
+  if (bands < 1 || bands > 128 || lines < 1 || samples < 1) return 0;
+  if (bands & 1) return 0;  // band pairs must be 4-byte aligned in every line
+  if (((uintptr_t)raw & 15) != 0) return 0;
+  if (((int64_t)samples * bands * 2) % 16 != 0) return 0;  // TMA line stride
+  if (tcs_ne(samples, bands) > 256) return 0;               // TMA box
+  if (lines > ((int64_t)1 << 31) - 1) return 0;
+  return tensor_map_encoder() != nullptr ? 1 : 0;
+}
+
+extern "C" int skyrx_score_tcs(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                               const void* records, int32_t* flags, float* scores,
+                               uint32_t* max_key, uint32_t* topk_hist0, void* stream) {
+  SKYRX_REQUIRE(skyrx_score_tcs_supported(lines, samples, bands, raw),
+                "exact-digit score path unsupported for this shape/alignment");
+  SKYRX_REQUIRE(flags != nullptr, "score_tcs needs the flags word");
+  tcs::Params p{};
+  p.rec = (const uint8_t*)records;
+  p.scores = scores;
+  p.max_key = max_key;
+  p.hist0 = topk_hist0;
+  p.flags = flags;
+  p.L = lines;
+  p.S = samples;
+  p.B = bands;
+  cudaStream_t st = as_stream(stream);
+  switch (tcs_kp(bands)) {
+    case 16: return launch_tcs<16>(raw, p, st);
+    case 32: return launch_tcs<32>(raw, p, st);
+    case 48: return launch_tcs<48>(raw, p, st);
+    case 64: return launch_tcs<64>(raw, p, st);
+    case 80: return launch_tcs<80>(raw, p, st);
+    case 96: return launch_tcs<96>(raw, p, st);
+    case 112: return launch_tcs<112>(raw, p, st);
+    case 128: return launch_tcs<128>(raw, p, st);
+  }
+  set_error("unsupported band count %d", bands);
+  return SKYRX_ERR_ARG;
+}

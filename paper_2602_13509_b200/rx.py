@@ -317,6 +317,8 @@ class DetectPlan:
         # per slot: every line gain is exactly 1 (set by run(); lets the score
         # kernel drop the per-line gain from its transform)
         self.gain_one = [False] * batch
+        self.gain_val = [None] * batch
+        self.used_raw = [False] * batch   # raw-byte moments ran (no-clamp proof available)
         lib = _lib.load()
         use_tc = os.environ.get("SKYRX_B200_TC", "1") != "0"
         self.tc = bands <= 80 and use_tc              # tensor-core score kernel
@@ -329,6 +331,10 @@ class DetectPlan:
         self.raw_stats = bands <= 128 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
         self.raw_ws_bytes = int(lib.skyrx_stats_raw_workspace(bands)) if self.raw_stats else 0
         self.raw_ws = _dev.empty((max(self.raw_ws_bytes, 8),), torch.uint8)
+        # exact-digit score kernel (per-sample records, B <= 128)
+        self.tcs = (self.raw_stats and os.environ.get("SKYRX_B200_TCS", "1") != "0")
+        self.rec_bytes = int(lib.skyrx_score_rec_bytes(bands)) * samples if self.tcs else 0
+        self.records = (_dev.empty((batch, self.rec_bytes), torch.uint8) if self.tcs else None)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
             precise: bool = False, force_ffma: bool = False, gain_const: float | None = None):
@@ -347,6 +353,8 @@ class DetectPlan:
         s = _dev.stream_ptr()
         args = (raw.data_ptr(), L, S, B, dark.data_ptr(), coeff.data_ptr(), gains.data_ptr())
         self.gain_one[i] = gain_const == 1.0
+        self.gain_val[i] = gain_const
+        self.used_raw[i] = False
         ds.flags[i].zero_()
         lib = _lib.load()
         # small cubes take the f64 kernel (cheap there; the int8 quantiser's noise
@@ -358,6 +366,7 @@ class DetectPlan:
             # exact integer byte Grams on the tensor cores (constant line gain)
             if own_shift:
                 _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            self.used_raw[i] = True
             _lib.call("skyrx_stats_raw", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
@@ -390,7 +399,13 @@ class DetectPlan:
             self.finalize()
             for i in redo:
                 self.score(i, *cubes[i])
-        return redo
+        # raw counts >= 4096 under the exact-digit score kernel: rescore generally
+        fl = self.ds.flags.cpu().numpy()
+        rescore = [i for i in range(self.ds.batch) if i not in redo and fl[i] & 16]
+        for i in rescore:
+            self.used_raw[i] = False
+            self.score(i, *cubes[i])
+        return redo + rescore
 
     def finalize(self):
         self.ds.finalize()
@@ -442,9 +457,21 @@ class DetectPlan:
         if events is not None:
             events[0].record()
         fused = False
-        if self.tc and _lib.load().skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
-            hist = (_lib.load().skyrx_topk_histogram(self.topk_ws.data_ptr())
-                    if topk_hist0 else None)
+        lib = _lib.load()
+        hist = lib.skyrx_topk_histogram(self.topk_ws.data_ptr()) if topk_hist0 else None
+        if (self.tcs and self.used_raw[i]
+                and lib.skyrx_score_tcs_supported(L, S, B, raw.data_ptr())):
+            # exact integer digits: needs the raw path's no-clamp proof (a clamp
+            # makes the moments status ERR_RANGE and recover_range rescored generally)
+            rec = self.records[i].data_ptr()
+            _lib.call("skyrx_score_prep", ds.w64[i].data_ptr(), ds.mu_hilo[i].data_ptr(), S, B,
+                      dark.data_ptr(), coeff.data_ptr(), float(self.gain_val[i]), 1, rec, s)
+            _lib.call("skyrx_score_tcs", raw.data_ptr(), L, S, B, rec,
+                      ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
+                      self.max_key[i:i + 1].data_ptr(), hist, s)
+            fused = topk_hist0
+            self.launches += 1
+        elif self.tc and lib.skyrx_score_tc_supported(L, S, B, raw.data_ptr()):
             _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), None if self.gain_one[i] else gains.data_ptr(),
                       ds.mu_hilo[i].data_ptr(),

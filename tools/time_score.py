@@ -39,3 +39,13 @@ def mask_only():
     _lib.call("skyrx_mask_gt", plan.scores[0].data_ptr(), L * S, plan.thr[0:1].data_ptr(),
               plan.mask[0].data_ptr(), _dev.stream_ptr())
 print(json.dumps({'tc_only_ms': t(tc_only), 'topk_ms': t(topk_only), 'mask_ms': t(mask_only)}))
+
+def prep_only():
+    _lib.call("skyrx_score_prep", ds.w64[0].data_ptr(), ds.mu_hilo[0].data_ptr(), S, B, d.data_ptr(),
+              c.data_ptr(), 1.0, 1, plan.records[0].data_ptr(), _dev.stream_ptr())
+def tcs_only():
+    _lib.call("skyrx_score_tcs", raw.data_ptr(), L, S, B, plan.records[0].data_ptr(),
+              ds.flags[0:1].data_ptr(), plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(),
+              None, _dev.stream_ptr())
+if plan.tcs:
+    print(json.dumps({'prep_ms': t(prep_only), 'tcs_only_ms': t(tcs_only)}))
