@@ -331,8 +331,11 @@ class DetectPlan:
         self.raw_stats = bands <= 128 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
         self.raw_ws_bytes = int(lib.skyrx_stats_raw_workspace(bands)) if self.raw_stats else 0
         self.raw_ws = _dev.empty((max(self.raw_ws_bytes, 8),), torch.uint8)
-        # exact-digit score kernel (per-sample records, B <= 128)
-        self.tcs = (self.raw_stats and os.environ.get("SKYRX_B200_TCS", "1") != "0")
+        # exact-digit score kernel (per-sample records, B <= 128): the path for
+        # 80 < B <= 128 (K4-TC's tables no longer fit); SKYRX_B200_TCS=1 forces it
+        # for smaller B too, =0 disables it
+        tcs_env = os.environ.get("SKYRX_B200_TCS", "")
+        self.tcs = self.raw_stats and tcs_env != "0" and (bands > 80 or tcs_env == "1")
         self.rec_bytes = int(lib.skyrx_score_rec_bytes(bands)) * samples if self.tcs else 0
         self.records = (_dev.empty((batch, self.rec_bytes), torch.uint8) if self.tcs else None)
 

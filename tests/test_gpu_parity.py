@@ -353,6 +353,38 @@ class TestDetect:
         rel = np.abs(det_tc.scores - det_ff.scores) / np.maximum(det_ff.scores, 1e-12)
         assert rel.max() < 2e-5, rel.max()
 
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 300), (256, 128, 1100), (64, 96, 4200),
+                                       (48, 16, 5600)])
+    def test_exact_digit_score_kernel(self, P, monkeypatch, S, B, L):
+        """score_tcs (integer deviations in two f16-exact digits, per-sample V_s)
+        against the oracle; forced on for every B (by default it serves B > 80)."""
+        from paper_2602_13509_b200 import _lib
+
+        monkeypatch.setenv("SKYRX_B200_TCS", "1")
+        t = osynth.make_tables(47, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        plan = P.DetectPlan(L, S, B)
+        assert plan.tcs
+        assert L * S >= P.rx.TC_MIN_PIXELS
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        assert plan.used_raw[0]
+        assert int(plan.ds.flags[0].item()) & 16 == 0
+        check_detection(det, raw, t)
+
+    def test_exact_digit_kernel_rejects_wide_counts(self, P, monkeypatch):
+        """Counts >= 4096 (not 12-bit) flag the digit kernel; detect() rescores with
+        the general tensor-core kernel and still matches the oracle."""
+        monkeypatch.setenv("SKYRX_B200_TCS", "1")
+        S, B, L = 900, 70, 300
+        t = osynth.make_tables(48, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L).copy()
+        raw[7, 100:140, 3] = 5000
+        raw[201, 5, :] = 4600
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        assert int(plan.ds.flags[0].item()) & 16
+        check_detection(det, raw, t)
+
     @pytest.mark.parametrize("L", [1, 33, 129])
     def test_tensor_core_score_schedule_edges(self, P, L):
         """Fewer tiles than sample blocks, and ragged narrow-block tiles (2-D TMA box
