@@ -255,6 +255,7 @@ __global__ void fold_kernel(double* __restrict__ state, const double* __restrict
 // ------------------------------------------------------------------ K3
 constexpr int kFinThreads = 512;
 constexpr int kSmemCholMaxB = 160;
+constexpr int kSmemInvMaxB = 118;  // L and W = L^-1 both in shared memory (2 B^2 doubles)
 
 __device__ __forceinline__ double block_sum_fixed(double v, double* scratch) {
   // deterministic: warp tree then serial over warps
@@ -359,16 +360,16 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
       if (tid == 0) A[(size_t)j * B + j] = ljj;
       for (int i = j + 1 + tid; i < B; i += NT) A[(size_t)i * B + j] /= ljj;
       __syncthreads();
+      // trailing update of the lower triangle: a warp per row, lanes along it
       const int r = B - j - 1;  // trailing order
-      const int cnt = r * (r + 1) / 2;
-      for (int e = tid; e < cnt; e += NT) {
-        int ii = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-        while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-        while (ii * (ii + 1) / 2 > e) --ii;
-        const int kk = e - ii * (ii + 1) / 2;
-        const int i = j + 1 + ii, k = j + 1 + kk;
-        A[(size_t)i * B + k] = __dsub_rn(A[(size_t)i * B + k],
-                                        __dmul_rn(A[(size_t)i * B + j], A[(size_t)k * B + j]));
+      const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
+      for (int ii = wid; ii < r; ii += nw) {
+        const int i = j + 1 + ii;
+        const double lij = A[(size_t)i * B + j];
+        for (int kk = ln; kk <= ii; kk += 32) {
+          const int k = j + 1 + kk;
+          A[(size_t)i * B + k] = __dsub_rn(A[(size_t)i * B + k], __dmul_rn(lij, A[(size_t)k * B + j]));
+        }
       }
       __syncthreads();
     }
@@ -385,37 +386,41 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   if (A != chol)
     for (size_t e = tid; e < BB; e += NT) chol[e] = A[e];
   __syncthreads();
-  // W = L^-1, one column per thread (forward substitution on e_c)
+  // W = L^-1 (forward substitution on e_c, one column per thread) in shared memory
+  // next to L when both fit, so the O(B^3) inner loops never touch global memory
+  double* Wm = (A == fsm && B <= kSmemInvMaxB) ? fsm + BB : w64;
   for (int c = tid; c < B; c += NT) {
-    for (int i = 0; i < c; ++i) w64[(size_t)i * B + c] = 0.0;
+    for (int i = 0; i < c; ++i) Wm[(size_t)i * B + c] = 0.0;
     for (int i = c; i < B; ++i) {
       double a0 = (i == c) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int k = c;
       for (; k + 3 < i; k += 4) {
-        a0 -= A[(size_t)i * B + k] * w64[(size_t)k * B + c];
-        a1 -= A[(size_t)i * B + k + 1] * w64[(size_t)(k + 1) * B + c];
-        a2 -= A[(size_t)i * B + k + 2] * w64[(size_t)(k + 2) * B + c];
-        a3 -= A[(size_t)i * B + k + 3] * w64[(size_t)(k + 3) * B + c];
+        a0 -= A[(size_t)i * B + k] * Wm[(size_t)k * B + c];
+        a1 -= A[(size_t)i * B + k + 1] * Wm[(size_t)(k + 1) * B + c];
+        a2 -= A[(size_t)i * B + k + 2] * Wm[(size_t)(k + 2) * B + c];
+        a3 -= A[(size_t)i * B + k + 3] * Wm[(size_t)(k + 3) * B + c];
       }
-      for (; k < i; ++k) a0 -= A[(size_t)i * B + k] * w64[(size_t)k * B + c];
-      w64[(size_t)i * B + c] = ((a0 + a1) + (a2 + a3)) / A[(size_t)i * B + i];
+      for (; k < i; ++k) a0 -= A[(size_t)i * B + k] * Wm[(size_t)k * B + c];
+      Wm[(size_t)i * B + c] = ((a0 + a1) + (a2 + a3)) / A[(size_t)i * B + i];
     }
   }
   __syncthreads();
+  if (Wm != w64)
+    for (size_t e = tid; e < BB; e += NT) w64[e] = Wm[e];
   __threadfence_block();
   // sigma_inv = W^T W (= cho_solve(L, I)), exactly symmetric by construction
   for (size_t e = tid; e < BB; e += NT) {
     const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
     if (j > i) continue;
     double acc = 0.0;
-    for (int k = i; k < B; ++k) acc += w64[(size_t)k * B + i] * w64[(size_t)k * B + j];
+    for (int k = i; k < B; ++k) acc += Wm[(size_t)k * B + i] * Wm[(size_t)k * B + j];
     inv[(size_t)i * B + j] = acc;
     inv[(size_t)j * B + i] = acc;
   }
   // f32 whitening matrix, transposed (wf[k * ld_w + j] = W[j][k]) for K4
   for (size_t e = tid; e < (size_t)ld_w * ld_w; e += NT) {
     const int k = (int)(e / ld_w), j = (int)(e - (size_t)k * ld_w);
-    wf[e] = (j < B && k < B && k <= j) ? (float)w64[(size_t)j * B + k] : 0.0f;
+    wf[e] = (j < B && k < B && k <= j) ? (float)Wm[(size_t)j * B + k] : 0.0f;
   }
   if (tid == 0) {
     status_all[m] = SKYRX_OK;
@@ -561,7 +566,9 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
   SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
   SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
-  const size_t sm = bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double) : 0;
+  const size_t sm = bands <= kSmemInvMaxB    ? 2 * (size_t)bands * bands * sizeof(double)
+                    : bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double)
+                                             : 0;
   cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   finalize_kernel<<<batch, kFinThreads, sm, as_stream(stream)>>>(
       moments, shift, flags, bands, mu, sigma, chol, sigma_inv, whiten64, whiten, ld_w, mu_hilo,

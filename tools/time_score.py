@@ -49,3 +49,4 @@ def tcs_only():
               None, _dev.stream_ptr())
 if plan.tcs:
     print(json.dumps({'prep_ms': t(prep_only), 'tcs_only_ms': t(tcs_only)}))
+print(json.dumps({'finalize_ms': t(lambda: plan.ds.finalize())}))
