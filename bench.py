@@ -353,6 +353,10 @@ def run_stream(args, cfg, rank, world, local):
                 lat.append((time.perf_counter() - t0) * 1e3)
 
     srx = StreamingRX(tabs, L, cfg["forget"])
+    l0 = srx.plan.launches
+    srx.update(chunks[0])
+    per_chunk = srx.plan.launches - l0 + 4  # + shift, accumulate, fold, flag reset
+    srx.reset()
     for _ in range(args.warmup):
         srx.reset()
         one_pass(srx, chunks)
@@ -394,7 +398,7 @@ def run_stream(args, cfg, rank, world, local):
                                  "host_e2e": {"p50": pct(lat, 50), "p99": pct(lat, 99),
                                               "max": max(lat)},
                                  "realtime_budget": 1000.0},
-        "gpu_launches": srx.plan.launches // max(1, (args.steps + args.warmup) * nch),
+        "gpu_launches": per_chunk * nch,
         "clocks": clocks.summary(),
         "e2e": {"value": L * S * nch / sec, "unit": "pixels/s",
                 "h2d_bytes_per_step": L * S * B * 2 * nch,

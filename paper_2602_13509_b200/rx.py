@@ -360,10 +360,11 @@ class DetectPlan:
         self.used_raw[i] = False
         ds.flags[i].zero_()
         lib = _lib.load()
-        # small cubes take the f64 kernel (cheap there; the int8 quantiser's noise
-        # averages out only over many pixels); a quantiser overflow is redone in f64
+        # the raw-byte path is exact at any size; small cubes skip only the int8
+        # quantiser (its noise averages out over many pixels); a quantiser overflow
+        # or a clamp is redone in f64 (force_ffma)
         small = L * S < TC_MIN_PIXELS
-        precise = precise or small or force_ffma
+        precise = precise or force_ffma
         if (self.raw_stats and not precise and gain_const is not None
                 and lib.skyrx_stats_raw_supported(L, S, B, raw.data_ptr())):
             # exact integer byte Grams on the tensor cores (constant line gain)
@@ -374,7 +375,7 @@ class DetectPlan:
                       coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.raw_ws.data_ptr(), self.raw_ws_bytes, s)
-        elif (self.tc_stats and not precise and own_shift
+        elif (self.tc_stats and not precise and not small and own_shift
                 and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
             _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
                       self.qinv[i].data_ptr(), s)

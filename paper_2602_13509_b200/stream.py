@@ -27,7 +27,7 @@ import torch
 
 from . import _dev, _lib
 from .calibrate import line_gains, tables_of
-from .rx import CubeStats, DetectPlan, key_to_float, topk_count
+from .rx import CubeStats, DetectPlan, constant_gain, key_to_float, topk_count
 
 
 @dataclass
@@ -64,49 +64,70 @@ class StreamingRX:
         self.dark, self.coeff = self.tables.device()
         self.raw = _dev.zeros(self.shape, torch.int16).view(torch.uint16)
         self.gains = _dev.zeros((chunk_lines,), torch.float32) + 1.0
-        self.chunk_moments = _dev.zeros((int(_lib.load().skyrx_moments_len(B)),),
-                                        torch.float64)
+        nm = int(_lib.load().skyrx_moments_len(B))
+        self.chunk_moments = _dev.zeros((nm,), torch.float64)
+        self.prev_state = _dev.zeros((nm,), torch.float64)
+        lib = _lib.load()
+        # exact raw-byte moments on the tensor cores when the chunk geometry allows
+        self.raw_ok = bool(lib.skyrx_stats_raw_supported(chunk_lines, S, B, self.raw.data_ptr()))
         self.use_graph = use_graph
         self.graph = None
         self.chunks = 0
+        self.gain = 1.0
 
     # ------------------------------------------------------------------ device chain
-    def _enqueue(self, first: bool):
+    def _enqueue(self, first: bool, gain: float | None, precise: bool = False):
+        """The per-chunk device chain.  gain = the chunk's common line gain (None if
+        the lines differ): then, unless ``precise``, the moments are the exact
+        raw-byte tensor-core Grams; otherwise the f64 kernel."""
         L, S, B = self.shape
         plan, ds = self.plan, self.plan.ds
         s = _dev.stream_ptr()
         args = (self.raw.data_ptr(), L, S, B, self.dark.data_ptr(), self.coeff.data_ptr(),
                 self.gains.data_ptr())
         ds.flags.zero_()
+        self.prev_state.copy_(ds.moments[0])  # undo point if this chunk must be redone
         if first:
             _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(), s)
-        # chunk moments in f64 (a chunk is 224 100 px: the f64 kernel costs ~30 us)
-        _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(), 1,
-                  self.chunk_moments.data_ptr(), ds.flags.data_ptr(), plan.ws.data_ptr(),
-                  plan.ws_bytes, s)
+        use_raw = self.raw_ok and gain is not None and not precise
+        plan.used_raw[0] = use_raw
+        plan.gain_one[0] = gain == 1.0
+        plan.gain_val[0] = gain
+        if use_raw:
+            _lib.call("skyrx_stats_raw", self.raw.data_ptr(), L, S, B, self.dark.data_ptr(),
+                      self.coeff.data_ptr(), float(gain), ds.shift[0].data_ptr(),
+                      self.chunk_moments.data_ptr(), ds.flags.data_ptr(), plan.raw_ws.data_ptr(),
+                      plan.raw_ws_bytes, s)
+        else:
+            _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(),
+                      1, self.chunk_moments.data_ptr(), ds.flags.data_ptr(), plan.ws.data_ptr(),
+                      plan.ws_bytes, s)
         _lib.call("skyrx_moments_fold", ds.moments[0].data_ptr(), self.chunk_moments.data_ptr(),
                   B, self.forget, s)
         plan.finalize()
         plan.score(0, self.raw, self.dark, self.coeff, self.gains, self.k)
 
-    def _run(self):
+    def _run(self, gain):
         if self.chunks == 0:
             self.plan.ds.moments.zero_()
-            self._enqueue(first=True)
+            self._enqueue(first=True, gain=gain)
             return
-        if not self.use_graph:
-            self._enqueue(first=False)
+        if not self.use_graph or gain != 1.0:
+            self._enqueue(first=False, gain=gain)
             return
         if self.graph is None:
-            # capture the steady-state chain once (shift fixed, buffers static)
+            # capture the steady-state chain once (shift fixed, buffers static, gain 1)
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=side):
-                self._enqueue(first=False)
+                self._enqueue(first=False, gain=1.0)
             torch.cuda.current_stream().wait_stream(side)
             self.graph = g
         self.graph.replay()
+        self.plan.used_raw[0] = self.raw_ok
+        self.plan.gain_one[0] = True
+        self.plan.gain_val[0] = 1.0
 
     # ------------------------------------------------------------------ public API
     def update(self, chunk, *, with_stats: bool = False) -> ChunkResult:
@@ -122,14 +143,24 @@ class StreamingRX:
             a = np.ascontiguousarray(np.asarray(values, np.uint16))
             self.raw.copy_(torch.from_numpy(a.view(np.int16)).view(torch.uint16),
                            non_blocking=True)
+        gain = 1.0
         if getattr(chunk, "gains", None) is not None or len(getattr(chunk, "line_meta", ())):
             g = line_gains(chunk)
+            gain = constant_gain(g, self.tables)
             g = g if isinstance(g, torch.Tensor) else torch.from_numpy(np.asarray(g, np.float32))
             self.gains.copy_(g, non_blocking=True)
         else:
             self.gains.fill_(1.0)
-        self._run()
+        first = self.chunks == 0
+        self._run(gain)
         ds = self.plan.ds
+        if int(ds.status[0].item()) == _lib.ERR_RANGE:
+            # a value below dark (clamp): the raw-byte moments do not apply -> redo
+            # this chunk's moments in f64 from the pre-chunk state
+            ds.moments[0].copy_(self.prev_state)
+            if first:
+                ds.moments[0].zero_()
+            self._enqueue(first=first, gain=gain, precise=True)
         ds.check(0, L * S)  # synchronises: raises the reference's errors
         idx = self.chunks
         self.chunks += 1
@@ -143,6 +174,6 @@ class StreamingRX:
                            _dev.to_host(self.plan.mask[0]).view(bool), thr, mx, stats)
 
     def reset(self):
-        """Forget the background (the next chunk re-seeds the shift)."""
+        """Forget the background (the next chunk re-seeds the shift).  The captured
+        chunk graph stays valid: it reads the shift and state from device buffers."""
         self.chunks = 0
-        self.graph = None
