@@ -223,9 +223,14 @@ def main():
 
     ev = {"gram": [], "score": [], "kernel": []}
 
+    step_ev = []
+
     def step(instrument=False):
         if flush is not None:
-            flush.zero_()
+            flush.zero_()  # outside the per-step events below
+        if instrument:
+            sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            sa.record(stream)
         for j in range(len(mine)):
             raw = raws[j]
             d, c = tabs[j]
@@ -249,6 +254,9 @@ def main():
                 b.record(stream)
                 ev["score"].append((a, b))
                 ev["kernel"].append(kev)
+        if instrument:
+            sb.record(stream)
+            step_ev.append((sa, sb))
 
     for _ in range(args.warmup):
         step()
@@ -268,6 +276,8 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
+    if flush is not None:  # device time of the steps themselves, L2 flushes excluded
+        ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
     launches = (plan.launches - launches0) // args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
