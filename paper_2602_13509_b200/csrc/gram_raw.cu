@@ -35,6 +35,20 @@
 namespace skyrx {
 using namespace umma;
 
+// -DSKYRX_GR_PROFILE builds accumulate per-CTA wait cycles of each role
+// (tools/gr_profile.py reads them through skyrx_gr_profile); compiled out otherwise
+#ifdef SKYRX_GR_PROFILE
+__device__ unsigned long long gr_prof[160][8];
+#define GR_PW(idx, stmt)                                        \
+  do {                                                          \
+    const unsigned long long t0_ = clock64();                   \
+    stmt;                                                       \
+    gr_prof[blockIdx.x][idx] += clock64() - t0_;                \
+  } while (0)
+#else
+#define GR_PW(idx, stmt) stmt
+#endif
+
 constexpr int kGrThreads = 320;
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
@@ -138,6 +152,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef SKYRX_GR_PROFILE
+  const unsigned long long kt0 = clock64();
+#endif
 
   auto unit_geom = [&](int64_t u, int& s, int64_t& l0, int64_t& nl) {
     s = (int)(u % p.S);
@@ -157,7 +174,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kGrStages;
-          mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1);
+          GR_PW(0, mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1));
           mbar_arrive_expect_tx(&full[st], STAGE);
           tma_load_2d(stages + st * STAGE, &tmap, 16 * c0, (int)(l0 + (int64_t)k * kGrLb),
                       &full[st]);
@@ -179,12 +196,12 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
         const int buf = NBUF == 2 ? (unit & 1) : 0;
         const int use = NBUF == 2 ? (unit >> 1) : unit;
-        mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+        GR_PW(1, mbar_wait(&acc_empty[buf], (use & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + buf * BUFC;
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kGrStages;
-          mbar_wait(&full[st], (t / kGrStages) & 1);
+          GR_PW(2, mbar_wait(&full[st], (t / kGrStages) & 1));
           tc_fence_after();
           const uint8_t* base = stages + st * STAGE;
 #pragma unroll
@@ -221,7 +238,8 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       uint32_t sm8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int k = 0; k < ntile; ++k, ++t) {
         const int st = t % kGrStages;
-        mbar_wait(&full[st], (t / kGrStages) & 1);
+        if (tid == 0) GR_PW(3, mbar_wait(&full[st], (t / kGrStages) & 1));
+        else mbar_wait(&full[st], (t / kGrStages) & 1);
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
@@ -274,8 +292,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       const int buf = NBUF == 2 ? (unit & 1) : 0;
       const int use = NBUF == 2 ? (unit >> 1) : unit;
       const int ub = unit & 1;
-      mbar_wait(&scan_full[ub], (unit >> 1) & 1);
-      mbar_wait(&acc_full[buf], use & 1);
+      if (tid == kGrWorkers) GR_PW(4, mbar_wait(&scan_full[ub], (unit >> 1) & 1));
+      else mbar_wait(&scan_full[ub], (unit >> 1) & 1);
+      if (tid == kGrWorkers) GR_PW(5, mbar_wait(&acc_full[buf], use & 1));
+      else mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
       const uint32_t* mnv = minv + ub * NCH * 8;
       const uint32_t* smv = sumv + ub * NCH * 8;
@@ -359,8 +379,17 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#ifdef SKYRX_GR_PROFILE
+  if (tid == 0) gr_prof[blockIdx.x][7] += clock64() - kt0;
+#endif
   if (warp == 9) tmem_dealloc(tmem, 512);
 }
+
+#ifdef SKYRX_GR_PROFILE
+extern "C" int skyrx_gr_profile(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, gr_prof, sizeof(gr_prof));
+}
+#endif
 
 // Deterministic reduction of the per-CTA partials [Sxx | Sx | n]: a block owns 32
 // elements (one per lane); its 8 warps sum fixed, contiguous slices of the

@@ -1,4 +1,8 @@
-"""Per-role wait breakdown of gram_raw_kernel (variant built with -DSKYRX_GR_PROFILE)."""
+"""Per-role wait breakdown of gram_raw_kernel.
+
+Build a variant with the probes compiled in and run this against it:
+    nvcc ... -DSKYRX_GR_PROFILE -c csrc/gram_raw.cu, relink, run.
+"""
 import ctypes, sys, json
 import numpy as np
 import torch
