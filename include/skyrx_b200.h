@@ -88,7 +88,11 @@ int skyrx_stats_workspace(int64_t lines, int32_t samples, int32_t bands, size_t*
  *              (fast path; SURVEY §7 precision budget);
  * precise = 1: f64 products and sums throughout (reference-grade, for the
  *              drop-in compute_stats and the reference's 1e-9 suites).
- * flags[0] |= 1 if any calibrated value is non-finite (rx.py:53-54). */
+ * flags[0] |= 1 if any calibrated value is non-finite (rx.py:53-54); for RAW
+ * input also |= 128 (the clamp check ran) and |= 64 if a raw value was below
+ * dark (calibrate.py:99 clamps it).  "No clamp anywhere" = flags 8 without 4
+ * (raw-byte pass) or 128 without 64 (this pass): the exact-digit score kernels
+ * need it. */
 int skyrx_stats_accumulate(int32_t kind, const void* pixels, int64_t lines, int32_t samples,
                            int32_t bands, const float* dark, const float* coeff,
                            const float* gain, const double* shift, int32_t precise,
@@ -194,6 +198,19 @@ int skyrx_score_tcs_supported(int64_t lines, int32_t samples, int32_t bands, con
 int skyrx_score_tcs(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                     const void* records, int32_t* flags, float* scores, uint32_t* max_key,
                     uint32_t* topk_hist0, void* stream);
+
+/* The same for wide cubes, 128 < B <= 272 (even B): V_s streamed in N-blocks of
+ * 64 rows per tile (records from skyrx_scorew_prep, skyrx_scorew_rec_bytes(B)
+ * each).  The kernel scores nothing and sets flags |= 32 unless the moments
+ * pass proved "no clamp" (flags 8 w/o 4 or 128 w/o 64); raw >= 4096 sets 16. */
+size_t skyrx_scorew_rec_bytes(int32_t bands);
+int skyrx_scorew_prep(const double* whiten64, const float* mu_hilo, int32_t samples,
+                      int32_t bands, const float* dark, const float* coeff, double gain,
+                      int32_t batch, void* records, void* stream);
+int skyrx_scorew_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
+int skyrx_scorew(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                 const void* records, int32_t* flags, float* scores, uint32_t* max_key,
+                 uint32_t* topk_hist0, void* stream);
 
 /* The kernel slot itself: _accel.mahalanobis_sq(pixels, mu, chol_lower)
  * (_accel.py:109-131) with FP64 arithmetic; pixels f32 or f64 (kind F32/F64).

@@ -56,6 +56,10 @@ SIGNATURES = {
     "skyrx_score_prep": (C.c_int, [vp, vp, i32, i32, vp, vp, f64, i32, vp, vp]),
     "skyrx_score_tcs_supported": (C.c_int, [i64, i32, i32, vp]),
     "skyrx_score_tcs": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "skyrx_scorew_rec_bytes": (sz, [i32]),
+    "skyrx_scorew_prep": (C.c_int, [vp, vp, i32, i32, vp, vp, f64, i32, vp, vp]),
+    "skyrx_scorew_supported": (C.c_int, [i64, i32, i32, vp]),
+    "skyrx_scorew": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "skyrx_mahalanobis_sq":(C.c_int, [i32, vp, i64, i32, vp, vp, vp, vp, vp]),
     "skyrx_max": (C.c_int, [vp, i64, vp, vp]),
     "skyrx_normalize": (C.c_int, [vp, i64, vp, vp, vp]),

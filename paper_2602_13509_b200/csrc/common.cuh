@@ -93,6 +93,12 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return r;
 }
 
+// moments-pass flags word (include/skyrx_b200.h): proven "no raw value below dark"
+// either by the raw-byte tensor-core pass (8 without 4) or the general pass (128 without 64)
+__device__ __forceinline__ bool flags_noclamp(int32_t f) {
+  return (f & 12) == 8 || (f & 192) == 128;
+}
+
 // 16-byte vectors for shared-memory operand loads
 template <typename T>
 struct Vec16;

@@ -405,7 +405,7 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     mbar_wait(w_bar, 0);
     // one arithmetic mode for the whole launch (uniform branch):
     //   odd B -> 3; per-line gains given -> 2; moments pass proved raw >= dark -> 0; else 1
-    const bool noclamp = p.flags != nullptr && (__ldg(p.flags) & 12) == 8;
+    const bool noclamp = p.flags != nullptr && flags_noclamp(__ldg(p.flags));
     // chunks per thread: sized for B = KP; a smaller B runs fewer (cnt, runtime)
     constexpr int NG = sc_groups(KP), NCH = KP / 8;
     constexpr int CHT = (NCH + NG - 1) / NG;

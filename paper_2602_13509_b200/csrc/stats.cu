@@ -110,12 +110,13 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
   double s64 = 0.0, s64b = 0.0;
   int since_flush = 0;
   bool finite_ok = true;
+  bool clamped = false;
   const int per_thread = ceil_div(kGramTileP, geo.groups);
 
   for (int64_t t = blockIdx.x; t < geo.ptiles; t += gridDim.x) {
     __syncthreads();
     finite_ok &= load_tile<KIND, T>(cube, t * kGramTileP, kGramTileP, geo.ld, geo.bp, c_f,
-                                    nullptr, c64, d, s_line, s_samp);
+                                    nullptr, c64, d, s_line, s_samp, &clamped);
     __syncthreads();
     if (do_s) {  // band sums over the tile, then FP64 across tiles
       T cs = T(0);
@@ -180,6 +181,11 @@ __global__ void __launch_bounds__(kGramThreads, 1) gram_kernel(
   if (do_s) part_s[(size_t)blockIdx.x * geo.bp + tid] = s64;
   if (do_s2) part_s[(size_t)blockIdx.x * geo.bp + tid + kGramThreads] = s64b;
   if (!finite_ok) atomicOr(flags, 1);
+  // 128: the general path's clamp check ran; 64: a raw value was below dark
+  if (KIND == SKYRX_IN_RAW_U16) {
+    if (blockIdx.x == 0 && tid == 0) atomicOr(flags, 128);
+    if (__any_sync(0xffffffffu, clamped) && (tid & 31) == 0) atomicOr(flags, 64);
+  }
 }
 
 // moments[0] = n, moments[1..B] = s, moments[1+B ..] = Q (full, symmetric)

@@ -28,7 +28,8 @@ __device__ __forceinline__ bool load_tile(const CubeRef& c, int64_t p0, int P, i
                                           const float* __restrict__ sub_hi,
                                           const float* __restrict__ sub_lo,
                                           const double* __restrict__ sub64, T* __restrict__ d,
-                                          int32_t* s_line, int32_t* s_samp) {
+                                          int32_t* s_line, int32_t* s_samp,
+                                          bool* clamped = nullptr) {
   const int B = c.bands;
   const int NT = blockDim.x;
   if constexpr (KIND == SKYRX_IN_RAW_U16) {
@@ -63,8 +64,10 @@ __device__ __forceinline__ bool load_tile(const CubeRef& c, int64_t p0, int P, i
         float x;
         if constexpr (KIND == SKYRX_IN_RAW_U16) {
           const int64_t tb = (int64_t)s_samp[p] * B + b;
-          x = calib((float)__ldg(reinterpret_cast<const uint16_t*>(c.pixels) + gi),
-                    __ldg(c.dark + tb), __ldg(c.coeff + tb), __ldg(c.gain + s_line[p]));
+          const float r = (float)__ldg(reinterpret_cast<const uint16_t*>(c.pixels) + gi);
+          const float dk = __ldg(c.dark + tb);
+          if (clamped && r < dk) *clamped = true;  // calibrate.py:99 clamps this value
+          x = calib(r, dk, __ldg(c.coeff + tb), __ldg(c.gain + s_line[p]));
         } else {
           x = __ldg(reinterpret_cast<const float*>(c.pixels) + gi);
         }

@@ -337,7 +337,12 @@ class DetectPlan:
         tcs_env = os.environ.get("SKYRX_B200_TCS", "")
         self.tcs = self.raw_stats and tcs_env != "0" and (bands > 80 or tcs_env == "1")
         self.rec_bytes = int(lib.skyrx_score_rec_bytes(bands)) * samples if self.tcs else 0
-        self.records = (_dev.empty((batch, self.rec_bytes), torch.uint8) if self.tcs else None)
+        # ... and its wide form for 128 < B <= 272 (N-blocked V_s), whatever moments path
+        self.tcw = 128 < bands <= 272 and use_tc and tcs_env != "0"
+        if self.tcw:
+            self.rec_bytes = int(lib.skyrx_scorew_rec_bytes(bands)) * samples
+        self.records = (_dev.empty((batch, self.rec_bytes), torch.uint8)
+                        if (self.tcs or self.tcw) else None)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
             precise: bool = False, force_ffma: bool = False, gain_const: float | None = None):
@@ -403,12 +408,15 @@ class DetectPlan:
             self.finalize()
             for i in redo:
                 self.score(i, *cubes[i])
-        # raw counts >= 4096 under the exact-digit score kernel: rescore generally
+        # the exact-digit score kernels could not apply (raw counts >= 4096: 16, or no
+        # no-clamp proof: 32): rescore with the general kernels
         fl = self.ds.flags.cpu().numpy()
-        rescore = [i for i in range(self.ds.batch) if i not in redo and fl[i] & 16]
+        rescore = [i for i in range(self.ds.batch) if i not in redo and fl[i] & 48]
         for i in rescore:
             self.used_raw[i] = False
+            keep, self.tcw = self.tcw, False
             self.score(i, *cubes[i])
+            self.tcw = keep
         return redo + rescore
 
     def finalize(self):
@@ -471,6 +479,18 @@ class DetectPlan:
             _lib.call("skyrx_score_prep", ds.w64[i].data_ptr(), ds.mu_hilo[i].data_ptr(), S, B,
                       dark.data_ptr(), coeff.data_ptr(), float(self.gain_val[i]), 1, rec, s)
             _lib.call("skyrx_score_tcs", raw.data_ptr(), L, S, B, rec,
+                      ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
+                      self.max_key[i:i + 1].data_ptr(), hist, s)
+            fused = topk_hist0
+            self.launches += 1
+        elif (self.tcw and self.gain_val[i] is not None
+                and lib.skyrx_scorew_supported(L, S, B, raw.data_ptr())):
+            # wide exact-digit kernel; it checks the no-clamp proof itself (flags |= 32
+            # when missing: recover_range rescores generally)
+            rec = self.records[i].data_ptr()
+            _lib.call("skyrx_scorew_prep", ds.w64[i].data_ptr(), ds.mu_hilo[i].data_ptr(), S, B,
+                      dark.data_ptr(), coeff.data_ptr(), float(self.gain_val[i]), 1, rec, s)
+            _lib.call("skyrx_scorew", raw.data_ptr(), L, S, B, rec,
                       ds.flags[i:i + 1].data_ptr(), sc.data_ptr(),
                       self.max_key[i:i + 1].data_ptr(), hist, s)
             fused = topk_hist0

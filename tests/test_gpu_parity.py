@@ -371,6 +371,29 @@ class TestDetect:
         assert int(plan.ds.flags[0].item()) & 16 == 0
         check_detection(det, raw, t)
 
+    @pytest.mark.parametrize("S,B,L", [(1024, 270, 70), (128, 160, 300), (64, 144, 129)])
+    def test_wide_exact_digit_score_kernel(self, P, S, B, L):
+        """score_tcw (128 < B <= 272: V_s streamed in N-blocks) against the oracle."""
+        t = osynth.make_tables(49, S, B, 8)
+        raw = osynth.generate_lines(t, 0, L)
+        plan = P.DetectPlan(L, S, B)
+        assert plan.tcw
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        fl = int(plan.ds.flags[0].item())
+        assert fl & 128 and not fl & (16 | 32 | 64)  # proof present, kernel applied
+        check_detection(det, raw, t)
+
+    def test_wide_kernel_without_clamp_proof_rescores(self, P):
+        S, B, L = 128, 160, 100
+        t = osynth.make_tables(50, S, B, 8)
+        raw = osynth.generate_lines(t, 0, L).copy()
+        raw[3, 4, 5] = 0  # below dark: clamps
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        fl = int(plan.ds.flags[0].item())
+        assert fl & 64 and fl & 32
+        check_detection(det, raw, t)
+
     def test_exact_digit_kernel_rejects_wide_counts(self, P, monkeypatch):
         """Counts >= 4096 (not 12-bit) flag the digit kernel; detect() rescores with
         the general tensor-core kernel and still matches the oracle."""
