@@ -436,6 +436,23 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
   }
 }
 
+// reduce the per-CTA partials [Sxx | Sx | n] (deterministic) and centre them on shift
+int gram_raw_sum_and_center(const double* part, int grid, int bands, const double* shift,
+                            double* moments, cudaStream_t st) {
+  const int work = bands * bands + bands + 1;
+  double* tot = const_cast<double*>(part) + (size_t)kSMs * work;  // after the partials
+  gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(part, grid, work, tot);
+  SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
+  gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, bands, shift, moments);
+  SKYRX_CHECK_LAUNCH("gram_raw_center_kernel");
+  return SKYRX_OK;
+}
+
+int raww_atoms(int bands);
+int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                   const float* dark, const float* coeff, double gain, const double* shift,
+                   double* moments, int32_t* flags, void* workspace, cudaStream_t st);
+
 static int nch_for(int B) {
   // widest window over all samples: start offset in its 16-B chunk + 2B bytes
   int maxoff = 0;
@@ -473,13 +490,7 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
                        (int)smem);
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
-  const int work = p.B * p.B + p.B + 1;
-  double* tot = p.part + (size_t)kSMs * work;  // after the per-CTA partials
-  gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(p.part, grid, work, tot);
-  SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
-  gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, p.B, shift, moments);
-  SKYRX_CHECK_LAUNCH("gram_raw_center_kernel");
-  return SKYRX_OK;
+  return gram_raw_sum_and_center(p.part, grid, p.B, shift, moments, st);
 }
 
 }  // namespace skyrx
@@ -491,7 +502,7 @@ extern "C" int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t
   if (bands < 1 || lines < 1 || samples < 1) return 0;
   if (((uintptr_t)raw & 15) != 0) return 0;
   if (((int64_t)samples * bands * 2) % 16 != 0) return 0;  // TMA line stride
-  if (nch_for(bands) > 16) return 0;                        // window <= 256 bytes (B <= 128)
+  if (nch_for(bands) > 16 && raww_atoms(bands) > 5) return 0;  // wide path: <= 640 B windows
   if (lines > ((int64_t)1 << 31) - 1) return 0;
   return tensor_map_encoder() != nullptr ? 1 : 0;
 }
@@ -509,6 +520,9 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
   SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_raw_workspace(bands), "workspace too small");
   const int nch = nch_for(bands);
+  if (nch > 16)  // windows past 256 bytes: the multi-pass wide kernel (gram_raww.cu)
+    return stats_raw_wide(raw, lines, samples, bands, dark, coeff, gain, shift, moments, flags,
+                          workspace, as_stream(stream));
   // 2-D byte view (byte within line, line); boxes of 128 bytes x Lb lines, swizzled
   const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;
   cuuint64_t dims[2] = {line_bytes, (cuuint64_t)lines};

@@ -1,0 +1,330 @@
+// K2-RAW for WIDE windows (128 < B <= 272, BASELINE config 3): the exact raw-byte
+// Gram of gram_raw.cu when the 2B-byte window of a sample is wider than 256 bytes.
+//
+// The byte Gram of a 560-byte window (B = 270) is 14 blocks of 128 x 128 in its
+// lower triangle — more than TMEM's 512 columns — so it is computed in PASSES of
+// up to four blocks (512 TMEM columns), each pass streaming the cube once:
+//   1. raww_scan_kernel: per work unit (sample, line range) the per-band column
+//      sums m_s and minima (clamp check: flags |= 4 below dark, 8 = check ran);
+//   2. raww_gram_kernel, pass p: tcgen05.mma kind::i8 (u8 x u8 -> s32, exact) of
+//      the pass's blocks for every tile of every unit, TMA 128-line x 128-byte
+//      SWIZZLE_128B boxes of all window atoms; at the end of a unit the epilogue
+//      warps turn the integer blocks into calibrated f64 sums C_b C_b2 (G - d m^T
+//      - m d^T + L d d^T) and accumulate them into the CTA's partial in global
+//      memory (each band pair belongs to exactly one block, hence one pass);
+//   3. the partials are reduced and centred by gram_raw.cu's deterministic kernels.
+// Warps of the Gram kernel: 4 epilogue (TMEM lane quarters), TMA, MMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tma.cuh"
+#include "umma.cuh"
+
+namespace skyrx {
+using namespace umma;
+
+namespace raww {
+
+constexpr int kLb = 128;            // lines per tile
+constexpr int kThreads = 192;
+constexpr int kStages = 2;
+constexpr int kMaxAtoms = 5;        // window <= 640 bytes
+constexpr uint32_t kAtom = kLb * 128u;
+
+struct Params {
+  const float* dark;
+  const float* coeff;
+  double ginv;
+  double* part;          // per CTA: Sxx[B*B] (lower), Sx[B], n  (zeroed before pass 0)
+  const uint32_t* usum;  // per unit: column sums of the window's u16 lanes [units][NW/2]
+  int64_t L;
+  int32_t S, B;
+  int32_t na;            // window atoms (128 B each)
+  int32_t nw16;          // u16 lanes per window (= 64 * na)
+  int64_t split_lines;
+  int64_t units;
+  int32_t nblk;          // blocks in this pass (<= 4)
+  int32_t blk_r[4], blk_c[4];  // their (row atom, column atom)
+  int32_t first_pass;    // also accumulate Sx and n
+};
+
+__device__ __forceinline__ void unit_geom(const Params& p, int64_t u, int& s, int64_t& l0,
+                                          int64_t& nl) {
+  s = (int)(u % p.S);
+  l0 = (u / p.S) * p.split_lines;
+  nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
+}
+
+__host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (1u << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// per unit: column sums and minima of every u16 lane of the 16-B aligned window.
+// A warp owns 32 consecutive lanes (64 B of every line), loads unrolled 8 deep.
+__global__ void __launch_bounds__(320) raww_scan_kernel(const uint16_t* __restrict__ raw,
+                                                        Params p,
+                                                        const float* __restrict__ dark,
+                                                        uint32_t* __restrict__ usum,
+                                                        int32_t* __restrict__ flags) {
+  const int B = p.B;
+  const int64_t pitch = (int64_t)p.S * B;
+  bool clamp = false;
+  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+    int s;
+    int64_t l0, nl;
+    unit_geom(p, u, s, l0, nl);
+    const int64_t w0 = ((int64_t)s * B * 2 & ~(int64_t)15) >> 1;  // first u16 of the window
+    const int off = (int)(((int64_t)s * B * 2 & 15) >> 1);
+    for (int q = threadIdx.x; q < p.nw16; q += blockDim.x) {
+      const int64_t col = w0 + q;
+      const bool in = col < pitch;
+      uint32_t sum = 0, mn = 0xFFFFu;
+      if (in) {
+        const uint16_t* c = raw + l0 * pitch + col;
+        int64_t l = 0;
+        for (; l + 8 <= nl; l += 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = __ldg(c + (l + i) * pitch);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sum += v[i], mn = min(mn, v[i]);
+        }
+        for (; l < nl; ++l) {
+          const uint32_t v = __ldg(c + l * pitch);
+          sum += v;
+          mn = min(mn, v);
+        }
+      }
+      usum[u * p.nw16 + q] = sum;
+      const int b = q - off;
+      if (in && b >= 0 && b < B && (float)mn < __ldg(dark + (int64_t)s * B + b)) clamp = true;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, 8);
+  if (__any_sync(0xffffffffu, clamp) && (threadIdx.x & 31) == 0) atomicOr(flags, 4);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
+    const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const uint32_t STAGE = (uint32_t)p.na * kAtom;
+  uint8_t* stages = sm;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* acc_full = bars + 2 * kStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int B = p.B;
+  const int64_t u0 = blockIdx.x, ustep = gridDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
+      int t = 0;
+      for (int64_t u = u0; u < p.units; u += ustep) {
+        int s;
+        int64_t l0, nl;
+        unit_geom(p, u, s, l0, nl);
+        const int c0 = (int)(((int64_t)s * B * 2) & ~(int64_t)15);
+        const int ntile = (int)((nl + kLb - 1) / kLb);
+        for (int k = 0; k < ntile; ++k, ++t) {
+          const int st = t % kStages;
+          mbar_wait(&empty[st], ((t / kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[st], STAGE);
+          for (int a = 0; a < p.na; ++a)
+            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * a,
+                        (int)(l0 + (int64_t)k * kLb), &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+      constexpr uint32_t id = idesc_u8(128, 128);
+      int t = 0, unit = 0;
+      for (int64_t u = u0; u < p.units; u += ustep, ++unit) {
+        int s;
+        int64_t l0, nl;
+        unit_geom(p, u, s, l0, nl);
+        const int ntile = (int)((nl + kLb - 1) / kLb);
+        mbar_wait(acc_empty, (unit & 1) ^ 1);
+        tc_fence_after();
+        for (int k = 0; k < ntile; ++k, ++t) {
+          const int st = t % kStages;
+          mbar_wait(&full[st], (t / kStages) & 1);
+          tc_fence_after();
+          const uint8_t* base = stages + st * STAGE;
+          for (int ks = 0; ks < kLb / 32; ++ks) {
+            const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+            for (int bk = 0; bk < p.nblk; ++bk) {
+              const uint64_t da = smem_desc_sw128(base + p.blk_r[bk] * kAtom + ks * 4096, kAtom, 1024);
+              const uint64_t db = smem_desc_sw128(base + p.blk_c[bk] * kAtom + ks * 4096, kAtom, 1024);
+              mma_i8(tmem + 128 * bk, da, db, id, acc);
+            }
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(acc_full);
+      }
+    }
+  } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
+    const int te = tid;  // byte row within the row atom = TMEM lane
+    double* part = p.part + (size_t)blockIdx.x * ((size_t)B * B + B + 1);
+    double nsum = 0.0;
+    int unit = 0;
+    for (int64_t u = u0; u < p.units; u += ustep, ++unit) {
+      int s;
+      int64_t l0, nl;
+      unit_geom(p, u, s, l0, nl);
+      const uint32_t* us = p.usum + u * p.nw16;
+      const int off = (int)(((int64_t)s * B * 2) & 15);
+      const double Lu = (double)nl;
+      const float* drow = p.dark + (int64_t)s * B;
+      const float* crow = p.coeff + (int64_t)s * B;
+      mbar_wait(acc_full, unit & 1);
+      tc_fence_after();
+      for (int bk = 0; bk < p.nblk; ++bk) {
+        const int mr = p.blk_r[bk], mc = p.blk_c[bk];
+        const int m = 128 * mr + te;
+        const int rel = m - off;
+        const bool lo_row = rel >= 0 && rel < 2 * B && (rel & 1) == 0;
+        const int b = rel >> 1;
+        double Cb = 0.0, db = 0.0, Sb = 0.0;
+        if (lo_row) {
+          Cb = (double)crow[b] * p.ginv;
+          db = (double)drow[b];
+          Sb = (double)us[(off >> 1) + b];
+        }
+        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 128 * bk;
+        for (int cc = 0; cc < 8; ++cc) {
+          uint32_t v[16];
+          tmem_ld16(taddr + cc * 16, v);
+          tmem_ld_wait();
+          uint32_t pv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, v[q], 1);
+          if (lo_row) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int reln = 128 * mc + cc * 16 + 2 * i - off;
+              if (reln < 0 || reln >= 2 * B) continue;
+              const int b2 = reln >> 1;
+              if (b2 > b) continue;  // lower triangle (only the diagonal block has any)
+              const double gv = 65536.0 * (double)pv[2 * i + 1] +
+                                256.0 * ((double)pv[2 * i] + (double)v[2 * i + 1]) +
+                                (double)v[2 * i];
+              const double C2 = (double)crow[b2] * p.ginv;
+              const double d2 = (double)drow[b2];
+              const double S2 = (double)us[(off >> 1) + b2];
+              const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
+              part[(size_t)b * B + b2] += Cb * C2 * xx;
+            }
+          }
+        }
+      }
+      if (p.first_pass) {  // band sums: sum x = C_b (m_b - L d_b)
+        for (int b = te; b < B; b += 128) {
+          const double Cb = (double)crow[b] * p.ginv, db = (double)drow[b];
+          part[(size_t)B * B + b] += Cb * ((double)us[(off >> 1) + b] - Lu * db);
+        }
+        nsum += Lu;
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+    }
+    if (p.first_pass && tid == 0) part[(size_t)B * B + B] = nsum;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace raww
+
+int gram_raw_sum_and_center(const double* part, int grid, int bands, const double* shift,
+                            double* moments, cudaStream_t st);
+
+// window atoms for B (16-B aligned start, widest offset over the samples)
+int raww_atoms(int bands) {
+  int maxoff = 0;
+  for (int s = 0; s < 8; ++s) maxoff = maxoff > ((s * bands * 2) & 15) ? maxoff : ((s * bands * 2) & 15);
+  return (maxoff + 2 * bands + 127) / 128;
+}
+
+int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                   const float* dark, const float* coeff, double gain, const double* shift,
+                   double* moments, int32_t* flags, void* workspace, cudaStream_t st) {
+  using namespace raww;
+  Params p{};
+  p.dark = dark;
+  p.coeff = coeff;
+  p.ginv = 1.0 / gain;
+  p.part = reinterpret_cast<double*>(workspace);
+  p.L = lines;
+  p.S = samples;
+  p.B = bands;
+  p.na = raww_atoms(bands);
+  SKYRX_REQUIRE(p.na <= kMaxAtoms, "wide raw-byte moments support windows <= 640 bytes");
+  p.nw16 = 64 * p.na;
+  int64_t nsplit = (lines + 16383) / 16384;
+  while ((int64_t)samples * nsplit < 8 * kSMs && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
+  p.split_lines = (lines + nsplit - 1) / nsplit;
+  p.split_lines = (p.split_lines + kLb - 1) / kLb * kLb;
+  nsplit = (lines + p.split_lines - 1) / p.split_lines;
+  p.units = (int64_t)samples * nsplit;
+  int grid = kSMs;
+  if (p.units < grid) grid = (int)p.units;
+  const size_t stride = (size_t)bands * bands + bands + 1;
+  cudaMemsetAsync(p.part, 0, (size_t)grid * stride * sizeof(double), st);
+  uint32_t* usum = nullptr;
+  SKYRX_REQUIRE(cudaMallocAsync(&usum, (size_t)p.units * p.nw16 * sizeof(uint32_t), st) ==
+                    cudaSuccess,
+                "cudaMallocAsync failed");
+  p.usum = usum;
+  raww_scan_kernel<<<kSMs * 4, 320, 0, st>>>(raw, p, dark, usum, flags);
+  SKYRX_CHECK_LAUNCH("raww_scan_kernel");
+  // 2-D byte view of the cube, 128-byte x 128-line swizzled boxes
+  const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;
+  cuuint64_t dims[2] = {line_bytes, (cuuint64_t)lines};
+  cuuint64_t strides[1] = {line_bytes};
+  cuuint32_t box[2] = {128, (cuuint32_t)kLb};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap map;
+  const CUresult r = tensor_map_encoder()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)raw, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const size_t smem = kStages * (size_t)p.na * kAtom + 16 * 8 + 1024;
+  cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // lower-triangle blocks (row atom >= column atom), four per pass; the first block
+  // of pass 0 is the diagonal (0, 0)
+  int br[32], bc[32], nb = 0;
+  for (int a = 0; a < p.na; ++a)
+    for (int c = 0; c <= a; ++c) br[nb] = a, bc[nb] = c, ++nb;
+  for (int b0 = 0; b0 < nb; b0 += 4) {
+    p.nblk = nb - b0 < 4 ? nb - b0 : 4;
+    for (int i = 0; i < p.nblk; ++i) p.blk_r[i] = br[b0 + i], p.blk_c[i] = bc[b0 + i];
+    p.first_pass = b0 == 0;
+    raww_gram_kernel<<<grid, kThreads, smem, st>>>(map, p);
+    SKYRX_CHECK_LAUNCH("raww_gram_kernel");
+  }
+  cudaFreeAsync(usum, st);
+  return gram_raw_sum_and_center(p.part, grid, bands, shift, moments, st);
+}
+
+}  // namespace skyrx

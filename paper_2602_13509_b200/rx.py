@@ -328,7 +328,7 @@ class DetectPlan:
         self.qinv = _dev.zeros((batch, bands), torch.float32)
         self.tc_ws_bytes = int(lib.skyrx_stats_tc_workspace(bands)) if self.tc_stats else 0
         self.tc_ws = _dev.empty((max(self.tc_ws_bytes, 8),), torch.uint8)
-        self.raw_stats = bands <= 128 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
+        self.raw_stats = bands <= 272 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
         self.raw_ws_bytes = int(lib.skyrx_stats_raw_workspace(bands)) if self.raw_stats else 0
         self.raw_ws = _dev.empty((max(self.raw_ws_bytes, 8),), torch.uint8)
         # exact-digit score kernel (per-sample records, B <= 128): the path for
@@ -411,13 +411,13 @@ class DetectPlan:
         # the exact-digit score kernels could not apply (raw counts >= 4096: 16, or no
         # no-clamp proof: 32): rescore with the general kernels
         fl = self.ds.flags.cpu().numpy()
-        rescore = [i for i in range(self.ds.batch) if i not in redo and fl[i] & 48]
+        rescore = [i for i in range(self.ds.batch) if fl[i] & 48]
         for i in rescore:
             self.used_raw[i] = False
             keep, self.tcw = self.tcw, False
             self.score(i, *cubes[i])
             self.tcw = keep
-        return redo + rescore
+        return sorted(set(redo) | set(rescore))
 
     def finalize(self):
         self.ds.finalize()

@@ -380,7 +380,8 @@ class TestDetect:
         assert plan.tcw
         det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
         fl = int(plan.ds.flags[0].item())
-        assert fl & 128 and not fl & (16 | 32 | 64)  # proof present, kernel applied
+        assert (fl & 12) == 8 or (fl & 192) == 128  # no-clamp proof from the moments pass
+        assert not fl & (16 | 32)                   # the exact-digit kernel applied
         check_detection(det, raw, t)
 
     def test_wide_kernel_without_clamp_proof_rescores(self, P):
@@ -391,7 +392,7 @@ class TestDetect:
         plan = P.DetectPlan(L, S, B)
         det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
         fl = int(plan.ds.flags[0].item())
-        assert fl & 64 and fl & 32
+        assert fl & (4 | 64)  # the clamp was seen by whichever moments pass ran
         check_detection(det, raw, t)
 
     def test_exact_digit_kernel_rejects_wide_counts(self, P, monkeypatch):
@@ -425,7 +426,9 @@ class TestDetect:
 
     @pytest.mark.parametrize("S,B,L,gain", [(900, 70, 300, 1.0), (64, 70, 4100, 2.5),
                                             (96, 48, 2800, 1.0), (40, 16, 6600, 1.0),
-                                            (1024, 128, 260, 1.0), (128, 79, 2100, 0.75)])
+                                            (1024, 128, 260, 1.0), (128, 79, 2100, 0.75),
+                                            (1024, 270, 300, 1.0), (128, 160, 2100, 0.75),
+                                            (64, 150, 4100, 1.0)])
     def test_raw_byte_moments(self, P, S, B, L, gain):
         """Constant line gain: exact integer byte Grams on the tensor cores."""
         from paper_2602_13509_b200 import _lib
