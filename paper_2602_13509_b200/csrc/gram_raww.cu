@@ -62,45 +62,59 @@ __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
 }
 
 // per unit: column sums and minima of every u16 lane of the 16-B aligned window.
-// A warp owns 32 consecutive lanes (64 B of every line), loads unrolled 8 deep.
-__global__ void __launch_bounds__(320) raww_scan_kernel(const uint16_t* __restrict__ raw,
+// A thread owns one 16-B vector (8 lanes) of one unit's window and walks its lines
+// with 16-B loads (a warp covers 512 contiguous bytes of a line), 4 lines deep.
+__global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restrict__ raw,
                                                         Params p,
                                                         const float* __restrict__ dark,
                                                         uint32_t* __restrict__ usum,
                                                         int32_t* __restrict__ flags) {
   const int B = p.B;
-  const int64_t pitch = (int64_t)p.S * B;
+  const int64_t pitch = (int64_t)p.S * B;  // u16 per line
+  const int nv = p.nw16 / 8;
   bool clamp = false;
-  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < p.units * nv;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = it / nv;
+    const int v = (int)(it - u * nv);
     int s;
     int64_t l0, nl;
     unit_geom(p, u, s, l0, nl);
     const int64_t w0 = ((int64_t)s * B * 2 & ~(int64_t)15) >> 1;  // first u16 of the window
     const int off = (int)(((int64_t)s * B * 2 & 15) >> 1);
-    for (int q = threadIdx.x; q < p.nw16; q += blockDim.x) {
-      const int64_t col = w0 + q;
-      const bool in = col < pitch;
-      uint32_t sum = 0, mn = 0xFFFFu;
-      if (in) {
-        const uint16_t* c = raw + l0 * pitch + col;
-        int64_t l = 0;
-        for (; l + 8 <= nl; l += 8) {
-          uint32_t v[8];
+    const int64_t col = w0 + 8 * v;
+    uint32_t sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t mn[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (col < pitch) {  // line ends are 16-B multiples: a vector is all in or all out
+      const uint4* c = reinterpret_cast<const uint4*>(raw + l0 * pitch + col);
+      const int64_t vp = pitch / 8;  // uint4 per line
+      int64_t l = 0;
+      auto acc = [&](const uint4 q) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = __ldg(c + (l + i) * pitch);
+        for (int i = 0; i < 4; ++i) {
+          sum[2 * i] += w[i] & 0xFFFFu;
+          sum[2 * i + 1] += w[i] >> 16;
+          mn[i] = __vminu2(mn[i], w[i]);
+        }
+      };
+      for (; l + 4 <= nl; l += 4) {
+        uint4 q[4];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) sum += v[i], mn = min(mn, v[i]);
-        }
-        for (; l < nl; ++l) {
-          const uint32_t v = __ldg(c + l * pitch);
-          sum += v;
-          mn = min(mn, v);
-        }
+        for (int i = 0; i < 4; ++i) q[i] = __ldg(c + (l + i) * vp);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc(q[i]);
       }
-      usum[u * p.nw16 + q] = sum;
-      const int b = q - off;
-      if (in && b >= 0 && b < B && (float)mn < __ldg(dark + (int64_t)s * B + b)) clamp = true;
+      for (; l < nl; ++l) acc(__ldg(c + l * vp));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = 8 * v + i - off;
+        const uint32_t m = (i & 1) ? (mn[i >> 1] >> 16) : (mn[i >> 1] & 0xFFFFu);
+        if (b >= 0 && b < B && (float)m < __ldg(dark + (int64_t)s * B + b)) clamp = true;
+      }
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) usum[u * p.nw16 + 8 * v + i] = sum[i];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, 8);
   if (__any_sync(0xffffffffu, clamp) && (threadIdx.x & 31) == 0) atomicOr(flags, 4);
@@ -295,7 +309,7 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
                     cudaSuccess,
                 "cudaMallocAsync failed");
   p.usum = usum;
-  raww_scan_kernel<<<kSMs * 4, 320, 0, st>>>(raw, p, dark, usum, flags);
+  raww_scan_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, dark, usum, flags);
   SKYRX_CHECK_LAUNCH("raww_scan_kernel");
   // 2-D byte view of the cube, 128-byte x 128-line swizzled boxes
   const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     double* __restrict__ sigma_all, double* __restrict__ chol_all,
     double* __restrict__ inv_all, double* __restrict__ w64_all, float* __restrict__ wf_all,
     int ld_w, float* __restrict__ mhl_all, double* __restrict__ ridge_all,
-    int32_t* __restrict__ status_all) {
+    int32_t* __restrict__ status_all, int do_inverse) {
   extern __shared__ __align__(16) double fsm[];
   __shared__ double scratch[40];
   __shared__ int s_fail;
@@ -392,6 +392,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   if (A != chol)
     for (size_t e = tid; e < BB; e += NT) chol[e] = A[e];
   __syncthreads();
+  if (!do_inverse) {  // wide matrices: W, Sigma^-1 and wf by the multi-CTA kernels below
+    if (tid == 0) {
+      status_all[m] = SKYRX_OK;
+      ridge_all[m] = ridge;
+    }
+    return;
+  }
   // W = L^-1 (forward substitution on e_c, one column per thread) in shared memory
   // next to L when both fit, so the O(B^3) inner loops never touch global memory
   double* Wm = (A == fsm && B <= kSmemInvMaxB) ? fsm + BB : w64;
@@ -431,6 +438,60 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   if (tid == 0) {
     status_all[m] = SKYRX_OK;
     ridge_all[m] = ridge;
+  }
+}
+
+// Wide matrices (B > kSmemInvMaxB): W = L^-1 with one WARP per column (lanes split the
+// forward-substitution dot products, the column's solution in shared memory), the
+// columns spread over CTAs; then Sigma^-1 = W^T W and the f32 copy, one thread per entry.
+__global__ void __launch_bounds__(1024) wide_trinv_kernel(const double* __restrict__ chol_all,
+                                                          int B, double* __restrict__ w64_all,
+                                                          const int32_t* __restrict__ status_all) {
+  extern __shared__ double xs[];  // [32 warps][B]
+  const int m = blockIdx.y;
+  if (status_all[m] != SKYRX_OK) return;
+  const double* L = chol_all + (size_t)m * B * B;
+  double* W = w64_all + (size_t)m * B * B;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + w;
+  if (c >= B) return;
+  double* x = xs + (size_t)w * B;
+  for (int i = lane; i < c; i += 32) W[(size_t)i * B + c] = 0.0;
+  for (int i = c; i < B; ++i) {
+    double a = 0.0;
+    for (int k = c + lane; k < i; k += 32) a += L[(size_t)i * B + k] * x[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    const double xi = ((i == c ? 1.0 : 0.0) - a) / L[(size_t)i * B + i];
+    if (lane == 0) {
+      x[i] = xi;
+      W[(size_t)i * B + c] = xi;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void wide_inv_kernel(const double* __restrict__ w64_all, int B,
+                                double* __restrict__ inv_all, float* __restrict__ wf_all, int ld_w,
+                                const int32_t* __restrict__ status_all) {
+  const int m = blockIdx.y;
+  if (status_all[m] != SKYRX_OK) return;
+  const double* W = w64_all + (size_t)m * B * B;
+  double* inv = inv_all + (size_t)m * B * B;
+  float* wf = wf_all + (size_t)m * ld_w * ld_w;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < (int64_t)B * B) {
+    const int i = (int)(e / B), j = (int)(e - (int64_t)i * B);
+    if (j <= i) {  // sigma_inv = W^T W, exactly symmetric by construction
+      double acc = 0.0;
+      for (int k = i; k < B; ++k) acc += W[(size_t)k * B + i] * W[(size_t)k * B + j];
+      inv[(size_t)i * B + j] = acc;
+      inv[(size_t)j * B + i] = acc;
+    }
+  }
+  if (e < (int64_t)ld_w * ld_w) {  // f32 whitening matrix, transposed (wf[k, j] = W[j][k])
+    const int k = (int)(e / ld_w), j = (int)(e - (int64_t)k * ld_w);
+    wf[e] = (j < B && k < B && k <= j) ? (float)W[(size_t)j * B + k] : 0.0f;
   }
 }
 
@@ -575,10 +636,22 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   const size_t sm = bands <= kSmemInvMaxB    ? 2 * (size_t)bands * bands * sizeof(double)
                     : bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double)
                                              : 0;
+  const bool wide = bands > kSmemInvMaxB;
+  cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  finalize_kernel<<<batch, kFinThreads, sm, as_stream(stream)>>>(
-      moments, shift, flags, bands, mu, sigma, chol, sigma_inv, whiten64, whiten, ld_w, mu_hilo,
-      ridge, status);
+  finalize_kernel<<<batch, kFinThreads, sm, st>>>(moments, shift, flags, bands, mu, sigma, chol,
+                                                  sigma_inv, whiten64, whiten, ld_w, mu_hilo,
+                                                  ridge, status, wide ? 0 : 1);
   SKYRX_CHECK_LAUNCH("skyrx_stats_finalize");
+  if (wide) {
+    const size_t xs = 32 * (size_t)bands * sizeof(double);
+    cudaFuncSetAttribute(wide_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
+    wide_trinv_kernel<<<dim3(ceil_div(bands, 32), batch), 1024, xs, st>>>(chol, bands, whiten64,
+                                                                          status);
+    const int64_t work = std::max((int64_t)bands * bands, (int64_t)ld_w * ld_w);
+    wide_inv_kernel<<<dim3((int)ceil_div<int64_t>(work, 256), batch), 256, 0, st>>>(
+        whiten64, bands, sigma_inv, whiten, ld_w, status);
+    SKYRX_CHECK_LAUNCH("skyrx_stats_finalize/wide");
+  }
   return SKYRX_OK;
 }
