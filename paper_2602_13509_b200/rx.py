@@ -345,9 +345,12 @@ class DetectPlan:
                         if (self.tcs or self.tcw) else None)
 
     def run(self, i: int, raw: torch.Tensor, dark, coeff, gains, k: int | None = None,
-            precise: bool = False, force_ffma: bool = False, gain_const: float | None = None):
-        """Enqueue the moments of cube i (no host synchronisation)."""
-        return self._moments(i, raw, dark, coeff, gains, precise, force_ffma, gain_const, True)
+            precise: bool = False, force_ffma: bool = False, gain_const: float | None = None,
+            events=None):
+        """Enqueue the moments of cube i (no host synchronisation).  ``events`` =
+        (start, end) CUDA events recorded around the moments kernel call alone."""
+        return self._moments(i, raw, dark, coeff, gains, precise, force_ffma, gain_const, True,
+                             events)
 
     def run_moments(self, i: int, raw: torch.Tensor, dark, coeff, gains, precise: bool = False,
                     force_ffma: bool = False, gain_const: float | None = None):
@@ -355,7 +358,8 @@ class DetectPlan:
         a shift common to every rank's block)."""
         return self._moments(i, raw, dark, coeff, gains, precise, force_ffma, gain_const, False)
 
-    def _moments(self, i, raw, dark, coeff, gains, precise, force_ffma, gain_const, own_shift):
+    def _moments(self, i, raw, dark, coeff, gains, precise, force_ffma, gain_const, own_shift,
+                 events=None):
         L, S, B = self.shape
         ds = self.ds
         s = _dev.stream_ptr()
@@ -376,10 +380,14 @@ class DetectPlan:
             if own_shift:
                 _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
             self.used_raw[i] = True
+            if events is not None:
+                events[0].record()
             _lib.call("skyrx_stats_raw", raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.raw_ws.data_ptr(), self.raw_ws_bytes, s)
+            if events is not None:
+                events[1].record()
         elif (self.tc_stats and not precise and not small and own_shift
                 and lib.skyrx_stats_tc_supported(L, S, B, raw.data_ptr())):
             _lib.call("skyrx_quant_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
