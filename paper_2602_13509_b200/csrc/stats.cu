@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     int32_t* __restrict__ status_all, int do_inverse) {
   extern __shared__ __align__(16) double fsm[];
   __shared__ double scratch[40];
+  __shared__ double dg[1024];  // Cholesky pivots l_jj
   __shared__ int s_fail;
   const int B = bands;
   const size_t BB = (size_t)B * B;
@@ -353,17 +354,16 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     }
     if (tid == 0) s_fail = 0;
     __syncthreads();
-    // right-looking Cholesky, lower triangle
+    // right-looking Cholesky, lower triangle; the pivots go to dg[] (A's diagonal is
+    // rewritten at the end) so every thread reads the same final a_jj without a barrier
     for (int j = 0; j < B; ++j) {
       const double ajj = A[(size_t)j * B + j];
-      if (!(ajj > 0.0)) {  // LAPACK potrf: non-positive or NaN pivot fails
+      if (!(ajj > 0.0)) {  // LAPACK potrf: non-positive or NaN pivot fails (uniform branch)
         if (tid == 0) s_fail = 1;
-        __syncthreads();
         break;
       }
       const double ljj = sqrt(ajj);
-      __syncthreads();
-      if (tid == 0) A[(size_t)j * B + j] = ljj;
+      if (tid == 0) dg[j] = ljj;
       for (int i = j + 1 + tid; i < B; i += NT) A[(size_t)i * B + j] /= ljj;
       __syncthreads();
       // trailing update of the lower triangle: a warp per row, lanes along it
@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
       }
       __syncthreads();
     }
+    __syncthreads();
     ok = (s_fail == 0);
+    if (ok)
+      for (int j = tid; j < B; j += NT) A[(size_t)j * B + j] = dg[j];
     __syncthreads();
   }
   if (!ok) {
