@@ -227,21 +227,30 @@ __global__ void __launch_bounds__(256) shift_kernel(CubeRef cube, double* __rest
   const int64_t m = n > 0 ? (n + step - 1) / step : 0;
   const int B = cube.bands;
   const int b = blockIdx.x;
-  double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+  auto value = [&](int64_t i) -> float {
     const int64_t pix = i * step;
     const int64_t gi = pix * B + b;
-    float x;
     if constexpr (KIND == SKYRX_IN_RAW_U16) {
       const int64_t line = pix / cube.samples;
       const int64_t tb = (pix - line * cube.samples) * B + b;
-      x = calib((float)reinterpret_cast<const uint16_t*>(cube.pixels)[gi], cube.dark[tb],
-                cube.coeff[tb], cube.gain[line]);
+      return calib((float)__ldg(reinterpret_cast<const uint16_t*>(cube.pixels) + gi),
+                   __ldg(cube.dark + tb), __ldg(cube.coeff + tb), __ldg(cube.gain + line));
     } else {
-      x = reinterpret_cast<const float*>(cube.pixels)[gi];
+      return __ldg(reinterpret_cast<const float*>(cube.pixels) + gi);
     }
-    acc += (double)x;
+  };
+  // the strided sample is scattered over the whole cube: issue 8 loads before
+  // summing (same order as a plain loop, so the shift is unchanged)
+  double acc = 0.0;
+  int64_t i = threadIdx.x;
+  for (; i + 7 * (int64_t)blockDim.x < m; i += 8 * (int64_t)blockDim.x) {
+    float x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = value(i + q * (int64_t)blockDim.x);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += (double)x[q];
   }
+  for (; i < m; i += blockDim.x) acc += (double)value(i);
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
   __syncthreads();

@@ -50,3 +50,7 @@ def tcs_only():
 if plan.tcs:
     print(json.dumps({'prep_ms': t(prep_only), 'tcs_only_ms': t(tcs_only)}))
 print(json.dumps({'finalize_ms': t(lambda: plan.ds.finalize())}))
+def shift_only():
+    _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, raw.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(),
+              g.data_ptr(), ds.shift[0].data_ptr(), _dev.stream_ptr())
+print(json.dumps({'shift_ms': t(shift_only)}))
