@@ -28,6 +28,7 @@ from .rx import (
     DeviceStats,
     compute_stats,
     detect,
+    detect_batch,
     normalize_scores,
     rx_scores,
     threshold_scores,
@@ -42,7 +43,7 @@ __all__ = [
     "GroundTruthMask", "InsSample", "LineMeta", "RadianceCube", "RawCube", "ScoreMap",
     "band_nearest", "CalibrationTables", "apply_calibration", "bin_bands", "calibrate_bin_rgb",
     "discard_oob_bands", "extract_rgb", "CubeStats", "DetectPlan", "DeviceStats",
-    "compute_stats", "detect", "normalize_scores", "rx_scores", "threshold_scores",
+    "compute_stats", "detect", "detect_batch", "normalize_scores", "rx_scores", "threshold_scores",
     "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install", "__version__",
 ]
 

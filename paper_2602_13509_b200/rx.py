@@ -84,13 +84,15 @@ class DeviceStats:
         self.ridge = _dev.zeros((batch,), f64)
         self.status = _dev.zeros((batch,), torch.int32)
 
-    def finalize(self):
-        _lib.call("skyrx_stats_finalize", self.moments.data_ptr(), self.shift.data_ptr(),
-                  self.flags.data_ptr(), self.bands, self.batch, self.mu.data_ptr(),
-                  self.sigma.data_ptr(), self.chol.data_ptr(), self.sigma_inv.data_ptr(),
-                  self.w64.data_ptr(), self.whiten.data_ptr(), self.ld,
-                  self.mu_hilo.data_ptr(), self.ridge.data_ptr(), self.status.data_ptr(),
-                  _dev.stream_ptr())
+    def finalize(self, slot: int | None = None):
+        """Factor every slot's moments, or only ``slot``."""
+        sl = slice(None) if slot is None else slice(slot, slot + 1)
+        n = self.batch if slot is None else 1
+        t = lambda x: x[sl].data_ptr()  # noqa: E731
+        _lib.call("skyrx_stats_finalize", t(self.moments), t(self.shift), t(self.flags),
+                  self.bands, n, t(self.mu), t(self.sigma), t(self.chol), t(self.sigma_inv),
+                  t(self.w64), t(self.whiten), self.ld, t(self.mu_hilo), t(self.ridge),
+                  t(self.status), _dev.stream_ptr())
         return self
 
     def check(self, i: int = 0, npix: int | None = None):
@@ -409,7 +411,7 @@ class DetectPlan:
 
         ``cubes[i] = (raw, dark, coeff, gains)``.  Returns the recomputed slots."""
         st = self.ds.status.cpu().numpy()
-        redo = [i for i in range(self.ds.batch) if st[i] == _lib.ERR_RANGE]
+        redo = [i for i in cubes if st[i] == _lib.ERR_RANGE]
         if redo:
             for i in redo:
                 self.run(i, *cubes[i], force_ffma=True)
@@ -419,7 +421,7 @@ class DetectPlan:
         # the exact-digit score kernels could not apply (raw counts >= 4096: 16, or no
         # no-clamp proof: 32): rescore with the general kernels
         fl = self.ds.flags.cpu().numpy()
-        rescore = [i for i in range(self.ds.batch) if fl[i] & 48]
+        rescore = [i for i in cubes if fl[i] & 48]
         for i in rescore:
             self.used_raw[i] = False
             keep, self.tcw = self.tcw, False
@@ -427,12 +429,14 @@ class DetectPlan:
             self.tcw = keep
         return sorted(set(redo) | set(rescore))
 
-    def finalize(self):
-        self.ds.finalize()
+    def finalize(self, slot: int | None = None):
+        self.ds.finalize(slot)
         self.launches += 1
         if self.tc:
-            _lib.call("skyrx_pack_whiten", self.ds.w64.data_ptr(), self.ds.bands, self.ds.batch,
-                      self.wpack.data_ptr(), _dev.stream_ptr())
+            sl = slice(None) if slot is None else slice(slot, slot + 1)
+            _lib.call("skyrx_pack_whiten", self.ds.w64[sl].data_ptr(), self.ds.bands,
+                      self.ds.batch if slot is None else 1, self.wpack[sl].data_ptr(),
+                      _dev.stream_ptr())
             self.launches += 1
         return self
 
@@ -568,3 +572,108 @@ def detect(raw, tables, *, k: int | None = None, device: bool | None = None,
         return Detection(ds, plan.scores[0], plan.mask[0].to(torch.bool), thr, mx)
     return Detection(ds.host(0, n), _dev.to_host(plan.scores[0]),
                      _dev.to_host(plan.mask[0]).view(bool), thr, mx)
+
+
+def detect_batch(raws, tables, *, k: int | None = None,
+                 plan: DetectPlan | None = None) -> list[Detection]:
+    """:func:`detect` over a sequence of HOST cubes of one shape, pipelined.
+
+    Two device slots: while the GPU works on cube i, the copy stream uploads cube
+    i + 1 and downloads the scores, mask and statistics of cube i - 1 (PCIe is full
+    duplex), so a stream of strips runs at the host-link rate.  ``tables`` is one
+    CalibrationTables for all cubes or one per cube.  Results are host numpy
+    (pinned) like :func:`detect`; a cube whose fast path did not apply (clamp,
+    counts >= 4096) is redone with :func:`detect` after the pipeline drains.
+    """
+    raws = list(raws)
+    if not raws:
+        return []
+    tabs = list(tables) if isinstance(tables, (list, tuple)) else [tables] * len(raws)
+    if len(tabs) != len(raws):
+        raise ValueError("one CalibrationTables per cube, or one for all")
+    L, S, B = raws[0].lines, raws[0].samples, raws[0].bands
+    for r in raws:
+        if (r.lines, r.samples, r.bands) != (L, S, B):
+            raise ValueError("detect_batch: every cube must have the same shape")
+    n = L * S
+    if n <= B:
+        raise ValueError(f"insufficient samples: {n} pixels for {B} bands")
+    plan = plan or DetectPlan(L, S, B, batch=2)
+    if plan.ds.batch < 2 or plan.shape != (L, S, B):
+        raise ValueError("detect_batch needs a DetectPlan of this shape with batch >= 2")
+    dev = _dev.require_cuda()
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    bufs = [torch.empty((L, S, B), dtype=torch.uint16, device=dev) for _ in range(2)]
+    nm = plan.ds.moments.shape[1]
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    h2d, comp_done, d2h = [], [], []
+    outs = []
+    for i, cube in enumerate(raws):
+        j = i % 2
+        tab = tables_of(tabs[i])
+        _check_tables(cube, tab)
+        gains = line_gains(cube)
+        gain_const = constant_gain(gains, tab)
+        dark, coeff = tab.device()
+        v = cube.values
+        src = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v))
+        h2d.append(ev())
+        with torch.cuda.stream(copy):
+            if i >= 2:
+                copy.wait_event(comp_done[i - 2])  # slot j's raw buffer is free
+            bufs[j].copy_(src.view(torch.uint16) if src.dtype != torch.uint16 else src,
+                          non_blocking=True)
+            h2d[i].record(copy)
+        comp.wait_event(h2d[i])
+        if i >= 2:
+            comp.wait_event(d2h[i - 2])  # slot j's outputs were downloaded
+        # gains: a pinned staging copy, so the upload does not block the host (a pageable
+        # copy would wait for the compute stream and serialise the pipeline)
+        gsrc = gains if isinstance(gains, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(gains, np.float32))
+        gd = gsrc.to(dev, non_blocking=True) if gsrc.is_cuda else \
+            gsrc.pin_memory().to(dev, non_blocking=True)
+        plan.run(j, bufs[j], dark, coeff, gd, gain_const=gain_const)
+        plan.finalize(j).score(j, bufs[j], dark, coeff, gd, k)
+        comp_done.append(ev())
+        comp_done[i].record(comp)
+        o = {name: torch.empty(shape, dtype=dt, pin_memory=True) for name, shape, dt in (
+            ("scores", (L, S), torch.float32), ("mask", (L, S), torch.uint8),
+            ("mu", (B,), torch.float64), ("sigma", (B, B), torch.float64),
+            ("inv", (B, B), torch.float64), ("chol", (B, B), torch.float64),
+            ("ridge", (1,), torch.float64), ("status", (1,), torch.int32),
+            ("flags", (1,), torch.int32), ("thr", (1,), torch.float32),
+            ("key", (1,), torch.int32))}
+        ds = plan.ds
+        with torch.cuda.stream(copy):
+            copy.wait_event(comp_done[i])
+            for name, t in (("scores", plan.scores[j]), ("mask", plan.mask[j]),
+                            ("mu", ds.mu[j]), ("sigma", ds.sigma[j]), ("inv", ds.sigma_inv[j]),
+                            ("chol", ds.chol[j]), ("ridge", ds.ridge[j:j + 1]),
+                            ("status", ds.status[j:j + 1]), ("flags", ds.flags[j:j + 1]),
+                            ("thr", plan.thr[j:j + 1]),
+                            ("key", plan.max_key[j:j + 1].view(torch.int32))):
+                o[name].copy_(t, non_blocking=True)
+            d2h.append(ev())
+            d2h[i].record(copy)
+        outs.append(o)
+    copy.synchronize()
+    comp.synchronize()
+    dets = []
+    for i, o in enumerate(outs):
+        st, fl = int(o["status"][0]), int(o["flags"][0])
+        if st == _lib.ERR_RANGE or fl & 48:
+            dets.append(detect(raws[i], tabs[i], k=k, device=False))  # general path
+            continue
+        if st == _lib.ERR_INSUFFICIENT:
+            raise ValueError(f"insufficient samples: {n} pixels for {B} bands")
+        if st != _lib.OK:
+            raise ValueError(_STATUS_MSG.get(st, f"stats failed with status {st}"))
+        stats = CubeStats(mu=o["mu"].numpy(), sigma=o["sigma"].numpy(),
+                          sigma_inv=o["inv"].numpy(), ridge_used=float(o["ridge"][0]),
+                          chol_lower=o["chol"].numpy())
+        key = torch.tensor([int(o["key"][0]) & 0xFFFFFFFF])
+        dets.append(Detection(stats, o["scores"].numpy(), o["mask"].numpy().view(bool),
+                              float(o["thr"][0]), key_to_float(key)))
+    return dets

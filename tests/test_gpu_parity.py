@@ -409,6 +409,26 @@ class TestDetect:
         assert int(plan.ds.flags[0].item()) & 16
         check_detection(det, raw, t)
 
+    def test_detect_batch_matches_detect(self, P):
+        """The pipelined host-buffer batch (two device slots, copy stream) returns what
+        detect() returns cube by cube, including a cube that needs the general path."""
+        S, B, L = 900, 70, 64
+        tabs, raws = [], []
+        for i in range(5):
+            t = osynth.make_tables(60 + i, S, B, 5)
+            raw = osynth.generate_lines(t, 0, L).copy()
+            if i == 3:
+                raw[5, 6, 7] = 0  # clamps: redone through detect()
+            tabs.append(P.CalibrationTables(t.dark, t.coeff))
+            raws.append(raw_cube(P, raw))
+        got = P.detect_batch(raws, tabs)
+        for g, r, tb in zip(got, raws, tabs):
+            want = P.detect(r, tb)
+            assert np.array_equal(g.scores, want.scores)
+            assert np.array_equal(g.mask, want.mask)
+            assert g.threshold == want.threshold and g.max_score == want.max_score
+            assert np.array_equal(g.stats.sigma_inv, want.stats.sigma_inv)
+
     @pytest.mark.parametrize("L", [1, 33, 129])
     def test_tensor_core_score_schedule_edges(self, P, L):
         """Fewer tiles than sample blocks, and ragged narrow-block tiles (2-D TMA box
