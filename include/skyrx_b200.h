@@ -249,6 +249,16 @@ int skyrx_topk_pick(int32_t digit, void* workspace, float* thr, void* stream);
 uint32_t* skyrx_topk_histogram(void* workspace);
 int32_t skyrx_topk_hist_len(void);
 
+/* ---------------------------------------------------------------- link payload (next to the path)
+ * datalink.py:141-177: per pixel [RGB565 | half(sqrt(score / max))] little-endian u16
+ * words.  skyrx_link_maxima: keys[0..3] = order-preserving u32 keys of the cube's max
+ * score and max R, G, B (rgb is (n, 3) f32); skyrx_link_payload encodes with them,
+ * or (keys == NULL) with max_host_host[0..3] = max_score, max_r, max_g, max_b. */
+int skyrx_link_maxima(const float* scores, const float* rgb, int64_t n, uint32_t* keys,
+                      void* stream);
+int skyrx_link_payload(const float* scores, const float* rgb, int64_t n, const uint32_t* keys,
+                       const double* max_host, uint16_t* payload, void* stream);
+
 /* ---------------------------------------------------------------- synthetic sensor (bench/test inputs)
  * Bit-identical to oracle/synth.py generate_lines(): raw counts for lines
  * [line0, line0 + nlines) of the seeded scene.  Tables as in SceneTables. */

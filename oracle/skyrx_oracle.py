@@ -328,3 +328,62 @@ def detect(raw, dark, coeff, gains, k: int | None = None):
     scores = rx_scores(rad, stats)
     mask = topk_mask(scores, k)
     return stats, scores, mask
+
+
+# --------------------------------------------------------------------------- link payload
+# datalink.py:1-24 (layout), 141-177 (per-pixel encodings), 205-240 (packetize_cube)
+PAYLOAD_SAMPLES = 900         # datalink.py:36
+HEADER_LEN = 128              # datalink.py:35
+
+
+def quantize(channel, channel_max: float, levels: int) -> np.ndarray:
+    """datalink.py:141-145: round-half-up of x / max * levels in f64, clipped; 0 if max <= 0."""
+    if channel_max <= 0.0:
+        return np.zeros(np.shape(channel), np.uint16)
+    q = np.floor(np.asarray(channel, np.float32).astype(np.float64) / channel_max * levels + 0.5)
+    return np.clip(q, 0, levels).astype(np.uint16)
+
+
+def pack_rgb565(rgb, max_r: float, max_g: float, max_b: float) -> np.ndarray:
+    """datalink.py:148-152: R in the high 5 bits, G the middle 6, B the low 5."""
+    rgb = np.asarray(rgb)
+    return ((quantize(rgb[..., 0], max_r, 31) << 11) | (quantize(rgb[..., 1], max_g, 63) << 5)
+            | quantize(rgb[..., 2], max_b, 31)).astype(np.uint16)
+
+
+def encode_scores_half(scores, max_score: float) -> np.ndarray:
+    """datalink.py:163-168: IEEE half of sqrt(score / max) (f64 math), as u16 bits."""
+    s = np.asarray(scores, np.float32)
+    if max_score <= 0.0:
+        return np.zeros(s.shape, np.uint16)
+    return np.sqrt(s.astype(np.float64) / max_score).astype(np.float16).view(np.uint16)
+
+
+def pack_header(cube_id, line_index, lines_per_cube, samples, exposure_start_us, max_score,
+                max_r, max_g, max_b, ins_before, ins_after) -> bytes:
+    """datalink.py:48-77 + 130-133: the 128-byte little-endian line header."""
+    import struct
+
+    head = struct.pack("<4sHHIIIIQffff", b"SKRX", 1, HEADER_LEN, cube_id, line_index,
+                       lines_per_cube, samples, exposure_start_us, max_score, max_r, max_g, max_b)
+    ins = lambda s: struct.pack("<Qddffff", *s)  # noqa: E731  (ts, lat, lon, alt, roll, pitch, yaw)
+    return head + ins(ins_before) + ins(ins_after)
+
+
+def packetize_cube(cube_id, rgb, scores, line_meta) -> list:
+    """datalink.py:205-240: one 3728-byte packet per line; cube maxima in every header.
+    ``line_meta``: per line (exposure_start_us, ins_before tuple, ins_after tuple)."""
+    rgb = np.asarray(rgb, np.float32)
+    scores = np.asarray(scores, np.float32)
+    lines = rgb.shape[0]
+    max_score = float(scores.max()) if scores.size else 0.0
+    mr, mg, mb = (float(rgb[:, :, c].max()) for c in range(3))
+    out = []
+    for i in range(lines):
+        exp, ib, ia = line_meta[i]
+        payload = np.empty((rgb.shape[1], 2), "<u2")
+        payload[:, 0] = pack_rgb565(rgb[i], mr, mg, mb)
+        payload[:, 1] = encode_scores_half(scores[i], max_score)
+        out.append(pack_header(cube_id, i, lines, rgb.shape[1], exp, max_score, mr, mg, mb, ib, ia)
+                   + payload.tobytes())
+    return out

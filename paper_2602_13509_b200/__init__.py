@@ -36,6 +36,7 @@ from .rx import (
     transmit_domain,
 )
 from .stream import ChunkResult, StreamingRX
+from .datalink import encode_scores_half, link_payload, pack_rgb565, packetize_cube
 
 __version__ = "0.1.0"
 
@@ -45,6 +46,7 @@ __all__ = [
     "discard_oob_bands", "extract_rgb", "CubeStats", "DetectPlan", "DeviceStats",
     "compute_stats", "detect", "detect_batch", "normalize_scores", "rx_scores", "threshold_scores",
     "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install", "__version__",
+    "link_payload", "pack_rgb565", "encode_scores_half", "packetize_cube",
 ]
 
 

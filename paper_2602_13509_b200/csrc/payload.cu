@@ -1,0 +1,93 @@
+// Link payload epilogue: the per-pixel words of the air-side line
+// packets, datalink.py:141-177, bit-exact.
+//   word 0: RGB565 of the pixel's colour normalised to the cube's channel maxima,
+//           round-half-up in f64: q = floor(x / max * levels + 0.5) clipped (datalink.py:141-152)
+//   word 1: IEEE half of sqrt(score / max_score) in f64 (datalink.py:163-168)
+// The cube maxima are order-preserving u32 keys reduced on the device (atomicMax,
+// exact), so the whole epilogue runs without a host round trip.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace skyrx {
+
+__global__ void link_maxima_kernel(const float* __restrict__ scores, const float* __restrict__ rgb,
+                                   int64_t n, uint32_t* __restrict__ keys) {
+  uint32_t m[4] = {0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    m[0] = max(m[0], f2ord(scores[i]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m[1 + c] = max(m[1 + c], f2ord(rgb[3 * i + c]));
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t v = m[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0 && v) atomicMax(&keys[c], v);
+  }
+}
+
+__device__ __forceinline__ uint32_t quantize(float x, double mx, double levels) {
+  if (!(mx > 0.0)) return 0u;
+  const double q = floor(__dadd_rn(__dmul_rn(__ddiv_rn((double)x, mx), levels), 0.5));
+  if (!(q >= 0.0)) return 0u;  // negative or NaN (numpy's uint16 cast of NaN gives 0)
+  return (uint32_t)(q > levels ? levels : q);
+}
+
+__global__ void link_payload_kernel(const float* __restrict__ scores,
+                                    const float* __restrict__ rgb, int64_t n,
+                                    const uint32_t* __restrict__ keys, double4 mh,
+                                    uint32_t* __restrict__ payload) {
+  // maxima: device keys (the cube's own, no host round trip) or caller values
+  const double ms = keys ? (double)ord2f(keys[0]) : mh.x;
+  const double mr = keys ? (double)ord2f(keys[1]) : mh.y;
+  const double mg = keys ? (double)ord2f(keys[2]) : mh.z;
+  const double mb = keys ? (double)ord2f(keys[3]) : mh.w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c565 = (quantize(rgb[3 * i], mr, 31.0) << 11) |
+                          (quantize(rgb[3 * i + 1], mg, 63.0) << 5) |
+                          quantize(rgb[3 * i + 2], mb, 31.0);
+    uint32_t h = 0;
+    if (ms > 0.0) {
+      const __half hv = __double2half(__dsqrt_rn(__ddiv_rn((double)scores[i], ms)));
+      h = (uint32_t)*reinterpret_cast<const uint16_t*>(&hv);
+    }
+    payload[i] = c565 | (h << 16);  // little-endian [rgb565, half]
+  }
+}
+
+}  // namespace skyrx
+
+using namespace skyrx;
+
+extern "C" int skyrx_link_maxima(const float* scores, const float* rgb, int64_t n, uint32_t* keys,
+                                 void* stream) {
+  SKYRX_REQUIRE(n >= 0, "bad pixel count");
+  cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(keys, 0, 4 * sizeof(uint32_t), st);
+  if (n > 0) {
+    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 4 * kSMs);
+    link_maxima_kernel<<<grid, 256, 0, st>>>(scores, rgb, n, keys);
+  }
+  SKYRX_CHECK_LAUNCH("skyrx_link_maxima");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_link_payload(const float* scores, const float* rgb, int64_t n,
+                                  const uint32_t* keys, const double* max_host,
+                                  uint16_t* payload, void* stream) {
+  SKYRX_REQUIRE(keys != nullptr || max_host != nullptr, "need keys or host maxima");
+  SKYRX_REQUIRE(n >= 0, "bad pixel count");
+  if (n == 0) return SKYRX_OK;
+  SKYRX_REQUIRE(((uintptr_t)payload & 3) == 0, "payload must be 4-byte aligned");
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 8 * kSMs);
+  const double4 mh = keys ? make_double4(0, 0, 0, 0)
+                          : make_double4(max_host[0], max_host[1], max_host[2], max_host[3]);
+  link_payload_kernel<<<grid, 256, 0, as_stream(stream)>>>(scores, rgb, n, keys, mh,
+                                                           reinterpret_cast<uint32_t*>(payload));
+  SKYRX_CHECK_LAUNCH("skyrx_link_payload");
+  return SKYRX_OK;
+}

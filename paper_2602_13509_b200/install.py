@@ -10,7 +10,7 @@ from __future__ import annotations
 import importlib
 import sys
 
-from . import _accel, calibrate, rx
+from . import _accel, calibrate, datalink, rx
 
 _TARGETS = {
     "calibrate": {
@@ -27,6 +27,11 @@ _TARGETS = {
         "threshold_scores": rx.threshold_scores,
         "transmit_domain": rx.transmit_domain,
     },
+    "datalink": {
+        "pack_rgb565": datalink.pack_rgb565,
+        "encode_scores_half": datalink.encode_scores_half,
+        "packetize_cube": datalink.packetize_cube,
+    },
     "_accel": {
         "mahalanobis_sq": _accel.mahalanobis_sq,
     },
@@ -35,6 +40,7 @@ _TARGETS = {
         "compute_stats": rx.compute_stats,
         "rx_scores": rx.rx_scores,
         "transmit_domain": rx.transmit_domain,
+        "packetize_cube": datalink.packetize_cube,
     },
     "": {
         "compute_stats": rx.compute_stats,

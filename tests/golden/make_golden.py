@@ -177,6 +177,28 @@ def main():
     nt["edge/t"] = np.float64(t_edge)
     nt["edge/mask"] = threshold_scores(ScoreMap(edge), t_edge)
     np.savez_compressed(HERE / "normalize.npz", **nt)
+
+    # ---------------------------------------------------------------- link payload
+    from skyrx.datalink import encode_scores_half, pack_rgb565, packetize_cube
+    lk = {}
+    rgb = rng.random((900, 3)).astype(np.float32) * np.float32(40.0)
+    sc = (rng.random(900) ** 3 * 500).astype(np.float32)
+    # round-half-up edges: exact multiples of max/levels and their half steps
+    rgb[:6, 0] = np.float32(40.0) * np.array([0, 1, 0.5 / 31, 1.5 / 31, 30.5 / 31, 2.0 / 31],
+                                              np.float32)
+    sc[:4] = np.array([0.0, 500.0, 1e-30, 499.99997], np.float32)
+    lk["row/rgb"], lk["row/scores"] = rgb, sc
+    lk["row/rgb565"] = pack_rgb565(rgb, 40.0, 37.5, 12.25)
+    lk["row/half"] = encode_scores_half(sc, 500.0)
+    lk["row/half_zero_max"] = encode_scores_half(sc, 0.0)
+    lk["row/rgb565_zero_max"] = pack_rgb565(rgb, 0.0, 37.5, -1.0)
+    lines = 3
+    cube_rgb = (rng.random((lines, 900, 3)) * 30).astype(np.float32)
+    cube_sc = (rng.random((lines, 900)) ** 4 * 900).astype(np.float32)
+    pk = packetize_cube(7, cube_rgb, cube_sc, metas([1.0] * lines))
+    lk["cube/rgb"], lk["cube/scores"] = cube_rgb, cube_sc
+    lk["cube/packets"] = np.frombuffer(b"".join(pk), np.uint8)
+    np.savez_compressed(HERE / "datalink.npz", **lk)
     print("wrote", sorted(p.name for p in HERE.glob("*.npz")))
 
 

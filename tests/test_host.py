@@ -113,14 +113,14 @@ def test_device_scene_tables_match_oracle():
 
 def test_install_patches_pipeline_bindings():
     import paper_2602_13509_b200 as P
-    from paper_2602_13509_b200 import calibrate, rx
+    from paper_2602_13509_b200 import calibrate, datalink, rx
 
     fake = types.ModuleType("skyrx")
     subs = {}
-    for sub in ("calibrate", "rx", "_accel", "pipeline"):
+    for sub in ("calibrate", "rx", "_accel", "datalink", "pipeline"):
         m = types.ModuleType(f"skyrx.{sub}")
         for attr in ("apply_calibration", "calibrate_bin_rgb", "compute_stats", "rx_scores",
-                     "mahalanobis_sq", "transmit_domain"):
+                     "mahalanobis_sq", "transmit_domain", "packetize_cube", "pack_rgb565"):
             setattr(m, attr, None)
         subs[sub] = m
     fake.compute_stats = None
@@ -135,6 +135,8 @@ def test_install_patches_pipeline_bindings():
         assert subs["_accel"].mahalanobis_sq is not None
         assert fake.compute_stats is rx.compute_stats
         assert "skyrx.pipeline.rx_scores" in patched
+        assert subs["pipeline"].packetize_cube is datalink.packetize_cube
+        assert subs["datalink"].pack_rgb565 is datalink.pack_rgb565
     finally:
         for k, v in saved.items():
             if v is None:

@@ -192,3 +192,25 @@ class TestGenerator:
     def test_golden_inputs_regenerate(self, golden):
         t = synth.make_tables(21, 64, 70)
         assert np.array_equal(synth.generate_lines(t, 0, 48), golden["stats"]["synth70/raw"])
+
+
+# ----------------------------------------------------------------------------- link payload
+def test_link_payload_matches_reference(golden):
+    g = golden["datalink"]
+    assert np.array_equal(O.pack_rgb565(g["row/rgb"], 40.0, 37.5, 12.25), g["row/rgb565"])
+    assert np.array_equal(O.encode_scores_half(g["row/scores"], 500.0), g["row/half"])
+    assert np.array_equal(O.encode_scores_half(g["row/scores"], 0.0), g["row/half_zero_max"])
+    assert np.array_equal(O.pack_rgb565(g["row/rgb"], 0.0, 37.5, -1.0), g["row/rgb565_zero_max"])
+
+
+def test_packetize_cube_matches_reference(golden):
+    g = golden["datalink"]
+    lines = g["cube/rgb"].shape[0]
+    metas = []
+    for i in range(lines):  # tests/golden/make_golden.py metas()
+        t = 1_600_000_000_000_000 + i * 4016
+        metas.append((t, (t - 1000, 35.0, -90.0, 40.0, 0.0, 0.0, 0.0),
+                      (t + 4000, 35.0, -90.0, 40.0, 0.0, 0.0, 0.0)))
+    pk = O.packetize_cube(7, g["cube/rgb"], g["cube/scores"], metas)
+    assert all(len(p) == 3728 for p in pk)
+    assert np.array_equal(np.frombuffer(b"".join(pk), np.uint8), g["cube/packets"])
