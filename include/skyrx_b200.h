@@ -258,6 +258,27 @@ int skyrx_link_maxima(const float* scores, const float* rgb, int64_t n, uint32_t
                       void* stream);
 int skyrx_link_payload(const float* scores, const float* rgb, int64_t n, const uint32_t* keys,
                        const double* max_host, uint16_t* payload, void* stream);
+/* Whole line packets (datalink.py:176-189, 205-240): row l of `packets` (lines x (128 + 4S)
+ * bytes) = headers[l] (128 bytes, host-built, its four f32 maxima at bytes 32..47 replaced by
+ * the device keys) followed by the S payload words of line l. */
+int skyrx_link_packets(const float* scores, const float* rgb, int lines, int samples,
+                       const uint32_t* keys, const uint8_t* headers, uint8_t* packets,
+                       void* stream);
+
+/* ---- GF(256) Reed-Solomon erasure code (fec.py:101-195) ----------------
+ * skyrx_gf_matmul: for g < groups, out_g (r x n, row pitch opitch) = M_g (r x k, row-major)
+ * times D_g (k x n, row pitch dpitch) over GF(2^8) with polynomial 0x11D; M_g = mat +
+ * g * mat_gstride (0: one matrix for all), D_g = data + g * d_gstride, out_g likewise.
+ * Replaces _accel.gf256_matmul (_accel.py:50-70, 92-107): parity = E[k:] @ group payloads
+ * (fec.py:140-155), recovered = inv(E[rows])[absent] @ received (fec.py:182-191). */
+int skyrx_gf_matmul(const uint8_t* mat, int64_t mat_gstride, int r, int k, const uint8_t* data,
+                    int64_t dpitch, int64_t d_gstride, int64_t n, uint8_t* out, int64_t opitch,
+                    int64_t o_gstride, int groups, void* stream);
+/* skyrx_gf_invert: per problem g, invert the k x k matrix whose row i is row rows[g*k + i] of
+ * `mat` (row length ld) by Gauss-Jordan (fec.py:82-98) and write its rows sel[g*k + 0 ..
+ * nsel[g]-1] to out + g*k*k, zero rows after them; status[g] = 1 if singular, else 0. */
+int skyrx_gf_invert(const uint8_t* mat, int ld, const int32_t* rows, int k, const int32_t* sel,
+                    const int32_t* nsel, int groups, uint8_t* out, int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------- synthetic sensor (bench/test inputs)
  * Bit-identical to oracle/synth.py generate_lines(): raw counts for lines

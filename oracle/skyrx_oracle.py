@@ -387,3 +387,133 @@ def packetize_cube(cube_id, rgb, scores, line_meta) -> list:
         out.append(pack_header(cube_id, i, lines, rgb.shape[1], exp, max_score, mr, mg, mb, ib, ia)
                    + payload.tobytes())
     return out
+
+
+# --------------------------------------------------------------------------- GF(256) erasure code
+# fec.py:28-195 and _accel.py:50-70 / 92-107 (gf256_matmul), datalink.py:243-285 (frames)
+GF_POLY = 0x11D               # fec.py:28 (generator 2, fec.py:29)
+FRAME_HEAD = "<IBBH"          # datalink.py:51: group_id, index, kind, payload length
+
+
+def gf_tables():
+    """fec.py:36-50: antilog table doubled to 510 entries (products need no mod 255), log[0] = 0."""
+    exp = np.zeros(510, np.uint8)
+    log = np.zeros(256, np.int16)
+    v = 1
+    for e in range(255):
+        exp[e], log[v] = v, e
+        v = (v << 1) ^ (GF_POLY if v & 0x80 else 0)
+    exp[255:] = exp[:255]
+    return log, exp
+
+
+GF_LOG_T, GF_EXP_T = gf_tables()
+
+
+def gf_mul(a: int, b: int) -> int:
+    return 0 if a == 0 or b == 0 else int(GF_EXP_T[int(GF_LOG_T[a]) + int(GF_LOG_T[b])])
+
+
+def gf_inv(a: int) -> int:
+    if a == 0:
+        raise ZeroDivisionError("no inverse of 0 in GF(256)")
+    return int(GF_EXP_T[255 - int(GF_LOG_T[a])])
+
+
+def gf_pow(x: int, n: int) -> int:
+    """fec.py:65-70 including its int16 arithmetic: log[x] * n is an int16 product (NEP 50),
+    so it wraps for log[x] * n > 32767 (codes with more than ~129 data rows) before the
+    floor-mod 255."""
+    if n == 0:
+        return 1
+    if x == 0:
+        return 0
+    p = (int(GF_LOG_T[x]) * n + 32768) % 65536 - 32768
+    return int(GF_EXP_T[p % 255])
+
+
+def gf256_matmul(mat, data) -> np.ndarray:
+    """_accel.py:50-70: out[i] = XOR_j mat[i, j] * data[j] over GF(256) (row-vectorised)."""
+    mat = np.asarray(mat, np.uint8)
+    data = np.asarray(data, np.uint8)
+    out = np.zeros((mat.shape[0], data.shape[1]), np.uint8)
+    ld = GF_LOG_T[data].astype(np.int64)
+    nz = data != 0
+    for j in range(mat.shape[1]):
+        for i in np.nonzero(mat[:, j])[0]:
+            prod = GF_EXP_T[int(GF_LOG_T[mat[i, j]]) + ld[j]]
+            out[i] ^= np.where(nz[j], prod, 0).astype(np.uint8)
+    return out
+
+
+def gf_mat_inv(m) -> np.ndarray:
+    """fec.py:82-98: Gauss-Jordan on [m | I]; pivot = first nonzero at or below the diagonal."""
+    m = np.asarray(m, np.uint8)
+    k = m.shape[0]
+    a = np.concatenate([m, np.eye(k, dtype=np.uint8)], axis=1)
+
+    def scaled(row, s):
+        return gf256_matmul(np.array([[s]], np.uint8), row[None, :])[0]
+
+    for c in range(k):
+        nz = np.nonzero(a[c:, c])[0]
+        if nz.size == 0:
+            raise np.linalg.LinAlgError("singular matrix over GF(256)")
+        p = c + int(nz[0])
+        a[[c, p]] = a[[p, c]]
+        a[c] = scaled(a[c], gf_inv(int(a[c, c])))
+        for r in range(k):
+            if r != c and a[r, c]:
+                a[r] ^= scaled(a[c], int(a[r, c]))
+    return a[:, k:].copy()
+
+
+def encoding_matrix(k: int, total: int) -> np.ndarray:
+    """fec.py:101-115: Vandermonde (total x k) at points 0..total-1, times inv(top k rows)."""
+    vand = np.array([[gf_pow(i, j) for j in range(k)] for i in range(total)], np.uint8)
+    return gf256_matmul(vand, gf_mat_inv(vand[:k]))
+
+
+def rs_encode(matrix, k: int, payloads) -> list:
+    """fec.py:140-155: parity rows = matrix[k:] @ data over GF(256)."""
+    data = np.frombuffer(b"".join(payloads), np.uint8).reshape(k, -1)
+    return [row.tobytes() for row in gf256_matmul(np.asarray(matrix)[k:], data)]
+
+
+def rs_decode(matrix, k: int, received):
+    """fec.py:157-195: (data dict, (received, recovered, missing)) from (coded index, bytes)
+    pairs; the first k by index are solved against when a data slot is absent."""
+    ent = sorted(received, key=lambda e: e[0])
+    idx = [i for i, _ in ent]
+    if len(set(idx)) != len(idx):
+        raise ValueError("duplicate coded index in group")
+    out = {i: p for i, p in ent if i < k}
+    absent = tuple(i for i in range(k) if i not in out)
+    direct = tuple(sorted(out))
+    if len(ent) < k or not absent:
+        return out, (direct, (), absent)
+    use = ent[:k]
+    inv = gf_mat_inv(np.asarray(matrix)[[i for i, _ in use]])
+    stacked = np.frombuffer(b"".join(p for _, p in use), np.uint8).reshape(k, -1)
+    rec = gf256_matmul(inv[list(absent)], stacked)
+    for s, row in zip(absent, rec):
+        out[s] = row.tobytes()
+    return out, (direct, absent, ())
+
+
+def frames_for_cube(cube_id: int, packets, k: int = 50, parity: int = 25, matrix=None) -> list:
+    """datalink.py:243-285: per group of k packets, k data frames then `parity` parity frames;
+    group id = cube_id * groups + g; frame = <IBBH header (group, index, kind, length) + payload."""
+    import struct
+
+    matrix = encoding_matrix(k, k + parity) if matrix is None else matrix
+    groups = len(packets) // k
+    out = []
+    for g in range(groups):
+        chunk = list(packets[g * k:(g + 1) * k])
+        gid = cube_id * groups + g
+        for i, p in enumerate(chunk):
+            out.append(struct.pack(FRAME_HEAD, gid, i, 0, len(p)) + p)
+        for i, p in enumerate(rs_encode(matrix, k, chunk)):
+            out.append(struct.pack(FRAME_HEAD, gid, k + i, 1, len(p)) + p)
+    return out

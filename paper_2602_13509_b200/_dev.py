@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -57,6 +59,10 @@ def to_device(x, dtype=None) -> torch.Tensor:
         if a.dtype != want:
             a = a.astype(want)
     a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # e.g. np.frombuffer(bytes): only read by the copy below
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            return torch.from_numpy(a).to(dev)
     return torch.from_numpy(a).to(dev)
 
 

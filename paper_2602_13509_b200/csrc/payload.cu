@@ -36,26 +36,65 @@ __device__ __forceinline__ uint32_t quantize(float x, double mx, double levels) 
   return (uint32_t)(q > levels ? levels : q);
 }
 
+struct LinkMax {
+  double s, r, g, b;
+};
+
+__device__ __forceinline__ LinkMax link_max(const uint32_t* keys, double4 mh) {
+  // maxima: device keys (the cube's own, no host round trip) or caller values
+  if (keys) return {(double)ord2f(keys[0]), (double)ord2f(keys[1]), (double)ord2f(keys[2]),
+                    (double)ord2f(keys[3])};
+  return {mh.x, mh.y, mh.z, mh.w};
+}
+
+__device__ __forceinline__ uint32_t payload_word(const float* __restrict__ scores,
+                                                 const float* __restrict__ rgb, int64_t i,
+                                                 const LinkMax& m) {
+  const uint32_t c565 = (quantize(rgb[3 * i], m.r, 31.0) << 11) |
+                        (quantize(rgb[3 * i + 1], m.g, 63.0) << 5) |
+                        quantize(rgb[3 * i + 2], m.b, 31.0);
+  uint32_t h = 0;
+  if (m.s > 0.0) {
+    const __half hv = __double2half(__dsqrt_rn(__ddiv_rn((double)scores[i], m.s)));
+    h = (uint32_t)*reinterpret_cast<const uint16_t*>(&hv);
+  }
+  return c565 | (h << 16);  // little-endian [rgb565, half]
+}
+
 __global__ void link_payload_kernel(const float* __restrict__ scores,
                                     const float* __restrict__ rgb, int64_t n,
                                     const uint32_t* __restrict__ keys, double4 mh,
                                     uint32_t* __restrict__ payload) {
-  // maxima: device keys (the cube's own, no host round trip) or caller values
-  const double ms = keys ? (double)ord2f(keys[0]) : mh.x;
-  const double mr = keys ? (double)ord2f(keys[1]) : mh.y;
-  const double mg = keys ? (double)ord2f(keys[2]) : mh.z;
-  const double mb = keys ? (double)ord2f(keys[3]) : mh.w;
+  const LinkMax m = link_max(keys, mh);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t c565 = (quantize(rgb[3 * i], mr, 31.0) << 11) |
-                          (quantize(rgb[3 * i + 1], mg, 63.0) << 5) |
-                          quantize(rgb[3 * i + 2], mb, 31.0);
-    uint32_t h = 0;
-    if (ms > 0.0) {
-      const __half hv = __double2half(__dsqrt_rn(__ddiv_rn((double)scores[i], ms)));
-      h = (uint32_t)*reinterpret_cast<const uint16_t*>(&hv);
+       i += (int64_t)gridDim.x * blockDim.x)
+    payload[i] = payload_word(scores, rgb, i, m);
+}
+
+// Whole line packets (datalink.py:176-189): the host-built 128-byte headers with the cube
+// maxima patched in from the device keys (header bytes 32..47, `ffff` of datalink.py:49),
+// then the payload words, one 128 + 4S byte row per line.
+__global__ void link_packets_kernel(const float* __restrict__ scores,
+                                    const float* __restrict__ rgb, int lines, int samples,
+                                    const uint32_t* __restrict__ keys,
+                                    const uint32_t* __restrict__ headers,
+                                    uint32_t* __restrict__ packets) {
+  const LinkMax m = link_max(keys, make_double4(0, 0, 0, 0));
+  const int64_t row = 32 + samples, total = (int64_t)lines * row;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t line = w / row;
+    const int c = (int)(w - line * row);
+    uint32_t v;
+    if (c >= 32) {
+      v = payload_word(scores, rgb, line * samples + (c - 32), m);
+    } else if (c >= 8 && c < 12) {
+      const uint32_t key = keys[c - 8];
+      v = key ? __float_as_uint(ord2f(key)) : 0u;
+    } else {
+      v = headers[line * 32 + c];
     }
-    payload[i] = c565 | (h << 16);  // little-endian [rgb565, half]
+    packets[w] = v;
   }
 }
 
@@ -89,5 +128,21 @@ extern "C" int skyrx_link_payload(const float* scores, const float* rgb, int64_t
   link_payload_kernel<<<grid, 256, 0, as_stream(stream)>>>(scores, rgb, n, keys, mh,
                                                            reinterpret_cast<uint32_t*>(payload));
   SKYRX_CHECK_LAUNCH("skyrx_link_payload");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_link_packets(const float* scores, const float* rgb, int lines, int samples,
+                                  const uint32_t* keys, const uint8_t* headers, uint8_t* packets,
+                                  void* stream) {
+  SKYRX_REQUIRE(lines >= 0 && samples >= 0 && keys != nullptr, "bad packet geometry");
+  SKYRX_REQUIRE((((uintptr_t)headers | (uintptr_t)packets) & 3) == 0,
+                "headers / packets must be 4-byte aligned");
+  const int64_t total = (int64_t)lines * (32 + samples);
+  if (total == 0) return SKYRX_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 8 * kSMs);
+  link_packets_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      scores, rgb, lines, samples, keys, reinterpret_cast<const uint32_t*>(headers),
+      reinterpret_cast<uint32_t*>(packets));
+  SKYRX_CHECK_LAUNCH("skyrx_link_packets");
   return SKYRX_OK;
 }

@@ -10,7 +10,7 @@ from __future__ import annotations
 import importlib
 import sys
 
-from . import _accel, calibrate, datalink, rx
+from . import _accel, calibrate, datalink, errors, fec, rx
 
 _TARGETS = {
     "calibrate": {
@@ -31,9 +31,15 @@ _TARGETS = {
         "pack_rgb565": datalink.pack_rgb565,
         "encode_scores_half": datalink.encode_scores_half,
         "packetize_cube": datalink.packetize_cube,
+        "frames_for_cube": datalink.frames_for_cube,
+    },
+    "fec": {
+        "ErasureCode": fec.ErasureCode,
+        "gf_mat_inv": fec.gf_mat_inv,
     },
     "_accel": {
         "mahalanobis_sq": _accel.mahalanobis_sq,
+        "gf256_matmul": fec.gf256_matmul,
     },
     "pipeline": {
         "calibrate_bin_rgb": calibrate.calibrate_bin_rgb,
@@ -41,6 +47,7 @@ _TARGETS = {
         "rx_scores": rx.rx_scores,
         "transmit_domain": rx.transmit_domain,
         "packetize_cube": datalink.packetize_cube,
+        "frames_for_cube": datalink.frames_for_cube,
     },
     "": {
         "compute_stats": rx.compute_stats,
@@ -54,6 +61,10 @@ _TARGETS = {
 def install(skyrx_module=None) -> list[str]:
     base = skyrx_module or sys.modules.get("skyrx") or importlib.import_module("skyrx")
     name = base.__name__
+    ref_err = sys.modules.get(f"{name}.errors")
+    for cls in ("FormatError", "ProtocolError"):  # raise the reference's own classes
+        if ref_err is not None and hasattr(ref_err, cls):
+            setattr(errors, cls, getattr(ref_err, cls))
     patched = []
     for sub, attrs in _TARGETS.items():
         mod = base if not sub else sys.modules.get(f"{name}.{sub}")

@@ -199,6 +199,48 @@ def main():
     lk["cube/rgb"], lk["cube/scores"] = cube_rgb, cube_sc
     lk["cube/packets"] = np.frombuffer(b"".join(pk), np.uint8)
     np.savez_compressed(HERE / "datalink.npz", **lk)
+
+    # ---------------------------------------------------------------- GF(256) erasure code
+    from skyrx import fec
+    from skyrx.datalink import frames_for_cube
+
+    fc = {"gf_log": fec.GF_LOG, "gf_exp": fec.GF_EXP}
+    code = fec.ErasureCode(50, 25)
+    fc["matrix_50_25"] = code.matrix
+    fc["matrix_4_3"] = fec.ErasureCode(4, 3).matrix
+    fc["matrix_1_0"] = fec.ErasureCode(1, 0).matrix
+    fc["matrix_200_56"] = fec.ErasureCode(200, 56).matrix
+    r2 = np.random.default_rng(2024)
+    mat = r2.integers(0, 256, (7, 13), dtype=np.uint8)
+    mat[0, :] = 0
+    mat[:, 3] = 0
+    data = r2.integers(0, 256, (13, 333), dtype=np.uint8)
+    data[5, :] = 0
+    data[:, 17] = 0
+    fc["mm/mat"], fc["mm/data"] = mat, data
+    fc["mm/out"] = _accel.gf256_matmul_numpy(mat, data, fec.GF_LOG, fec.GF_EXP)
+    m6 = np.random.default_rng(3).integers(0, 256, (6, 6), dtype=np.uint8)
+    m6 += np.eye(6, dtype=np.uint8)
+    fc["inv/m"], fc["inv/minv"] = m6, fec.gf_mat_inv(m6)
+    payloads = [r2.integers(0, 256, 211, dtype=np.uint8).tobytes() for _ in range(50)]
+    coded = payloads + code.encode(payloads)
+    fc["enc/coded"] = np.frombuffer(b"".join(coded), np.uint8).reshape(75, 211)
+    keeps = [np.arange(25, 75)] + [np.sort(r2.permutation(75)[:50]) for _ in range(6)]
+    keeps += [np.sort(r2.permutation(75)[:49]), np.arange(0, 50), np.sort(r2.permutation(75)[:60])]
+    for c, keep in enumerate(keeps):
+        rec, rep = code.decode([(int(i), coded[int(i)]) for i in keep])
+        fc[f"dec{c}/keep"] = keep.astype(np.int64)
+        fc[f"dec{c}/slots"] = np.array(sorted(rec), np.int64)
+        fc[f"dec{c}/data"] = np.frombuffer(b"".join(rec[i] for i in sorted(rec)), np.uint8)
+        fc[f"dec{c}/report"] = np.array([len(rep.received), len(rep.recovered), len(rep.missing)])
+        fc[f"dec{c}/recovered"] = np.array(rep.recovered, np.int64)
+        fc[f"dec{c}/missing"] = np.array(rep.missing, np.int64)
+    pk = [r2.integers(0, 256, 97, dtype=np.uint8).tobytes() for _ in range(100)]
+    frames = frames_for_cube(3, pk)
+    fc["frames/packets"] = np.frombuffer(b"".join(pk), np.uint8)
+    fc["frames/frames"] = np.frombuffer(b"".join(frames), np.uint8)
+    fc["frames/lengths"] = np.array([len(f) for f in frames], np.int64)
+    np.savez_compressed(HERE / "fec.npz", **fc)
     print("wrote", sorted(p.name for p in HERE.glob("*.npz")))
 
 

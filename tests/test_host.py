@@ -113,17 +113,24 @@ def test_device_scene_tables_match_oracle():
 
 def test_install_patches_pipeline_bindings():
     import paper_2602_13509_b200 as P
-    from paper_2602_13509_b200 import calibrate, datalink, rx
+    from paper_2602_13509_b200 import calibrate, datalink, errors, fec, rx
 
     fake = types.ModuleType("skyrx")
     subs = {}
-    for sub in ("calibrate", "rx", "_accel", "datalink", "pipeline"):
+    for sub in ("calibrate", "rx", "_accel", "datalink", "fec", "errors", "pipeline"):
         m = types.ModuleType(f"skyrx.{sub}")
         for attr in ("apply_calibration", "calibrate_bin_rgb", "compute_stats", "rx_scores",
-                     "mahalanobis_sq", "transmit_domain", "packetize_cube", "pack_rgb565"):
+                     "mahalanobis_sq", "transmit_domain", "packetize_cube", "pack_rgb565", "frames_for_cube",
+                     "ErasureCode", "gf256_matmul"):
             setattr(m, attr, None)
         subs[sub] = m
     fake.compute_stats = None
+    saved_err = (errors.FormatError, errors.ProtocolError)
+
+    class RefProtocolError(ValueError):
+        pass
+
+    subs["errors"].ProtocolError = RefProtocolError
     saved = {k: sys.modules.get(k) for k in ["skyrx"] + [f"skyrx.{s}" for s in subs]}
     try:
         sys.modules["skyrx"] = fake
@@ -137,7 +144,12 @@ def test_install_patches_pipeline_bindings():
         assert "skyrx.pipeline.rx_scores" in patched
         assert subs["pipeline"].packetize_cube is datalink.packetize_cube
         assert subs["datalink"].pack_rgb565 is datalink.pack_rgb565
+        assert subs["pipeline"].frames_for_cube is datalink.frames_for_cube
+        assert subs["fec"].ErasureCode is fec.ErasureCode
+        assert errors.ProtocolError is RefProtocolError
+        assert subs["_accel"].gf256_matmul is fec.gf256_matmul
     finally:
+        errors.FormatError, errors.ProtocolError = saved_err
         for k, v in saved.items():
             if v is None:
                 sys.modules.pop(k, None)

@@ -214,3 +214,32 @@ def test_packetize_cube_matches_reference(golden):
     pk = O.packetize_cube(7, g["cube/rgb"], g["cube/scores"], metas)
     assert all(len(p) == 3728 for p in pk)
     assert np.array_equal(np.frombuffer(b"".join(pk), np.uint8), g["cube/packets"])
+
+
+def test_gf_oracle_matches_reference(golden):
+    g = golden["fec"]
+    assert np.array_equal(O.GF_LOG_T, g["gf_log"]) and np.array_equal(O.GF_EXP_T, g["gf_exp"])
+    assert np.array_equal(O.gf256_matmul(g["mm/mat"], g["mm/data"]), g["mm/out"])
+    assert np.array_equal(O.gf_mat_inv(g["inv/m"]), g["inv/minv"])
+    for k, p in ((50, 25), (4, 3), (1, 0), (200, 56)):
+        assert np.array_equal(O.encoding_matrix(k, k + p), g[f"matrix_{k}_{p}"]), (k, p)
+
+
+def test_rs_oracle_matches_reference(golden):
+    g = golden["fec"]
+    m = g["matrix_50_25"]
+    coded = [r.tobytes() for r in g["enc/coded"]]
+    assert O.rs_encode(m, 50, coded[:50]) == coded[50:]
+    c = 0
+    while f"dec{c}/keep" in g:
+        out, (rec, recov, miss) = O.rs_decode(m, 50, [(int(i), coded[i]) for i in g[f"dec{c}/keep"]])
+        assert sorted(out) == g[f"dec{c}/slots"].tolist()
+        assert b"".join(out[i] for i in sorted(out)) == g[f"dec{c}/data"].tobytes()
+        assert [len(rec), len(recov), len(miss)] == g[f"dec{c}/report"].tolist()
+        assert list(recov) == g[f"dec{c}/recovered"].tolist()
+        assert list(miss) == g[f"dec{c}/missing"].tolist()
+        c += 1
+    assert c == 10
+    pk = g["frames/packets"].reshape(100, -1)
+    fr = b"".join(O.frames_for_cube(3, [r.tobytes() for r in pk], matrix=m))
+    assert fr == g["frames/frames"].tobytes()
