@@ -264,6 +264,14 @@ int skyrx_link_payload(const float* scores, const float* rgb, int64_t n, const u
 int skyrx_link_packets(const float* scores, const float* rgb, int lines, int samples,
                        const uint32_t* keys, const uint8_t* headers, uint8_t* packets,
                        void* stream);
+/* The cube's whole frame stream in one matrix (datalink.py:243-285): lines / group_k groups of
+ * group_k data frames then group_r parity frames, each row 8 + 128 + 4S bytes = frame head
+ * (u32 group id = gid0 + g, u8 index, u8 kind, u16 length) + packet. Data rows are filled
+ * here; parity payloads are left to skyrx_gf_matmul over the data rows (their heads are
+ * written here). */
+int skyrx_link_frames(const float* scores, const float* rgb, int lines, int samples,
+                      const uint32_t* keys, const uint8_t* headers, int group_k, int group_r,
+                      int gid0, uint8_t* frames, void* stream);
 
 /* ---- GF(256) Reed-Solomon erasure code (fec.py:101-195) ----------------
  * skyrx_gf_matmul: for g < groups, out_g (r x n, row pitch opitch) = M_g (r x k, row-major)

@@ -36,7 +36,11 @@ from .rx import (
     transmit_domain,
 )
 from .stream import ChunkResult, StreamingRX
-from .datalink import encode_scores_half, link_payload, pack_rgb565, packetize_cube
+from .datalink import (cube_frames, encode_scores_half, frames_for_cube, link_payload,
+                       pack_rgb565, packetize_cube)
+from .air import AirResult, StageTiming, run_air
+from .fec import ErasureCode
+from .formats import read_cube, write_cube
 
 __version__ = "0.1.0"
 
@@ -46,7 +50,9 @@ __all__ = [
     "discard_oob_bands", "extract_rgb", "CubeStats", "DetectPlan", "DeviceStats",
     "compute_stats", "detect", "detect_batch", "normalize_scores", "rx_scores", "threshold_scores",
     "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install", "__version__",
-    "link_payload", "pack_rgb565", "encode_scores_half", "packetize_cube",
+    "link_payload", "pack_rgb565", "encode_scores_half", "packetize_cube", "frames_for_cube",
+    "cube_frames", "ErasureCode", "run_air", "AirResult", "StageTiming", "read_cube",
+    "write_cube",
 ]
 
 

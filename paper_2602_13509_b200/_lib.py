@@ -76,6 +76,7 @@ SIGNATURES = {
     "skyrx_link_maxima": (C.c_int, [vp, vp, i64, vp, vp]),
     "skyrx_link_payload": (C.c_int, [vp, vp, i64, vp, C.POINTER(f64), vp, vp]),
     "skyrx_link_packets": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, vp]),
+    "skyrx_link_frames": (C.c_int, [vp, vp, i32, i32, vp, vp, i32, i32, i32, vp, vp]),
     "skyrx_gf_matmul": (C.c_int, [vp, i64, i32, i32, vp, i64, i64, i64, vp, i64, i64, i32, vp]),
     "skyrx_gf_invert": (C.c_int, [vp, i32, vp, i32, vp, vp, i32, vp, vp, vp]),
     "skyrx_synth_raw": (C.c_int, [u32, u32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,

@@ -71,18 +71,40 @@ __global__ void link_payload_kernel(const float* __restrict__ scores,
     payload[i] = payload_word(scores, rgb, i, m);
 }
 
+// Where the packet rows go. Plain packets: row l at l * pitch. Frames (datalink.py:243-285):
+// groups of gk packets, each followed by gr parity rows (gstride = gk + gr rows of 8 + packet
+// bytes), the packet at word off_w = 2 after the frame head; heads (u32 group id, u8 index,
+// u8 kind, u16 length) are written for data and parity rows alike.
+struct PacketLayout {
+  int64_t pitch_w;  // row pitch in words
+  int gk, gstride, off_w;
+  int gr;           // parity rows per group (frames only)
+  int gid0;         // first group id (frames only)
+  int frames;       // 1: write frame heads
+};
+
 // Whole line packets (datalink.py:176-189): the host-built 128-byte headers with the cube
 // maxima patched in from the device keys (header bytes 32..47, `ffff` of datalink.py:49),
-// then the payload words, one 128 + 4S byte row per line.
+// then the payload words, one 128 + 4S byte packet per line.
 __global__ void link_packets_kernel(const float* __restrict__ scores,
                                     const float* __restrict__ rgb, int lines, int samples,
                                     const uint32_t* __restrict__ keys,
                                     const uint32_t* __restrict__ headers,
-                                    uint32_t* __restrict__ packets) {
+                                    uint32_t* __restrict__ out, PacketLayout lay) {
   const LinkMax m = link_max(keys, make_double4(0, 0, 0, 0));
   const int64_t row = 32 + samples, total = (int64_t)lines * row;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+  const int64_t groups = lay.frames ? lines / lay.gk : 0;
+  const int64_t heads = groups * lay.gstride;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total + heads;
        w += (int64_t)gridDim.x * blockDim.x) {
+    if (w >= total) {  // frame head of row h
+      const int64_t h = w - total;
+      const int g = (int)(h / lay.gstride), idx = (int)(h - (int64_t)g * lay.gstride);
+      uint32_t* dst = out + h * lay.pitch_w;
+      dst[0] = (uint32_t)(lay.gid0 + g);
+      dst[1] = (uint32_t)idx | ((idx >= lay.gk ? 1u : 0u) << 8) | ((uint32_t)(4 * row) << 16);
+      continue;
+    }
     const int64_t line = w / row;
     const int c = (int)(w - line * row);
     uint32_t v;
@@ -94,7 +116,8 @@ __global__ void link_packets_kernel(const float* __restrict__ scores,
     } else {
       v = headers[line * 32 + c];
     }
-    packets[w] = v;
+    const int64_t r = (line / lay.gk) * lay.gstride + line % lay.gk;
+    out[r * lay.pitch_w + lay.off_w + c] = v;
   }
 }
 
@@ -131,18 +154,39 @@ extern "C" int skyrx_link_payload(const float* scores, const float* rgb, int64_t
   return SKYRX_OK;
 }
 
-extern "C" int skyrx_link_packets(const float* scores, const float* rgb, int lines, int samples,
-                                  const uint32_t* keys, const uint8_t* headers, uint8_t* packets,
-                                  void* stream) {
+static int launch_packets(const float* scores, const float* rgb, int lines, int samples,
+                          const uint32_t* keys, const uint8_t* headers, uint8_t* out,
+                          const PacketLayout& lay, void* stream, const char* what) {
   SKYRX_REQUIRE(lines >= 0 && samples >= 0 && keys != nullptr, "bad packet geometry");
-  SKYRX_REQUIRE((((uintptr_t)headers | (uintptr_t)packets) & 3) == 0,
+  SKYRX_REQUIRE((((uintptr_t)headers | (uintptr_t)out) & 3) == 0,
                 "headers / packets must be 4-byte aligned");
-  const int64_t total = (int64_t)lines * (32 + samples);
+  const int64_t total = (int64_t)lines * (32 + samples) +
+                        (lay.frames ? (int64_t)(lines / lay.gk) * lay.gstride : 0);
   if (total == 0) return SKYRX_OK;
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 8 * kSMs);
   link_packets_kernel<<<grid, 256, 0, as_stream(stream)>>>(
       scores, rgb, lines, samples, keys, reinterpret_cast<const uint32_t*>(headers),
-      reinterpret_cast<uint32_t*>(packets));
-  SKYRX_CHECK_LAUNCH("skyrx_link_packets");
+      reinterpret_cast<uint32_t*>(out), lay);
+  SKYRX_CHECK_LAUNCH(what);
   return SKYRX_OK;
+}
+
+extern "C" int skyrx_link_packets(const float* scores, const float* rgb, int lines, int samples,
+                                  const uint32_t* keys, const uint8_t* headers, uint8_t* packets,
+                                  void* stream) {
+  const PacketLayout lay{32 + samples, max(lines, 1), max(lines, 1), 0, 0, 0, 0};
+  return launch_packets(scores, rgb, lines, samples, keys, headers, packets, lay, stream,
+                        "skyrx_link_packets");
+}
+
+extern "C" int skyrx_link_frames(const float* scores, const float* rgb, int lines, int samples,
+                                 const uint32_t* keys, const uint8_t* headers, int group_k,
+                                 int group_r, int gid0, uint8_t* frames, void* stream) {
+  SKYRX_REQUIRE(group_k >= 1 && group_r >= 0 && group_k + group_r <= 256,
+                "bad group geometry");
+  SKYRX_REQUIRE(lines % group_k == 0, "line count not a multiple of group size");
+  SKYRX_REQUIRE(128 + 4 * (int64_t)samples < 65536, "packet too long for a frame");
+  const PacketLayout lay{34 + samples, group_k, group_k + group_r, 2, group_r, gid0, 1};
+  return launch_packets(scores, rgb, lines, samples, keys, headers, frames, lay, stream,
+                        "skyrx_link_frames");
 }

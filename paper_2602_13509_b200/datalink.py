@@ -209,9 +209,42 @@ def frames_for_cube(cube_id: int, packets) -> list[bytes]:
     return _frames(cube_id, host.reshape(data.shape), _dev.to_host(parity))
 
 
+def cube_frames_device(cube_id: int, rgb, scores, line_meta) -> torch.Tensor:
+    """The cube's whole frame stream as one device matrix (frames, 8 + 3728) u8, in link
+    order: packets written straight into their frame rows (skyrx_link_frames), then every
+    group's parity rows by one RS launch over those rows (skyrx_gf_matmul)."""
+    codec = _codec()
+    k, r = codec.data_count, codec.parity_count
+    rgb_d = _dev.to_device(rgb, torch.float32).contiguous()
+    sc_d = _dev.to_device(scores, torch.float32).contiguous()
+    lines = int(sc_d.shape[0])
+    if rgb_d.shape[0] != lines or len(line_meta) != lines:
+        raise ValueError("rgb, scores, and line_meta must cover the same lines")
+    if (tuple(rgb_d.shape[1:]) != (PAYLOAD_SAMPLES, 3)
+            or tuple(sc_d.shape[1:]) != (PAYLOAD_SAMPLES,)):
+        raise ValueError(f"rows must be ({PAYLOAD_SAMPLES}, 3) rgb and ({PAYLOAD_SAMPLES},) score")
+    if lines % k != 0:
+        raise ValueError(f"line count {lines} not a multiple of group size {k}")
+    groups = lines // k
+    s = _dev.stream_ptr()
+    keys = _dev.empty((4,), torch.int32)
+    _lib.call("skyrx_link_maxima", sc_d.data_ptr(), rgb_d.data_ptr(), sc_d.numel(),
+              keys.data_ptr(), s)
+    heads = _dev.to_device(_headers(cube_id, lines, PAYLOAD_SAMPLES, line_meta))
+    pitch = FRAME_OVERHEAD + PACKET_LEN
+    frames = _dev.empty((groups * (k + r), pitch), torch.uint8)
+    _lib.call("skyrx_link_frames", sc_d.data_ptr(), rgb_d.data_ptr(), lines, PAYLOAD_SAMPLES,
+              keys.data_ptr(), heads.data_ptr(), k, r, cube_id * groups, frames.data_ptr(), s)
+    if r and groups:
+        base = frames.data_ptr() + FRAME_OVERHEAD
+        _lib.call("skyrx_gf_matmul", codec._parity_d.data_ptr(), 0, r, k, base, pitch,
+                  (k + r) * pitch, PACKET_LEN, base + k * pitch, pitch, (k + r) * pitch, groups,
+                  s)
+    return frames
+
+
 def cube_frames(cube_id: int, rgb, scores, line_meta) -> list[bytes]:
     """The air side's transmit stage (pipeline.py:176-180) fused on the device:
-    packetize_cube + frames_for_cube with the packets never leaving HBM before parity."""
-    pk = cube_packets(cube_id, rgb, scores, line_meta)
-    data, parity = _group_parity(pk)
-    return _frames(cube_id, _dev.to_host(data), _dev.to_host(parity))
+    frames_for_cube(packetize_cube(...)) with one D2H of the finished frame stream."""
+    host = _dev.to_host(cube_frames_device(cube_id, rgb, scores, line_meta))
+    return [row.tobytes() for row in host]

@@ -10,7 +10,7 @@ from __future__ import annotations
 import importlib
 import sys
 
-from . import _accel, calibrate, datalink, errors, fec, rx
+from . import _accel, air, calibrate, datalink, errors, fec, rx
 
 _TARGETS = {
     "calibrate": {
@@ -48,6 +48,7 @@ _TARGETS = {
         "transmit_domain": rx.transmit_domain,
         "packetize_cube": datalink.packetize_cube,
         "frames_for_cube": datalink.frames_for_cube,
+        "run_air": air.run_air,
     },
     "": {
         "compute_stats": rx.compute_stats,

@@ -26,7 +26,7 @@ def load_golden(name):
 
 @pytest.fixture(scope="session")
 def golden():
-    return {n: load_golden(n) for n in ("calibrate", "stats", "accel", "normalize", "datalink", "fec")}
+    return {n: load_golden(n) for n in ("calibrate", "stats", "accel", "normalize", "datalink", "fec", "air")}
 
 
 @pytest.fixture

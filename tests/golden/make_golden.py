@@ -12,6 +12,7 @@ the reference and the -m gpu tests pin the CUDA path to the same numbers.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import sys
 from pathlib import Path
@@ -32,6 +33,22 @@ from skyrx.rx import compute_stats, normalize_scores, rx_scores, threshold_score
 from skyrx.scene import band_grid  # noqa: E402
 
 from oracle import synth  # noqa: E402  (generator only; outputs below come from skyrx)
+
+
+AIR_BANDS, AIR_LINES, AIR_CUBES, AIR_SEED = 44, 50, 3, 2602
+
+
+def air_inputs(tables_cls, raw_cls, band_grid_fn, metas_fn):
+    """The run_air fixture's inputs (shared with tests/test_gpu_air.py): AIR_CUBES cubes of
+    AIR_LINES x 900 x AIR_BANDS from one synthetic scene, per-line gains varying."""
+    st = synth.make_tables(AIR_SEED, 900, AIR_BANDS)
+    wl = band_grid_fn(AIR_BANDS)
+    cubes = []
+    for c in range(AIR_CUBES):
+        raw = synth.generate_lines(st, c * AIR_LINES, AIR_LINES)
+        gains = [1.0 + 0.25 * ((c + i) % 3) for i in range(AIR_LINES)]
+        cubes.append(raw_cls(raw, wl, metas_fn(gains)))
+    return {"cubes": cubes, "tables": tables_cls(st.dark, st.coeff)}
 
 
 def metas(gains):
@@ -241,6 +258,32 @@ def main():
     fc["frames/frames"] = np.frombuffer(b"".join(frames), np.uint8)
     fc["frames/lengths"] = np.array([len(f) for f in frames], np.int64)
     np.savez_compressed(HERE / "fec.npz", **fc)
+
+    # ---------------------------------------------------------------- air pipeline (run_air)
+    # cubes from oracle/synth (tests regenerate them bit-identically), run through the
+    # reference's own four-stage pipeline; what is stored is the reference's output.
+    from skyrx.formats import write_cube
+    from skyrx.pipeline import FlightData, PipelineConfig, run_air
+
+    ap = air_inputs(CalibrationTables, RawCube, band_grid, metas)
+    config = PipelineConfig(bands=AIR_BANDS, samples=900, bin_factor=4, queue_depth=2)
+    res = run_air(config, FlightData(cubes=ap["cubes"], track=None, masks=[],
+                                     tables=ap["tables"]))
+    assert not res.dropped, res.dropped
+    ag = {"frames": np.frombuffer(b"".join(res.frames), np.uint8),
+          "lengths": np.array([len(f) for f in res.frames], np.int64)}
+    for c, (sc, rgb) in enumerate(zip(res.scores, res.rgb)):
+        ag[f"scores{c}"] = sc.values
+        ag[f"rgb{c}_sha256"] = np.frombuffer(
+            hashlib.sha256(np.ascontiguousarray(rgb, np.float32).tobytes()).digest(), np.uint8)
+    tiny = RawCube(np.arange(3 * 4 * 5, dtype=np.uint16).reshape(3, 4, 5) * 7,
+                   band_grid(25)[:5], metas([1.0, 0.5, 2.0]))
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        write_cube(Path(td) / "t.hsc", tiny)
+        ag["tiny_hsc"] = np.frombuffer((Path(td) / "t.hsc").read_bytes(), np.uint8)
+    np.savez_compressed(HERE / "air.npz", **ag)
     print("wrote", sorted(p.name for p in HERE.glob("*.npz")))
 
 

@@ -121,7 +121,7 @@ def test_install_patches_pipeline_bindings():
         m = types.ModuleType(f"skyrx.{sub}")
         for attr in ("apply_calibration", "calibrate_bin_rgb", "compute_stats", "rx_scores",
                      "mahalanobis_sq", "transmit_domain", "packetize_cube", "pack_rgb565", "frames_for_cube",
-                     "ErasureCode", "gf256_matmul"):
+                     "ErasureCode", "gf256_matmul", "run_air"):
             setattr(m, attr, None)
         subs[sub] = m
     fake.compute_stats = None
@@ -145,6 +145,7 @@ def test_install_patches_pipeline_bindings():
         assert subs["pipeline"].packetize_cube is datalink.packetize_cube
         assert subs["datalink"].pack_rgb565 is datalink.pack_rgb565
         assert subs["pipeline"].frames_for_cube is datalink.frames_for_cube
+        assert subs["pipeline"].run_air is P.run_air
         assert subs["fec"].ErasureCode is fec.ErasureCode
         assert errors.ProtocolError is RefProtocolError
         assert subs["_accel"].gf256_matmul is fec.gf256_matmul
