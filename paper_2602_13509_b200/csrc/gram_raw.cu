@@ -14,7 +14,10 @@
 // canonical MN-major SWIZZLE_128B UMMA layout, so no thread touches the data on its way to
 // the tensor core.  The CUDA cores only scan each tile for m_s and for the
 // per-band minimum (a value below dark would clamp: the cube is then redone by
-// the generic path, flags |= 4).  Everything after the integer Gram is f64;
+// the generic path, flags |= 4); for 129..160-byte windows (B = 57..72, the c4 shape)
+// m_s comes from the tensor core too (a ones atom appended to the small MMAs' B operand)
+// and the scan is the minimum alone.  The scan reads conflict-free: a quarter-warp takes
+// 128 contiguous bytes of a tile.  Everything after the integer Gram is f64;
 // the result is the exact Gram up to f64 rounding (~1e-13 after centring).
 //
 // Work unit = (sample s, line range of <= 32768 lines); units are dealt to
@@ -38,7 +41,7 @@ using namespace umma;
 // -DSKYRX_GR_PROFILE builds accumulate per-CTA wait cycles of each role
 // (tools/gr_profile.py reads them through skyrx_gr_profile); compiled out otherwise
 #ifdef SKYRX_GR_PROFILE
-__device__ unsigned long long gr_prof[160][8];
+__device__ unsigned long long gr_prof[160][12];
 #define GR_PW(idx, stmt)                                        \
   do {                                                          \
     const unsigned long long t0_ = clock64();                   \
@@ -53,9 +56,9 @@ constexpr int kGrThreads = 320;
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
 // TMA ring depth (stage = 128 lines x (128 + second-box) bytes) within the shared memory
-// left beside the f64 accumulator: 8 stages, 6 for windows > 160 B, 2 for > 192 B
+// left beside the f64 accumulator: 8 stages, 5 for windows > 160 B, 2 for > 192 B
 template <int NCH>
-__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 6 : 8); }
+__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 5 : 8); }
 constexpr int64_t kGrMaxUnitLines = 32768;
 
 struct GramRawParams {
@@ -83,9 +86,14 @@ template <int NCH>
 __host__ __device__ constexpr uint32_t gr_w2b() {
   return NCH <= 8 ? 0u : (16 * NCH - 128 <= 32 ? 32u : (16 * NCH - 128 <= 64 ? 64u : 128u));
 }
+// windows of 129..160 bytes (the c4 shape, B = 57..72) take their column sums from the
+// tensor core: the two small MMAs get a 32-column atom of ones appended to B (N = 64), so
+// D[m][ones] = sum over lines of byte m, and the scan warps only track the minima
+template <int NCH>
+__host__ __device__ constexpr bool gr_ones() { return NCH > 8 && gr_w2b<NCH>() == 32u; }
 template <int NCH>
 __host__ __device__ constexpr int gr_bufcols() {
-  return ((16 * NCH + (NCH > 8 ? 16 * NCH - 128 : 0)) + 31) / 32 * 32;
+  return gr_ones<NCH>() ? 256 : ((16 * NCH + (NCH > 8 ? 16 * NCH - 128 : 0)) + 31) / 32 * 32;
 }
 template <int NCH>
 __host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 512 ? 2 : 1; }
@@ -106,20 +114,30 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   constexpr uint32_t ATOM1 = TWO_M ? kGrLb * W2B : 0u;
   constexpr uint32_t STAGE = ATOM + ATOM1;
   constexpr uint32_t LT1 = W2B == 32 ? 6u : (W2B == 64 ? 4u : 2u);
-  constexpr int G = kGrWorkers / NCH;             // scan line groups
+  // scan mapping (conflict-free 128-bit shared loads): each thread owns one logical 16-B
+  // chunk of the window; a quarter-warp reads 128 contiguous bytes (one 128-B line of box 0,
+  // or 128/W2B lines of box 1). W0 warps scan box 0, the other 4 - W0 scan box 1.
+  constexpr int W0 = TWO_M ? (W2B == 32 ? 3 : 2) : 4;
+  constexpr int NQ1 = W2B > 0 ? (int)W2B / 16 : 1;
   constexpr int BUFC = gr_bufcols<NCH>();
+  constexpr bool ONES = gr_ones<NCH>();
+  constexpr uint32_t P1OFF = ONES ? 192u : (uint32_t)NW;  // TMEM column of the part-1 block
   constexpr int NBUF = gr_nbuf<NCH>();
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
   uint8_t* stages = sm;
   double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE);
   double* sacc = qacc + B * B;
-  uint32_t* smin = reinterpret_cast<uint32_t*>(sacc + B);  // [G][NCH][4] packed u16 mins
-  uint32_t* ssum = smin + G * NCH * 4;                       // [G][NCH][8]
-  uint32_t* minv = ssum + G * NCH * 8;                       // [2][NCH*8]
+  uint8_t* ones = reinterpret_cast<uint8_t*>(sacc + B);      // ONES: [128 lines][32 B] of 1
+  uint32_t* smin = reinterpret_cast<uint32_t*>(ones + (ONES ? kGrLb * 32 : 0));  // [thread][4]
+  uint32_t* ssum = smin + kGrWorkers * 4;                    // [scan thread][8]
+  uint32_t* minv = ssum + kGrWorkers * 8;                    // [2][NCH*8]
   uint32_t* sumv = minv + 2 * NCH * 8;                       // [2][NCH*8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(sumv + 2 * NCH * 8) + 7) & ~uintptr_t(7));
+  double* bandC = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(sumv + 2 * NCH * 8) + 7) & ~uintptr_t(7));  // [B] per unit
+  double* bandD = bandC + B;
+  double* bandS = bandD + B;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bandS + B);
   uint64_t* full = bars;
   uint64_t* empty = full + kGrStages;
   uint64_t* acc_full = empty + kGrStages;   // [NBUF]
@@ -148,6 +166,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   // bit 8: this cube's clamp check ran (bit 4 would report a value below dark)
   if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 8);
   for (int e = tid; e < B * B + B; e += blockDim.x) qacc[e] = 0.0;
+  if (ONES) {
+    for (int e = tid; e < kGrLb * 8; e += blockDim.x)
+      reinterpret_cast<uint32_t*>(ones)[e] = 0x01010101u;
+    fence_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -187,7 +210,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   } else if (warp == 9) {
     if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
       constexpr uint32_t id = idesc_u8_s32(128, TWO_M ? 128 : NW);
-      constexpr uint32_t id2 = idesc_u8_s32(128, N2 > 0 ? N2 : 16);
+      constexpr uint32_t id2 = idesc_u8_s32(128, ONES ? 64 : (N2 > 0 ? N2 : 16));
       int t = 0, unit = 0;
       for (int64_t u = u0; u < u1; u += ustep, ++unit) {
         int s;
@@ -215,9 +238,14 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
               // 0..127, and rows 128..NW-1 x columns 128..NW-1 (the rest is the
               // transpose); the 128-row A of the second MMA re-reads its one atom
               // (LBO 0): rows >= NW-128 are never used
-              const uint64_t d1 = smem_desc_swz(base + ATOM + ks * 32 * W2B, 0, 8 * W2B, LT1);
-              mma_i8(d + 128, d0, d1, id2, acc);
-              mma_i8(d + NW, d1, d1, id2, acc);
+              const uint8_t* b1 = base + ATOM + ks * 32 * W2B;
+              const uint64_t d1 = smem_desc_swz(b1, 0, 8 * W2B, LT1);
+              // ONES: B = [bytes 128..159 | ones] as two SW32 atoms, LBO = their distance
+              const uint64_t d1b =
+                  ONES ? smem_desc_swz(b1, (uint32_t)(ones + ks * 32 * W2B - b1), 8 * W2B, LT1)
+                       : d1;
+              mma_i8(d + 128, d0, d1b, id2, acc);
+              mma_i8(d + P1OFF, d1, d1b, id2, acc);
             }
           }
           mma_commit(&empty[st]);
@@ -226,8 +254,16 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
     }
   } else if (warp < 4) {  // ---------------------------------------------- scan
-    const int c = tid % NCH, g = tid / NCH;
-    const bool scanner = g < G;
+    const int lane = tid & 31;
+    const bool box1 = warp >= W0;
+    const int q = box1 ? lane % NQ1 : lane & 7;            // logical chunk within the box
+    const int c = box1 ? 8 + q : q;                        // chunk of the window
+    const int lr = box1 ? lane / NQ1 : lane >> 3;          // line within a warp step
+    const int lpw = box1 ? 32 / NQ1 : 4;                   // lines per warp step
+    const int lw = box1 ? warp - W0 : warp;
+    const int lstep = lpw * (box1 ? 4 - W0 : W0);
+    const uint32_t wdt = box1 ? W2B : 128u;
+    const bool scanner = c < NCH;
     int t = 0, unit = 0;
     for (int64_t u = u0; u < u1; u += ustep, ++unit) {
       int s;
@@ -243,37 +279,42 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
-          const bool in1 = c >= 8;
-          const uint32_t wdt = in1 ? W2B : 128u;
-          const uint8_t* atom = stages + st * STAGE + (in1 ? ATOM : 0u);
-          const int q = c & 7;
+          const uint8_t* atom = stages + st * STAGE + (box1 ? ATOM : 0u);
 #pragma unroll 4
-          for (int l = g; l < valid; l += G) {
+          for (int l = lr + lpw * lw; l < valid; l += lstep) {
             const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
             const uint4 v = *reinterpret_cast<const uint4*>(atom + l * wdt + ((q ^ sw) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
-            sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu, sm8[3] += v.y >> 16;
-            sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16, sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+            if (!ONES) {  // (ONES: the column sums come from the tensor core)
+              sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu;
+              sm8[3] += v.y >> 16, sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16;
+              sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+            }
           }
         }
         mbar_arrive(&empty[st]);
       }
-      // per-unit reduction of the scans (fixed order over line groups) into buffer ub
-      if (scanner) {
-        for (int q = 0; q < 4; ++q) smin[(g * NCH + c) * 4 + q] = mn[q];
-        for (int q = 0; q < 8; ++q) ssum[(g * NCH + c) * 8 + q] = sm8[q];
-      }
+      // per-unit reduction of the scans (fixed member order per chunk) into buffer ub
+      for (int i = 0; i < 4; ++i) smin[tid * 4 + i] = mn[i];
+      for (int i = 0; i < 8; ++i) ssum[tid * 8 + i] = sm8[i];
       const int ub = unit & 1;
       mbar_wait(&scan_empty[ub], ((unit >> 1) & 1) ^ 1);
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
       if (tid < NCH * 8) {
-        const int cc = tid >> 3, q = tid & 7;
+        const int cc = tid >> 3, qq = tid & 7;
+        // members of chunk cc: box 0 -> threads cc + 8m (m < 4 W0); box 1 -> threads
+        // 32 W0 + (cc - 8) + NQ1 m (m < 32 (4 - W0) / NQ1)
+        const bool b1 = cc >= 8;
+        const int first = b1 ? 32 * W0 + (cc - 8) : cc;
+        const int stride = b1 ? NQ1 : 8;
+        const int nmem = b1 ? 32 * (4 - W0) / NQ1 : 4 * W0;
         uint32_t mv = 0xffffu, sv = 0;
-        for (int gg = 0; gg < G; ++gg) {
-          const uint32_t w = smin[(gg * NCH + cc) * 4 + (q >> 1)];
-          mv = min(mv, (q & 1) ? (w >> 16) : (w & 0xffffu));
-          sv += ssum[(gg * NCH + cc) * 8 + q];
+        for (int m = 0; m < nmem; ++m) {
+          const int mt = first + stride * m;
+          const uint32_t w = smin[mt * 4 + (qq >> 1)];
+          mv = min(mv, (qq & 1) ? (w >> 16) : (w & 0xffffu));
+          sv += ssum[mt * 8 + qq];
         }
         minv[ub * NCH * 8 + tid] = mv;
         sumv[ub * NCH * 8 + tid] = sv;
@@ -297,6 +338,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       if (tid == kGrWorkers) GR_PW(5, mbar_wait(&acc_full[buf], use & 1));
       else mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
+#ifdef SKYRX_GR_PROFILE
+      const unsigned long long et0 = clock64();
+#endif
       const uint32_t* mnv = minv + ub * NCH * 8;
       const uint32_t* smv = sumv + ub * NCH * 8;
       const int off = (int)(((int64_t)s * B * 2) & 15);
@@ -304,56 +348,107 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       const float* drow = p.dark + (int64_t)s * B;
       const float* crow = p.coeff + (int64_t)s * B;
       bool clamp = false;
+      // this unit's per-band terms, once, for every epilogue thread
+      if (ONES) {  // band sums = 256 sum(hi) + sum(lo) from the ones columns
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
+          uint32_t sv[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? 224u : 160u), sv);
+          tmem_ld_wait();
+          const uint32_t partner = __shfl_xor_sync(0xffffffffu, sv[0], 1);
+          const int rel = 128 * part + te - off;
+          if (rel >= 0 && rel < 2 * B && (rel & 1) == 0)
+            bandS[rel >> 1] = 256.0 * (double)partner + (double)sv[0];
+        }
+      }
+      for (int bb = te; bb < B; bb += kGrWorkers) {
+        bandC[bb] = (double)crow[bb] * p.ginv;
+        bandD[bb] = (double)drow[bb];
+        if (!ONES) bandS[bb] = (double)smv[(off >> 1) + bb];
+        clamp |= (float)mnv[(off >> 1) + bb] < drow[bb];
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(kGrWorkers) : "memory");
+#ifdef SKYRX_GR_PROFILE
+      const unsigned long long et1 = clock64();
+      if (tid == kGrWorkers) gr_prof[blockIdx.x][8] += et1 - et0;
+#endif
 #pragma unroll
       for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
         if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
         const int m = 128 * part + te;
         const int rel = m - off;
-        const bool lo_row = rel >= 0 && rel < 2 * B && (rel & 1) == 0;
+        const bool in_band = rel >= 0 && rel < 2 * B;
+        const int hi = rel & 1;    // 0: this row is band b's lo byte, 1: its hi byte
         const int b = rel >> 1;
         double Cb = 0.0, db = 0.0, Sb = 0.0;
-        if (lo_row) {
-          Cb = (double)crow[b] * p.ginv;
-          db = (double)drow[b];
-          Sb = (double)smv[(off >> 1) + b];
-          clamp |= (float)mnv[(off >> 1) + b] < drow[b];
-        }
+        if (in_band) Cb = bandC[b], db = bandD[b], Sb = bandS[b];
         // part 0: byte columns 0..NW-1 of the full-width block; part 1: columns 128..NW-1
-        const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? NW : 0);
+        const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? P1OFF : 0);
         const int cc0 = part ? 8 : 0;
-        for (int cc = cc0; cc < NCH; ++cc) {
-          uint32_t v[16];
-          tmem_ld16(taddr + (cc - cc0) * 16, v);
+        // chunks this warp's rows need (warp-uniform): the lower triangle reaches byte
+        // column 128 part + 32 we + 31; part-0 rows also own every column past byte 128
+        const int cmax = 128 * part + 32 * we + 31;
+        auto needed = [&](int cc) {
+          return cc < NCH && (cc * 16 <= cmax || (part == 0 && TWO_M && cc >= 8));
+        };
+        // two chunks per TMEM wait: the loads queue behind the next unit's MMAs
+        for (int cc = cc0; cc < NCH; cc += 2) {
+          const bool n0 = needed(cc), n1 = needed(cc + 1);
+          if (!n0 && !n1) continue;
+          uint32_t v2[32];
+          if (n0) tmem_ld16(taddr + (cc - cc0) * 16, v2);
+          if (n1) tmem_ld16(taddr + (cc + 1 - cc0) * 16, v2 + 16);
           tmem_ld_wait();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+          if (!(h ? n1 : n0)) continue;
+          const int c = cc + h;
+          const uint32_t* v = v2 + 16 * h;
           uint32_t pv[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, v[q], 1);
-          if (lo_row) {
+          if (in_band) {
+            // the lo-byte row of the pair takes the even band columns, the hi-byte row
+            // the odd ones; each has both rows (own + partner) of the pair
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const int reln = cc * 16 + 2 * i - off;
+              if ((i & 1) != hi) continue;
+              const int reln = c * 16 + 2 * i - off;
               if (reln < 0 || reln >= 2 * B) continue;
               const int b2 = reln >> 1;
-              // lower triangle (b2 <= b) from this row; a part-0 row also owns the
+              // lower triangle (b2 <= b) from this row pair; a part-0 pair also owns the
               // (b2 > b) entries whose columns lie past byte 128: their part-1 rows
               // only see columns >= 128
-              const bool mine = b2 <= b || (part == 0 && TWO_M && cc >= 8);
+              const bool mine = b2 <= b || (part == 0 && TWO_M && c >= 8);
               if (!mine) continue;
-              // own row = lo byte of band b, partner row = hi byte of band b
-              const double gv = 65536.0 * (double)pv[2 * i + 1] +
-                                256.0 * ((double)pv[2 * i] + (double)v[2 * i + 1]) +
-                                (double)v[2 * i];
-              const double C2 = (double)crow[b2] * p.ginv;
-              const double d2 = (double)drow[b2];
-              const double S2 = (double)smv[(off >> 1) + b2];
+              // H_b H_b2, H_b L_b2 + L_b H_b2, L_b L_b2 from (own, partner) rows
+              const uint32_t hh = hi ? v[2 * i + 1] : pv[2 * i + 1];
+              const uint32_t hl = hi ? v[2 * i] : pv[2 * i];
+              const uint32_t lh = hi ? pv[2 * i + 1] : v[2 * i + 1];
+              const uint32_t ll = hi ? pv[2 * i] : v[2 * i];
+              // exact integer G entry (< 2^48), to f64 through the 2^52 exponent trick
+              const uint64_t gi = ((uint64_t)hh << 16) + (((uint64_t)hl + lh) << 8) + ll;
+              const double gv = __hiloint2double(0x43300000 | (int)(gi >> 32), (int)(uint32_t)gi) -
+                                4503599627370496.0;
+              const double C2 = bandC[b2], d2 = bandD[b2], S2 = bandS[b2];
               const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
               const int e = b2 <= b ? b * B + b2 : b2 * B + b;
               qacc[e] += Cb * C2 * xx;
             }
           }
+          }
         }
-        if (lo_row) sacc[b] += Cb * (Sb - Lu * db);
+        if (in_band && !hi) sacc[b] += Cb * (Sb - Lu * db);
+#ifdef SKYRX_GR_PROFILE
+        if (tid == kGrWorkers) gr_prof[blockIdx.x][9 + part] += clock64() - et1;
+#endif
       }
+      // the band terms are rewritten by the next unit only after every thread is done here
+      asm volatile("bar.sync 2, %0;" ::"n"(kGrWorkers) : "memory");
+#ifdef SKYRX_GR_PROFILE
+      if (tid == kGrWorkers) gr_prof[blockIdx.x][6] += clock64() - et0;
+#endif
       if (clamp) atomicOr(p.flags, 4);
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
@@ -386,7 +481,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 }
 
 #ifdef SKYRX_GR_PROFILE
-extern "C" int skyrx_gr_profile(unsigned long long* out) {
+extern "C" __attribute__((visibility("default"))) int skyrx_gr_profile(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, gr_prof, sizeof(gr_prof));
 }
 #endif
@@ -480,10 +575,11 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
-  constexpr int G = kGrWorkers / NCH;
   constexpr int kGrStages = gr_stages<NCH>();
   const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
-                      (size_t)G * NCH * 12 * 4 + NCH * 8 * 16 + 16 * 8 + 1024;
+                      (size_t)kGrWorkers * 12 * 4 + NCH * 8 * 16 + 3 * (size_t)p.B * 8 +
+                      (gr_ones<NCH>() ? kGrLb * 32 : 0) +
+                      16 * 8 + 1024;
   int grid = kSMs;
   if (p.units < grid) grid = (int)p.units;
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
