@@ -96,7 +96,8 @@ __device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint32_t thi
 //   MODE 2: per-line gain g              d = max(r c - dark c, 0) / g - mu
 //   MODE 3: odd B (2-byte aligned rows), general formula
 template <int MODE, int CHT>
-__device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&tco)[CHT * 4],
+__device__ __forceinline__ void transform_row(const uint8_t* rr, uint32_t rr32,
+                                              const float2 (&tco)[CHT * 4],
                                               const float2 (&tnof)[CHT * 4], const float2* nm,
                                               float g, uint32_t thi, uint32_t tlo, int cnt) {
   const float gi = 1.0f / g;
@@ -106,9 +107,12 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, const float2 (&
     if (cc >= cnt) break;  // warp-uniform
     float2 rf[4];
     if (MODE != 3) {  // 4-byte aligned rows: two counts per LDS.32
+      uint32_t wv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) wv[q] = ld_shared_u32(rr32 + 16 * cc + 4 * q);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint32_t v = *reinterpret_cast<const uint32_t*>(rr + 16 * cc + 4 * q);
+        const uint32_t v = wv[q];
         // exact u16 -> f32 on the ALU pipes: (2^23 + r) - 2^23
         rf[q] = fadd2(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)),
                                   __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632))),
@@ -197,6 +201,9 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
     tmem_st_wait();
   }
   const float2* nm0 = mu + 8 * c_lo;
+  const uint32_t ring32 = smem_u32(raw_ring), raw_full32 = smem_u32(raw_full);
+  const uint32_t raw_empty32 = smem_u32(raw_empty), a_full32 = smem_u32(a_full);
+  const uint32_t a_empty32 = smem_u32(a_empty);
   int s = 0, as = 0;
   uint32_t ph = 0, aph = 0;
   for (int t = 0; t < n; ++t) {
@@ -208,18 +215,19 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
       const int64_t line = ti.line0 + r / ti.w;
       g = __ldg(p.gain + (line < p.ts.L ? line : p.ts.L - 1));
     }
-    mbar_wait(&raw_full[s], ph);
-    mbar_wait(&a_empty[as], aph ^ 1);
+    mbar_wait(raw_full32 + 8 * s, ph);
+    mbar_wait(a_empty32 + 8 * as, aph ^ 1);
     tc_fence_after();
-    const uint8_t* rr = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * 2 + 16 * c_lo;
+    const uint32_t roff = s * p.raw_stage_bytes + r * B * 2 + 16 * c_lo;
     const uint32_t thi = tl + as * KP;
-    transform_row<MODE, CHT>(rr, tco, tnof, nm0, g, thi, thi + KP / 2, cnt);
+    transform_row<MODE, CHT>(raw_ring + roff, ring32 + roff, tco, tnof, nm0, g, thi,
+                             thi + KP / 2, cnt);
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {  // one arrival per warp
-      mbar_arrive(&a_full[as]);
-      mbar_arrive(&raw_empty[s]);
+      mbar_arrive(a_full32 + 8 * as);
+      mbar_arrive(raw_empty32 + 8 * s);
     }
     if (++s == NR) s = 0, ph ^= 1;
     if (++as == kScoreAStages) as = 0, aph ^= 1;
@@ -360,11 +368,15 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     uint32_t local_max = 0;
     TileInfo ti = tile_at(p.ts, blk, g0);
+    // the CTA never leaves its block, so a row's (line, sample) offsets are fixed
+    const int li = n > 0 ? r / ti.w : 0;
+    const int sc = r - li * ti.w;
+    const uint32_t acc_full32 = smem_u32(acc_full), acc_empty32 = smem_u32(acc_empty);
     int acs = 0;
     uint32_t cph = 0;
     for (int t = 0; t < n; ++t) {
       if (t > 0) tile_next_in_block(p.ts, ti, gstep);
-      mbar_wait(&acc_full[acs], cph);
+      mbar_wait(acc_full32 + 8 * acs, cph);
       tc_fence_after();
       float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -380,13 +392,12 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acs]);  // one arrival per warp
+      if (lane == 0) mbar_arrive(acc_empty32 + 8 * acs);  // one arrival per warp
       const bool valid = r < ti.rows;
       uint32_t key = 0;
       if (valid) {
-        const int li = r / ti.w;
         const float sum = (acc.x + acc.y) * ws2;
-        p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + (r - li * ti.w)] = sum;
+        p.scores[(ti.line0 + li) * (int64_t)p.ts.S + ti.s0 + sc] = sum;
         key = f2ord(sum);
         local_max = max(local_max, key);
       }
