@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // 32-bit shared addresses for the per-tile barriers and loads (no per-tile conversion)
+  const uint32_t full32 = smem_u32(full), empty32 = smem_u32(empty), stages32 = smem_u32(stages);
 #ifdef SKYRX_GR_PROFILE
   const unsigned long long kt0 = clock64();
 #endif
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kGrStages;
-          GR_PW(0, mbar_wait(&empty[st], ((t / kGrStages) & 1) ^ 1));
+          GR_PW(0, mbar_wait(empty32 + 8 * st, ((t / kGrStages) & 1) ^ 1));
           mbar_arrive_expect_tx(&full[st], STAGE);
           tma_load_2d(stages + st * STAGE, &tmap, 16 * c0, (int)(l0 + (int64_t)k * kGrLb),
                       &full[st]);
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         const uint32_t d = tmem + buf * BUFC;
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kGrStages;
-          GR_PW(2, mbar_wait(&full[st], (t / kGrStages) & 1));
+          GR_PW(2, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
           tc_fence_after();
           const uint8_t* base = stages + st * STAGE;
 #pragma unroll
@@ -274,16 +276,16 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       uint32_t sm8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int k = 0; k < ntile; ++k, ++t) {
         const int st = t % kGrStages;
-        if (tid == 0) GR_PW(3, mbar_wait(&full[st], (t / kGrStages) & 1));
-        else mbar_wait(&full[st], (t / kGrStages) & 1);
+        if (tid == 0) GR_PW(3, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
+        else mbar_wait(full32 + 8 * st, (t / kGrStages) & 1);
         if (scanner) {
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
-          const uint8_t* atom = stages + st * STAGE + (box1 ? ATOM : 0u);
+          const uint32_t atom = stages32 + st * STAGE + (box1 ? ATOM : 0u);
 #pragma unroll 4
           for (int l = lr + lpw * lw; l < valid; l += lstep) {
             const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
-            const uint4 v = *reinterpret_cast<const uint4*>(atom + l * wdt + ((q ^ sw) << 4));
+            const uint4 v = ld_shared_v4(atom + l * wdt + ((q ^ sw) << 4));
             mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
             mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
             if (!ONES) {  // (ONES: the column sums come from the tensor core)
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             }
           }
         }
-        mbar_arrive(&empty[st]);
+        mbar_arrive(empty32 + 8 * st);
       }
       // per-unit reduction of the scans (fixed member order per chunk) into buffer ub
       for (int i = 0; i < 4; ++i) smin[tid * 4 + i] = mn[i];
