@@ -268,7 +268,23 @@ __global__ void fold_kernel(double* __restrict__ state, const double* __restrict
 }
 
 // ------------------------------------------------------------------ K3
-constexpr int kFinThreads = 512;
+constexpr int kFinThreads = 1024;
+// -DSKYRX_FIN_PROFILE: clock64 at the phase boundaries of matrix 0 (skyrx_fin_profile)
+#ifdef SKYRX_FIN_PROFILE
+__device__ long long fin_prof[8];
+#define FIN_T(k)                                                    \
+  do {                                                              \
+    __syncthreads();                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) fin_prof[k] = clock64(); \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int skyrx_fin_profile(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fin_prof, sizeof(fin_prof));
+}
+#else
+#define FIN_T(k) \
+  do {           \
+  } while (0)
+#endif
 constexpr int kSmemCholMaxB = 160;
 constexpr int kSmemInvMaxB = 118;  // L and W = L^-1 both in shared memory (2 B^2 doubles)
 
@@ -298,7 +314,6 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     int32_t* __restrict__ status_all, int do_inverse) {
   extern __shared__ __align__(16) double fsm[];
   __shared__ double scratch[40];
-  __shared__ double dg[1024];  // Cholesky pivots l_jj
   __shared__ int s_fail;
   const int B = bands;
   const size_t BB = (size_t)B * B;
@@ -314,6 +329,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   float* mhl = mhl_all + (size_t)m * 2 * B;
   const int tid = threadIdx.x;
   const int NT = blockDim.x;
+  FIN_T(0);
 
   const double n = mom[0];
   const double* s = mom + 1;
@@ -351,7 +367,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   const double trace = block_sum_fixed(tr, scratch);
   const double scale = trace > 0.0 ? trace / B : 1.0;
 
-  double* A = (B <= kSmemCholMaxB) ? fsm : chol;  // working factor
+  // dynamic shared memory: [l_jj | 1 / l_jj] (2B), then A (B <= kSmemCholMaxB), then W
+  double* dg = fsm;
+  FIN_T(1);
+  double* A = (B <= kSmemCholMaxB) ? fsm + 2 * B : chol;  // working factor
   const double eps_tab[6] = {0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6};
   double ridge = 0.0;
   bool ok = false;
@@ -362,28 +381,59 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
       A[e] = (j <= i) ? sigma[e] + (i == j ? ridge : 0.0) : 0.0;
     }
     if (tid == 0) s_fail = 0;
-    __syncthreads();
-    // right-looking Cholesky, lower triangle; the pivots go to dg[] (A's diagonal is
-    // rewritten at the end) so every thread reads the same final a_jj without a barrier
-    for (int j = 0; j < B; ++j) {
-      const double ajj = A[(size_t)j * B + j];
-      if (!(ajj > 0.0)) {  // LAPACK potrf: non-positive or NaN pivot fails (uniform branch)
-        if (tid == 0) s_fail = 1;
-        break;
+    // right-looking Cholesky, lower triangle, ONE barrier per column: the trailing update
+    // uses l_ij = a_ij / l_jj on the fly (FMA-free, so an exactly rank-deficient input
+    // still meets an exactly zero pivot and fails like LAPACK potrf), and column j is
+    // scaled in place one step later, when nobody reads it any more. The pivot j+1 is
+    // final as soon as step j has updated it: the thread that does so takes its root and
+    // reciprocal right away (lookahead), the other warps read them after the barrier.
+    const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
+    auto pivot = [&](int jj, double v) {
+      if (!(v > 0.0)) {  // LAPACK potrf: non-positive or NaN pivot fails
+        s_fail = 1;
+        return;
       }
-      const double ljj = sqrt(ajj);
-      if (tid == 0) dg[j] = ljj;
-      for (int i = j + 1 + tid; i < B; i += NT) A[(size_t)i * B + j] /= ljj;
-      __syncthreads();
-      // trailing update of the lower triangle: a warp per row, lanes along it
+      const double l = sqrt(v);
+      dg[jj] = l, dg[B + jj] = 1.0 / l;
+    };
+    __syncthreads();
+    if (tid == 0) pivot(0, A[0]);
+    __syncthreads();
+    for (int j = 0; j < B; ++j) {
+      if (s_fail) break;  // uniform: written before the previous barrier
+      const double rl = dg[B + j];
       const int r = B - j - 1;  // trailing order
-      const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
-      for (int ii = wid; ii < r; ii += nw) {
-        const int i = j + 1 + ii;
-        const double lij = A[(size_t)i * B + j];
-        for (int kk = ln; kk <= ii; kk += 32) {
-          const int k = j + 1 + kk;
-          A[(size_t)i * B + k] = __dsub_rn(A[(size_t)i * B + k], __dmul_rn(lij, A[(size_t)k * B + j]));
+      // warp 0: rows j and j+1 (the lookahead pivot, a serial root + reciprocal), the
+      // other warps: the trailing rows j+2.. (a warp per row)
+      for (int ii = wid == 0 ? 0 : wid + 1; ii <= r; ii += wid == 0 ? 1 : nw - 1) {
+        if (wid == 0 && ii > 1) break;
+        const int i = j + ii;
+        double* Ai = A + i * B;
+        if (j > 0 && ln == 0) Ai[j - 1] *= dg[B + j - 1];
+        if (ii == 0) continue;
+        const double lij = Ai[j] * rl;
+        if (ii == 1) {  // row j+1 has one entry: the next pivot
+          if (ln == 0) {
+            const double v = __dsub_rn(Ai[j + 1], __dmul_rn(lij, lij));
+            Ai[j + 1] = v;
+            pivot(i, v);
+          }
+          continue;
+        }
+        // up to 4 of the lane's entries: all loads, then the updates (the stores would
+        // otherwise order every next load behind them)
+        for (int k0 = j + 1; k0 <= i; k0 += 128) {
+          double x[4], z[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int k = k0 + ln + 32 * q;
+            if (k <= i) x[q] = Ai[k], z[q] = A[k * B + j];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int k = k0 + ln + 32 * q;
+            if (k <= i) Ai[k] = __dsub_rn(x[q], __dmul_rn(lij, z[q] * rl));
+          }
         }
       }
       __syncthreads();
@@ -401,6 +451,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     }
     return;
   }
+  FIN_T(2);
   if (A != chol)
     for (size_t e = tid; e < BB; e += NT) chol[e] = A[e];
   __syncthreads();
@@ -411,42 +462,74 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     }
     return;
   }
-  // W = L^-1 (forward substitution on e_c, one column per thread) in shared memory
-  // next to L when both fit, so the O(B^3) inner loops never touch global memory
-  double* Wm = (A == fsm && B <= kSmemInvMaxB) ? fsm + BB : w64;
-  for (int c = tid; c < B; c += NT) {
-    for (int i = 0; i < c; ++i) Wm[(size_t)i * B + c] = 0.0;
-    for (int i = c; i < B; ++i) {
-      double a0 = (i == c) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int k = c;
-      for (; k + 3 < i; k += 4) {
-        a0 -= A[(size_t)i * B + k] * Wm[(size_t)k * B + c];
-        a1 -= A[(size_t)i * B + k + 1] * Wm[(size_t)(k + 1) * B + c];
-        a2 -= A[(size_t)i * B + k + 2] * Wm[(size_t)(k + 2) * B + c];
-        a3 -= A[(size_t)i * B + k + 3] * Wm[(size_t)(k + 3) * B + c];
-      }
-      for (; k < i; ++k) a0 -= A[(size_t)i * B + k] * Wm[(size_t)k * B + c];
-      Wm[(size_t)i * B + c] = ((a0 + a1) + (a2 + a3)) / A[(size_t)i * B + i];
-    }
+  // W = L^-1 in shared memory next to L when both fit (so the O(B^3) loops never touch
+  // global memory), right-looking: after step j row j of W is final (R_j * 1/l_jj, scaled
+  // in place one step later) and every later row has subtracted l_ij * W_j; one barrier per
+  // row, the (i, c) updates of a step spread over the whole CTA
+  double* Wm = (A != chol && B <= kSmemInvMaxB) ? A + BB : w64;
+  for (size_t e = tid; e < BB; e += NT) {
+    const int i = (int)(e / B), c = (int)(e - (size_t)i * B);
+    Wm[e] = (i == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  {
+    const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
+    for (int j = 0; j < B; ++j) {
+      const double rj = dg[B + j];
+      if (j > 0 && wid == nw - 1)
+        for (int c = ln; c < j; c += 32) Wm[(j - 1) * B + c] *= dg[B + j - 1];
+      const double* Wj = Wm + j * B;
+      for (int i = j + 1 + wid; i < B; i += nw) {  // a warp per row, lanes along c <= j
+        const double lij = A[i * B + j];
+        double* Wi = Wm + i * B;
+        for (int c0 = 0; c0 <= j; c0 += 128) {
+          double x[4], z[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = c0 + ln + 32 * q;
+            if (c <= j) x[q] = Wi[c], z[q] = Wj[c];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = c0 + ln + 32 * q;
+            if (c <= j) Wi[c] = x[q] - lij * (z[q] * rj);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int c = tid; c < B; c += NT) Wm[(size_t)(B - 1) * B + c] *= dg[B + B - 1];
+  __syncthreads();
+  FIN_T(3);
   if (Wm != w64)
     for (size_t e = tid; e < BB; e += NT) w64[e] = Wm[e];
   __threadfence_block();
+  FIN_T(4);
   // sigma_inv = W^T W (= cho_solve(L, I)), exactly symmetric by construction
-  for (size_t e = tid; e < BB; e += NT) {
-    const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
-    if (j > i) continue;
-    double acc = 0.0;
-    for (int k = i; k < B; ++k) acc += Wm[(size_t)k * B + i] * Wm[(size_t)k * B + j];
-    inv[(size_t)i * B + j] = acc;
-    inv[(size_t)j * B + i] = acc;
+  {  // a warp per row i (rows dealt so the long dot products spread), lanes along j <= i
+    const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
+    for (int i = wid; i < B; i += nw)
+      for (int j = ln; j <= i; j += 32) {
+        double a0 = 0.0, a1 = 0.0;
+        int k = i;
+        for (; k + 1 < B; k += 2) {
+          a0 += Wm[k * B + i] * Wm[k * B + j];
+          a1 += Wm[(k + 1) * B + i] * Wm[(k + 1) * B + j];
+        }
+        if (k < B) a0 += Wm[k * B + i] * Wm[k * B + j];
+        const double acc = a0 + a1;
+        inv[(size_t)i * B + j] = acc;
+        inv[(size_t)j * B + i] = acc;
+      }
   }
+  FIN_T(5);
   // f32 whitening matrix, transposed (wf[k * ld_w + j] = W[j][k]) for K4
   for (size_t e = tid; e < (size_t)ld_w * ld_w; e += NT) {
     const int k = (int)(e / ld_w), j = (int)(e - (size_t)k * ld_w);
     wf[e] = (j < B && k < B && k <= j) ? (float)Wm[(size_t)j * B + k] : 0.0f;
   }
+  FIN_T(6);
   if (tid == 0) {
     status_all[m] = SKYRX_OK;
     ridge_all[m] = ridge;
@@ -645,9 +728,10 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
   SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
   SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
-  const size_t sm = bands <= kSmemInvMaxB    ? 2 * (size_t)bands * bands * sizeof(double)
-                    : bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double)
-                                             : 0;
+  const size_t sm = 2 * (size_t)bands * sizeof(double) +
+                    (bands <= kSmemInvMaxB    ? 2 * (size_t)bands * bands * sizeof(double)
+                     : bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double)
+                                              : 0);
   const bool wide = bands > kSmemInvMaxB;
   cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
