@@ -371,6 +371,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   double* dg = fsm;
   FIN_T(1);
   double* A = (B <= kSmemCholMaxB) ? fsm + 2 * B : chol;  // working factor
+  // row stride of A: odd in shared memory, so a column walk (lanes over rows) spreads over
+  // the banks instead of hitting every 4th one (B = 70: stride 140 words)
+  const int la = (A != chol) ? (B | 1) : B;
   const double eps_tab[6] = {0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6};
   double ridge = 0.0;
   bool ok = false;
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     ridge = eps_tab[a] * scale;
     for (size_t e = tid; e < BB; e += NT) {
       const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
-      A[e] = (j <= i) ? sigma[e] + (i == j ? ridge : 0.0) : 0.0;
+      A[i * la + j] = (j <= i) ? sigma[e] + (i == j ? ridge : 0.0) : 0.0;
     }
     if (tid == 0) s_fail = 0;
     // right-looking Cholesky, lower triangle, ONE barrier per column: the trailing update
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
       for (int ii = wid == 0 ? 0 : wid + 1; ii <= r; ii += wid == 0 ? 1 : nw - 1) {
         if (wid == 0 && ii > 1) break;
         const int i = j + ii;
-        double* Ai = A + i * B;
+        double* Ai = A + i * la;
         if (j > 0 && ln == 0) Ai[j - 1] *= dg[B + j - 1];
         if (ii == 0) continue;
         const double lij = Ai[j] * rl;
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int k = k0 + ln + 32 * q;
-            if (k <= i) x[q] = Ai[k], z[q] = A[k * B + j];
+            if (k <= i) x[q] = Ai[k], z[q] = A[k * la + j];
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     __syncthreads();
     ok = (s_fail == 0);
     if (ok)
-      for (int j = tid; j < B; j += NT) A[(size_t)j * B + j] = dg[j];
+      for (int j = tid; j < B; j += NT) A[j * la + j] = dg[j];
     __syncthreads();
   }
   if (!ok) {
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   }
   FIN_T(2);
   if (A != chol)
-    for (size_t e = tid; e < BB; e += NT) chol[e] = A[e];
+    for (size_t e = tid; e < BB; e += NT) chol[e] = A[(e / B) * la + e % B];
   __syncthreads();
   if (!do_inverse) {  // wide matrices: W, Sigma^-1 and wf by the multi-CTA kernels below
     if (tid == 0) {
@@ -466,7 +469,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   // global memory), right-looking: after step j row j of W is final (R_j * 1/l_jj, scaled
   // in place one step later) and every later row has subtracted l_ij * W_j; one barrier per
   // row, the (i, c) updates of a step spread over the whole CTA
-  double* Wm = (A != chol && B <= kSmemInvMaxB) ? A + BB : w64;
+  double* Wm = (A != chol && B <= kSmemInvMaxB) ? A + (size_t)B * la : w64;
   for (size_t e = tid; e < BB; e += NT) {
     const int i = (int)(e / B), c = (int)(e - (size_t)i * B);
     Wm[e] = (i == c) ? 1.0 : 0.0;
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
         for (int c = ln; c < j; c += 32) Wm[(j - 1) * B + c] *= dg[B + j - 1];
       const double* Wj = Wm + j * B;
       for (int i = j + 1 + wid; i < B; i += nw) {  // a warp per row, lanes along c <= j
-        const double lij = A[i * B + j];
+        const double lij = A[i * la + j];
         double* Wi = Wm + i * B;
         for (int c0 = 0; c0 <= j; c0 += 128) {
           double x[4], z[4];
@@ -729,8 +732,9 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
   SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
   const size_t sm = 2 * (size_t)bands * sizeof(double) +
-                    (bands <= kSmemInvMaxB    ? 2 * (size_t)bands * bands * sizeof(double)
-                     : bands <= kSmemCholMaxB ? (size_t)bands * bands * sizeof(double)
+                    (bands <= kSmemInvMaxB ? ((size_t)bands * (bands | 1) + (size_t)bands * bands) *
+                                                 sizeof(double)
+                     : bands <= kSmemCholMaxB ? (size_t)bands * (bands | 1) * sizeof(double)
                                               : 0);
   const bool wide = bands > kSmemInvMaxB;
   cudaStream_t st = as_stream(stream);
