@@ -28,7 +28,7 @@ namespace raww {
 
 constexpr int kLb = 128;            // lines per tile
 constexpr int kThreads = 192;
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;
 constexpr int kMaxAtoms = 5;        // window <= 640 bytes
 constexpr uint32_t kAtom = kLb * 128u;
 
@@ -45,7 +45,11 @@ struct Params {
   int64_t split_lines;
   int64_t units;
   int32_t nblk;          // blocks in this pass (<= 4)
-  int32_t blk_r[4], blk_c[4];  // their (row atom, column atom)
+  int32_t blk_r[4], blk_c[4];  // their (row atom, column atom) of the window
+  int32_t natom;         // window atoms this pass loads (the ones its blocks use)
+  int32_t atom_id[kMaxAtoms];  // ... which, in stage-slot order
+  int32_t blk_rs[4], blk_cs[4];  // the blocks' row / column atoms as stage slots
+  int32_t nstages;       // TMA ring depth (<= kMaxStages)
   int32_t first_pass;    // also accumulate Sx and n
 };
 
@@ -72,14 +76,22 @@ __global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restri
   const int B = p.B;
   const int64_t pitch = (int64_t)p.S * B;  // u16 per line
   const int nv = p.nw16 / 8;
+  // a work item = (unit, vector, slice of <= kScanSlice lines): integer sums of the slices
+  // are added atomically (exact, order-free), so a long unit still spreads over the GPU
+  constexpr int64_t kScanSlice = 1024;
+  const int64_t nsl = (p.split_lines + kScanSlice - 1) / kScanSlice;
   bool clamp = false;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < p.units * nv;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < p.units * nsl * nv;
        it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t u = it / nv;
-    const int v = (int)(it - u * nv);
+    const int64_t uz = it / nv;
+    const int v = (int)(it - uz * nv);
+    const int64_t u = uz / nsl, z = uz - u * nsl;
     int s;
     int64_t l0, nl;
     unit_geom(p, u, s, l0, nl);
+    l0 += z * kScanSlice;
+    nl = nl - z * kScanSlice < kScanSlice ? nl - z * kScanSlice : kScanSlice;
+    if (nl <= 0) continue;
     const int64_t w0 = ((int64_t)s * B * 2 & ~(int64_t)15) >> 1;  // first u16 of the window
     const int off = (int)(((int64_t)s * B * 2 & 15) >> 1);
     const int64_t col = w0 + 8 * v;
@@ -114,7 +126,7 @@ __global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restri
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) usum[u * p.nw16 + 8 * v + i] = sum[i];
+    for (int i = 0; i < 8; ++i) atomicAdd(&usum[u * p.nw16 + 8 * v + i], sum[i]);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flags, 8);
   if (__any_sync(0xffffffffu, clamp) && (threadIdx.x & 31) == 0) atomicOr(flags, 4);
@@ -123,14 +135,15 @@ __global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restri
 __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
     const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const uint32_t STAGE = (uint32_t)p.na * kAtom;
+  const uint32_t STAGE = (uint32_t)p.natom * kAtom;
+  const int kStages = p.nstages;
   uint8_t* stages = sm;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * STAGE);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* acc_full = bars + 2 * kStages;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);  // band terms follow
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int B = p.B;
@@ -159,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
           const int st = t % kStages;
           mbar_wait(&empty[st], ((t / kStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[st], STAGE);
-          for (int a = 0; a < p.na; ++a)
-            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * a,
+          for (int a = 0; a < p.natom; ++a)  // only the atoms this pass's blocks use
+            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * p.atom_id[a],
                         (int)(l0 + (int64_t)k * kLb), &full[st]);
         }
       }
@@ -184,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
           for (int ks = 0; ks < kLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
             for (int bk = 0; bk < p.nblk; ++bk) {
-              const uint64_t da = smem_desc_sw128(base + p.blk_r[bk] * kAtom + ks * 4096, kAtom, 1024);
-              const uint64_t db = smem_desc_sw128(base + p.blk_c[bk] * kAtom + ks * 4096, kAtom, 1024);
+              const uint64_t da = smem_desc_sw128(base + p.blk_rs[bk] * kAtom + ks * 4096, kAtom, 1024);
+              const uint64_t db = smem_desc_sw128(base + p.blk_cs[bk] * kAtom + ks * 4096, kAtom, 1024);
               mma_i8(tmem + 128 * bk, da, db, id, acc);
             }
           }
@@ -197,6 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
     const int te = tid;  // byte row within the row atom = TMEM lane
     double* part = p.part + (size_t)blockIdx.x * ((size_t)B * B + B + 1);
+    double* bandC = reinterpret_cast<double*>(bars + 2 * kStages + 2 + 2);  // [B] per unit
+    double* bandD = bandC + B;
+    double* bandS = bandD + B;
     double nsum = 0.0;
     int unit = 0;
     for (int64_t u = u0; u < p.units; u += ustep, ++unit) {
@@ -208,41 +224,56 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
       const double Lu = (double)nl;
       const float* drow = p.dark + (int64_t)s * B;
       const float* crow = p.coeff + (int64_t)s * B;
+      // this unit's per-band terms, once, for the four epilogue warps
+      for (int b = te; b < B; b += 128) {
+        bandC[b] = (double)crow[b] * p.ginv;
+        bandD[b] = (double)drow[b];
+        bandS[b] = (double)us[(off >> 1) + b];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(acc_full, unit & 1);
       tc_fence_after();
       for (int bk = 0; bk < p.nblk; ++bk) {
         const int mr = p.blk_r[bk], mc = p.blk_c[bk];
         const int m = 128 * mr + te;
         const int rel = m - off;
-        const bool lo_row = rel >= 0 && rel < 2 * B && (rel & 1) == 0;
+        const bool in_band = rel >= 0 && rel < 2 * B;
+        const int hi = rel & 1;  // 0: this row is band b's lo byte, 1: its hi byte
         const int b = rel >> 1;
         double Cb = 0.0, db = 0.0, Sb = 0.0;
-        if (lo_row) {
-          Cb = (double)crow[b] * p.ginv;
-          db = (double)drow[b];
-          Sb = (double)us[(off >> 1) + b];
-        }
+        if (in_band) Cb = bandC[b], db = bandD[b], Sb = bandS[b];
         const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 128 * bk;
-        for (int cc = 0; cc < 8; ++cc) {
-          uint32_t v[16];
-          tmem_ld16(taddr + cc * 16, v);
+        for (int cc = 0; cc < 8; cc += 2) {  // two chunks per TMEM wait
+          uint32_t v2[32];
+          tmem_ld16(taddr + cc * 16, v2);
+          tmem_ld16(taddr + (cc + 1) * 16, v2 + 16);
           tmem_ld_wait();
-          uint32_t pv[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, v[q], 1);
-          if (lo_row) {
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t* v = v2 + 16 * h;
+            uint32_t pv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pv[q] = __shfl_xor_sync(0xffffffffu, v[q], 1);
+            if (!in_band) continue;
+            // the lo-byte row of a band's pair takes the even band columns, the hi-byte row
+            // the odd ones; each has both rows (own + partner)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const int reln = 128 * mc + cc * 16 + 2 * i - off;
+              if ((i & 1) != hi) continue;
+              const int reln = 128 * mc + (cc + h) * 16 + 2 * i - off;
               if (reln < 0 || reln >= 2 * B) continue;
               const int b2 = reln >> 1;
               if (b2 > b) continue;  // lower triangle (only the diagonal block has any)
-              const double gv = 65536.0 * (double)pv[2 * i + 1] +
-                                256.0 * ((double)pv[2 * i] + (double)v[2 * i + 1]) +
-                                (double)v[2 * i];
-              const double C2 = (double)crow[b2] * p.ginv;
-              const double d2 = (double)drow[b2];
-              const double S2 = (double)us[(off >> 1) + b2];
+              const uint32_t hh = hi ? v[2 * i + 1] : pv[2 * i + 1];
+              const uint32_t hl = hi ? v[2 * i] : pv[2 * i];
+              const uint32_t lh = hi ? pv[2 * i + 1] : v[2 * i + 1];
+              const uint32_t ll = hi ? pv[2 * i] : v[2 * i];
+              // exact integer G entry (< 2^48) to f64 through the 2^52 exponent trick
+              const uint64_t gi = ((uint64_t)hh << 16) + (((uint64_t)hl + lh) << 8) + ll;
+              const double gv =
+                  __hiloint2double(0x43300000 | (int)(gi >> 32), (int)(uint32_t)gi) -
+                  4503599627370496.0;
+              const double C2 = bandC[b2], d2 = bandD[b2], S2 = bandS[b2];
               const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
               part[(size_t)b * B + b2] += Cb * C2 * xx;
             }
@@ -250,14 +281,13 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         }
       }
       if (p.first_pass) {  // band sums: sum x = C_b (m_b - L d_b)
-        for (int b = te; b < B; b += 128) {
-          const double Cb = (double)crow[b] * p.ginv, db = (double)drow[b];
-          part[(size_t)B * B + b] += Cb * ((double)us[(off >> 1) + b] - Lu * db);
-        }
+        for (int b = te; b < B; b += 128)
+          part[(size_t)B * B + b] += bandC[b] * (bandS[b] - Lu * bandD[b]);
         nsum += Lu;
       }
       tc_fence_before();
       mbar_arrive(acc_empty);
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // band terms reused by the next unit
     }
     if (p.first_pass && tid == 0) part[(size_t)B * B + B] = nsum;
   }
@@ -294,8 +324,10 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
   p.na = raww_atoms(bands);
   SKYRX_REQUIRE(p.na <= kMaxAtoms, "wide raw-byte moments support windows <= 640 bytes");
   p.nw16 = 64 * p.na;
+  // long units: the epilogue (integer blocks -> calibrated f64) is not overlapped with the
+  // tensor core (the pass's blocks fill TMEM), so fewer, longer units (>= 4 per SM)
   int64_t nsplit = (lines + 16383) / 16384;
-  while ((int64_t)samples * nsplit < 8 * kSMs && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
+  while ((int64_t)samples * nsplit < 4 * kSMs && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
   p.split_lines = (lines + nsplit - 1) / nsplit;
   p.split_lines = (p.split_lines + kLb - 1) / kLb * kLb;
   nsplit = (lines + p.split_lines - 1) / p.split_lines;
@@ -309,6 +341,7 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
                     cudaSuccess,
                 "cudaMallocAsync failed");
   p.usum = usum;
+  cudaMemsetAsync(usum, 0, (size_t)p.units * p.nw16 * sizeof(uint32_t), st);
   raww_scan_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, dark, usum, flags);
   SKYRX_CHECK_LAUNCH("raww_scan_kernel");
   // 2-D byte view of the cube, 128-byte x 128-line swizzled boxes
@@ -323,17 +356,50 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  const size_t smem = kStages * (size_t)p.na * kAtom + 16 * 8 + 1024;
-  cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // lower-triangle blocks (row atom >= column atom), four per pass; the first block
-  // of pass 0 is the diagonal (0, 0)
-  int br[32], bc[32], nb = 0;
-  for (int a = 0; a < p.na; ++a)
-    for (int c = 0; c <= a; ++c) br[nb] = a, bc[nb] = c, ++nb;
-  for (int b0 = 0; b0 < nb; b0 += 4) {
-    p.nblk = nb - b0 < 4 ? nb - b0 : 4;
-    for (int i = 0; i < p.nblk; ++i) p.blk_r[i] = br[b0 + i], p.blk_c[i] = bc[b0 + i];
-    p.first_pass = b0 == 0;
+  // lower-triangle blocks (row atom >= column atom), at most four per pass (TMEM), grouped so
+  // each pass touches few atoms: a pass streams only the atoms its blocks use (B = 270:
+  // 4 passes x 3 of the 5 atoms instead of 4 x 5)
+  static const int8_t plan3[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {-1, -1}},
+                                       {{2, 0}, {2, 1}, {2, 2}, {-1, -1}}};
+  static const int8_t plan4[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
+                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
+                                       {{3, 0}, {3, 3}, {-1, -1}, {-1, -1}}};
+  static const int8_t plan5[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
+                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
+                                       {{3, 0}, {3, 3}, {4, 0}, {4, 3}},
+                                       {{4, 1}, {4, 2}, {4, 4}, {-1, -1}}};
+  int8_t gen[16][4][2];
+  const int8_t(*plan)[4][2] = nullptr;
+  int npass = 0;
+  if (p.na == 3) plan = plan3, npass = 2;
+  else if (p.na == 4) plan = plan4, npass = 3;
+  else if (p.na == 5) plan = plan5, npass = 4;
+  else {  // one or two atoms: every block in one pass
+    int nb = 0;
+    for (int a = 0; a < p.na; ++a)
+      for (int c = 0; c <= a; ++c) gen[0][nb][0] = (int8_t)a, gen[0][nb][1] = (int8_t)c, ++nb;
+    for (; nb < 4; ++nb) gen[0][nb][0] = gen[0][nb][1] = -1;
+    plan = gen, npass = 1;
+  }
+  for (int ps = 0; ps < npass; ++ps) {
+    p.nblk = 0;
+    p.natom = 0;
+    auto slot = [&](int atom) {
+      for (int i = 0; i < p.natom; ++i)
+        if (p.atom_id[i] == atom) return i;
+      p.atom_id[p.natom] = atom;
+      return p.natom++;
+    };
+    for (int i = 0; i < 4 && plan[ps][i][0] >= 0; ++i) {
+      p.blk_r[i] = plan[ps][i][0], p.blk_c[i] = plan[ps][i][1];
+      p.blk_rs[i] = slot(p.blk_r[i]), p.blk_cs[i] = slot(p.blk_c[i]);
+      ++p.nblk;
+    }
+    const size_t stage = (size_t)p.natom * kAtom;
+    p.nstages = (int)std::min<size_t>(kMaxStages, (kSmemMax - 12288) / stage);
+    const size_t smem = p.nstages * stage + 16 * 8 + 3 * (size_t)bands * 8 + 1024;
+    p.first_pass = ps == 0;
+    cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     raww_gram_kernel<<<grid, kThreads, smem, st>>>(map, p);
     SKYRX_CHECK_LAUNCH("raww_gram_kernel");
   }
