@@ -268,16 +268,18 @@ __global__ void fold_kernel(double* __restrict__ state, const double* __restrict
 }
 
 // ------------------------------------------------------------------ K3
-constexpr int kFinThreads = 1024;
+constexpr int kFinThreads = 512;
 // -DSKYRX_FIN_PROFILE: clock64 at the phase boundaries of matrix 0 (skyrx_fin_profile)
 #ifdef SKYRX_FIN_PROFILE
 __device__ long long fin_prof[8];
+__device__ long long fin_acc[4];
 #define FIN_T(k)                                                    \
   do {                                                              \
     __syncthreads();                                                \
     if (blockIdx.x == 0 && threadIdx.x == 0) fin_prof[k] = clock64(); \
   } while (0)
 extern "C" __attribute__((visibility("default"))) int skyrx_fin_profile(long long* out) {
+  cudaMemcpyFromSymbol(out + 8, fin_acc, sizeof(fin_acc));
   return (int)cudaMemcpyFromSymbol(out, fin_prof, sizeof(fin_prof));
 }
 #else
@@ -354,8 +356,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
     mhl[b] = hi;
     mhl[B + b] = (float)(mb - (double)hi);
   }
-  for (size_t e = tid; e < BB; e += NT) {
-    const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
+  // (row, column) loops: a warp per row, lanes along it (no 64-bit index divisions)
+  const int nwarp = NT >> 5, wrp = tid >> 5, lan = tid & 31;
+  for (int i = wrp; i < B; i += nwarp)
+    for (int j = lan; j < B; j += 32) {
+    const size_t e = (size_t)i * B + j;
     const double vij = (q[(size_t)i * B + j] - s[i] * s[j] / n) / (n - 1.0);
     const double vji = (q[(size_t)j * B + i] - s[j] * s[i] / n) / (n - 1.0);
     sigma[e] = (vij + vji) / 2.0;
@@ -379,11 +384,125 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   bool ok = false;
   for (int a = 0; a < 6 && !ok; ++a) {
     ridge = eps_tab[a] * scale;
-    for (size_t e = tid; e < BB; e += NT) {
-      const int i = (int)(e / B), j = (int)(e - (size_t)i * B);
-      A[i * la + j] = (j <= i) ? sigma[e] + (i == j ? ridge : 0.0) : 0.0;
-    }
+    for (int i = wrp; i < B; i += nwarp)
+      for (int j = lan; j < B; j += 32)
+        A[(size_t)i * la + j] = (j <= i) ? sigma[(size_t)i * B + j] + (i == j ? ridge : 0.0) : 0.0;
     if (tid == 0) s_fail = 0;
+    if (A == chol) {  // ---- wide B: the factor lives in global memory (L2): blocked
+      // Panels of NBP columns in shared memory (column-major P[jj * B + row]); the panel is
+      // factored there and the trailing matrix gets the panel's NBP updates per element in
+      // one read-modify-write, applied in the same order, with the same rounded l values
+      // and FMA-free operations as the unblocked loop below: bit-identical factors, a
+      // fraction of the L2 traffic of one column at a time.
+      double* P = fsm + 2 * B;
+      const int NBP = B <= 750 ? 32 : 16;
+      __syncthreads();
+      for (int p0 = 0; p0 < B && !s_fail; p0 += NBP) {
+        const int nb = min(NBP, B - p0), rows = B - p0;
+        for (int e = tid; e < nb * rows; e += NT) {
+          const int jj = e / rows, r = p0 + (e - jj * rows);
+          P[jj * B + r] = (r >= p0 + jj) ? A[(size_t)r * B + p0 + jj] : 0.0;
+        }
+        __syncthreads();
+#ifdef SKYRX_FIN_PROFILE
+        const long long pt0 = clock64();
+#endif
+        // the panel: a thread per row r, one barrier per column; the owner of row j+1 takes
+        // the next pivot right after its update (lookahead), column jj is scaled one step
+        // later (when nobody reads it any more)
+        auto piv = [&](int j, double v) {
+          if (!(v > 0.0)) {
+            s_fail = 1;
+            return;
+          }
+          const double l = sqrt(v);
+          dg[j] = l, dg[B + j] = 1.0 / l;
+        };
+        if (tid == 0) piv(p0, P[p0]);
+        __syncthreads();
+        const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
+        for (int jj = 0; jj < nb; ++jj) {
+          if (s_fail) break;  // uniform: set before the previous barrier
+          const int j = p0 + jj;
+          const double rl = dg[B + j];
+          if (jj > 0)  // delayed scaling of column jj-1 (rows >= j)
+            for (int r = j + tid; r < B; r += NT) P[(jj - 1) * B + r] *= dg[B + j - 1];
+          // a warp per panel column jj2 > jj, lanes along the rows r >= p0 + jj2; each lane
+          // loads up to 8 of its rows before it stores any
+          for (int jj2 = jj + 1 + wid; jj2 < nb; jj2 += nw) {
+            const double lkj = P[jj * B + p0 + jj2] * rl;
+            double* Pc = P + jj2 * B;
+            const double* Pj = P + jj * B;
+            for (int r0 = p0 + jj2 + ln; r0 < B; r0 += 256) {
+              double x[8], y[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int r = r0 + 32 * q;
+                if (r < B) x[q] = Pc[r], y[q] = Pj[r];
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int r = r0 + 32 * q;
+                if (r < B) {
+                  const double v = __dsub_rn(x[q], __dmul_rn(y[q] * rl, lkj));
+                  Pc[r] = v;
+                  if (jj2 == jj + 1 && r == j + 1) piv(r, v);  // the next pivot
+                }
+              }
+            }
+          }
+          __syncthreads();
+        }
+        if (!s_fail) {
+          for (int r = p0 + nb - 1 + tid; r < B; r += NT)  // the last column's scaling
+            if (r > p0 + nb - 1) P[(nb - 1) * B + r] *= dg[B + p0 + nb - 1];
+          for (int jj = tid; jj < nb; jj += NT) P[jj * B + p0 + jj] = dg[p0 + jj];
+        }
+        __syncthreads();
+        if (s_fail) break;
+        for (int e = tid; e < nb * rows; e += NT) {  // the finished panel of L
+          const int jj = e / rows, r = p0 + (e - jj * rows);
+          if (r >= p0 + jj) A[(size_t)r * B + p0 + jj] = P[jj * B + r];
+        }
+#ifdef SKYRX_FIN_PROFILE
+        __syncthreads();
+        const long long pt1 = clock64();
+        if (tid == 0 && blockIdx.x == 0) fin_acc[0] += pt1 - pt0;
+#endif
+        // trailing update: a warp per row i, lanes along k <= i, the nb updates in order
+        const int q0 = p0 + nb;
+        for (int i = q0 + wid; i < B; i += nw)
+          for (int k0 = q0 + ln; k0 <= i; k0 += 128) {  // 4 independent chains per lane
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int k = k0 + 32 * q;
+              v[q] = k <= i ? A[(size_t)i * B + k] : 0.0;
+            }
+            for (int jj = 0; jj < nb; ++jj) {
+              const double lij = P[jj * B + i];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int k = min(k0 + 32 * q, i);
+                v[q] = __dsub_rn(v[q], __dmul_rn(lij, P[jj * B + k]));
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int k = k0 + 32 * q;
+              if (k <= i) A[(size_t)i * B + k] = v[q];
+            }
+          }
+        __syncthreads();
+#ifdef SKYRX_FIN_PROFILE
+        if (tid == 0 && blockIdx.x == 0) fin_acc[1] += clock64() - pt1;
+#endif
+      }
+      __syncthreads();
+      ok = (s_fail == 0);
+      __syncthreads();
+      continue;
+    }
     // right-looking Cholesky, lower triangle, ONE barrier per column: the trailing update
     // uses l_ij = a_ij / l_jj on the fly (FMA-free, so an exactly rank-deficient input
     // still meets an exactly zero pivot and fails like LAPACK potrf), and column j is
@@ -456,7 +575,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   }
   FIN_T(2);
   if (A != chol)
-    for (size_t e = tid; e < BB; e += NT) chol[e] = A[(e / B) * la + e % B];
+    for (int i = wrp; i < B; i += nwarp)
+      for (int j = lan; j < B; j += 32) chol[(size_t)i * B + j] = A[(size_t)i * la + j];
   __syncthreads();
   if (!do_inverse) {  // wide matrices: W, Sigma^-1 and wf by the multi-CTA kernels below
     if (tid == 0) {
@@ -470,10 +590,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   // in place one step later) and every later row has subtracted l_ij * W_j; one barrier per
   // row, the (i, c) updates of a step spread over the whole CTA
   double* Wm = (A != chol && B <= kSmemInvMaxB) ? A + (size_t)B * la : w64;
-  for (size_t e = tid; e < BB; e += NT) {
-    const int i = (int)(e / B), c = (int)(e - (size_t)i * B);
-    Wm[e] = (i == c) ? 1.0 : 0.0;
-  }
+  for (int i = wrp; i < B; i += nwarp)
+    for (int c = lan; c < B; c += 32) Wm[i * B + c] = (i == c) ? 1.0 : 0.0;
   __syncthreads();
   {
     const int nw = NT >> 5, wid = tid >> 5, ln = tid & 31;
@@ -734,8 +852,9 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   const size_t sm = 2 * (size_t)bands * sizeof(double) +
                     (bands <= kSmemInvMaxB ? ((size_t)bands * (bands | 1) + (size_t)bands * bands) *
                                                  sizeof(double)
-                     : bands <= kSmemCholMaxB ? (size_t)bands * (bands | 1) * sizeof(double)
-                                              : 0);
+                     : bands <= kSmemCholMaxB
+                         ? (size_t)bands * (bands | 1) * sizeof(double)
+                         : (size_t)(bands <= 750 ? 32 : 16) * bands * sizeof(double));  // panel
   const bool wide = bands > kSmemInvMaxB;
   cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -27,9 +27,10 @@ plan.run(0, raw, d, c, g, gain_const=1.0)
 for _ in range(3):
     plan.ds.finalize()
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * 8)()
+buf = (ctypes.c_longlong * 12)()
 lib.skyrx_fin_profile(buf)
 t = np.array(buf[:7], dtype=np.float64)
 names = ['moments+sigma+trace', 'cholesky', 'W=L^-1', 'copy W', 'sigma_inv', 'wf']
-print({n: int(t[i + 1] - t[i]) for i, n in enumerate(names)}, 'total cycles', int(t[6] - t[0]))
+print({n: int(t[i + 1] - t[i]) for i, n in enumerate(names)}, 'total cycles', int(t[6] - t[0]),
+      'wide blocked: panel / trailing cycles (all calls)', buf[8], buf[9])
 PY
