@@ -249,6 +249,16 @@ int skyrx_topk_pick(int32_t digit, void* workspace, float* thr, void* stream);
 uint32_t* skyrx_topk_histogram(void* workspace);
 int32_t skyrx_topk_hist_len(void);
 
+/* R-TOPK threshold AND mask in one pass over the scores (single rank): after
+ * skyrx_topk_init(n, k, ws) and — if hist0_done — the digit-0 histogram fused
+ * into a score kernel (topk_hist0 = skyrx_topk_histogram(ws)), writes
+ * thr = the (k+1)-th largest value and mask = v > thr, identical to
+ * skyrx_topk_threshold + skyrx_mask_gt.  cand: cand_cap 8-byte slots for the
+ * values inside the threshold's top-11-bit bin (overflow or n >= 2^32 falls
+ * back to a rescan, still exact).  v 16-B aligned, mask 4-B aligned. */
+int skyrx_topk_mask(const float* v, int64_t n, int32_t hist0_done, float* thr, uint8_t* mask,
+                    void* workspace, void* cand, int64_t cand_cap, void* stream);
+
 /* ---------------------------------------------------------------- link payload (next to the path)
  * datalink.py:141-177: per pixel [RGB565 | half(sqrt(score / max))] little-endian u16
  * words.  skyrx_link_maxima: keys[0..3] = order-preserving u32 keys of the cube's max

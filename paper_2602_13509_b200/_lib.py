@@ -73,6 +73,7 @@ SIGNATURES = {
     "skyrx_topk_pick": (C.c_int, [i32, vp, vp, vp]),
     "skyrx_topk_histogram": (vp, [vp]),
     "skyrx_topk_hist_len": (i32, []),
+    "skyrx_topk_mask": (C.c_int, [vp, i64, i32, vp, vp, vp, vp, i64, vp]),
     "skyrx_link_maxima": (C.c_int, [vp, vp, i64, vp, vp]),
     "skyrx_link_payload": (C.c_int, [vp, vp, i64, vp, C.POINTER(f64), vp, vp]),
     "skyrx_link_packets": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, vp]),

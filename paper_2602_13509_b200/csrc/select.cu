@@ -15,9 +15,10 @@ namespace skyrx {
 constexpr int kHistBins = 2048;
 struct TopkState {
   uint32_t prefix;   // key bits selected so far
-  uint32_t pad;
+  uint32_t ncand;    // skyrx_topk_mask: candidates appended by the mask pass
   uint64_t rank;     // 1-based rank (from the top) still to find inside the prefix
   uint32_t all;      // 1 -> k >= n: select everything
+  uint32_t done;     // skyrx_topk_mask: CTAs of the mask pass that finished
 };
 
 __global__ void max_kernel(const float* __restrict__ v, int64_t n, uint32_t* __restrict__ out) {
@@ -91,6 +92,8 @@ __global__ void topk_init_kernel(int64_t n, int64_t k, TopkState* st, uint32_t* 
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist[i] = 0;
   if (threadIdx.x == 0) {
     st->prefix = 0;
+    st->ncand = 0;
+    st->done = 0;
     st->rank = (uint64_t)k + 1;
     st->all = (k >= n) ? 1u : 0u;
   }
@@ -174,6 +177,214 @@ __global__ void __launch_bounds__(256) topk_pick_kernel(int digit, TopkState* st
   for (int i = t; i < kHistBins; i += blockDim.x) hist[i] = 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// One-pass select + mask (skyrx_topk_mask).  After the digit-0 histogram (fused
+// into the score kernel, or one topk_hist pass) every CTA of the mask pass
+// picks the digit-0 bin itself (the same suffix scan as topk_pick_kernel, on
+// read-only bins), then streams the scores once: keys above the bin are in the
+// mask, keys below are not, keys inside it are written 0 and appended as
+// (index, key) candidates.  One CTA then finishes digits 1 and 2 on the
+// candidates only and sets the mask bytes of those above the threshold.  The
+// threshold and mask are the ones the 3 x (hist + pick) + mask_gt sequence
+// gives (same bins, same picks); it just reads the scores once instead of three
+// times and launches twice instead of six times.
+
+// block-wide (NT threads) pick over nb = 2^bits bins from the top: the bin that
+// holds `rank` and the count above it
+template <int NT>
+__device__ __forceinline__ void pick_bin(const uint32_t* hist, int bits, uint64_t rank,
+                                         int& bin_out, uint64_t& cum_out, uint64_t* wsum,
+                                         int* sbin, uint64_t* scum) {
+  const int nb = 1 << bits;
+  const int per = nb / NT;
+  const int t = threadIdx.x;
+  const int hi = nb - per * t;
+  uint32_t c[8];
+  uint64_t mine = 0;
+  for (int q = 0; q < per; ++q) c[q] = hist[hi - 1 - q], mine += c[q];
+  uint64_t incl = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += v;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  if (t == 0) *sbin = 0, *scum = 0;
+  __syncthreads();
+  uint64_t before = incl - mine;
+  for (int w = 0; w < (t >> 5); ++w) before += wsum[w];
+  if (before < rank && before + mine >= rank) {
+    uint64_t cum = before;
+    int q = 0;
+    for (; q < per - 1; ++q) {
+      if (cum + c[q] >= rank) break;
+      cum += c[q];
+    }
+    *sbin = hi - 1 - q;
+    *scum = cum;
+  }
+  __syncthreads();
+  bin_out = *sbin;
+  cum_out = *scum;
+  __syncthreads();
+}
+
+// digits 1 and 2 over the candidates (or, if they overflowed the buffer, over
+// every score inside the digit-0 bin), the threshold, and the mask bytes of the
+// candidates above it; leaves the workspace as topk_pick(2) does.  Block-wide.
+template <int NT>
+__device__ void topk_mask_finish(const float* __restrict__ v, int64_t n, TopkState* st,
+                                 uint32_t* hist, uint8_t* mask, const uint2* cand, uint32_t cap,
+                                 float* thr, uint32_t* sh, uint64_t* wsum, int* sbin,
+                                 uint64_t* scum) {
+  const int t = threadIdx.x;
+  int bin;
+  uint64_t cum;
+  uint64_t rank = st->rank;
+  pick_bin<NT>(hist, 11, rank, bin, cum, wsum, sbin, scum);
+  rank -= cum;
+  uint32_t prefix = (uint32_t)bin;
+  const uint32_t nc = __ldcg(&st->ncand);
+  const bool over = nc > cap;
+  for (int digit = 1; digit < 3; ++digit) {
+    const int shift = digit == 1 ? 10 : 0, bits = digit == 1 ? 11 : 10;
+    const int hs = shift + bits;
+    const uint32_t dm = (1u << bits) - 1u;
+    for (int i = t; i < kHistBins; i += NT) sh[i] = 0;
+    __syncthreads();
+    if (!over) {
+      // four independent loads in flight per thread (the loop is latency-bound)
+      for (uint32_t j0 = t; j0 < nc; j0 += 4 * NT) {
+        uint32_t key[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t j = j0 + u * NT;
+          key[u] = j < nc ? __ldcg(&cand[j].y) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + u * NT < nc && (key[u] >> hs) == prefix)
+            atomicAdd(&sh[(key[u] >> shift) & dm], 1u);
+      }
+    } else {
+      for (int64_t j = t; j < n; j += NT) {
+        const uint32_t key = f2ord(v[j]);
+        if ((key >> hs) == prefix) atomicAdd(&sh[(key >> shift) & dm], 1u);
+      }
+    }
+    __syncthreads();
+    pick_bin<NT>(sh, bits, rank, bin, cum, wsum, sbin, scum);
+    rank -= cum;
+    prefix = (prefix << bits) | (uint32_t)bin;
+  }
+  const float tv = ord2f(prefix);
+  const uint32_t b0 = prefix >> 21;
+  if (!over) {
+    for (uint32_t j0 = t; j0 < nc; j0 += 4 * NT) {
+      uint2 c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * NT;
+        c[u] = j < nc ? __ldcg(&cand[j]) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u * NT < nc && ord2f(c[u].y) > tv) mask[c[u].x] = 1;
+    }
+  } else {
+    for (int64_t j = t; j < n; j += NT) {
+      const float x = v[j];
+      if ((f2ord(x) >> 21) == b0 && x > tv) mask[j] = 1;
+    }
+  }
+  for (int i = t; i < kHistBins; i += NT) hist[i] = 0;
+  if (t == 0) {
+    st->rank = rank;
+    st->prefix = prefix;
+    st->done = 0;
+    *thr = tv;
+  }
+}
+
+constexpr int kMaskThreads = 512;
+__global__ void __launch_bounds__(kMaskThreads) topk_mask_pass_kernel(
+    const float* __restrict__ v, int64_t n, TopkState* st, uint32_t* hist,
+    uint8_t* __restrict__ mask, uint2* __restrict__ cand, uint32_t cap, float* thr) {
+  __shared__ uint32_t sh[kHistBins];
+  __shared__ uint64_t wsum[kMaskThreads / 32];
+  __shared__ int sbin;
+  __shared__ uint64_t scum;
+  __shared__ int last;
+  const bool all = st->all != 0;
+  int bin = 0;
+  uint64_t cum = 0;
+  if (!all) pick_bin<kMaskThreads>(hist, 11, st->rank, bin, cum, wsum, &sbin, &scum);
+  const uint32_t b0 = (uint32_t)bin;
+  const int lane = threadIdx.x & 31;
+  const int64_t n4 = n / 4;
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  uint32_t* m4 = reinterpret_cast<uint32_t*>(mask);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // every thread of a warp runs the same number of iterations (ballots below)
+  const int64_t iters = (n4 + stride - 1) / stride;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool ok = i < n4;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) x = __ldcs(v4 + i);
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t key = f2ord(xv[q]);
+      const uint32_t d0 = key >> 21;
+      bool in = false;
+      if (all) {
+        word |= (uint32_t)(xv[q] > -INFINITY) << (8 * q);
+      } else {
+        word |= (uint32_t)(d0 > b0) << (8 * q);
+        in = ok && d0 == b0;
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, in);
+      if (bal) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&st->ncand, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (in && slot < cap) cand[slot] = make_uint2((uint32_t)(4 * i + q), key);
+      }
+    }
+    if (ok) m4[i] = word;
+  }
+  // the n % 4 tail (block 0)
+  if (blockIdx.x == 0) {
+    for (int64_t i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t key = f2ord(v[i]);
+      if (all) {
+        mask[i] = v[i] > -INFINITY;
+      } else {
+        mask[i] = (key >> 21) > b0;
+        if ((key >> 21) == b0) {
+          const uint32_t slot = atomicAdd(&st->ncand, 1u);
+          if (slot < cap) cand[slot] = make_uint2((uint32_t)i, key);
+        }
+      }
+    }
+  }
+  // the last CTA to finish runs digits 1 and 2 on the candidates
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (all) {
+    if (threadIdx.x == 0) *thr = -INFINITY, st->done = 0;
+    return;
+  }
+  topk_mask_finish<kMaskThreads>(v, n, st, hist, mask, cand, cap, thr, sh, wsum, &sbin, &scum);
+}
+
 static int grid_n(int64_t n, int threads, int per_sm) {
   int64_t b = ceil_div<int64_t>(n, threads);
   const int64_t cap = (int64_t)kSMs * per_sm;
@@ -207,6 +418,8 @@ extern "C" int skyrx_threshold(const float* v, int64_t n, float t, uint8_t* mask
   SKYRX_CHECK_LAUNCH("skyrx_threshold");
   return SKYRX_OK;
 }
+
+static_assert(sizeof(TopkState) <= 32, "the histogram starts 32 bytes into the workspace");
 
 extern "C" size_t skyrx_topk_workspace(void) {
   return sizeof(TopkState) + 16 + kHistBins * sizeof(uint32_t);
@@ -255,6 +468,29 @@ extern "C" int skyrx_topk_pick(int32_t digit, void* workspace, float* thr, void*
   topk_pick_kernel<<<1, 256, 0, as_stream(stream)>>>(
       digit, reinterpret_cast<TopkState*>(workspace), skyrx_topk_histogram(workspace), thr);
   SKYRX_CHECK_LAUNCH("skyrx_topk_pick");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_topk_mask(const float* v, int64_t n, int32_t hist0_done, float* thr,
+                               uint8_t* mask, void* workspace, void* cand, int64_t cand_cap,
+                               void* stream) {
+  SKYRX_REQUIRE(n >= 0 && cand_cap >= 0, "bad top-k mask arguments n=%lld cap=%lld",
+                (long long)n, (long long)cand_cap);
+  SKYRX_REQUIRE(((uintptr_t)v % 16) == 0 && ((uintptr_t)mask % 4) == 0 &&
+                    ((uintptr_t)cand % 8) == 0,
+                "skyrx_topk_mask: scores 16-B, mask 4-B and candidates 8-B aligned");
+  cudaStream_t st = as_stream(stream);
+  TopkState* state = reinterpret_cast<TopkState*>(workspace);
+  uint32_t* hist = skyrx_topk_histogram(workspace);
+  // candidate indices are 32-bit: larger inputs take the in-bin rescan
+  const uint32_t cap = n < (int64_t)0xFFFFFFFFu
+                           ? (uint32_t)(cand_cap < (int64_t)0xFFFFFFFFu ? cand_cap : 0xFFFFFFFEu)
+                           : 0u;
+  if (n > 0 && !hist0_done)
+    topk_hist_kernel<<<grid_n(n, 512, 4), 512, 0, st>>>(v, n, 0, state, hist);
+  topk_mask_pass_kernel<<<grid_n(n / 4 + 1, kMaskThreads, 4), kMaskThreads, 0, st>>>(
+      v, n, state, hist, mask, reinterpret_cast<uint2*>(cand), cap, thr);
+  SKYRX_CHECK_LAUNCH("skyrx_topk_mask");
   return SKYRX_OK;
 }
 

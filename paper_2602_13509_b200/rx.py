@@ -262,6 +262,13 @@ def transmit_domain(values, max_score: float):
 
 
 # --------------------------------------------------------------------------- R-TOPK
+def topk_cand_cap(n: int) -> int:
+    """Candidate slots of skyrx_topk_mask: the top-11-bit bin holding the
+    threshold rarely holds more than a few k values; beyond this the kernel
+    rescans (exact, slower)."""
+    return n // 64 + 4096
+
+
 def topk_count(n: int) -> int:
     """k = ceil(0.001 * N) in integers (SURVEY.md §8(a) R-TOPK)."""
     return (n + 999) // 1000
@@ -275,14 +282,27 @@ def topk_threshold_device(v: torch.Tensor, k: int) -> torch.Tensor:
     return thr
 
 
+def topk_mask_device(v: torch.Tensor, k: int, cand_cap: int | None = None):
+    """(mask u8, thr) of R-TOPK on device scores in one mask pass
+    (skyrx_topk_mask); ``cand_cap`` overrides the candidate slots (tests)."""
+    n = v.numel()
+    cap = topk_cand_cap(n) if cand_cap is None else int(cand_cap)
+    ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,), torch.int32)
+    cand = _dev.empty((2 * max(cap, 1),), torch.int32)
+    thr = _dev.empty((1,), torch.float32)
+    mask = _dev.empty(tuple(v.shape), torch.uint8)
+    s = _dev.stream_ptr()
+    _lib.call("skyrx_topk_init", n, k, ws.data_ptr(), s)
+    _lib.call("skyrx_topk_mask", v.data_ptr(), n, 0, thr.data_ptr(), mask.data_ptr(),
+              ws.data_ptr(), cand.data_ptr(), cap, s)
+    return mask, thr
+
+
 def topk_mask(scores, k: int | None = None):
     """R-TOPK: mask = delta > delta_(k+1), the top ceil(0.1%) of raw f32 scores."""
-    v = _scores_device(scores)
+    v = _scores_device(scores).contiguous()
     k = topk_count(v.numel()) if k is None else int(k)
-    thr = topk_threshold_device(v, k)
-    mask = _dev.empty(tuple(v.shape), torch.uint8)
-    _lib.call("skyrx_mask_gt", v.data_ptr(), v.numel(), thr.data_ptr(), mask.data_ptr(),
-              _dev.stream_ptr())
+    mask, _ = topk_mask_device(v, k)
     src = scores.values if hasattr(scores, "values") else scores
     return _dev.like_input(src, mask.to(torch.bool))
 
@@ -315,6 +335,9 @@ class DetectPlan:
         self.thr = _dev.empty((batch,), torch.float32)
         self.topk_ws = _dev.empty((int(_lib.load().skyrx_topk_workspace()) // 4 + 4,),
                                   torch.int32)
+        # (index, key) slots for the scores inside the threshold's top digit bin
+        self.cand_cap = topk_cand_cap(lines * samples)
+        self.cand = _dev.empty((2 * self.cand_cap,), torch.int32)
         self.launches = 0
         # per slot: every line gain is exactly 1 (set by run(); lets the score
         # kernel drop the per-line gain from its transform)
@@ -455,17 +478,15 @@ class DetectPlan:
         s = _dev.stream_ptr()
         ws = self.topk_ws.data_ptr()
         # R-TOPK as init -> (digit-0 histogram fused into the score kernel) ->
-        # pick 0 -> hist 1 -> pick 1 -> hist 2 -> pick 2
+        # one mask pass (digit-0 pick per CTA, in-bin candidates appended) ->
+        # digits 1 and 2 on the candidates
         _lib.call("skyrx_topk_init", n, k, ws, s)
         fused = self.score_only(i, raw, dark, coeff, gains, events, topk_hist0=True)
         sc = self.scores[i]
         thr = self.thr[i:i + 1].data_ptr()
-        for digit in range(3):
-            if digit > 0 or not fused:
-                _lib.call("skyrx_topk_hist", sc.data_ptr(), n, digit, ws, s)
-            _lib.call("skyrx_topk_pick", digit, ws, thr, s)
-        _lib.call("skyrx_mask_gt", sc.data_ptr(), n, thr, self.mask[i].data_ptr(), s)
-        self.launches += 1 + (5 if fused else 6) + 1
+        _lib.call("skyrx_topk_mask", sc.data_ptr(), n, int(fused), thr, self.mask[i].data_ptr(),
+                  ws, self.cand.data_ptr(), self.cand_cap, s)
+        self.launches += 1 + (2 if fused else 3)
         return self
 
     def score_only(self, i: int, raw: torch.Tensor, dark, coeff, gains, events=None,

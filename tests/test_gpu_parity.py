@@ -295,6 +295,23 @@ class TestTopK:
         v = np.full(5000, 3.0, np.float32)
         assert not P.topk_mask(v).any()
 
+    @pytest.mark.parametrize("n,cap", [(100_003, 0), (100_003, 7), (1_843_201, None),
+                                       (4099, None), (3, None)])
+    def test_one_pass_mask_equals_threshold_then_mask(self, P, rng, n, cap):
+        """skyrx_topk_mask (candidates, or the in-bin rescan when they overflow
+        the slots) == skyrx_topk_threshold + skyrx_mask_gt, threshold bits too."""
+        import torch
+        from paper_2602_13509_b200 import rx
+
+        v = (rng.standard_normal(n) ** 2 * 70).astype(np.float32)
+        v[rng.integers(0, n, n // 50)] = np.float32(91.25)   # a tie-heavy threshold bin
+        vt = torch.from_numpy(v).cuda()
+        k = rx.topk_count(n)
+        mask, thr = rx.topk_mask_device(vt, k, cap)
+        thr0 = rx.topk_threshold_device(vt, k)
+        assert bits(thr.cpu().numpy()) == bits(thr0.cpu().numpy())
+        assert np.array_equal(mask.cpu().numpy().astype(bool), O.topk_mask(v, k))
+
 
 # ----------------------------------------------------------------------------- the fused path
 def check_detection(det, raw, t, gains=None):
