@@ -234,7 +234,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
             const uint8_t* kb = base + ks * 4096;  // 32 lines = 4 swizzle atoms of 8 x 128 B
             const uint64_t d0 = smem_desc_sw128(kb, ATOM, 1024);
+#ifndef GRX_NO_M1  // ablation switches (tools/build_gr_var.sh), off in the product
             mma_i8(d, d0, d0, id, acc);
+#endif
             if (TWO_M) {
               // bytes 128.. in their own (narrower) swizzle: columns 128..NW-1 of rows
               // 0..127, and rows 128..NW-1 x columns 128..NW-1 (the rest is the
@@ -246,8 +248,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
               const uint64_t d1b =
                   ONES ? smem_desc_swz(b1, (uint32_t)(ones + ks * 32 * W2B - b1), 8 * W2B, LT1)
                        : d1;
+#ifndef GRX_NO_M23
               mma_i8(d + 128, d0, d1b, id2, acc);
               mma_i8(d + P1OFF, d1, d1b, id2, acc);
+#endif
             }
           }
           mma_commit(&empty[st]);
@@ -278,7 +282,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         const int st = t % kGrStages;
         if (tid == 0) GR_PW(3, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
         else mbar_wait(full32 + 8 * st, (t / kGrStages) & 1);
+#ifdef GRX_NO_SCAN
+        if (false) {
+#else
         if (scanner) {
+#endif
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
           const uint32_t atom = stages32 + st * STAGE + (box1 ? ATOM : 0u);
@@ -378,6 +386,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #pragma unroll
       for (int part = 0; part < (TWO_M ? 2 : 1); ++part) {
         if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
+#ifdef GRX_NO_EPI
+        continue;
+#endif
         const int m = 128 * part + te;
         const int rel = m - off;
         const bool in_band = rel >= 0 && rel < 2 * B;

@@ -220,8 +220,10 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
     tc_fence_after();
     const uint32_t roff = s * p.raw_stage_bytes + r * B * 2 + 16 * c_lo;
     const uint32_t thi = tl + as * KP;
+#ifndef SCX_NO_XFORM  // ablation switches (tools/build_sc_var.sh), off in the product
     transform_row<MODE, CHT>(raw_ring + roff, ring32 + roff, tco, tnof, nm0, g, thi,
                              thi + KP / 2, cnt);
+#endif
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
@@ -350,9 +352,13 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
           const uint64_t blo = smem_desc(wsm + W_BYTES + off_b, 128, SBO_B);
           const uint32_t idk = idesc_f16_f32(128, NP - 16 * ks, 0, 0);
           const uint32_t dk = d + 16 * ks;
+#ifndef SCX_NO_MMA
           mma_f16_ts(dk, ahi, bhi, idk, ks > 0);
+#ifndef SCX_ONE_PRODUCT
           mma_f16_ts(dk, ahi, blo, idk, 1);
           mma_f16_ts(dk, alo, bhi, idk, 1);
+#endif
+#endif
         }
         mma_commit(&a_empty[as]);
         mma_commit(&acc_full[acs]);
@@ -379,6 +385,9 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
       mbar_wait(acc_full32 + 8 * acs, cph);
       tc_fence_after();
       float2 acc = make_float2(0.0f, 0.0f);
+#ifdef SCX_NO_EPI
+      if (false)
+#endif
 #pragma unroll
       for (int c = 0; c < NCH; c += 2) {
         uint32_t v[16];

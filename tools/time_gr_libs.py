@@ -1,0 +1,27 @@
+"""Time the raw-byte moments call of one c4 strip with each library given
+(experiment variants of gram_raw: tools/gr_variant.sh builds them)."""
+import os, sys, json, subprocess
+libs = sys.argv[1:]
+if len(libs) > 1:
+    for l in libs:
+        subprocess.run([sys.executable, __file__, l])
+    sys.exit(0)
+import torch
+sys.path.insert(0, '.')
+from paper_2602_13509_b200 import _lib
+_lib.load(libs[0])
+import paper_2602_13509_b200 as P
+from paper_2602_13509_b200.synth import Scene
+L, S, B = 16384, 900, 70
+sc = Scene(4000, S, B, 5)
+raw = sc.generate(0, L)
+d, c = torch.from_numpy(sc.dark).cuda(), torch.from_numpy(sc.coeff).cuda()
+g = torch.ones(L, dtype=torch.float32, device='cuda')
+plan = P.DetectPlan(L, S, B)
+fn = lambda: plan.run(0, raw, d, c, g, gain_const=1.0)
+fn(); torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(10): fn()
+b.record(); torch.cuda.synchronize()
+print(json.dumps({"lib": libs[0], "stats_ms": a.elapsed_time(b) / 10}), flush=True)
