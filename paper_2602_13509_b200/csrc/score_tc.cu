@@ -42,8 +42,20 @@ __host__ __device__ constexpr int sc_maxreg(int kp) {
 constexpr int kTcEpilogue = 128;
 constexpr int kScoreRawStagesMax = 8;
 constexpr int kScoreAStages = 2;
-constexpr int kScoreAcc = 3;    // TMEM accumulator ring: columns [0, 3 KP)
+// NCAT: the two products that read D_hi run as ONE MMA against B = [W_hi | W_lo]
+// (N = 2 KP - 16 ks): each accumulator holds z_hi-part (columns [0, KP)) and the
+// D_hi W_lo part (columns [KP, 2 KP)), summed by the epilogue.  10 instead of 15
+// MMAs per tile: every tcgen05.mma re-reads its 4 KB A slice from TMEM, and those
+// reads bound the tensor side (profiles/r01_ablation.md).
+#ifndef SCX_NO_NCAT
+constexpr bool kScoreNcat = true;
+constexpr int kScoreAcc = 2;      // TMEM accumulator ring: columns [0, 2 * 2 KP)
+constexpr int kScoreABase = 320;  // A ring (f16 hi/lo, from the transform warps): [320, 320 + 2 KP)
+#else
+constexpr bool kScoreNcat = false;
+constexpr int kScoreAcc = 3;      // TMEM accumulator ring: columns [0, 3 KP)
 constexpr int kScoreABase = 256;  // A ring (f16 hi/lo, from the transform warps): [256, 256 + 2 KP)
+#endif
 constexpr int kScoreWmax = 128;
 constexpr int kTopkBins = 2048;  // digit 0 of the top-k radix select (select.cu)
 
@@ -249,7 +261,9 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
   constexpr uint32_t W_BYTES = NP * KP * 2u;
   constexpr uint32_t SBO_B = (KP / 8) * 128u;
   constexpr uint32_t TMEM_COLS = 512;
-  static_assert(kScoreAcc * NP <= kScoreABase, "accumulators below the A ring");
+  constexpr int AW = kScoreNcat ? 2 * NP : NP;  // TMEM columns per accumulator
+  static_assert(kScoreAcc * AW <= kScoreABase, "accumulators below the A ring");
+  static_assert(!kScoreNcat || 2 * NP <= 256, "N = 2 KP fits one MMA");
   static_assert(kScoreABase + kScoreAStages * KP <= 512, "A ring fits TMEM");
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.ts.B;
@@ -338,7 +352,7 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
         mbar_wait(&acc_empty[acs], cph ^ 1);
         tc_fence_after();
         const uint32_t abase = tmem + kScoreABase + as * KP;  // A from TMEM
-        const uint32_t d = tmem + acs * NP;
+        const uint32_t d = tmem + acs * AW;
         // W = L^-1 is lower triangular: k-step ks (k in [16ks, 16ks+16)) only feeds
         // outputs j >= 16ks, so its MMAs cover N = KP - 16ks columns from column 16ks
         // (40 % fewer tensor cycles at KP = 80); k-step 0 spans every column and
@@ -353,11 +367,18 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
           const uint32_t idk = idesc_f16_f32(128, NP - 16 * ks, 0, 0);
           const uint32_t dk = d + 16 * ks;
 #ifndef SCX_NO_MMA
-          mma_f16_ts(dk, ahi, bhi, idk, ks > 0);
+          if constexpr (kScoreNcat) {
+            // B rows: W_hi rows 16ks.. then (contiguous in shared memory) all of W_lo
+            (void)blo;
+            mma_f16_ts(dk, ahi, bhi, idesc_f16_f32(128, 2 * NP - 16 * ks, 0, 0), ks > 0);
+            mma_f16_ts(dk, alo, bhi, idk, 1);
+          } else {
+            mma_f16_ts(dk, ahi, bhi, idk, ks > 0);
 #ifndef SCX_ONE_PRODUCT
-          mma_f16_ts(dk, ahi, blo, idk, 1);
-          mma_f16_ts(dk, alo, bhi, idk, 1);
+            mma_f16_ts(dk, ahi, blo, idk, 1);
+            mma_f16_ts(dk, alo, bhi, idk, 1);
 #endif
+          }
 #endif
         }
         mma_commit(&a_empty[as]);
@@ -391,12 +412,24 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
 #pragma unroll
       for (int c = 0; c < NCH; c += 2) {
         uint32_t v[16];
-        tmem_ld16(tbase + acs * NP + c * 8, v);
-        tmem_ld_wait();
+        tmem_ld16(tbase + acs * AW + c * 8, v);
+        if constexpr (kScoreNcat) {
+          uint32_t w[16];
+          tmem_ld16(tbase + acs * AW + NP + c * 8, w);
+          tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          const float2 z = make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1]));
-          acc = ffma2(z, z, acc);
+          for (int q = 0; q < 16; q += 2) {
+            const float2 z = fadd2(make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])),
+                                   make_float2(__uint_as_float(w[q]), __uint_as_float(w[q + 1])));
+            acc = ffma2(z, z, acc);
+          }
+        } else {
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+            const float2 z = make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1]));
+            acc = ffma2(z, z, acc);
+          }
         }
       }
       tc_fence_before();

@@ -44,7 +44,20 @@ __host__ __device__ constexpr int threads(int kp) { return 128 * groups(kp) + 12
 __host__ __device__ constexpr int maxreg(int kp) {
   return (16384 / (32 * ((threads(kp) / 32 + 3) / 4))) / 8 * 8;
 }
-__host__ __device__ constexpr int nacc(int kp) { return 2 * kp + 3 * kp <= 512 ? 3 : 2; }
+// NCAT (KP <= 80): the two products of each A digit run as ONE MMA against
+// B = [V_hi | V_lo] (N = 2 KP - 16 ks), so a tile takes 2 instead of 4 MMAs per
+// k-step; every tcgen05.mma re-reads its 4 KB A slice from TMEM and those reads
+// bound the tensor side (profiles/r01_ablation.md).  An accumulator then holds
+// the V_hi part in columns [0, KP) and the V_lo part in [KP, 2 KP).
+#ifndef TCSX_NO_NCAT
+__host__ __device__ constexpr bool ncat(int kp) { return kp <= 80; }
+#else
+__host__ __device__ constexpr bool ncat(int kp) { return false; }
+#endif
+__host__ __device__ constexpr int accw(int kp) { return ncat(kp) ? 2 * kp : kp; }
+__host__ __device__ constexpr int nacc(int kp) {
+  return ncat(kp) ? 2 : (2 * kp + 3 * kp <= 512 ? 3 : 2);
+}
 
 // per-sample record: V hi | V lo (KP x KP f16, K-major canonical layout) | T (KP u16:
 // 4096 - R, 0 for padding bands) | q' (KP f32, = q / inv_scale) | inv_scale (f32)
@@ -121,10 +134,14 @@ __device__ __forceinline__ void transform_unit(const Params& p, int ntile, uint8
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = c4[OFFW + i];
       uint32_t hw[4], lw[4];
+#ifndef TCSX_NO_XFORM  // ablation switches (tools/build_tcs_var.sh), off in the product
       digits4(w, tt + 4 * cc, hw, lw, chk);
       const uint32_t col = tl + as * KP + 4 * (c_lo + cc);
       tmem_st4(col, hw[0], hw[1], hw[2], hw[3]);
       tmem_st4(col + KP / 2, lw[0], lw[1], lw[2], lw[3]);
+#else
+      chk |= w[0] & 0;
+#endif
       cur = nxt;
     }
     tmem_st_wait();
@@ -148,7 +165,9 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
   constexpr int NCH = KP / 8;
   constexpr int CHT = (NCH + NG - 1) / NG;
   constexpr int NACC = nacc(KP);
-  constexpr int ABASE = NACC * KP;       // A ring TMEM columns [ABASE, ABASE + 2 KP)
+  constexpr int AW = accw(KP);            // TMEM columns per accumulator
+  constexpr bool NC = ncat(KP);
+  constexpr int ABASE = NACC * AW;       // A ring TMEM columns [ABASE, ABASE + 2 KP)
   constexpr uint32_t VB = rec_vbytes(KP);
   constexpr uint32_t RB = rec_bytes(KP);
   constexpr uint32_t SBO_B = (KP / 8) * 128u;
@@ -231,7 +250,7 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
           mbar_wait(&acc_empty[acs], cph ^ 1);
           tc_fence_after();
           const uint32_t abase = tmem + ABASE + as * KP;
-          const uint32_t d = tmem + acs * KP;
+          const uint32_t d = tmem + acs * AW;
           // V lower triangular: k-step ks feeds outputs j >= 16 ks only
 #pragma unroll
           for (int ks = 0; ks < KP / 16; ++ks) {
@@ -241,10 +260,20 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
             const uint64_t blo = smem_desc(vl + ob, 128, SBO_B);
             const uint32_t id = idesc_f16_f32(128, KP - 16 * ks, 0, 0);
             const uint32_t dk = d + 16 * ks;
-            mma_f16_ts(dk, ahi, bhi, id, ks > 0);
-            mma_f16_ts(dk, ahi, blo, id, 1);
-            mma_f16_ts(dk, alo, bhi, id, 1);
-            mma_f16_ts(dk, alo, blo, id, 1);
+#ifndef TCSX_NO_MMA
+            if constexpr (NC) {
+              // B rows: V_hi rows 16ks.. then (contiguous in the record) all of V_lo
+              (void)blo;
+              const uint32_t idn = idesc_f16_f32(128, 2 * KP - 16 * ks, 0, 0);
+              mma_f16_ts(dk, ahi, bhi, idn, ks > 0);
+              mma_f16_ts(dk, alo, bhi, idn, 1);
+            } else {
+              mma_f16_ts(dk, ahi, bhi, id, ks > 0);
+              mma_f16_ts(dk, ahi, blo, id, 1);
+              mma_f16_ts(dk, alo, bhi, id, 1);
+              mma_f16_ts(dk, alo, blo, id, 1);
+            }
+#endif
           }
           mma_commit(&a_empty[as]);
           mma_commit(&acc_full[acs]);
@@ -274,11 +303,26 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
         mbar_wait(&acc_full[acs], cph);
         tc_fence_after();
         float2 acc = make_float2(0.0f, 0.0f);
+#ifdef TCSX_NO_EPI
+        if (false)
+#endif
 #pragma unroll
         for (int c = 0; c < KP; c += 16) {
           uint32_t v[16];
-          tmem_ld16(tb + acs * KP + c, v);
-          tmem_ld_wait();
+          tmem_ld16(tb + acs * AW + c, v);
+          if constexpr (NC) {  // + the V_lo part
+            uint32_t w[16];
+            tmem_ld16(tb + acs * AW + KP + c, w);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) {
+              const float2 t = fadd2(make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])),
+                                     make_float2(__uint_as_float(w[q]), __uint_as_float(w[q + 1])));
+              v[q] = __float_as_uint(t.x), v[q + 1] = __float_as_uint(t.y);
+            }
+          } else {
+            tmem_ld_wait();
+          }
 #pragma unroll
           for (int q = 0; q < 16; q += 4) {
             const float4 qq = *reinterpret_cast<const float4*>(qv + c + q);  // broadcast
