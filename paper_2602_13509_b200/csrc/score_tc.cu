@@ -59,6 +59,20 @@ constexpr int kScoreABase = 256;  // A ring (f16 hi/lo, from the transform warps
 constexpr int kScoreWmax = 128;
 constexpr int kTopkBins = 2048;  // digit 0 of the top-k radix select (select.cu)
 
+// -DSKYRX_SC_PROFILE builds accumulate per-CTA wait cycles of each role
+// (tools/sc_profile.py reads them through skyrx_sc_profile); compiled out otherwise
+#ifdef SKYRX_SC_PROFILE
+__device__ unsigned long long sc_prof[160][10];
+#define SC_PW(idx, ...)                                                   \
+  do {                                                                    \
+    const unsigned long long t0_ = clock64();                             \
+    __VA_ARGS__;                                                          \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&sc_prof[blockIdx.x][idx], clock64() - t0_); \
+  } while (0)
+#else
+#define SC_PW(idx, ...) __VA_ARGS__
+#endif
+
 struct ScoreTcParams {
   const uint16_t* raw;
   const float* dark;
@@ -99,6 +113,41 @@ __device__ __forceinline__ void store_split8(const float2 (&dv)[4], uint32_t thi
   }
   tmem_st4(thi, hw[0], hw[1], hw[2], hw[3]);
   tmem_st4(tlo, lw[0], lw[1], lw[2], lw[3]);
+}
+
+// MODE 0 with exactly CHT chunks per thread, batched: every raw word of the row
+// is loaded first, then all the arithmetic (12 independent band-pair chains at
+// CHT = 3 instead of 4 between two tcgen05.st), then all the TMEM stores.  The
+// tcgen05.st asm is a compiler barrier, so the chunk-by-chunk form serialises
+// each chunk's dependency chain (profiles/r01_ablation.md: the transform warps
+// were latency-bound at ~0.45 issue/cycle).
+template <int CHT>
+__device__ __forceinline__ void transform_row_batched(uint32_t rr32, const float2 (&tco)[CHT * 4],
+                                                      const float2 (&tnof)[CHT * 4], uint32_t thi,
+                                                      uint32_t tlo) {
+  const float2 bias = make_float2(-8388608.0f, -8388608.0f);
+  uint32_t wv[CHT * 4];
+#pragma unroll
+  for (int i = 0; i < CHT * 4; ++i) wv[i] = ld_shared_u32(rr32 + 4 * i);
+  uint32_t hw[CHT * 4], lw[CHT * 4];
+#pragma unroll
+  for (int i = 0; i < CHT * 4; ++i) {
+    const uint32_t v = wv[i];
+    const float2 rf = fadd2(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)),
+                                        __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632))),
+                            bias);
+    const float2 d = ffma2(rf, tco[i], tnof[i]);
+    const __half2 h = __floats2half2_rn(d.x, d.y);
+    const float2 res = fsub2(d, __half22float2(h));
+    const __half2 l = __floats2half2_rn(res.x, res.y);
+    hw[i] = *reinterpret_cast<const uint32_t*>(&h);
+    lw[i] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+#pragma unroll
+  for (int cc = 0; cc < CHT; ++cc) {
+    tmem_st4(thi + 4 * cc, hw[4 * cc], hw[4 * cc + 1], hw[4 * cc + 2], hw[4 * cc + 3]);
+    tmem_st4(tlo + 4 * cc, lw[4 * cc], lw[4 * cc + 1], lw[4 * cc + 2], lw[4 * cc + 3]);
+  }
 }
 
 // One pixel row's share (CHT 8-band chunks) of the A operand.  Per band pair
@@ -157,7 +206,7 @@ __device__ __forceinline__ void transform_row(const uint8_t* rr, uint32_t rr32,
 
 // Transform warps: calibrate + centre + f16-split every tile of this CTA into
 // the A ring.  MODE is uniform over the launch (see transform_row).
-template <int KP, int MODE, int CHT>
+template <int KP, int MODE, int CHT, bool BATCHED = false>
 __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, int blk, int64_t g0,
                                                int64_t gstep, uint8_t* raw_ring, uint32_t tmem,
                                                const float2* mu, uint64_t* raw_full,
@@ -227,16 +276,20 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
       const int64_t line = ti.line0 + r / ti.w;
       g = __ldg(p.gain + (line < p.ts.L ? line : p.ts.L - 1));
     }
-    mbar_wait(raw_full32 + 8 * s, ph);
-    mbar_wait(a_empty32 + 8 * as, aph ^ 1);
+    SC_PW(0, mbar_wait(raw_full32 + 8 * s, ph));
+    SC_PW(1, mbar_wait(a_empty32 + 8 * as, aph ^ 1));
     tc_fence_after();
     const uint32_t roff = s * p.raw_stage_bytes + r * B * 2 + 16 * c_lo;
     const uint32_t thi = tl + as * KP;
 #ifndef SCX_NO_XFORM  // ablation switches (tools/build_sc_var.sh), off in the product
-    transform_row<MODE, CHT>(raw_ring + roff, ring32 + roff, tco, tnof, nm0, g, thi,
-                             thi + KP / 2, cnt);
+    if constexpr (BATCHED) {
+      SC_PW(2, transform_row_batched<CHT>(ring32 + roff, tco, tnof, thi, thi + KP / 2));
+    } else {
+      SC_PW(2, transform_row<MODE, CHT>(raw_ring + roff, ring32 + roff, tco, tnof, nm0, g, thi,
+                                        thi + KP / 2, cnt));
+    }
 #endif
-    tmem_st_wait();
+    SC_PW(3, tmem_st_wait());
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {  // one arrival per warp
@@ -286,6 +339,9 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+#ifdef SKYRX_SC_PROFILE
+  const unsigned long long sc_t0 = clock64();
+#endif
   // block-pinned schedule: this CTA walks line groups g0, g0 + gstep, ... of block blk
   const int blk = p.plan.block[blockIdx.x];
   const int64_t g0 = p.plan.rank[blockIdx.x];
@@ -348,8 +404,8 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
       int as = 0, acs = 0;
       uint32_t aph = 0, cph = 0;
       for (int t = 0; t < n; ++t) {
-        mbar_wait(&a_full[as], aph);
-        mbar_wait(&acc_empty[acs], cph ^ 1);
+        SC_PW(4, mbar_wait(&a_full[as], aph));
+        SC_PW(5, mbar_wait(&acc_empty[acs], cph ^ 1));
         tc_fence_after();
         const uint32_t abase = tmem + kScoreABase + as * KP;  // A from TMEM
         const uint32_t d = tmem + acs * AW;
@@ -403,7 +459,7 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     uint32_t cph = 0;
     for (int t = 0; t < n; ++t) {
       if (t > 0) tile_next_in_block(p.ts, ti, gstep);
-      mbar_wait(acc_full32 + 8 * acs, cph);
+      SC_PW(6, mbar_wait(acc_full32 + 8 * acs, cph));
       tc_fence_after();
       float2 acc = make_float2(0.0f, 0.0f);
 #ifdef SCX_NO_EPI
@@ -468,6 +524,14 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     else if (p.gain != nullptr)
       transform_loop<KP, 2, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
                                  a_full, a_empty);
+#ifndef SCX_NO_BATCHED
+    else if (noclamp && KP == 80 && (B + 7) / 8 == 9) {
+      // B = 65..72 (c1-c4): exactly three chunks per thread, batched
+      if constexpr (KP == 80)
+        transform_loop<KP, 0, 3, true>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full,
+                                       raw_empty, a_full, a_empty);
+    }
+#endif
     else if (noclamp)
       transform_loop<KP, 0, CHT>(p, n, blk, g0, gstep, raw_ring, tmem, mu, raw_full, raw_empty,
                                  a_full, a_empty);
@@ -479,6 +543,9 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
   __syncthreads();
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc(tmem, TMEM_COLS);
+#ifdef SKYRX_SC_PROFILE
+  if (tid == 0) sc_prof[blockIdx.x][9] += clock64() - sc_t0;
+#endif
   if (p.hist0)
     for (int i = tid; i < kTopkBins; i += blockDim.x)
       if (shist[i]) atomicAdd(&p.hist0[i], shist[i]);
@@ -626,3 +693,9 @@ extern "C" int skyrx_score_tc(const uint16_t* raw, int64_t lines, int32_t sample
   set_error("unsupported band count %d", bands);
   return SKYRX_ERR_ARG;
 }
+
+#ifdef SKYRX_SC_PROFILE
+extern "C" __attribute__((visibility("default"))) int skyrx_sc_profile(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, skyrx::sc_prof, sizeof(skyrx::sc_prof)) == cudaSuccess ? 0 : 1;
+}
+#endif
