@@ -96,7 +96,11 @@ __host__ __device__ constexpr int gr_bufcols() {
   return gr_ones<NCH>() ? 256 : ((16 * NCH + (NCH > 8 ? 16 * NCH - 128 : 0)) + 31) / 32 * 32;
 }
 template <int NCH>
+#ifndef GRX_NBUF1
 __host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 512 ? 2 : 1; }
+#else  // experiment: one accumulator (no MMA runs ahead of the epilogue loads)
+__host__ __device__ constexpr int gr_nbuf() { return 1; }
+#endif
 
 template <int NCH>
 __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -657,6 +661,9 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   // also split so that there are at least ~2 units per SM
   // and into enough units (>= 8 per SM) that the static round-robin tail stays small
   while ((int64_t)samples * p.nsplit < 8 * kSMs && lines / (p.nsplit + 1) >= 4 * kGrLb) ++p.nsplit;
+#ifdef GRX_NSPLIT_ENV  // experiment: units per sample column from the environment
+  if (const char* e = getenv("SKYRX_GR_NSPLIT")) p.nsplit = atoi(e) > 0 ? atoi(e) : p.nsplit;
+#endif
   p.split_lines = (lines + p.nsplit - 1) / p.nsplit;
   p.split_lines = ((p.split_lines + kGrLb - 1) / kGrLb) * kGrLb;
   p.nsplit = (int)((lines + p.split_lines - 1) / p.split_lines);
