@@ -313,18 +313,27 @@ def main():
     # the dominant of the two passes over the raw cube: fused calibrate+score
     # (2B raw read + 4 B score write per pixel) or raw-byte moments (2B raw read;
     # the call also runs the two tiny partial-reduction kernels)
-    if gram_k_ms > kern_ms:
-        kname, dom_bytes, kern_ms, other = ("gram_raw_kernel (+reduce)", npix * 2 * B, gram_k_ms,
-                                            ("score_tc_kernel", kern_ms))
+    # the kernels this geometry runs (rx.DetectPlan dispatch)
+    if B > 128:
+        gname, sname = "raww_gram_kernel (+scan, per-pass)", "score_tcw_kernel"
     else:
-        kname = "score_tc_kernel" if plan.tc else "score_kernel"
-        dom_bytes, other = npix * (2 * B + 4), ("gram_raw_kernel (+reduce)", gram_k_ms)
+        gname = "gram_raw_kernel (+reduce)"
+        sname = ("score_tcs_kernel" if plan.tcs else
+                 "score_tc_kernel" if plan.tc else "score_kernel")
+    if gram_k_ms > kern_ms:
+        kname, dom_bytes, kern_ms, other = (gname, npix * 2 * B, gram_k_ms, (sname, kern_ms))
+    else:
+        kname, dom_bytes, other = sname, npix * (2 * B + 4), (gname, gram_k_ms)
     achieved = dom_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(kname.split()[0])
+            # captured for the c4 kernels (profiles/ncu_traffic.json): per launch of
+            # that geometry only
+            tj = json.loads(tp.read_text())
+            if tj.get("geometry") == [lines, S, B]:
+                traffic = tj.get(kname.split()[0])
         except Exception:
             traffic = None
 

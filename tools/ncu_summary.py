@@ -82,7 +82,9 @@ def full(rep, out, traffic_out=None):
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
     if traffic_out:
-        tr = {k: v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for k, v in res.items()
+        # keyed by the bare kernel name (bench.py looks them up that way)
+        tr = {re.sub(r"<.*", "", k.replace("void ", "")).strip():
+              v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for k, v in res.items()
               if "dram__bytes_read.sum" in v}
         json.dump(tr, open(traffic_out, "w"), indent=1)
 
