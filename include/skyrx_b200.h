@@ -125,6 +125,12 @@ int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t
                     const float* dark, const float* coeff, double gain, const double* shift,
                     double* moments, int32_t* flags, void* workspace, size_t workspace_bytes,
                     void* stream);
+/* The same, with the shift chosen by the call: shift (OUT, B f64) = f32(mean) of
+ * the cube from its exact sums, so no separate skyrx_stats_shift pass is needed. */
+int skyrx_stats_raw_own_shift(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                              const float* dark, const float* coeff, double gain, double* shift,
+                              double* moments, int32_t* flags, void* workspace,
+                              size_t workspace_bytes, void* stream);
 
 /* state = forget * state + chunk (R-STREAM exponential forgetting) */
 int skyrx_moments_fold(double* state, const double* chunk, int32_t bands, double forget,

@@ -43,6 +43,7 @@ SIGNATURES = {
     "skyrx_stats_raw_supported": (C.c_int, [i64, i32, i32, vp]),
     "skyrx_stats_raw_workspace": (sz, [i32]),
     "skyrx_stats_raw": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
+    "skyrx_stats_raw_own_shift": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "skyrx_moments_fold":(C.c_int, [vp, vp, i32, f64, vp]),
     "skyrx_stats_finalize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp,
                                        vp, vp, vp]),

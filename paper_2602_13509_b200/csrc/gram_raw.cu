@@ -526,43 +526,51 @@ __global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restr
   }
 }
 
-// moments about the shift c: s = Sx - n c, Q = Sxx - c Sx^T - Sx c^T + n c c^T
+// moments about the shift c: s = Sx - n c, Q = Sxx - c Sx^T - Sx c^T + n c c^T.
+// own: c is not given but chosen here, c = f32(Sx / n) (written to shift): the sums
+// are exact integer Grams calibrated in f64, so any c near the mean centres them to
+// ~1e-13, and the separate shift pass over the cube is not needed
 __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
-                                       const double* __restrict__ shift,
+                                       double* __restrict__ shift, int own,
                                        double* __restrict__ moments) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const double* sx = tot + B * B;
   const double n = tot[B * B + B];
+  auto c_of = [&](int i) -> double {
+    return own ? (n > 0.0 ? (double)(float)(sx[i] / n) : 0.0) : shift[i];
+  };
   if (e < B * B) {
     const int i = e / B, j = e - i * B;
     if (j > i) return;
-    const double ci = shift[i], cj = shift[j];
+    const double ci = c_of(i), cj = c_of(j);
     const double q = tot[i * B + j] - ci * sx[j] - sx[i] * cj + n * ci * cj;
     moments[1 + B + (size_t)i * B + j] = q;
     moments[1 + B + (size_t)j * B + i] = q;
   } else if (e < B * B + B) {
     const int i = e - B * B;
-    moments[1 + i] = sx[i] - n * shift[i];
+    const double ci = c_of(i);
+    moments[1 + i] = sx[i] - n * ci;
+    if (own) shift[i] = ci;
   } else if (e == B * B + B) {
     moments[0] = n;
   }
 }
 
 // reduce the per-CTA partials [Sxx | Sx | n] (deterministic) and centre them on shift
-int gram_raw_sum_and_center(const double* part, int grid, int bands, const double* shift,
+int gram_raw_sum_and_center(const double* part, int grid, int bands, double* shift, int own,
                             double* moments, cudaStream_t st) {
   const int work = bands * bands + bands + 1;
   double* tot = const_cast<double*>(part) + (size_t)kSMs * work;  // after the partials
   gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(part, grid, work, tot);
   SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
-  gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, bands, shift, moments);
+  gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, bands, shift, own, moments);
   SKYRX_CHECK_LAUNCH("gram_raw_center_kernel");
   return SKYRX_OK;
 }
 
 int raww_atoms(int bands);
 int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
-                   const float* dark, const float* coeff, double gain, const double* shift,
+                   const float* dark, const float* coeff, double gain, double* shift, int own,
                    double* moments, int32_t* flags, void* workspace, cudaStream_t st);
 
 static int nch_for(int B) {
@@ -574,7 +582,7 @@ static int nch_for(int B) {
 
 template <int NCH>
 static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawParams p,
-                           double* moments, const double* shift, cudaStream_t st) {
+                           double* moments, double* shift, int own, cudaStream_t st) {
   constexpr uint32_t W2B = gr_w2b<NCH>();
   constexpr uint32_t STAGE = kGrLb * (128u + W2B);
   CUtensorMap map1 = map;
@@ -603,7 +611,7 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
                        (int)smem);
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
-  return gram_raw_sum_and_center(p.part, grid, p.B, shift, moments, st);
+  return gram_raw_sum_and_center(p.part, grid, p.B, shift, own, moments, st);
 }
 
 }  // namespace skyrx
@@ -624,18 +632,18 @@ extern "C" size_t skyrx_stats_raw_workspace(int32_t bands) {
   return (size_t)(kSMs + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double);
 }
 
-extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
-                               const float* dark, const float* coeff, double gain,
-                               const double* shift, double* moments, int32_t* flags,
-                               void* workspace, size_t workspace_bytes, void* stream) {
+static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                          const float* dark, const float* coeff, double gain, double* shift,
+                          int own, double* moments, int32_t* flags, void* workspace,
+                          size_t workspace_bytes, void* stream) {
   SKYRX_REQUIRE(skyrx_stats_raw_supported(lines, samples, bands, raw),
                 "raw-byte tensor-core moments unsupported for this shape/alignment");
   SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
   SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_raw_workspace(bands), "workspace too small");
   const int nch = nch_for(bands);
   if (nch > 16)  // windows past 256 bytes: the multi-pass wide kernel (gram_raww.cu)
-    return stats_raw_wide(raw, lines, samples, bands, dark, coeff, gain, shift, moments, flags,
-                          workspace, as_stream(stream));
+    return stats_raw_wide(raw, lines, samples, bands, dark, coeff, gain, shift, own, moments,
+                          flags, workspace, as_stream(stream));
   // 2-D byte view (byte within line, line); boxes of 128 bytes x Lb lines, swizzled
   const cuuint64_t line_bytes = (cuuint64_t)samples * bands * 2;
   cuuint64_t dims[2] = {line_bytes, (cuuint64_t)lines};
@@ -672,7 +680,7 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   switch (nch) {
 #define SKYRX_NCH(k) \
   case k:            \
-    return launch_gram_raw<k>(map, raw, p, moments, shift, st);
+    return launch_gram_raw<k>(map, raw, p, moments, shift, own, st);
     SKYRX_NCH(1) SKYRX_NCH(2) SKYRX_NCH(3) SKYRX_NCH(4) SKYRX_NCH(5) SKYRX_NCH(6) SKYRX_NCH(7)
     SKYRX_NCH(8) SKYRX_NCH(9) SKYRX_NCH(10) SKYRX_NCH(11) SKYRX_NCH(12) SKYRX_NCH(13)
     SKYRX_NCH(14) SKYRX_NCH(15) SKYRX_NCH(16)
@@ -680,4 +688,22 @@ extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t sampl
   }
   set_error("unsupported band count %d", bands);
   return SKYRX_ERR_ARG;
+}
+
+extern "C" int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
+                               const float* dark, const float* coeff, double gain,
+                               const double* shift, double* moments, int32_t* flags,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  return stats_raw_impl(raw, lines, samples, bands, dark, coeff, gain,
+                        const_cast<double*>(shift), 0, moments, flags, workspace,
+                        workspace_bytes, stream);
+}
+
+extern "C" int skyrx_stats_raw_own_shift(const uint16_t* raw, int64_t lines, int32_t samples,
+                                         int32_t bands, const float* dark, const float* coeff,
+                                         double gain, double* shift, double* moments,
+                                         int32_t* flags, void* workspace, size_t workspace_bytes,
+                                         void* stream) {
+  return stats_raw_impl(raw, lines, samples, bands, dark, coeff, gain, shift, 1, moments, flags,
+                        workspace, workspace_bytes, stream);
 }

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
 
 }  // namespace raww
 
-int gram_raw_sum_and_center(const double* part, int grid, int bands, const double* shift,
+int gram_raw_sum_and_center(const double* part, int grid, int bands, double* shift, int own,
                             double* moments, cudaStream_t st);
 
 // window atoms for B (16-B aligned start, widest offset over the samples)
@@ -310,7 +310,7 @@ int raww_atoms(int bands) {
 }
 
 int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
-                   const float* dark, const float* coeff, double gain, const double* shift,
+                   const float* dark, const float* coeff, double gain, double* shift, int own,
                    double* moments, int32_t* flags, void* workspace, cudaStream_t st) {
   using namespace raww;
   Params p{};
@@ -404,7 +404,7 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
     SKYRX_CHECK_LAUNCH("raww_gram_kernel");
   }
   cudaFreeAsync(usum, st);
-  return gram_raw_sum_and_center(p.part, grid, bands, shift, moments, st);
+  return gram_raw_sum_and_center(p.part, grid, bands, shift, own, moments, st);
 }
 
 }  // namespace skyrx

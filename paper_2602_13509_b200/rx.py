@@ -401,13 +401,13 @@ class DetectPlan:
         precise = precise or force_ffma
         if (self.raw_stats and not precise and gain_const is not None
                 and lib.skyrx_stats_raw_supported(L, S, B, raw.data_ptr())):
-            # exact integer byte Grams on the tensor cores (constant line gain)
-            if own_shift:
-                _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
+            # exact integer byte Grams on the tensor cores (constant line gain); with
+            # its own shift the call centres on f32(mean) itself (no shift pass)
             self.used_raw[i] = True
             if events is not None:
                 events[0].record()
-            _lib.call("skyrx_stats_raw", raw.data_ptr(), L, S, B, dark.data_ptr(),
+            _lib.call("skyrx_stats_raw_own_shift" if own_shift else "skyrx_stats_raw",
+                      raw.data_ptr(), L, S, B, dark.data_ptr(),
                       coeff.data_ptr(), float(gain_const), ds.shift[i].data_ptr(),
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.raw_ws.data_ptr(), self.raw_ws_bytes, s)
