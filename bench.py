@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-strips", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every step eagerly instead of replaying one captured CUDA graph")
     return ap.parse_args()
 
 
@@ -274,23 +276,44 @@ def main():
         step()
     torch.cuda.synchronize()
     plan.ds.check(0, npix)
-    launches0 = plan.launches
+    # the step as one CUDA graph (every kernel of every strip, no host work between
+    # launches); inputs larger than L2 only — the L2-flushed configs time eager steps
+    graph = None
+    if not args.no_graph and flush is None:
+        launches0 = plan.launches
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        launches = plan.launches - launches0
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = plan.launches
     with ClockSampler(local) as clocks:
         start.record(stream)
         for _ in range(args.steps):
-            step(instrument=True)
+            if graph is not None:
+                graph.replay()
+            else:
+                step(instrument=True)
         end.record(stream)
         torch.cuda.synchronize()
+        if graph is not None:
+            # per-kernel events (roofline) from eager steps, outside the timed region
+            for _ in range(max(1, min(args.steps, 2))):
+                step(instrument=True)
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
     if flush is not None:  # device time of the steps themselves, L2 flushes excluded
         ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
-    launches = (plan.launches - launches0) // args.steps
+    if graph is None:
+        launches = (plan.launches - launches0) // args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -352,6 +375,7 @@ def main():
                      "stats_ms_per_strip": gram_ms, "score_path_ms_per_strip": score_ms,
                      "other_pass": {"kernel": other[0], "ms_per_launch": other[1]}},
         "gpu_launches": launches,
+        "launch_mode": "cuda_graph (one captured step replayed)" if graph is not None else "eager",
         "clocks": clocks.summary(),
     }
 
