@@ -52,6 +52,9 @@ __device__ unsigned long long gr_prof[160][12];
 #define GR_PW(idx, stmt) stmt
 #endif
 
+#ifndef GRX_L2PROMO  // experiment switch: the TMA boxes' L2 promotion
+#define GRX_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 constexpr int kGrThreads = 320;
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
@@ -597,7 +600,7 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
         CU_TENSOR_MAP_INTERLEAVE_NONE,
         W2B == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                   : (W2B == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B),
-        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        GRX_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
   constexpr int kGrStages = gr_stages<NCH>();
@@ -606,6 +609,9 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
                       (gr_ones<NCH>() ? kGrLb * 32 : 0) +
                       16 * 8 + 1024;
   int grid = kSMs;
+#ifdef GRX_NSPLIT_ENV  // experiment: fewer CTAs than SMs
+  if (const char* e = getenv("SKYRX_GR_GRID")) grid = atoi(e) > 0 ? atoi(e) : grid;
+#endif
   if (p.units < grid) grid = (int)p.units;
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
@@ -653,7 +659,7 @@ static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, i
   CUtensorMap map;
   CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)raw, dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_SWIZZLE_128B, GRX_L2PROMO,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   GramRawParams p{};
