@@ -109,7 +109,7 @@ __device__ __forceinline__ void digits4(const uint32_t (&w)[4], const uint32_t* 
 
 // transform of one unit's tiles at window offset OFFW words (band 0 at word OFFW of
 // 16-B chunk 0); CHT = chunks per thread (compile time), cnt = this thread's count
-template <int KP, int CHT, int OFFW>
+template <int KP, int CHT, int OFFW, bool BATCHED = false>
 __device__ __forceinline__ void transform_unit(const Params& p, int ntile, uint8_t* raw_ring,
                                                uint32_t tl, const uint32_t* tt, int c_lo, int cnt,
                                                uint64_t* raw_full, uint64_t* raw_empty,
@@ -124,6 +124,35 @@ __device__ __forceinline__ void transform_unit(const Params& p, int ntile, uint8
     mbar_wait(&a_empty[as], aph ^ 1);
     tc_fence_after();
     const uint4* row = reinterpret_cast<const uint4*>(raw_ring + s * p.stage_bytes + r * rowb);
+    if constexpr (BATCHED) {
+      // exactly CHT chunks: all loads, then all digit words, then all TMEM stores (the
+      // tcgen05.st asm is a compiler barrier; chunk by chunk serialises the chains)
+      uint4 qv[CHT + 1];
+#pragma unroll
+      for (int i = 0; i <= CHT; ++i) qv[i] = row[c_lo + i];
+      uint32_t hw[CHT][4], lw[CHT][4];
+#pragma unroll
+      for (int cc = 0; cc < CHT; ++cc) {
+        const uint32_t c4[8] = {qv[cc].x,     qv[cc].y,     qv[cc].z,     qv[cc].w,
+                                qv[cc + 1].x, qv[cc + 1].y, qv[cc + 1].z, qv[cc + 1].w};
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = c4[OFFW + i];
+#ifndef TCSX_NO_XFORM
+        digits4(w, tt + 4 * cc, hw[cc], lw[cc], chk);
+#else
+        chk |= w[0] & 0;
+#endif
+      }
+#ifndef TCSX_NO_XFORM
+#pragma unroll
+      for (int cc = 0; cc < CHT; ++cc) {
+        const uint32_t col = tl + as * KP + 4 * (c_lo + cc);
+        tmem_st4(col, hw[cc][0], hw[cc][1], hw[cc][2], hw[cc][3]);
+        tmem_st4(col + KP / 2, lw[cc][0], lw[cc][1], lw[cc][2], lw[cc][3]);
+      }
+#endif
+    } else {
     uint4 cur = cnt > 0 ? row[c_lo] : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int cc = 0; cc < CHT; ++cc) {
@@ -143,6 +172,7 @@ __device__ __forceinline__ void transform_unit(const Params& p, int ntile, uint8
       chk |= w[0] & 0;
 #endif
       cur = nxt;
+    }
     }
     tmem_st_wait();
     tc_fence_before();
@@ -392,7 +422,20 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
       if (lane == 0) mbar_arrive(&rec_empty[rb]);
       const int ntile = (int)((nl + kLines - 1) / kLines);
       const int offw = (int)((((int64_t)smp * B * 2) & 15) >> 2);
-      if (offw == 0)
+      if (nchr == NG * CHT) {  // every thread owns exactly CHT chunks: batched
+        if (offw == 0)
+          transform_unit<KP, CHT, 0, true>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full,
+                                           raw_empty, a_full, a_empty, s, ph, as, aph, chk);
+        else if (offw == 1)
+          transform_unit<KP, CHT, 1, true>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full,
+                                           raw_empty, a_full, a_empty, s, ph, as, aph, chk);
+        else if (offw == 2)
+          transform_unit<KP, CHT, 2, true>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full,
+                                           raw_empty, a_full, a_empty, s, ph, as, aph, chk);
+        else
+          transform_unit<KP, CHT, 3, true>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full,
+                                           raw_empty, a_full, a_empty, s, ph, as, aph, chk);
+      } else if (offw == 0)
         transform_unit<KP, CHT, 0>(p, ntile, raw_ring, tl, tt, c_lo, cnt, raw_full, raw_empty,
                                    a_full, a_empty, s, ph, as, aph, chk);
       else if (offw == 1)
