@@ -281,13 +281,20 @@ def main():
     graph = None
     if not args.no_graph and flush is None:
         launches0 = plan.launches
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            launches = plan.launches - launches0
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # capture refused: time eager steps instead
+            print(f"bench: CUDA graph capture failed ({e}); eager steps", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize()
             step()
-        launches = plan.launches - launches0
-        for _ in range(args.warmup):
-            graph.replay()
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
