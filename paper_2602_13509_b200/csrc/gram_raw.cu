@@ -74,7 +74,13 @@ struct GramRawParams {
   int32_t S, B;
   int64_t split_lines;  // lines per unit
   int32_t nsplit;
-  int64_t units;
+  int64_t units;        // all work items: regular units, then the tail's pieces
+  // tail balancing: the S * nsplit regular units are dealt round-robin; the last,
+  // partial round (rem units) is cut into tail_k pieces each, so every CTA ends with
+  // at most one short piece instead of 24 CTAs running one whole extra unit
+  int64_t units_main;   // regular units dealt in full rounds
+  int32_t tail_k;       // pieces per leftover unit (1: no split)
+  int64_t tail_lines;   // lines per piece (multiple of the tile)
 };
 
 // idesc for kind::i8 with unsigned 8-bit operands, MN-major A and B, S32 accumulators
@@ -189,10 +195,18 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #endif
 
   auto unit_geom = [&](int64_t u, int& s, int64_t& l0, int64_t& nl) {
-    s = (int)(u % p.S);
-    const int64_t sp = u / p.S;
+    const int64_t ur = u < p.units_main ? u : p.units_main + (u - p.units_main) / p.tail_k;
+    s = (int)(ur % p.S);
+    const int64_t sp = ur / p.S;
     l0 = sp * p.split_lines;
     nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
+    if (u >= p.units_main) {  // a piece of a leftover unit
+      const int64_t piece = (u - p.units_main) % p.tail_k;
+      const int64_t a = piece * p.tail_lines;
+      const int64_t b = a + p.tail_lines < nl ? a + p.tail_lines : nl;
+      l0 += a;
+      nl = b > a ? b - a : 0;
+    }
   };
 
   if (warp == 8) {
@@ -355,6 +369,12 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       if (tid == kGrWorkers) GR_PW(5, mbar_wait(&acc_full[buf], use & 1));
       else mbar_wait(&acc_full[buf], use & 1);
       tc_fence_after();
+      if (nl == 0) {  // an empty tail piece: no tiles, nothing accumulated
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+        mbar_arrive(&scan_empty[ub]);
+        continue;
+      }
 #ifdef SKYRX_GR_PROFILE
       const unsigned long long et0 = clock64();
 #endif
@@ -613,6 +633,23 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   if (const char* e = getenv("SKYRX_GR_GRID")) grid = atoi(e) > 0 ? atoi(e) : grid;
 #endif
   if (p.units < grid) grid = (int)p.units;
+  // tail balancing (see GramRawParams): rem leftover units into tail_k pieces each
+  p.units_main = p.units;
+  p.tail_k = 1;
+  p.tail_lines = p.split_lines;
+  {
+    const int64_t rem = p.units % grid;
+    if (rem > 0 && 2 * rem <= grid) {
+      const int k = (int)(grid / rem);
+      const int64_t tl = ((p.split_lines + k - 1) / k + kGrLb - 1) / kGrLb * kGrLb;
+      if (k > 1 && tl < p.split_lines) {
+        p.units_main = p.units - rem;
+        p.tail_k = k;
+        p.tail_lines = tl;
+        p.units = p.units_main + rem * k;
+      }
+    }
+  }
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);

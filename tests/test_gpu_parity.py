@@ -465,7 +465,7 @@ class TestDetect:
                                             (96, 48, 2800, 1.0), (40, 16, 6600, 1.0),
                                             (1024, 128, 260, 1.0), (128, 79, 2100, 0.75),
                                             (1024, 270, 300, 1.0), (128, 160, 2100, 0.75),
-                                            (64, 150, 4100, 1.0)])
+                                            (64, 150, 4100, 1.0), (900, 70, 2100, 1.0)])
     def test_raw_byte_moments(self, P, S, B, L, gain):
         """Constant line gain: exact integer byte Grams on the tensor cores."""
         from paper_2602_13509_b200 import _lib
