@@ -306,7 +306,13 @@ __device__ void topk_mask_finish(const float* __restrict__ v, int64_t n, TopkSta
   }
 }
 
-constexpr int kMaskThreads = 512;
+#ifndef MASKX_THREADS  // experiment switches (threads per CTA, CTAs per SM of the mask pass)
+#define MASKX_THREADS 512
+#endif
+#ifndef MASKX_PERSM
+#define MASKX_PERSM 4
+#endif
+constexpr int kMaskThreads = MASKX_THREADS;
 __global__ void __launch_bounds__(kMaskThreads) topk_mask_pass_kernel(
     const float* __restrict__ v, int64_t n, TopkState* st, uint32_t* hist,
     uint8_t* __restrict__ mask, uint2* __restrict__ cand, uint32_t cap, float* thr) {
@@ -488,7 +494,7 @@ extern "C" int skyrx_topk_mask(const float* v, int64_t n, int32_t hist0_done, fl
                            : 0u;
   if (n > 0 && !hist0_done)
     topk_hist_kernel<<<grid_n(n, 512, 4), 512, 0, st>>>(v, n, 0, state, hist);
-  topk_mask_pass_kernel<<<grid_n(n / 4 + 1, kMaskThreads, 4), kMaskThreads, 0, st>>>(
+  topk_mask_pass_kernel<<<grid_n(n / 4 + 1, kMaskThreads, MASKX_PERSM), kMaskThreads, 0, st>>>(
       v, n, state, hist, mask, reinterpret_cast<uint2*>(cand), cap, thr);
   SKYRX_CHECK_LAUNCH("skyrx_topk_mask");
   return SKYRX_OK;
