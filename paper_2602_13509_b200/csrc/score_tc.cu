@@ -605,7 +605,13 @@ static int launch_score_tc(ScoreTcParams p, cudaStream_t st) {
     set_error("score_tc: %d sample blocks exceed the schedule table", p.ts.nb);
     return SKYRX_ERR_ARG;
   }
+#ifndef SCX_GRID_ENV
   const int grid = plan_ctas(p.ts, p.ts.items < kSMs ? (int)p.ts.items : kSMs, p.plan);
+#else  // experiment: fewer CTAs than SMs (run beside another kernel)
+  int g0 = kSMs;
+  if (const char* e = getenv("SKYRX_SC_GRID")) g0 = atoi(e) > 0 ? atoi(e) : g0;
+  const int grid = plan_ctas(p.ts, p.ts.items < g0 ? (int)p.ts.items : g0, p.plan);
+#endif
   // the narrow last block packs rl lines per tile: fetch each tile with ONE 2-D
   // TMA (u32 elements; box = wl*B/2 x rl) instead of rl tiny line copies
   CUtensorMap map;
