@@ -177,18 +177,17 @@ __global__ void __launch_bounds__(256) topk_pick_kernel(int digit, TopkState* st
   for (int i = t; i < kHistBins; i += blockDim.x) hist[i] = 0;
 }
 
-
 // ---------------------------------------------------------------------------
 // One-pass select + mask (skyrx_topk_mask).  After the digit-0 histogram (fused
 // into the score kernel, or one topk_hist pass) every CTA of the mask pass
 // picks the digit-0 bin itself (the same suffix scan as topk_pick_kernel, on
 // read-only bins), then streams the scores once: keys above the bin are in the
 // mask, keys below are not, keys inside it are written 0 and appended as
-// (index, key) candidates.  One CTA then finishes digits 1 and 2 on the
-// candidates only and sets the mask bytes of those above the threshold.  The
-// threshold and mask are the ones the 3 x (hist + pick) + mask_gt sequence
-// gives (same bins, same picks); it just reads the scores once instead of three
-// times and launches twice instead of six times.
+// (index, key) candidates.  The last CTA to finish (atomic count) then runs
+// digits 1 and 2 on the candidates only and sets the mask bytes of those above
+// the threshold.  The threshold and mask are the ones the 3 x (hist + pick) +
+// mask_gt sequence gives (same bins, same picks); it reads the scores once
+// instead of three times and is one launch instead of six.
 
 // block-wide (NT threads) pick over nb = 2^bits bins from the top: the bin that
 // holds `rank` and the count above it
