@@ -529,6 +529,7 @@ extern "C" __attribute__((visibility("default"))) int skyrx_gr_profile(unsigned 
 // Deterministic reduction of the per-CTA partials [Sxx | Sx | n]: a block owns 32
 // elements (one per lane); its 8 warps sum fixed, contiguous slices of the
 // partials in order, then warp 0 adds the 8 slice sums in order.
+constexpr int kSumBatch = 19;  // ceil(148 / 8): a warp's slice of the per-CTA partials
 __global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restrict__ part,
                                                            int nparts, int stride,
                                                            double* __restrict__ out) {
@@ -538,8 +539,20 @@ __global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restr
   const int per = (nparts + 7) / 8;
   const int c0 = w * per, c1 = min(nparts, c0 + per);
   double acc = 0.0;
-  if (e < stride)
-    for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
+  if (e < stride) {
+    if (per <= kSumBatch) {
+      // every load of the slice in flight at once, then the same in-order sum
+      double v[kSumBatch];
+#pragma unroll
+      for (int k = 0; k < kSumBatch; ++k)
+        v[k] = c0 + k < c1 ? __ldcg(part + (size_t)(c0 + k) * stride + e) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kSumBatch; ++k)
+        if (c0 + k < c1) acc += v[k];
+    } else {
+      for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
+    }
+  }
   red[w][lane] = acc;
   __syncthreads();
   if (w == 0 && e < stride) {
