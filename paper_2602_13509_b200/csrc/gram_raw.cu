@@ -61,7 +61,11 @@ constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
 // TMA ring depth (stage = 128 lines x (128 + second-box) bytes) within the shared memory
 // left beside the f64 accumulator: 8 stages, 5 for windows > 160 B, 2 for > 192 B
 template <int NCH>
+#ifndef GRX_STAGES
 __host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 5 : 8); }
+#else  // experiment: ring depth for NCH <= 10 (with -DGRX_NO_QACC: TMA-stream tests only)
+__host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 5 : GRX_STAGES); }
+#endif
 constexpr int64_t kGrMaxUnitLines = 32768;
 
 struct GramRawParams {
@@ -139,7 +143,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t sm[];
   const int B = p.B;
   uint8_t* stages = sm;
+#ifndef GRX_NO_QACC
   double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE);
+#else  // experiment: no f64 accumulator in shared memory (aliases the ring; timing only)
+  double* qacc = reinterpret_cast<double*>(stages + kGrStages * STAGE) - (B * B + B);
+#endif
   double* sacc = qacc + B * B;
   uint8_t* ones = reinterpret_cast<uint8_t*>(sacc + B);      // ONES: [128 lines][32 B] of 1
   uint32_t* smin = reinterpret_cast<uint32_t*>(ones + (ONES ? kGrLb * 32 : 0));  // [thread][4]
@@ -637,7 +645,12 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
     SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   }
   constexpr int kGrStages = gr_stages<NCH>();
-  const size_t smem = kGrStages * (size_t)STAGE + ((size_t)p.B * p.B + p.B) * 8 +
+#ifndef GRX_NO_QACC
+  const size_t qbytes = ((size_t)p.B * p.B + p.B) * 8;
+#else
+  const size_t qbytes = 0;
+#endif
+  const size_t smem = kGrStages * (size_t)STAGE + qbytes +
                       (size_t)kGrWorkers * 12 * 4 + NCH * 8 * 16 + 3 * (size_t)p.B * 8 +
                       (gr_ones<NCH>() ? kGrLb * 32 : 0) +
                       16 * 8 + 1024;
