@@ -525,6 +525,40 @@ class TestDetect:
         assert (np.abs(det.scores - want) / np.maximum(want, 1e-12)).max() < 1e-4
         assert det.mask[1, 100]
 
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 2100), (64, 150, 4100), (128, 79, 700)])
+    def test_own_shift_equals_given_shift(self, P, S, B, L):
+        """skyrx_stats_raw_own_shift centres on f32(mean) itself; the same call with that
+        shift passed in (skyrx_stats_raw) gives the same moments, and the shift is the
+        f32 of the oracle's mean."""
+        import torch
+        from paper_2602_13509_b200 import _lib, _dev
+        from paper_2602_13509_b200.synth import Scene
+
+        sc = Scene(47, S, B, 5)
+        rv = sc.generate(0, L)
+        d, c = torch.from_numpy(sc.dark).cuda(), torch.from_numpy(sc.coeff).cuda()
+        f64 = torch.float64
+        ws_bytes = int(_lib.load().skyrx_stats_raw_workspace(B))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        shift = torch.zeros(B, dtype=f64, device="cuda")
+        m1 = torch.zeros(1 + B + B * B, dtype=f64, device="cuda")
+        m2 = torch.zeros_like(m1)
+        fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+        args = (rv.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(), 1.0)
+        _lib.call("skyrx_stats_raw_own_shift", *args, shift.data_ptr(), m1.data_ptr(),
+                  fl.data_ptr(), ws.data_ptr(), ws_bytes, _dev.stream_ptr())
+        _lib.call("skyrx_stats_raw", *args, shift.data_ptr(), m2.data_ptr(), fl.data_ptr(),
+                  ws.data_ptr(), ws_bytes, _dev.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(m1, m2)
+        raw = rv.cpu().numpy()
+        ref = O.compute_stats(O.apply_calibration(raw, sc.dark, sc.coeff, np.ones(L)))
+        assert np.array_equal(shift.cpu().numpy(), ref.mu.astype(np.float32).astype(np.float64)) \
+            or normwise(shift.cpu().numpy(), ref.mu) < 1e-7
+        n = m1[0].item()
+        mu = shift.cpu().numpy() + m1[1:1 + B].cpu().numpy() / n
+        assert normwise(mu, ref.mu) < 1e-8
+
     def test_raw_path_clamp_fallback(self, P):
         # a value below its dark level clamps to 0 (calibrate.py:99): the raw-byte
         # algebra no longer holds, so detect() must redo the fit in f64
