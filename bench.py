@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-strips", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the oracle check of strip 0 after the timed region")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every step eagerly instead of replaying one captured CUDA graph")
     return ap.parse_args()
@@ -120,7 +122,7 @@ class ClockSampler:
                 self.path.write_text(out)
             except (OSError, subprocess.TimeoutExpired):
                 pass
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, power = [], None, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for line in self.path.read_text().splitlines():
             parts = [x.strip() for x in line.split(",")]
@@ -129,48 +131,148 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 smax = float(parts[2])
+                power.append(float(parts[3]))
             except ValueError:
                 continue
             for name, val in zip(names, parts[4:8]):
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(power) if power else None,
+                "power_w_max": max(power) if power else None}
 
 
 # ----------------------------------------------------------------------------- reference arm
+def import_reference():
+    """The UNMODIFIED reference package, installed once with
+    ``pip install --no-index --no-build-isolation --no-deps --target baseline/_ref``
+    from a copy of /root/reference/pkg.  None when absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "skyrx" / "rx.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_skyrx_ref")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import skyrx._accel
+    import skyrx.calibrate
+    import skyrx.cube
+    import skyrx.rx
+    return skyrx
+
+
+def host_info():
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import threadpoolctl
+
+        info["blas_threads"] = sorted({d.get("num_threads") for d in
+                                       threadpoolctl.threadpool_info()
+                                       if d.get("user_api") == "blas"})
+    except Exception:
+        pass
+    return info
+
+
+class ReferenceDetect:
+    """One bounded sample of the workload through the reference's own public API:
+    skyrx.calibrate.apply_calibration -> skyrx.rx.compute_stats -> skyrx.rx.rx_scores
+    (its default numba scorer, _accel.py:75-90, or the numpy one with ``numpy=True``,
+    _accel.py:33-47) -> the top-0.1 % mask (R-TOPK is not in the reference: the
+    oracle's np.partition restatement).  Falls back to the oracle port when the
+    reference is not installed."""
+
+    def __init__(self, raw, dark, coeff, B, numpy_scorer=False):
+        from oracle import skyrx_oracle as O
+
+        self.O = O
+        self.raw, self.dark, self.coeff = raw, dark, coeff
+        self.sk = import_reference()
+        self.kind = "reference" if self.sk is not None else "port"
+        if self.sk is not None:
+            sk = self.sk
+            ins = sk.cube.InsSample(0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0)
+            meta = tuple(sk.cube.LineMeta(i, 1.0, ins, ins) for i in range(raw.shape[0]))
+            self.cube = sk.cube.RawCube(raw, np.linspace(400, 1000, B), meta)
+            self.tables = sk.calibrate.CalibrationTables(dark, coeff)
+            self.scorer = (sk._accel.mahalanobis_sq_numpy if numpy_scorer
+                           else sk._accel.mahalanobis_sq)
+            self.backend = ("numpy (SKYRX_NO_NUMBA path)" if numpy_scorer or not
+                            sk._accel.HAS_NUMBA else "numba (default)")
+        else:
+            self.backend = "oracle port (numpy/OpenBLAS/LAPACK)"
+
+    def __call__(self):
+        if self.sk is None:
+            return self.O.detect(self.raw, self.dark, self.coeff, np.ones(self.raw.shape[0]))
+        sk = self.sk
+        keep = sk._accel.mahalanobis_sq
+        sk._accel.mahalanobis_sq = self.scorer   # rx.py:96 looks it up per call
+        try:
+            rad = sk.calibrate.apply_calibration(self.cube, self.tables)
+            st = sk.rx.compute_stats(rad)
+            sc = sk.rx.rx_scores(rad, st)
+        finally:
+            sk._accel.mahalanobis_sq = keep
+        return st, sc.values, self.O.topk_mask(sc.values)
+
+
+def time_reference(raw, dark, coeff, B, steps, warmup, budget_s=None, numpy_scorer=False):
+    """Mean seconds per call of ReferenceDetect on ``raw`` (warm-up untimed)."""
+    fn = ReferenceDetect(raw, dark, coeff, B, numpy_scorer)
+    for _ in range(max(warmup, 1)):
+        fn()
+    times = []
+    t0 = time.perf_counter()
+    for _ in range(max(steps, 1)):
+        a = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - a)
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    return float(np.mean(times)), len(times), fn
+
+
+def cpu_sample_lines(cfg, lines):
+    return min(lines, 512 if cfg["bands"] <= 128 else 96)
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    from oracle import skyrx_oracle as O
     from oracle import synth as osynth
 
     lines = args.lines or cfg["lines"]
-    sample_lines = min(lines, 512 if cfg["bands"] <= 128 else 96)
+    sample_lines = cpu_sample_lines(cfg, lines)
     t = osynth.make_tables(cfg["seed"], cfg["samples"], cfg["bands"], cfg["components"])
     raw = osynth.generate_lines(t, 0, sample_lines)
-    gains = np.ones(sample_lines)
-    for _ in range(max(args.warmup, 1)):
-        O.detect(raw, t.dark, t.coeff, gains)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.detect(raw, t.dark, t.coeff, gains)
-        times.append(time.perf_counter() - t0)
+    sec, reps, fn = time_reference(raw, t.dark, t.coeff, cfg["bands"], args.steps, args.warmup)
     px = sample_lines * cfg["samples"]
-    sec = float(np.mean(times))
     value = px / sec
-    cores = os.cpu_count()
+    hi = host_info()
     line = {
         "impl": "reference", "metric": "calibrated+RX-scored pixels/sec", "value": value,
         "unit": "pixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle/synth.py, seeded)",
+        "vs_baseline": None, "dtype": "f32 radiance, f64 stats and scores",
+        "data": "synthetic (oracle/synth.py, seeded)",
         "config": config_key(args, cfg, world),
-        "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": hi["cpu_count"],
+                         "kind": fn.kind,
                          "sample": f"{sample_lines} lines x {cfg['samples']} samples of strip 0 "
-                                   f"(seed {cfg['seed']}), full oracle detect path "
-                                   "(numpy/OpenBLAS/LAPACK, all host threads)"},
+                                   f"(seed {cfg['seed']}) per step, {reps} steps; "
+                                   + ("skyrx apply_calibration -> compute_stats -> rx_scores "
+                                      f"[{fn.backend}] -> top-0.1% mask (baseline/_ref)"
+                                      if fn.kind == "reference" else
+                                      f"oracle detect [{fn.backend}]"),
+                         "host": hi},
         "e2e": {"value": value, "unit": "pixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -193,14 +295,54 @@ def config_key(args, cfg, world):
 
 
 # ----------------------------------------------------------------------------- b200 arm
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch(args):
+    """--gpus N without a torchrun environment: re-exec under torchrun with N
+    ranks (one process per GPU, NCCL).  Under torchrun, WORLD_SIZE must equal
+    --gpus.  Returns (rank, world, local)."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    world = int(ws or "1")
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch with "
+                         f"torchrun --nproc-per-node {args.gpus} or without torchrun")
+    return int(os.environ.get("RANK", "0")), world, int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def init_dist(local):
+    """One NCCL process group whenever torchrun launched us (N = 1 included, so
+    the collectives of the multi-GPU path run even on a one-GPU lease)."""
+    import torch
+    import torch.distributed as dist
+
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPUs")
+    torch.cuda.set_device(local)
+    if "WORLD_SIZE" in os.environ and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist.is_initialized()
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, cfg, rank, world)
+        ws = os.environ.get("WORLD_SIZE")
+        return run_reference(args, cfg, int(os.environ.get("RANK", "0")),
+                             int(ws) if ws else args.gpus)
+    rank, world, local = launch(args)
     if args.config == "c2":
         return run_stream(args, cfg, rank, world, local)
     if args.config == "c5":
@@ -209,65 +351,53 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    distributed = init_dist(local)
     import paper_2602_13509_b200 as P
     from paper_2602_13509_b200 import _dev
+    from paper_2602_13509_b200.strips import REDO_FLAGS, StripBatch, shard_strips
     from paper_2602_13509_b200.synth import Scene
 
     lines = args.lines or cfg["lines"]
     S, B = cfg["samples"], cfg["bands"]
     nstrips = args.strips or cfg["strips"]
-    mine = list(range(rank, nstrips, world))
+    # the package's strip sharding (strips.shard_strips: strip i -> rank i % world)
+    mine = shard_strips(nstrips, rank, world)
+    if not mine:
+        raise SystemExit(f"bench: {nstrips} strips leave rank {rank} of {world} without work")
     npix = lines * S
     scenes = [Scene(cfg["seed"] + i if nstrips > 1 else cfg["seed"], S, B, cfg["components"])
               for i in mine]
     raws = [sc.generate(0, lines) for sc in scenes]
     tabs = [(_dev.to_device(sc.dark), _dev.to_device(sc.coeff)) for sc in scenes]
-    gains = _dev.to_device(np.ones(lines, np.float32))
-    plan = P.DetectPlan(lines, S, B, batch=len(mine))
+    gains_t = _dev.to_device(np.ones(lines, np.float32))
+    gains = [gains_t] * len(mine)
+    gconst = [1.0] * len(mine)   # every line gain 1.0; tables are finite
+    batch = StripBatch(lines, S, B, len(mine))
+    plan = batch.plan
     stream = torch.cuda.current_stream()
     flush = None
     if len(mine) * npix * B * 2 <= 4 * 126e6:
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
-    ev = {"gram": [], "score": [], "kernel": [], "gram_kernel": []}
-
+    ev = {"gram": [], "score": []}
     step_ev = []
+
+    def pair():
+        return (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 
     def step(instrument=False):
         if flush is not None:
             flush.zero_()  # outside the per-step events below
         if instrument:
-            sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            sa, sb = pair()
             sa.record(stream)
-        for j in range(len(mine)):
-            raw = raws[j]
-            d, c = tabs[j]
-            gev = None
-            if instrument:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                gev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                a.record(stream)
-            plan.run(j, raw, d, c, gains, gain_const=1.0, events=gev)
-            if instrument:
-                b.record(stream)
-                ev["gram"].append((a, b))
-                ev["gram_kernel"].append(gev)
-        plan.finalize()
-        for j in range(len(mine)):
-            d, c = tabs[j]
-            kev = None
-            if instrument:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                a.record(stream)
-            plan.score(j, raws[j], d, c, gains, events=kev)
-            if instrument:
-                b.record(stream)
-                ev["score"].append((a, b))
-                ev["kernel"].append(kev)
+            gev = [pair() for _ in mine]
+            kev = [pair() for _ in mine]
+            ev["gram"] += gev
+            ev["score"] += kev
+        batch.enqueue(raws, tabs, gains, gconst,
+                      moment_events=gev if instrument else None,
+                      score_events=kev if instrument else None)
         if instrument:
             sb.record(stream)
             step_ev.append((sa, sb))
@@ -275,7 +405,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    plan.ds.check(0, npix)
+    batch.verify(raws, tabs, gains)
     # the step as one CUDA graph (every kernel of every strip, no host work between
     # launches); inputs larger than L2 only — the L2-flushed configs time eager steps
     graph = None
@@ -295,7 +425,7 @@ def main():
             torch.cuda.synchronize()
             step()
             torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -309,63 +439,52 @@ def main():
                 step(instrument=True)
         end.record(stream)
         torch.cuda.synchronize()
-        if graph is not None:
-            # per-kernel events (roofline) from eager steps, outside the timed region
-            for _ in range(max(1, min(args.steps, 2))):
-                step(instrument=True)
-            torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     ms = start.elapsed_time(end)
     if flush is not None:  # device time of the steps themselves, L2 flushes excluded
         ms = float(sum(a.elapsed_time(b) for a, b in step_ev))
     if graph is None:
         launches = (plan.launches - launches0) // args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    # what the timed steps produced, checked before anything else runs: status and
+    # flags of EVERY strip of this rank (a clamp, a counts >= 4096 or a missing
+    # no-clamp proof would mean the timed kernels computed the wrong thing)
+    st, fl = batch.flags()
+    bad = int(((st != 0) | ((fl & REDO_FLAGS) != 0)).sum())
+    if graph is not None:
+        # per-kernel events (roofline) from eager steps, outside the timed region
+        for _ in range(max(1, min(args.steps, 2))):
+            step(instrument=True)
+        torch.cuda.synchronize()
+    if distributed:
+        t = torch.tensor([ms, float(bad)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(t[0].item())
+        tb = torch.tensor([bad], device="cuda", dtype=torch.int64)
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        bad = int(tb.item())
     total_px = nstrips * npix * args.steps
     value = total_px / (ms / 1e3)
 
-    # dominant kernel and its roofline: CUDA events on `stream` around the
-    # fused calibrate+score kernel alone (its algorithmic bytes: 2B raw read +
-    # 4 B f32 delta write per pixel)
-    gram_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["gram"]]))
-    score_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["score"]]))
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["kernel"]]))
-    gk = [e for e in ev["gram_kernel"] if e is not None]
-    try:
-        gram_k_ms = float(np.mean([a.elapsed_time(b) for a, b in gk])) if gk else 0.0
-    except RuntimeError:  # events never recorded (moments took another path)
-        gram_k_ms = 0.0
+    # dominant kernel and its roofline: CUDA events on `stream` around each
+    # kernel call alone (moments: 2B raw read per pixel; fused calibrate+score:
+    # 2B raw read + 4 B f32 delta write per pixel)
+    gram_k_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["gram"]]))
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["score"]]))
     peak, peak_kind = load_peaks()
-    # the dominant of the two passes over the raw cube: fused calibrate+score
-    # (2B raw read + 4 B score write per pixel) or raw-byte moments (2B raw read;
-    # the call also runs the two tiny partial-reduction kernels)
-    # the kernels this geometry runs (rx.DetectPlan dispatch)
     if B > 128:
         gname, sname = "raww_gram_kernel (+scan, per-pass)", "score_tcw_kernel"
     else:
         gname = "gram_raw_kernel (+reduce)"
         sname = ("score_tcs_kernel" if plan.tcs else
                  "score_tc_kernel" if plan.tc else "score_kernel")
+    g_bytes, s_bytes = npix * 2 * B, npix * (2 * B + 4)
     if gram_k_ms > kern_ms:
-        kname, dom_bytes, kern_ms, other = (gname, npix * 2 * B, gram_k_ms, (sname, kern_ms))
+        kname, dom_bytes, dom_ms, other = gname, g_bytes, gram_k_ms, (sname, kern_ms, s_bytes)
     else:
-        kname, dom_bytes, other = sname, npix * (2 * B + 4), (gname, gram_k_ms)
-    achieved = dom_bytes / (kern_ms / 1e3) / 1e9
-    traffic = None
-    tp = ROOT / "profiles" / "ncu_traffic.json"
-    if tp.exists():
-        try:
-            # captured for the c4 kernels (profiles/ncu_traffic.json): per launch of
-            # that geometry only
-            tj = json.loads(tp.read_text())
-            if tj.get("geometry") == [lines, S, B]:
-                traffic = tj.get(kname.split()[0])
-        except Exception:
-            traffic = None
+        kname, dom_bytes, dom_ms, other = sname, s_bytes, kern_ms, (gname, gram_k_ms, g_bytes)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    traffic = ncu_traffic(kname, (lines, S, B))
 
     line = {
         "metric": "calibrated+RX-scored pixels/sec", "value": value, "unit": "pixels/s",
@@ -378,22 +497,87 @@ def main():
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "bytes_per_launch": dom_bytes, "ms_per_launch": kern_ms,
-                     "stats_ms_per_strip": gram_ms, "score_path_ms_per_strip": score_ms,
-                     "other_pass": {"kernel": other[0], "ms_per_launch": other[1]}},
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
+                     "other_pass": {"kernel": other[0], "ms_per_launch": other[1],
+                                    "bytes_per_launch": other[2],
+                                    "frac": other[2] / (other[1] / 1e3) / 1e9 / peak}},
         "gpu_launches": launches,
         "launch_mode": "cuda_graph (one captured step replayed)" if graph is not None else "eager",
         "clocks": clocks.summary(),
     }
-
+    parity = {"strips_checked": nstrips, "strips_not_ok": bad,
+              "check": "status == OK and flags & (2|4|16|32) == 0 for every strip of every rank "
+                       "after the timed steps"}
+    if bad:
+        line["invalid"] = f"{bad} strips did not take the timed fast path"
+    if rank == 0 and not args.no_parity:
+        parity.update(strip_parity(batch, raws[0], scenes[0], lines, cfg, mine[0]))
+    line["parity"] = parity
     if rank == 0 and not args.no_e2e:
         line["e2e"] = measure_e2e(args, P, cfg, lines, scenes[: max(1, args.e2e_strips)])
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, raws[0], scenes[0], lines)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
+
+
+def ncu_traffic(kname, geometry):
+    """dram read+write bytes per launch of that kernel from the committed
+    `ncu --set full` capture of this geometry (profiles/ncu_traffic.json)."""
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if not tp.exists():
+        return None
+    try:
+        tj = json.loads(tp.read_text())
+        for entry in tj if isinstance(tj, list) else [tj]:
+            if entry.get("geometry") == list(geometry):
+                return entry.get(kname.split()[0])
+    except Exception:
+        return None
+    return None
+
+
+def strip_parity(batch, raw_dev, scene, lines, cfg, index):
+    """The timed outputs of this rank's first strip against the CPU oracle on the
+    same raw counts (BASELINE tolerances: stats 1e-5, scores 1e-4 per pixel, mask
+    exact outside the 1e-4 band around the threshold), plus the Sigma^-1 error
+    split into its two parts: ours vs the reference's algorithm
+    on EXACT radiance, and the reference's own f32-radiance rounding."""
+    from oracle import skyrx_oracle as O
+
+    t0 = time.perf_counter()
+    raw = raw_dev.cpu().numpy()
+    det = batch.detection(0, host=True)
+    gains = np.ones(lines)
+    want_stats, want_sc, want_mask = O.detect(raw, scene.dark, scene.coeff, gains)
+    exact = O.compute_stats_exact(raw, scene.dark, scene.coeff, gains)
+
+    def nw(a, b):
+        return float(np.abs(np.asarray(a) - np.asarray(b)).max() / np.abs(np.asarray(b)).max())
+
+    rel = np.abs(det.scores - want_sc) / np.maximum(want_sc, 1e-12)
+    thr = O.topk_threshold(want_sc)
+    differ = det.mask != want_mask
+    near = np.abs(want_sc - thr) <= 1e-4 * abs(thr)
+    out = {
+        "strip": index, "pixels": int(want_sc.size),
+        "mu_rel": nw(det.stats.mu, want_stats.mu),
+        "sigma_rel": nw(det.stats.sigma, want_stats.sigma),
+        "sigma_inv_rel": nw(det.stats.sigma_inv, want_stats.sigma_inv),
+        "sigma_inv_rel_vs_exact_radiance": nw(det.stats.sigma_inv, exact.sigma_inv),
+        "reference_f32_rounding_sigma_inv_rel": nw(want_stats.sigma_inv, exact.sigma_inv),
+        "ridge_equal": det.stats.ridge_used == want_stats.ridge_used,
+        "score_max_rel": float(rel.max()),
+        "threshold_rel": abs(det.threshold - thr) / abs(thr),
+        "mask_differ": int(differ.sum()), "mask_differ_outside_band": int((differ & ~near).sum()),
+        "tolerances": {"stats": 1e-5, "scores": 1e-4, "mask_band": 1e-4},
+        "oracle_s": time.perf_counter() - t0,
+    }
+    out["pass"] = bool(out["mu_rel"] < 1e-5 and out["sigma_rel"] < 1e-5 and out["ridge_equal"]
+                       and out["score_max_rel"] < 1e-4 and out["mask_differ_outside_band"] == 0)
+    return out
 
 
 # ----------------------------------------------------------------------------- c2: streaming
@@ -407,7 +591,7 @@ def run_stream(args, cfg, rank, world, local):
     chunks (H2D, graph replay, D2H of scores + mask, host sync per chunk)."""
     import torch
 
-    torch.cuda.set_device(local)
+    init_dist(local)
     import paper_2602_13509_b200 as P
     from paper_2602_13509_b200.stream import StreamingRX
     from paper_2602_13509_b200.synth import Scene
@@ -491,9 +675,7 @@ def run_global(args, cfg, rank, world, local):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    distributed = init_dist(local)
     import paper_2602_13509_b200 as P
     from paper_2602_13509_b200.distributed import GlobalRX
     from paper_2602_13509_b200.synth import Scene
@@ -509,7 +691,7 @@ def run_global(args, cfg, rank, world, local):
     for _ in range(args.warmup):
         det = g.detect(raw)
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -519,7 +701,7 @@ def run_global(args, cfg, rank, world, local):
         end.record(stream)
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
-    if world > 1:
+    if distributed:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -537,9 +719,14 @@ def run_global(args, cfg, rank, world, local):
             "global_threshold": det.threshold, "global_max": det.max_score,
             "gpu_launches": g.ops.plan.launches // max(1, args.steps + args.warmup),
             "clocks": clocks.summary(),
+            "collectives": (f"{dist.get_backend()} (broadcast shift, SUM f64 moments, MAX flags "
+                            "and max key, 3 x SUM radix histogram)") if distributed else
+                           "none (single process: launch under torchrun for the NCCL path)",
         }
+        if distributed and dist.get_backend() == "nccl":
+            line["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
@@ -574,23 +761,26 @@ def measure_e2e(args, P, cfg, lines, scenes):
 
 
 def cpu_baseline(cfg, raw_dev, scene, lines):
-    from oracle import skyrx_oracle as O
-
-    sample = min(lines, 512 if cfg["bands"] <= 128 else 96)
+    """The reference's own CPU path (baseline/_ref, numba default scorer) on a
+    bounded sample of strip 0, on this box's host cores; the SKYRX_NO_NUMBA
+    numpy scorer beside it (_accel.py:21-31)."""
+    sample = cpu_sample_lines(cfg, lines)
     raw = raw_dev[:sample].cpu().numpy()
-    gains = np.ones(sample)
-    O.detect(raw, scene.dark, scene.coeff, gains)
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        O.detect(raw, scene.dark, scene.coeff, gains)
-        reps += 1
-        if time.perf_counter() - t0 > 10.0 or reps >= 20:
-            break
-    sec = (time.perf_counter() - t0) / reps
-    return {"value": sample * cfg["samples"] / sec, "unit": "pixels/s", "cores": os.cpu_count(),
-            "kind": "port", "sample": f"{sample} lines x {cfg['samples']} samples of strip 0, "
-                                      f"oracle detect (numpy/OpenBLAS/LAPACK), {reps} reps"}
+    sec, reps, fn = time_reference(raw, scene.dark, scene.coeff, cfg["bands"], 20, 1,
+                                   budget_s=10.0)
+    out = {"value": sample * cfg["samples"] / sec, "unit": "pixels/s",
+           "cores": os.cpu_count(), "kind": fn.kind,
+           "sample": f"{sample} lines x {cfg['samples']} samples of strip 0, {reps} reps; "
+                     + ("skyrx apply_calibration -> compute_stats -> rx_scores "
+                        f"[{fn.backend}] -> top-0.1% mask (baseline/_ref)"
+                        if fn.kind == "reference" else f"oracle detect [{fn.backend}]"),
+           "host": host_info()}
+    if fn.kind == "reference":
+        sec2, reps2, fn2 = time_reference(raw, scene.dark, scene.coeff, cfg["bands"], 5, 1,
+                                          budget_s=5.0, numpy_scorer=True)
+        out["numpy_scorer"] = {"value": sample * cfg["samples"] / sec2, "reps": reps2,
+                               "backend": fn2.backend}
+    return out
 
 
 if __name__ == "__main__":

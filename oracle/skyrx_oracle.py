@@ -182,6 +182,38 @@ def compute_stats(values, chunk: int = 65536) -> Stats:
     return factor_covariance(mu, cov)
 
 
+def compute_stats_exact(raw, dark, coeff, gains, chunk_lines: int = 256) -> Stats:
+    """rx.py:42-86's algorithm on the EXACT radiance max(raw - dark, 0) * coeff / gain
+    (f64 arithmetic, no f32 rounding of the radiance): a diagnostic that splits a
+    Sigma^-1 difference into the part the reference's own f32 radiance rounding
+    (calibrate.py:98-101) causes and the part a kernel causes.  Two passes over
+    line chunks, like rx.py:56-66, so full strips fit in host memory."""
+    raw = np.asarray(raw)
+    dark = np.asarray(dark, np.float64)
+    coeff = np.asarray(coeff, np.float64)
+    g = line_gains(gains).astype(np.float64)
+    L, S, B = raw.shape
+    n = L * S
+    if n <= B:
+        raise ValueError(f"insufficient samples: {n} pixels for {B} bands")
+
+    def rad(a, b):
+        x = np.maximum(raw[a:b].astype(np.float64) - dark[None], 0.0) * coeff[None]
+        return (x / g[a:b, None, None]).reshape(-1, B)
+
+    mu = np.zeros(B)
+    for a in range(0, L, chunk_lines):
+        mu += rad(a, min(L, a + chunk_lines)).sum(axis=0)
+    mu /= n
+    cov = np.zeros((B, B))
+    for a in range(0, L, chunk_lines):
+        d = rad(a, min(L, a + chunk_lines)) - mu
+        cov += d.T @ d
+    cov /= n - 1
+    cov = (cov + cov.T) / 2.0
+    return factor_covariance(mu, cov)
+
+
 # --------------------------------------------------------------------------- scoring
 def mahalanobis_sq(pixels, mu, chol_lower, chunk: int = 65536) -> np.ndarray:
     """_accel.py:33-47 — delta = ||L^-1 (x - mu)||^2 per row, float64."""

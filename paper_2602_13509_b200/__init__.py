@@ -36,6 +36,7 @@ from .rx import (
     transmit_domain,
 )
 from .stream import ChunkResult, StreamingRX
+from .strips import StripBatch, StripsResult, detect_strips, shard_strips
 from .datalink import (cube_frames, encode_scores_half, frames_for_cube, link_payload,
                        pack_rgb565, packetize_cube)
 from .air import AirResult, StageTiming, run_air
@@ -49,7 +50,8 @@ __all__ = [
     "band_nearest", "CalibrationTables", "apply_calibration", "bin_bands", "calibrate_bin_rgb",
     "discard_oob_bands", "extract_rgb", "CubeStats", "DetectPlan", "DeviceStats",
     "compute_stats", "detect", "detect_batch", "normalize_scores", "rx_scores", "threshold_scores",
-    "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install", "__version__",
+    "topk_mask", "transmit_domain", "StreamingRX", "ChunkResult", "install",
+    "StripBatch", "StripsResult", "detect_strips", "shard_strips", "__version__",
     "link_payload", "pack_rgb565", "encode_scores_half", "packetize_cube", "frames_for_cube",
     "cube_frames", "ErasureCode", "run_air", "AirResult", "StageTiming", "read_cube",
     "write_cube",

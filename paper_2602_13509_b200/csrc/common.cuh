@@ -44,7 +44,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // calibrate.py:98-101: out = max(0, f32(raw) - dark) * coeff / gain, each op RN.
 __device__ __forceinline__ float calib(float raw, float dark, float coeff, float gain) {
   float t = __fsub_rn(raw, dark);
-  t = fmaxf(t, 0.0f);
+  t = t < 0.0f ? 0.0f : t;  // np.maximum keeps NaN (a NaN dark must stay non-finite)
   t = __fmul_rn(t, coeff);
   return __fdiv_rn(t, gain);
 }

@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
             const int k = gi * 16 + q4 * 4 + q;
             int D = 0;
             if (valid && k < B) {
-              float x = __fmul_rn(fmaxf(__fsub_rn((float)rp[k], dk[k]), 0.0f), ck[k]);
+              const float t = __fsub_rn((float)rp[k], dk[k]);
+              float x = __fmul_rn(t < 0.0f ? 0.0f : t, ck[k]);
               if (g != 1.0f) x = __fdiv_rn(x, g);
               finite_ok &= isfinite(x);
               const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);

@@ -65,12 +65,16 @@ __global__ void mask_gt_kernel(const float* __restrict__ v, int64_t n,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float4 x = v4[i];
+    if (t == -INFINITY) {  // k >= n (topk_threshold's "select all"): oracle's np.ones
+      m4[i] = 0x01010101u;
+      continue;
+    }
     m4[i] = (uint32_t)(x.x > t) | ((uint32_t)(x.y > t) << 8) | ((uint32_t)(x.z > t) << 16) |
             ((uint32_t)(x.w > t) << 24);
   }
   for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    mask[i] = v[i] > t;
+    mask[i] = t == -INFINITY || v[i] > t;
 }
 
 __global__ void mask_gt_scalar_kernel(const float* __restrict__ v, int64_t n,
@@ -78,7 +82,7 @@ __global__ void mask_gt_scalar_kernel(const float* __restrict__ v, int64_t n,
   const float t = *thr;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    mask[i] = v[i] > t;
+    mask[i] = t == -INFINITY || v[i] > t;
 }
 
 __device__ __forceinline__ void digit_params(int digit, int& shift, int& bits) {
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kMaskThreads) topk_mask_pass_kernel(
       const uint32_t d0 = key >> 21;
       bool in = false;
       if (all) {
-        word |= (uint32_t)(xv[q] > -INFINITY) << (8 * q);
+        word |= 1u << (8 * q);  // k >= n: every score, -inf and NaN included
       } else {
         word |= (uint32_t)(d0 > b0) << (8 * q);
         in = ok && d0 == b0;
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kMaskThreads) topk_mask_pass_kernel(
     for (int64_t i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) {
       const uint32_t key = f2ord(v[i]);
       if (all) {
-        mask[i] = v[i] > -INFINITY;
+        mask[i] = 1;
       } else {
         mask[i] = (key >> 21) > b0;
         if ((key >> 21) == b0) {

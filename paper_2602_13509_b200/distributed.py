@@ -131,16 +131,18 @@ class CudaOps:
 
 def global_detect(raw_block, ops, n_total: int, group=None, k: int | None = None):
     """Run the R-GLOBAL protocol on this rank's block (collectives on `group`)."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    # every collective runs whenever a process group exists (N = 1 included, so
+    # the NCCL path is exercised on a single-GPU lease); none without one
+    distributed = dist.is_available() and dist.is_initialized()
 
     def allreduce(t, op):
-        if world > 1:
+        if distributed:
             dist.all_reduce(t, op=op, group=group)
         return t
 
     # 1. common shift from the first block
     shift = ops.shift(raw_block)
-    if world > 1:
+    if distributed:
         dist.broadcast(shift, src=dist.get_global_rank(group, 0) if group is not None else 0,
                        group=group)
     # 2. moments + flags, summed / or-ed over ranks; identical finalize everywhere

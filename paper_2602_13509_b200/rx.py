@@ -555,6 +555,10 @@ def constant_gain(gains, tables) -> float | None:
     g0 = float(np.float32(g.flat[0]))
     if not g0 > 0.0:
         return None
+    # a non-finite dark entry makes radiance non-finite (rx.py:53-54); only the
+    # general moments kernel flags that, so leave such tables to it
+    if not np.isfinite(np.asarray(tables.dark, np.float32)).all():
+        return None
     if not np.isfinite(np.float32(65535.0) * np.float32(tables.coeff.max()) / np.float32(g0)):
         return None
     return g0

@@ -119,6 +119,26 @@ class TestCalibration:
         with pytest.raises(ValueError, match="non-finite"):
             P.detect(raw, t)
 
+    def test_nan_dark_is_nonfinite(self, P):
+        # np.maximum keeps NaN (calibrate.py:99), so a NaN dark entry makes that
+        # radiance column NaN and the fit raises rx.py:53-54's error, on every path
+        L, S, B = 300, 900, 70
+        t = osynth.make_tables(46, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        dark = t.dark.copy()
+        dark[17, 3] = np.nan
+        tab = P.CalibrationTables(dark, t.coeff)
+        out = P.apply_calibration(raw_cube(P, raw), tab).values
+        want = O.apply_calibration(raw, dark, t.coeff, np.ones(L))
+        assert np.array_equal(np.isnan(out), np.isnan(want)) and np.isnan(want).sum() == L
+        ok = ~np.isnan(want)
+        assert np.array_equal(bits(out[ok]), bits(want[ok]))
+        with pytest.raises(ValueError, match="non-finite"):
+            P.detect(raw_cube(P, raw), tab)
+        with pytest.raises(ValueError, match="non-finite"):
+            P.compute_stats(P.RadianceCube(out, np.linspace(400, 1000, B),
+                                           P.cube.line_meta_for([1.0] * L)))
+
     @pytest.mark.parametrize("name", ["b300", "b44", "b340f8"])
     def test_fused_bin_rgb_bit_exact(self, P, golden, name):
         g = golden["calibrate"]
@@ -288,6 +308,14 @@ class TestTopK:
         v = (rng.random(n) * rng.choice([1, 10, 1e4], n)).astype(np.float32)
         got = P.topk_mask(v, k)
         assert np.array_equal(got, O.topk_mask(v, k))
+
+    @pytest.mark.parametrize("n", [3, 8, 4099])
+    def test_select_all_includes_inf_and_nan(self, P, n):
+        # k >= n: the oracle returns np.ones, so -inf and NaN scores are selected too
+        v = np.arange(n, dtype=np.float32)
+        v[0], v[-1] = -np.inf, np.nan
+        assert P.topk_mask(v, n).all() and O.topk_mask(v, n).all()
+        assert P.topk_mask(v, n + 5).all()
 
     def test_ties(self, P):
         v = np.array([1, 2, 2, 2, 0], np.float32)
