@@ -562,26 +562,28 @@ __global__ void pack_whiten_kernel(const double* __restrict__ w64, int B, uint8_
   // one power-of-two scale for the whole matrix (the epilogue then squares raw
   // accumulators and multiplies once); tiny rows stay accurate in absolute terms,
   // which is what delta = sum_j z_j^2 needs
-  __shared__ double smx[128];
+  __shared__ double smx[32];
   double m0 = 0.0;
-  for (size_t e = threadIdx.x; e < (size_t)B * B; e += blockDim.x) m0 = fmax(m0, fabs(W[e]));
-  smx[threadIdx.x] = m0;
+  for (int e = threadIdx.x; e < B * B; e += blockDim.x) m0 = fmax(m0, fabs(W[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = m0;
   __syncthreads();
   double mx = 0.0;
-  for (int i = 0; i < (int)blockDim.x; ++i) mx = fmax(mx, smx[i]);
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, smx[i]);
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);           // mx in [2^(e-1), 2^e)
   const double sc = ldexp(1.0, 14 - e);  // max scaled value in [2^13, 2^14)
-  for (int jn = threadIdx.x; jn < KP; jn += blockDim.x) {
-    colscale[jn] = (float)ldexp(1.0, e - 14);
-    for (int k = 0; k < KP; ++k) {
-      const double v = (jn < B && k < B && k <= jn) ? W[(size_t)jn * B + k] * sc : 0.0;
-      const __half hh = __double2half(v);
-      const __half l = __double2half(v - (double)__half2float(hh));
-      const uint32_t off = (jn >> 3) * SBO_B + (k >> 3) * 128u + (jn & 7) * 16u + (k & 7) * 2u;
-      *reinterpret_cast<__half*>(o + off) = hh;
-      *reinterpret_cast<__half*>(o + W_BYTES + off) = l;
-    }
+  for (int jn = threadIdx.x; jn < KP; jn += blockDim.x) colscale[jn] = (float)ldexp(1.0, e - 14);
+  // one thread per (jn, k) entry, k fastest: neighbouring threads write neighbouring halves
+  for (int t = threadIdx.x; t < KP * KP; t += blockDim.x) {
+    const int jn = t / KP, k = t - jn * KP;
+    const double v = (jn < B && k < B && k <= jn) ? W[(size_t)jn * B + k] * sc : 0.0;
+    const __half hh = __double2half(v);
+    const __half l = __double2half(v - (double)__half2float(hh));
+    const uint32_t off = (jn >> 3) * SBO_B + (k >> 3) * 128u + (jn & 7) * 16u + (k & 7) * 2u;
+    *reinterpret_cast<__half*>(o + off) = hh;
+    *reinterpret_cast<__half*>(o + W_BYTES + off) = l;
   }
 }
 
@@ -652,7 +654,7 @@ extern "C" int skyrx_pack_whiten(const double* whiten64, int32_t bands, int32_t 
   switch (kp_for(bands)) {
 #define SKYRX_KP(k) \
   case k:           \
-    pack_whiten_kernel<k><<<batch, 128, 0, st>>>(whiten64, bands, (uint8_t*)wpack); break;
+    pack_whiten_kernel<k><<<batch, 512, 0, st>>>(whiten64, bands, (uint8_t*)wpack); break;
     SKYRX_KP(16) SKYRX_KP(32) SKYRX_KP(48) SKYRX_KP(64) SKYRX_KP(80)
 #undef SKYRX_KP
   }

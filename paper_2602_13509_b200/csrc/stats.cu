@@ -15,6 +15,8 @@
 // tiles is distributed over threads (tile, pixel-group); each thread keeps an
 // 8x8 FP32 + 8x8 FP64 register accumulator and reads its two 8-band slices of
 // every pixel of its group from the shared-memory tile (4 LDS.128 / 64 FFMA).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tile_loader.cuh"
 
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int c = c0 + ln + 32 * q;
-            if (c <= j) Wi[c] = x[q] - lij * (z[q] * rj);
+            if (c <= j) Wi[c] = __dsub_rn(x[q], __dmul_rn(lij, z[q] * rj));  // FMA-free
           }
         }
       }
@@ -734,6 +736,11 @@ __global__ void whiten_prepare_kernel(const double* __restrict__ L, const double
   }
 }
 
+int launch_finalize_small(const double* moments, const double* shift, const int32_t* flags,
+                          int B, int batch, double* mu, double* sigma, double* chol,
+                          double* sigma_inv, double* w64, float* wf, int ld_w, float* mhl,
+                          double* ridge, int32_t* status, cudaStream_t st);
+
 }  // namespace skyrx
 
 using namespace skyrx;
@@ -849,6 +856,10 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
   SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
   SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
+  if (bands <= 80 && getenv("SKYRX_B200_FIN_GENERAL") == nullptr)  // latency kernel (finalize_small.cu)
+    return launch_finalize_small(moments, shift, flags, bands, batch, mu, sigma, chol, sigma_inv,
+                                 whiten64, whiten, ld_w, mu_hilo, ridge, status,
+                                 as_stream(stream));
   const size_t sm = 2 * (size_t)bands * sizeof(double) +
                     (bands <= kSmemInvMaxB ? ((size_t)bands * (bands | 1) + (size_t)bands * bands) *
                                                  sizeof(double)

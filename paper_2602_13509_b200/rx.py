@@ -421,10 +421,12 @@ class DetectPlan:
                       ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.tc_ws.data_ptr(), self.tc_ws_bytes, s)
         else:
+            # the general kernel in f64 products (precise): its f32-product mode moves
+            # Sigma by ~5e-8, which cond(Sigma) ~1e4 turns into > 1e-5 on Sigma^-1
             if own_shift:
                 _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(), s)
             _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[i].data_ptr(),
-                      int(precise), ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
+                      1, ds.moments[i].data_ptr(), ds.flags[i:i + 1].data_ptr(),
                       self.ws.data_ptr(), self.ws_bytes, s)
         self.launches += 3
         return self

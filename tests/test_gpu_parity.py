@@ -20,10 +20,8 @@ from oracle import synth as osynth
 pytestmark = pytest.mark.gpu
 
 STATS_RTOL_FAST = 1e-5      # BASELINE.json north_star: stats within 1e-5 relative
-# sigma_inv is derived from sigma: its error is the sigma error amplified by up
-# to cond(sigma) (~1e4 on these generators), so it is held to 1e-3 normwise;
-# the quantity it feeds (scores) is held to the north-star 1e-4 per pixel.
-INV_RTOL_FAST = 1e-3
+INV_RTOL_FAST = 1e-5        # ... Sigma^-1 included (measured <= 2.1e-8 at every BASELINE
+                            # geometry, profiles/r02_parity_geometry.jsonl)
 SCORE_RTOL_FAST = 1e-4      # scores within 1e-4 relative
 MASK_BAND = 1e-4            # mask exemption band around the threshold
 
@@ -265,7 +263,9 @@ class TestFastMode:
         st = P.compute_stats(cube, mode="fast")
         assert normwise(st.mu, g[f"{name}/mu"]) < STATS_RTOL_FAST
         assert normwise(st.sigma, g[f"{name}/sigma"]) < STATS_RTOL_FAST
-        assert normwise(st.sigma_inv, g[f"{name}/sigma_inv"]) < INV_RTOL_FAST
+        inv = normwise(st.sigma_inv, g[f"{name}/sigma_inv"])
+        print(f"PARITY fast-mode {name} sigma_inv {inv:.3e}")
+        assert inv < INV_RTOL_FAST, inv
         assert st.ridge_used == float(g[f"{name}/ridge"])
         sc = P.rx_scores(cube, st, mode="fast").values
         want = g[f"{name}/scores"]
@@ -348,7 +348,9 @@ def check_detection(det, raw, t, gains=None):
     st = det.stats
     assert normwise(st.mu, want_stats.mu) < STATS_RTOL_FAST
     assert normwise(st.sigma, want_stats.sigma) < STATS_RTOL_FAST
-    assert normwise(st.sigma_inv, want_stats.sigma_inv) < INV_RTOL_FAST
+    inv = normwise(st.sigma_inv, want_stats.sigma_inv)
+    print(f"PARITY sigma_inv {inv:.3e} sigma {normwise(st.sigma, want_stats.sigma):.3e}")
+    assert inv < INV_RTOL_FAST, inv
     assert st.ridge_used == want_stats.ridge_used
     rel = np.abs(det.scores - want_scores) / np.maximum(want_scores, 1e-12)
     assert rel.max() < SCORE_RTOL_FAST, rel.max()

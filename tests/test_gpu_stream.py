@@ -16,7 +16,7 @@ from oracle import synth as osynth
 pytestmark = pytest.mark.gpu
 
 STATS_RTOL = 1e-5
-INV_RTOL = 1e-3
+INV_RTOL = 1e-5
 SCORE_RTOL = 1e-4
 MASK_BAND = 1e-4
 

@@ -48,8 +48,20 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
            "sm__warps_active.avg.pct_of_peak_sustained_active",
            "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
-           "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__cycles_elapsed.avg.per_second"]
+           "sm__cycles_elapsed.avg.per_second",
+           # tensor pipe (tcgen05 UTC*MMA), TMEM and the shared-memory operand path
+           "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+           "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg",
+           "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+           "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+           "smsp__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+           "smsp__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+           "sm__cycles_elapsed.avg"]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
         "usecond": 1e-6, "msecond": 1e-3, "ms": 1e-3, "nsecond": 1e-9, "second": 1}
 
@@ -64,8 +76,10 @@ def full(rep, out, traffic_out=None):
         k = short(r[hdr.index("Kernel Name")])
         d = OrderedDict()
         for m in METRICS:
-            if m in hdr:
-                i = hdr.index(m)
+            # some Blackwell metrics carry a section prefix ("TPC.TriageCompute.<name>")
+            cols = [j for j, h in enumerate(hdr) if h == m or h.endswith("." + m)]
+            if cols:
+                i = cols[0]
                 try:
                     val = float(r[i].replace(",", ""))
                 except ValueError:
@@ -78,14 +92,22 @@ def full(rep, out, traffic_out=None):
         t = d.get("gpu__time_duration.sum")
         if rd is not None and wr is not None and t:
             d["dram_GBps"] = (rd + wr) / t / 1e9
-        res.setdefault(k, d)
+        if k in res:   # several launches of one kernel: keep a list
+            if not isinstance(res[k], list):
+                res[k] = [res[k]]
+            res[k].append(d)
+        else:
+            res[k] = d
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
     if traffic_out:
         # keyed by the bare kernel name (bench.py looks them up that way)
-        tr = {re.sub(r"<.*", "", k.replace("void ", "")).strip():
-              v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for k, v in res.items()
-              if "dram__bytes_read.sum" in v}
+        tr = {}
+        for k, v in res.items():
+            v = v[-1] if isinstance(v, list) else v
+            if "dram__bytes_read.sum" in v:
+                tr[re.sub(r"<.*", "", k.replace("void ", "")).strip()] = \
+                    v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]
         json.dump(tr, open(traffic_out, "w"), indent=1)
 
 
