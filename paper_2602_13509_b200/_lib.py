@@ -116,8 +116,12 @@ def last_error() -> str:
     return (load().skyrx_last_error() or b"").decode(errors="replace")
 
 
+CALLS: dict = {}   # entry point -> number of calls this process made (diagnostics)
+
+
 def call(name: str, *args) -> int:
     """Invoke an int-returning entry point; raise on a non-OK status."""
+    CALLS[name] = CALLS.get(name, 0) + 1
     rc = getattr(load(), name)(*args)
     if rc != OK:
         msg = last_error()

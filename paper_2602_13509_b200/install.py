@@ -63,6 +63,11 @@ def install(skyrx_module=None) -> list[str]:
     base = skyrx_module or sys.modules.get("skyrx") or importlib.import_module("skyrx")
     name = base.__name__
     ref_err = sys.modules.get(f"{name}.errors")
+    if ref_err is None:
+        try:
+            ref_err = importlib.import_module(f"{name}.errors")
+        except ImportError:
+            ref_err = None
     for cls in ("FormatError", "ProtocolError"):  # raise the reference's own classes
         if ref_err is not None and hasattr(ref_err, cls):
             setattr(errors, cls, getattr(ref_err, cls))
