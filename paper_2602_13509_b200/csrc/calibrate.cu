@@ -8,6 +8,9 @@
 //
 // HBM-bound elementwise map: 2 B read + 4 B write per element; the plain path
 // moves 16 B of raw per thread per iteration (uint4) with float4 table loads.
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace skyrx {
@@ -91,6 +94,142 @@ __global__ void __launch_bounds__(256) calibrate_bin_kernel(
   }
 }
 
+// tiled general path (R-FUSED at paper geometry, 1000 x 900 x 300 -> 70).  A CTA owns
+// a block of SB consecutive samples over a range of lines, and every thread owns up to
+// PO fixed (sample, output band) pairs of the block: their kept band indices and dark /
+// coeff words sit in registers for the whole line range (the one-thread-per-output
+// kernel above re-reads 2 * factor table words per output, four times the raw bytes it
+// calibrates, and spends most of its issue on index divisions).  Per line, the block's
+// SB x bands raw words are one contiguous range (16-byte loads into shared memory) and
+// its SB x nout outputs another (coalesced stores).  Same ops, same order as calib()
+// and the left-to-right band sum, so bit-identical.
+constexpr int kBinBufs = 2;
+
+template <int KIND, int PO, int FMAX>
+__global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
+    const void* __restrict__ src, int64_t lines, int32_t samples, int32_t bands,
+    const float* __restrict__ dark, const float* __restrict__ coeff,
+    const float* __restrict__ gain, const int32_t* __restrict__ keep, int32_t nout,
+    int32_t factor, int32_t sb, int64_t lines_per_cta, float* __restrict__ out, Rgb3 rgb_idx,
+    float* __restrict__ rgb) {
+  using T = typename std::conditional<KIND == SKYRX_IN_RAW_U16, uint16_t, float>::type;
+  constexpr bool kRaw = KIND == SKYRX_IN_RAW_U16;
+  extern __shared__ __align__(16) unsigned char cb_smem[];
+  T* tile = reinterpret_cast<T*>(cb_smem);  // [sb * bands] raw words of one line
+  const int s0 = blockIdx.x * sb;
+  const int ns = min(sb, samples - s0);
+  const int nrow = ns * bands;
+  const int nouts = ns * nout;
+  // this thread's fixed (sample, output) pairs e = tid + 256 q and their tables
+  int rowoff[PO], kbv[PO][FMAX];
+  float dkv[PO][FMAX], ckv[PO][FMAX];
+  int rgbc[PO];
+#pragma unroll
+  for (int q = 0; q < PO; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    const int sl = e < nouts ? e / nout : 0, o = e < nouts ? e - sl * nout : 0;
+    rowoff[q] = sl * bands;
+    rgbc[q] = -1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (rgb_idx.c[c] == o) rgbc[q] = c;
+#pragma unroll
+    for (int j = 0; j < FMAX; ++j) {
+      const int k = o * factor + (j < factor ? j : 0);
+      const int b = keep ? __ldg(keep + k) : k;
+      kbv[q][j] = b;
+      if (kRaw) {
+        const int64_t tb = (int64_t)(s0 + sl) * bands + b;
+        dkv[q][j] = __ldg(dark + tb);
+        ckv[q][j] = __ldg(coeff + tb);
+      }
+    }
+  }
+  const T* in = reinterpret_cast<const T*>(src);
+  const int64_t l0 = blockIdx.y * lines_per_cta;
+  const int64_t l1 = min(lines, l0 + lines_per_cta);
+  const int nbytes = nrow * (int)sizeof(T);
+  const int bufw = (nrow + 15) & ~15;  // words per buffer (16-byte aligned)
+  const bool vec = ((((uintptr_t)in) | ((uintptr_t)samples * bands * sizeof(T)) |
+                     ((uintptr_t)s0 * bands * sizeof(T))) & 15) == 0 && (nbytes & 15) == 0;
+  auto fetch = [&](int64_t line, T* dst) {
+    const T* g = in + (line * samples + s0) * (int64_t)bands;
+    if (vec) {
+      const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
+      for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + 16 * v),
+                     "l"(reinterpret_cast<const char*>(g) + 16 * (size_t)v));
+    } else {
+      for (int e = threadIdx.x; e < nrow; e += blockDim.x) dst[e] = g[e];
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  // kBinBufs line buffers: lines l+1 .. l+kBinBufs-1 are in flight while line l is
+  // calibrated (about 6 lines per SM cover the HBM latency at full bandwidth)
+  for (int b = 0; b < kBinBufs - 1; ++b) {
+    if (l0 + b < l1) fetch(l0 + b, tile + b * bufw);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int64_t line = l0; line < l1; ++line) {
+    const int cur = (int)((line - l0) % kBinBufs);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinBufs - 2));
+    __syncthreads();  // line `line` is in tile[cur]; the buffer fetched next is free
+    const int64_t nxt = line + kBinBufs - 1;
+    if (nxt < l1) fetch(nxt, tile + (int)((nxt - l0) % kBinBufs) * bufw);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    const T* tl = tile + cur * bufw;
+    const float gl = kRaw ? __ldg(gain + line) : 1.0f;
+    float* o_line = out + (line * samples + s0) * (int64_t)nout;
+#pragma unroll
+    for (int q = 0; q < PO; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      if (e < nouts) {
+        const T* row = tl + rowoff[q];
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < FMAX; ++j) {
+          if (j < factor) {
+            float x;
+            if constexpr (kRaw) {
+              x = calib((float)row[kbv[q][j]], dkv[q][j], ckv[q][j], gl);
+            } else {
+              x = row[kbv[q][j]];
+            }
+            acc = (j == 0) ? x : __fadd_rn(acc, x);
+          }
+        }
+        __stcs(o_line + e, acc);
+        if (rgb && rgbc[q] >= 0) rgb[(line * samples + s0 + rowoff[q] / bands) * 3 + rgbc[q]] = acc;
+      }
+    }
+  }
+}
+
+template <int KIND>
+static bool launch_bin_tiled(const void* src, int64_t lines, int32_t samples, int32_t bands,
+                             const float* dark, const float* coeff, const float* gain,
+                             const int32_t* keep, int32_t nout, int32_t factor, float* out,
+                             Rgb3 r, float* rgb, cudaStream_t st) {
+  constexpr int PO = 4, FMAX = 4;  // up to 1024 outputs per CTA, bin factors up to 4
+  if (factor > FMAX || nout > 256 * PO || lines < 1 || samples < 1) return false;
+  const int sb = std::min(samples, (256 * PO) / nout);
+  const size_t elem = KIND == SKYRX_IN_RAW_U16 ? 2 : 4;
+  const size_t sm = kBinBufs * (((size_t)sb * bands + 15) / 16 * 16) * elem;  // line buffers
+  if (sm > 200 * 1024) return false;
+  auto k = calibrate_bin_tiled_kernel<KIND, PO, FMAX>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int sblocks = (samples + sb - 1) / sb;
+  // about 6 CTAs per SM, each over a contiguous range of lines
+  int64_t ychunks = std::max<int64_t>(1, (int64_t)kSMs * 6 / sblocks);
+  ychunks = std::min<int64_t>(ychunks, lines);
+  const int64_t per = (lines + ychunks - 1) / ychunks;
+  ychunks = (lines + per - 1) / per;
+  k<<<dim3(sblocks, (unsigned)ychunks), 256, sm, st>>>(src, lines, samples, bands, dark, coeff,
+                                                       gain, keep, nout, factor, sb, per, out,
+                                                       r, rgb);
+  return true;
+}
+
 static int grid_for(int64_t work, int threads) {
   int64_t blocks = ceil_div<int64_t>(work, threads);
   const int64_t cap = (int64_t)kSMs * 16;
@@ -134,8 +273,10 @@ extern "C" int skyrx_calibrate(const uint16_t* raw, int64_t lines, int32_t sampl
     if (rgb && rgb_idx_host)
       for (int c = 0; c < 3; ++c) r.c[c] = rgb_idx_host[c];
     const int64_t total = pixels * nout;
-    calibrate_bin_kernel<SKYRX_IN_RAW_U16><<<grid_for(total, 256), 256, 0, st>>>(
-        raw, lines, samples, bands, dark, coeff, gain, keep, nout, factor, out, r, rgb);
+    if (!launch_bin_tiled<SKYRX_IN_RAW_U16>(raw, lines, samples, bands, dark, coeff, gain, keep,
+                                            nout, factor, out, r, rgb, st))
+      calibrate_bin_kernel<SKYRX_IN_RAW_U16><<<grid_for(total, 256), 256, 0, st>>>(
+          raw, lines, samples, bands, dark, coeff, gain, keep, nout, factor, out, r, rgb);
   }
   SKYRX_CHECK_LAUNCH("skyrx_calibrate");
   return SKYRX_OK;
@@ -155,10 +296,12 @@ extern "C" int skyrx_bin_radiance(const float* in, int64_t lines, int32_t sample
   Rgb3 r{{-1, -1, -1}};
   if (rgb && rgb_idx_host)
     for (int c = 0; c < 3; ++c) r.c[c] = rgb_idx_host[c];
-  calibrate_bin_kernel<SKYRX_IN_F32><<<grid_for(pixels * nout, 256), 256, 0,
-                                       as_stream(stream)>>>(in, lines, samples, bands, nullptr,
-                                                            nullptr, nullptr, keep, nout,
-                                                            factor, out, r, rgb);
+  if (!launch_bin_tiled<SKYRX_IN_F32>(in, lines, samples, bands, nullptr, nullptr, nullptr, keep,
+                                      nout, factor, out, r, rgb, as_stream(stream)))
+    calibrate_bin_kernel<SKYRX_IN_F32><<<grid_for(pixels * nout, 256), 256, 0,
+                                         as_stream(stream)>>>(in, lines, samples, bands,
+                                                              nullptr, nullptr, nullptr, keep,
+                                                              nout, factor, out, r, rgb);
   SKYRX_CHECK_LAUNCH("skyrx_bin_radiance");
   return SKYRX_OK;
 }
