@@ -117,10 +117,18 @@ int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
 /* Raw-byte tensor-core moments (RAW cubes, one constant line gain, B <= 128,
  * samples*bands*2 % 16 == 0): exact integer byte Grams per sample column
  * (tcgen05 kind::i8, TMA-fed), calibration applied per sample in f64.  Same
- * [n, s, Q] moments about `shift`; flags |= 4 if any value would clamp at 0
- * (caller recomputes with another path). */
+ * [n, s, Q] moments about `shift`; flags |= 4 if any value clamps at 0.  For
+ * windows <= 256 bytes (B <= 127) the clamped pixels are then corrected exactly
+ * in the same call (a re-scan of the flagged units only) and flags |= 256: the
+ * moments are final (finalize accepts 4 with 256).  Wider windows (B > 127) leave
+ * 4 without 256: the caller recomputes with another path.  workspace >=
+ * skyrx_stats_raw_workspace(bands) (>= skyrx_stats_raw_workspace_for(L, S, B) for the
+ * clamp correction). */
 int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
 size_t skyrx_stats_raw_workspace(int32_t bands);
+/* workspace that also holds the clamp correction's pixel bitmap (L * S bits); with only
+ * skyrx_stats_raw_workspace(bands) bytes a clamp leaves flags 4 without 256 */
+size_t skyrx_stats_raw_workspace_for(int64_t lines, int32_t samples, int32_t bands);
 int skyrx_stats_raw(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
                     const float* dark, const float* coeff, double gain, const double* shift,
                     double* moments, int32_t* flags, void* workspace, size_t workspace_bytes,

@@ -19,6 +19,14 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libskyrx_b200.so"
 
 OK, ERR_ARG, ERR_CUDA, ERR_INSUFFICIENT, ERR_NONFINITE, ERR_NOT_PD, ERR_RANGE = range(7)
+
+
+def flags_range(f: int) -> bool:
+    """Moments that must be recomputed (common.cuh flags_range): the int8 quantiser
+    overflowed (2), or a value clamped at 0 (4) that the raw-byte pass did not correct
+    (256 = clamp_fix_kernel corrected it)."""
+    f = int(f)
+    return bool(f & 2) or (bool(f & 4) and not f & 256)
 IN_RAW_U16, IN_F32, IN_F64 = 0, 1, 2
 
 vp, i32, i64, u32, f32, f64, sz = (C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_float,
@@ -42,6 +50,7 @@ SIGNATURES = {
     "skyrx_stats_tc": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     "skyrx_stats_raw_supported": (C.c_int, [i64, i32, i32, vp]),
     "skyrx_stats_raw_workspace": (sz, [i32]),
+    "skyrx_stats_raw_workspace_for": (sz, [i64, i32, i32]),
     "skyrx_stats_raw": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "skyrx_stats_raw_own_shift": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "skyrx_moments_fold":(C.c_int, [vp, vp, i32, f64, vp]),

@@ -93,6 +93,12 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return r;
 }
 
+// moments that must be recomputed: the int8 quantiser overflowed (2), or a value clamped
+// at 0 (4) on a raw-byte path that did not correct it (256: clamp_fix_kernel did)
+__host__ __device__ __forceinline__ bool flags_range(int32_t f) {
+  return (f & 2) || ((f & 4) && !(f & 256));
+}
+
 // moments-pass flags word (include/skyrx_b200.h): proven "no raw value below dark"
 // either by the raw-byte tensor-core pass (8 without 4) or the general pass (128 without 64)
 __device__ __forceinline__ bool flags_noclamp(int32_t f) {

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) finalize_small_kernel(
   const double* s = mom + 1;
   const double* q = mom + 1 + B;
   int status = SKYRX_OK;
-  if (flags_all && (flags_all[m] & 6)) status = SKYRX_ERR_RANGE;
+  if (flags_all && flags_range(flags_all[m])) status = SKYRX_ERR_RANGE;
   if (flags_all && (flags_all[m] & 1)) status = SKYRX_ERR_NONFINITE;
   if (!(n > (double)B)) status = SKYRX_ERR_INSUFFICIENT;  // rx.py:51 checks size first
   if (status != SKYRX_OK) {
@@ -313,7 +313,7 @@ int launch_finalize_small(const double* moments, const double* shift, const int3
     SKYRX_CHECK_LAUNCH("skyrx_stats_finalize/small");                                         \
     return SKYRX_OK;                                                                          \
   }
-  SKYRX_FS(2) SKYRX_FS(4) SKYRX_FS(8) SKYRX_FS(10) SKYRX_FS(14) SKYRX_FS(22)
+  SKYRX_FS(2) SKYRX_FS(4) SKYRX_FS(8) SKYRX_FS(10)
 #undef SKYRX_FS
   set_error("finalize_small: B = %d too large", B);
   return SKYRX_ERR_ARG;

@@ -28,6 +28,7 @@
 // producer, warp 9 MMA issuer.  Only the lower triangle of the byte Gram is
 // needed: windows wider than 128 bytes add one M=128 x N=(NW-128) MMA for the
 // bottom-right block instead of a second full-width one.
+#include <algorithm>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -67,6 +68,7 @@ __host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 1
 __host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 5 : GRX_STAGES); }
 #endif
 constexpr int64_t kGrMaxUnitLines = 32768;
+constexpr int64_t kGrMaxUnitBits = 1 << 20;  // units past this count are all re-scanned
 
 struct GramRawParams {
   const float* dark;
@@ -85,6 +87,8 @@ struct GramRawParams {
   int64_t units_main;   // regular units dealt in full rounds
   int32_t tail_k;       // pieces per leftover unit (1: no split)
   int64_t tail_lines;   // lines per piece (multiple of the tile)
+  uint32_t* unit_clamp;  // bit u: unit u holds a value below dark (clamp_mark_kernel)
+  uint32_t* pixbits;     // bit (line * S + s): that pixel has a clamped value, or null
 };
 
 // idesc for kind::i8 with unsigned 8-bit operands, MN-major A and B, S32 accumulators
@@ -497,7 +501,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #ifdef SKYRX_GR_PROFILE
       if (tid == kGrWorkers) gr_prof[blockIdx.x][6] += clock64() - et0;
 #endif
-      if (clamp) atomicOr(p.flags, 4);
+      if (clamp) {
+        atomicOr(p.flags, 4);
+        if (u < kGrMaxUnitBits) atomicOr(p.unit_clamp + (u >> 5), 1u << (u & 31));
+      }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       mbar_arrive(&scan_empty[ub]);
@@ -538,34 +545,50 @@ extern "C" __attribute__((visibility("default"))) int skyrx_gr_profile(unsigned 
 // elements (one per lane); its 8 warps sum fixed, contiguous slices of the
 // partials in order, then warp 0 adds the 8 slice sums in order.
 constexpr int kSumBatch = 19;  // ceil(148 / 8): a warp's slice of the per-CTA partials
-__global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restrict__ part,
-                                                           int nparts, int stride,
-                                                           double* __restrict__ out) {
-  __shared__ double red[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int e = blockIdx.x * 32 + lane;
+__device__ __forceinline__ double part_slice_sum(const double* __restrict__ part, int nparts,
+                                                 int stride, int e, int w) {
   const int per = (nparts + 7) / 8;
   const int c0 = w * per, c1 = min(nparts, c0 + per);
   double acc = 0.0;
-  if (e < stride) {
-    if (per <= kSumBatch) {
-      // every load of the slice in flight at once, then the same in-order sum
-      double v[kSumBatch];
+  if (per <= kSumBatch) {
+    // every load of the slice in flight at once, then the same in-order sum
+    double v[kSumBatch];
 #pragma unroll
-      for (int k = 0; k < kSumBatch; ++k)
-        v[k] = c0 + k < c1 ? __ldcg(part + (size_t)(c0 + k) * stride + e) : 0.0;
+    for (int k = 0; k < kSumBatch; ++k)
+      v[k] = c0 + k < c1 ? __ldcg(part + (size_t)(c0 + k) * stride + e) : 0.0;
 #pragma unroll
-      for (int k = 0; k < kSumBatch; ++k)
-        if (c0 + k < c1) acc += v[k];
-    } else {
-      for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
-    }
+    for (int k = 0; k < kSumBatch; ++k)
+      if (c0 + k < c1) acc += v[k];
+  } else {
+    for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
   }
-  red[w][lane] = acc;
+  return acc;
+}
+
+// out = sum of the nparts partials (fixed order); plus, when flags says the clamp
+// fix-up ran (256), the sum of its nfix partials (same order rule), added last
+__global__ void __launch_bounds__(256) gram_raw_sum_kernel(const double* __restrict__ part,
+                                                           int nparts, int stride,
+                                                           double* __restrict__ out,
+                                                           const double* __restrict__ fix,
+                                                           int nfix,
+                                                           const int32_t* __restrict__ flags) {
+  __shared__ double red[8][32];
+  __shared__ double red2[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const bool fixed = fix != nullptr && flags != nullptr && (__ldcg(flags) & 256);
+  red[w][lane] = e < stride ? part_slice_sum(part, nparts, stride, e, w) : 0.0;
+  red2[w][lane] = (fixed && e < stride) ? part_slice_sum(fix, nfix, stride, e, w) : 0.0;
   __syncthreads();
   if (w == 0 && e < stride) {
     double t = 0.0;
     for (int k = 0; k < 8; ++k) t += red[k][lane];
+    if (fixed) {
+      double t2 = 0.0;
+      for (int k = 0; k < 8; ++k) t2 += red2[k][lane];
+      t += t2;
+    }
     out[e] = t;
   }
 }
@@ -600,12 +623,219 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
   }
 }
 
+// ------------------------------------------------------------------ clamp fix-up
+// A raw count below its dark level calibrates to 0 (calibrate.py:99, max(r - d, 0)),
+// which breaks the raw-byte algebra x = C (r - d) the Gram above relies on.  Instead of
+// redoing the cube in f64 (round 1: ~20x the fast path at c4), the clamped pixels'
+// exact corrections are added to the uncentred sums: with x the unclamped and x' the
+// true radiance (x'_b = 0 where r_b < d_b), dx = x' - x is -x on the clamped bands and
+//     sum x' x'^T = sum x x^T + sum (x dx^T + dx x^T + dx dx^T),   sum x' = sum x + sum dx.
+// Two kernels, both no-ops (one flags read per CTA) when nothing clamped:
+//  clamp_mark_kernel  streams the flagged units' lines (bit u of unit_clamp, set by the
+//                     Gram epilogue from its per-band minima; sample-major units of one
+//                     sample are skipped 16 B at a time when unflagged) with coalesced
+//                     16-byte loads and sets bit (line * S + s) of a pixel bitmap for
+//                     every pixel with a value below dark (atomicOr: order-free);
+//  clamp_fix_kernel   CTA c walks a fixed contiguous range of the bitmap in pixel order,
+//                     stages the clamped pixels 32 at a time and adds, pixel by pixel,
+//                     only the row / column of each clamped band into a shared-memory
+//                     triangle (thread t takes entry (t, c)): a deterministic per-CTA
+//                     partial, joined to the Gram partials in gram_raw_sum_kernel's
+//                     fixed-order sum.
+constexpr int kFixThreads = 256;
+constexpr int kFixBatch = 32;  // clamped pixels staged per round
+
+__global__ void __launch_bounds__(256) clamp_mark_kernel(const uint16_t* __restrict__ raw,
+                                                         GramRawParams p,
+                                                         uint32_t* __restrict__ pixbits) {
+  if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;
+  const int B = p.B;
+  const int vpl = p.S * B / 8;  // 16-B vectors per line (S B 2 % 16 == 0)
+  // line-major: CTA rows walk lines, threads the line's vectors; element e of a line is
+  // sample e / B, band e % B, and its dark word is dark[e] (the (S, B) table, row-major).
+  // Four lines per round, their loads issued together (one load in flight per thread
+  // left the kernel latency-bound at 1.1 ms per c4 strip).
+  constexpr int kLines = 4;
+  const bool dark16 = (reinterpret_cast<uintptr_t>(p.dark) & 15) == 0;
+  for (int vx = blockIdx.x * blockDim.x + threadIdx.x; vx < vpl; vx += gridDim.x * blockDim.x) {
+    const int e0 = vx * 8;
+    const int s0 = e0 / B, s1 = (e0 + 7) / B;
+    float dv[8];
+    if (dark16) {
+      const float4 d0 = __ldg(reinterpret_cast<const float4*>(p.dark + e0));
+      const float4 d1 = __ldg(reinterpret_cast<const float4*>(p.dark + e0 + 4));
+      dv[0] = d0.x, dv[1] = d0.y, dv[2] = d0.z, dv[3] = d0.w;
+      dv[4] = d1.x, dv[5] = d1.y, dv[6] = d1.z, dv[7] = d1.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dv[q] = __ldg(p.dark + e0 + q);
+    }
+    auto flagged = [&](int64_t sp, int64_t lin, int s) {
+      int64_t u = sp * p.S + s;  // regular units: u = split * S + s
+      if (u >= p.units_main)     // a leftover unit cut into tail pieces
+        u = p.units_main + (u - p.units_main) * p.tail_k + lin / p.tail_lines;
+      return u >= kGrMaxUnitBits || ((p.unit_clamp[u >> 5] >> (u & 31)) & 1u);
+    };
+    for (int64_t l0 = blockIdx.y; l0 < p.L; l0 += (int64_t)kLines * gridDim.y) {
+      uint4 w[kLines];
+      bool on[kLines];
+#pragma unroll
+      for (int k = 0; k < kLines; ++k) {
+        const int64_t line = l0 + (int64_t)k * gridDim.y;
+        on[k] = false;
+        if (line < p.L) {
+          const int64_t sp = line / p.split_lines, lin = line - sp * p.split_lines;
+          on[k] = flagged(sp, lin, s0) || (s1 != s0 && flagged(sp, lin, s1));
+        }
+        if (on[k])
+          w[k] = __ldcs(reinterpret_cast<const uint4*>(raw + line * p.S * (int64_t)B) + vx);
+      }
+#pragma unroll
+      for (int k = 0; k < kLines; ++k) {
+        if (!on[k]) continue;
+        const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+        uint32_t hit = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t r = (q & 1) ? (ws[q >> 1] >> 16) : (ws[q >> 1] & 0xffffu);
+          hit |= (uint32_t)((float)r < dv[q]) << q;
+        }
+        while (hit) {  // rare
+          const int q = __ffs(hit) - 1;
+          hit &= hit - 1;
+          const int64_t pix = (l0 + (int64_t)k * gridDim.y) * p.S + (e0 + q) / B;
+          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFixThreads) clamp_fix_kernel(
+    const uint16_t* __restrict__ raw, GramRawParams p, const uint32_t* __restrict__ pixbits,
+    double* __restrict__ outpart) {
+  // shared: dQ (packed lower triangle, T) | xs, dx ([kFixBatch][B]) | clamped-band masks
+  extern __shared__ __align__(16) double fx[];
+  const int B = p.B;
+  const int T = B * (B + 1) / 2;
+  const int work = B * B + B + 1;
+  double* dq = fx;
+  double* xs = dq + T;
+  double* dx = xs + kFixBatch * B;
+  uint32_t* km = reinterpret_cast<uint32_t*>(dx + kFixBatch * B);  // [kFixBatch][4] (B<=128)
+  __shared__ int64_t list[kFixBatch];
+  __shared__ int cnt[kFixThreads];
+  __shared__ int nlist;
+  const int tid = threadIdx.x;
+  if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;  // nothing clamped
+  for (int e = tid; e < T; e += kFixThreads) dq[e] = 0.0;
+  double as = 0.0;  // thread t < B: sum of dx_t
+  const int64_t nwords = (p.L * p.S + 31) / 32;
+  const int64_t per = (nwords + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = blockIdx.x * per, w1 = min(nwords, w0 + per);
+  // walk the range in fixed order, kFixThreads words per round
+  for (int64_t wb = w0; wb < w1; wb += kFixThreads) {
+    const int64_t wi = wb + tid;
+    const uint32_t bits = wi < w1 ? pixbits[wi] : 0u;
+    __syncthreads();
+    cnt[tid] = __popc(bits);
+    __syncthreads();
+    if (tid < 32) {  // exclusive prefix over the 256 counts (one warp, 8 per lane)
+      int v[8], tsum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = cnt[tid * 8 + k], tsum += v[k];
+      int incl = tsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += n;
+      }
+      int run = incl - tsum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cnt[tid * 8 + k] = run, run += v[k];
+      if (tid == 31) nlist = incl;
+    }
+    __syncthreads();
+    const int total = nlist, mybase = cnt[tid];
+    for (int k0 = 0; k0 < total; k0 += kFixBatch) {
+      {  // this batch's pixels, in bitmap order
+        uint32_t bb = bits;
+        int rank = mybase;
+        while (bb && rank < k0 + kFixBatch) {
+          const int bit = __ffs(bb) - 1;
+          bb &= bb - 1;
+          if (rank >= k0) list[rank - k0] = wi * 32 + bit;
+          ++rank;
+        }
+      }
+      for (int t = tid; t < kFixBatch * 4; t += kFixThreads) km[t] = 0u;
+      __syncthreads();
+      const int nb = total - k0 < kFixBatch ? total - k0 : kFixBatch;
+      for (int t = tid; t < nb * B; t += kFixThreads) {
+        const int k = t / B, b = t - k * B;
+        const int64_t pix = list[k];
+        const int s = (int)(pix - (pix / p.S) * p.S);
+        const uint16_t r = __ldg(raw + pix * B + b);
+        const float df = __ldg(p.dark + (int64_t)s * B + b);
+        const double x = (double)__ldg(p.coeff + (int64_t)s * B + b) * p.ginv *
+                         ((double)r - (double)df);
+        const bool c = (float)r < df;
+        xs[t] = x;
+        dx[t] = c ? -x : 0.0;
+        if (c) atomicOr(km + k * 4 + (b >> 5), 1u << (b & 31));
+      }
+      __syncthreads();
+      // pixel by pixel (a barrier between pixels): for each clamped band c, thread t < B
+      // adds entry (max(t, c), min(t, c)); a pair of clamped bands is added once (by the
+      // smaller band's pass), so no two threads touch one entry within a pixel
+      for (int k = 0; k < nb; ++k) {
+        if (tid < B) {
+          const int t = tid;
+          const double* xk = xs + k * B;
+          const double* dk = dx + k * B;
+          const uint32_t* mk = km + k * 4;
+          const double xt = xk[t], dt = dk[t];
+          as += dt;
+          const bool tcl = dt != 0.0 || ((mk[t >> 5] >> (t & 31)) & 1u);
+          for (int m = 0; m < 4; ++m) {
+            uint32_t mm = mk[m];
+            while (mm) {
+              const int c = 32 * m + __ffs(mm) - 1;
+              mm &= mm - 1;
+              if (tcl && t < c) continue;  // added in band t's pass as (c, t)
+              const int i = t > c ? t : c, j = t > c ? c : t;
+              dq[i * (i + 1) / 2 + j] += xt * dk[c] + dt * xk[c] + dt * dk[c];
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  // this CTA's partial [dSxx (lower, row-major i >= j) | dSx | dn = 0]
+  double* out = outpart + (size_t)blockIdx.x * work;
+  for (int e = tid; e < B * B; e += kFixThreads) {
+    const int i = e / B, j = e - i * B;
+    out[e] = j > i ? 0.0 : dq[i * (i + 1) / 2 + j];
+  }
+  for (int b = tid; b < B; b += kFixThreads) out[B * B + b] = as;
+  if (tid == 0) out[B * B + B] = 0.0;
+  if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 256);  // clamps corrected
+}
+
+static size_t clamp_fix_smem(int B) {
+  return ((size_t)B * (B + 1) / 2 + 2 * (size_t)kFixBatch * B) * 8 + kFixBatch * 16;
+}
+
 // reduce the per-CTA partials [Sxx | Sx | n] (deterministic) and centre them on shift
 int gram_raw_sum_and_center(const double* part, int grid, int bands, double* shift, int own,
-                            double* moments, cudaStream_t st) {
+                            double* moments, cudaStream_t st, const double* fix, int nfix,
+                            const int32_t* flags) {
   const int work = bands * bands + bands + 1;
-  double* tot = const_cast<double*>(part) + (size_t)kSMs * work;  // after the partials
-  gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(part, grid, work, tot);
+  double* tot = const_cast<double*>(part) + (size_t)2 * kSMs * work;  // after the partials
+  gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(part, grid, work, tot, fix, nfix,
+                                                          flags);
   SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
   gram_raw_center_kernel<<<ceil_div(work, 256), 256, 0, st>>>(tot, bands, shift, own, moments);
   SKYRX_CHECK_LAUNCH("gram_raw_center_kernel");
@@ -678,9 +908,31 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   }
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  const int64_t nbits = p.units < kGrMaxUnitBits ? p.units : kGrMaxUnitBits;
+  cudaMemsetAsync(p.unit_clamp, 0, (size_t)((nbits + 31) / 32) * 4, st);
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
-  return gram_raw_sum_and_center(p.part, grid, p.B, shift, own, moments, st);
+  // exact corrections of the clamped pixels (no-op passes when nothing clamped)
+  const int fgrid = kSMs;
+  const int work = p.B * p.B + p.B + 1;
+  if (p.pixbits != nullptr) {
+    cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
+    const int vpl = p.S * p.B / 8;
+    const int gx = (vpl + 255) / 256;
+    const int gy = (int)std::min<int64_t>(p.L, std::max<int64_t>(1, (int64_t)kSMs * 8 / gx));
+    clamp_mark_kernel<<<dim3(gx, gy), 256, 0, st>>>(raw, p, p.pixbits);
+    SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
+  }
+  const size_t fsm = clamp_fix_smem(p.B);
+  if (fsm > 48 * 1024)
+    cudaFuncSetAttribute(clamp_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  if (p.pixbits != nullptr) {
+    clamp_fix_kernel<<<fgrid, kFixThreads, fsm, st>>>(raw, p, p.pixbits,
+                                                       p.part + (size_t)grid * work);
+    SKYRX_CHECK_LAUNCH("clamp_fix_kernel");
+  }  // no bitmap room (workspace from skyrx_stats_raw_workspace): flag 4 stays uncorrected
+  return gram_raw_sum_and_center(p.part, grid, p.B, shift, own, moments, st,
+                                 p.part + (size_t)grid * work, fgrid, p.flags);
 }
 
 }  // namespace skyrx
@@ -698,7 +950,15 @@ extern "C" int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t
 }
 
 extern "C" size_t skyrx_stats_raw_workspace(int32_t bands) {
-  return (size_t)(kSMs + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double);
+  // [2 kSMs partials (Gram CTAs, clamp fix-up CTAs) | total] doubles, then the unit bitmap
+  return (size_t)(2 * kSMs + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double) +
+         (size_t)kGrMaxUnitBits / 8;
+}
+
+extern "C" size_t skyrx_stats_raw_workspace_for(int64_t lines, int32_t samples,
+                                                int32_t bands) {
+  // ... plus the pixel bitmap of the clamp correction (L S bits)
+  return skyrx_stats_raw_workspace(bands) + (size_t)((lines * samples + 31) / 32) * 4 + 16;
 }
 
 static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, int32_t bands,
@@ -730,6 +990,11 @@ static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, i
   p.coeff = coeff;
   p.ginv = 1.0 / gain;
   p.part = reinterpret_cast<double*>(workspace);
+  p.unit_clamp = reinterpret_cast<uint32_t*>(
+      p.part + (size_t)(2 * kSMs + 1) * ((size_t)bands * bands + bands + 1));
+  p.pixbits = workspace_bytes >= skyrx_stats_raw_workspace_for(lines, samples, bands)
+                  ? p.unit_clamp + kGrMaxUnitBits / 32
+                  : nullptr;
   p.flags = flags;
   p.L = lines;
   p.S = samples;

@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
 }  // namespace raww
 
 int gram_raw_sum_and_center(const double* part, int grid, int bands, double* shift, int own,
-                            double* moments, cudaStream_t st);
+                            double* moments, cudaStream_t st, const double* fix, int nfix,
+                            const int32_t* flags);
 
 // window atoms for B (16-B aligned start, widest offset over the samples)
 int raww_atoms(int bands) {
@@ -404,7 +405,8 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
     SKYRX_CHECK_LAUNCH("raww_gram_kernel");
   }
   cudaFreeAsync(usum, st);
-  return gram_raw_sum_and_center(p.part, grid, bands, shift, own, moments, st);
+  return gram_raw_sum_and_center(p.part, grid, bands, shift, own, moments, st, nullptr, 0,
+                                 nullptr);
 }
 
 }  // namespace skyrx

@@ -222,6 +222,13 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
   const int lane = tid & 31;
   const int B = p.B;
   const int64_t u0 = blockIdx.x, ustep = gridDim.x;
+  // the exact-digit form needs "no raw value below dark" from the moments pass (a clamp
+  // the raw-byte pass corrected, flags 4 | 256, still breaks the linear form per pixel);
+  // without that proof nothing is scored and flags |= 32 asks for a general rescore
+  if (!flags_noclamp(__ldg(p.flags))) {
+    if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 32);
+    return;
+  }
 
   if (tid == 0) {
     for (int i = 0; i < p.nraw; ++i) mbar_init(&raw_full[i], 1), mbar_init(&raw_empty[i], NT / 32);

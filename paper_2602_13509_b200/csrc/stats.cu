@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(
   const double* q = mom + 1 + B;
   int status = SKYRX_OK;
   // 2: int8 quantiser overflow, 4: a value clamped at 0 on the raw-byte path
-  if (flags_all && (flags_all[m] & 6)) status = SKYRX_ERR_RANGE;
+  if (flags_all && flags_range(flags_all[m])) status = SKYRX_ERR_RANGE;
   if (flags_all && (flags_all[m] & 1)) status = SKYRX_ERR_NONFINITE;
   if (!(n > (double)B)) status = SKYRX_ERR_INSUFFICIENT;  // rx.py:51 checks size first
   if (status != SKYRX_OK) {

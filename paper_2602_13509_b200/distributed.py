@@ -80,13 +80,13 @@ class CudaOps:
         """Local moments about the common shift, and this block's non-finite flag.
 
         A tensor-core path that could not represent this block (quantiser range /
-        clamp at 0, flags & 6) is redone locally in the FFMA kernel BEFORE the
+        an uncorrected clamp at 0, _lib.flags_range) is redone locally in the FFMA kernel BEFORE the
         exchange, so only the non-finite bit is global."""
         plan = self.plan
         ds = plan.ds
         ds.shift[0].copy_(shift)
         plan.run_moments(0, raw, self.dark, self.coeff, self.gains, gain_const=self.gain_const)
-        if int(ds.flags[0].item()) & 6:
+        if _lib.flags_range(int(ds.flags[0].item())):
             plan.run_moments(0, raw, self.dark, self.coeff, self.gains, force_ffma=True)
         return ds.moments[0], ds.flags[0:1] & 1
 

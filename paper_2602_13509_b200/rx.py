@@ -354,7 +354,9 @@ class DetectPlan:
         self.tc_ws_bytes = int(lib.skyrx_stats_tc_workspace(bands)) if self.tc_stats else 0
         self.tc_ws = _dev.empty((max(self.tc_ws_bytes, 8),), torch.uint8)
         self.raw_stats = bands <= 272 and use_tc and os.environ.get("SKYRX_B200_RAWGRAM", "1") != "0"
-        self.raw_ws_bytes = int(lib.skyrx_stats_raw_workspace(bands)) if self.raw_stats else 0
+        # (with room for the clamp correction's pixel bitmap, skyrx_stats_raw_workspace_for)
+        self.raw_ws_bytes = (int(lib.skyrx_stats_raw_workspace_for(lines, samples, bands))
+                             if self.raw_stats else 0)
         self.raw_ws = _dev.empty((max(self.raw_ws_bytes, 8),), torch.uint8)
         # exact-digit score kernel (per-sample records, B <= 128): the path for
         # 80 < B <= 128 (K4-TC's tables no longer fit); SKYRX_B200_TCS=1 forces it

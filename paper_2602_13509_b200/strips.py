@@ -33,10 +33,14 @@ from . import _dev, _lib
 from .calibrate import _check_tables, _raw_device, line_gains, tables_of
 from .rx import _STATUS_MSG, DetectPlan, Detection, constant_gain, key_to_float
 
-# moments/score flags that mean "the fast kernels did not apply to this slot"
-# (include/skyrx_b200.h: 2 quantiser range, 4 clamp at 0, 16 counts >= 4096,
-# 32 no no-clamp proof for the exact-digit kernels)
-REDO_FLAGS = 2 | 4 | 16 | 32
+# score flags that mean "the exact-digit score kernel did not apply to this slot"
+# (include/skyrx_b200.h: 16 counts >= 4096, 32 no no-clamp proof); moments that must
+# be redone are _lib.flags_range (2 quantiser range, 4 clamp not corrected by 256)
+RESCORE_FLAGS = 16 | 32
+
+
+def needs_redo(flags: int) -> bool:
+    return _lib.flags_range(flags) or bool(int(flags) & RESCORE_FLAGS)
 
 
 def strip_owner(index: int, world: int) -> int:
@@ -129,7 +133,7 @@ class StripBatch:
         cubes = {j: (raws[j], tables[j][0], tables[j][1], gains[j]) for j in range(self.count)}
         redone = self.plan.recover_range(cubes)
         st, fl = self.flags()
-        bad = [j for j in range(self.count) if fl[j] & REDO_FLAGS and j not in redone]
+        bad = [j for j in range(self.count) if needs_redo(fl[j]) and j not in redone]
         if bad:
             # a slot still flagged after recover_range: the general kernels again
             for j in bad:

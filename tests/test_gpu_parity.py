@@ -589,18 +589,45 @@ class TestDetect:
         mu = shift.cpu().numpy() + m1[1:1 + B].cpu().numpy() / n
         assert normwise(mu, ref.mu) < 1e-8
 
-    def test_raw_path_clamp_fallback(self, P):
+    def test_raw_path_clamp_corrected(self, P):
         # a value below its dark level clamps to 0 (calibrate.py:99): the raw-byte
-        # algebra no longer holds, so detect() must redo the fit in f64
+        # algebra no longer holds for that pixel, so the clamped pixels' exact
+        # corrections are added in the same call (clamp_fix_kernel; flags 4 | 256)
+        # instead of redoing the cube in f64
         L, S, B = 300, 900, 70
         t = osynth.make_tables(45, S, B, 5)
         raw = osynth.generate_lines(t, 0, L)
         raw[5, 17, 3] = 20      # dark ~ 100 -> clamps
-        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff))
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        assert int(plan.ds.flags[0].item()) & (4 | 256) == (4 | 256)
+        assert plan.used_raw[0]
         rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
         assert rad[5, 17, 3] == 0.0
         ref = O.compute_stats(rad)
-        assert normwise(det.stats.sigma, ref.sigma) < 1e-12
+        exact = O.compute_stats_exact(raw, t.dark, t.coeff, np.ones(L))
+        assert normwise(det.stats.sigma, exact.sigma) < 1e-12   # exact correction
+        assert normwise(det.stats.sigma, ref.sigma) < 1e-7
+        check_detection(det, raw, t)
+
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 2100), (512, 128, 1100), (64, 40, 9000)])
+    def test_sparse_and_dead_pixel_clamps(self, P, S, B, L):
+        """0.01 % random sub-dark counts plus one dead detector element (a whole
+        (sample, band) column below dark): corrected moments, then scores (score_tc
+        clamps natively; B > 80 rescores through the general kernel)."""
+        rng = np.random.default_rng(S + B)
+        t = osynth.make_tables(46, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L).copy()
+        n = raw.size
+        idx = rng.choice(n, max(1, n // 10000), replace=False)
+        raw.reshape(-1)[idx] = rng.integers(0, 60, idx.size)
+        raw[:, S // 3, B // 2] = 5
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        assert int(plan.ds.flags[0].item()) & (4 | 256) == (4 | 256)
+        exact = O.compute_stats_exact(raw, t.dark, t.coeff, np.ones(L))
+        assert normwise(det.stats.sigma, exact.sigma) < 1e-11
+        assert normwise(det.stats.mu, exact.mu) < 1e-12
         check_detection(det, raw, t)
 
     def test_deterministic(self, P):

@@ -1,0 +1,29 @@
+"""One c4 strip with 0.01 % sub-dark counts (or a dead element with --dead) through
+StripBatch, for an ncu launch list of the clamp-corrected path."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+from paper_2602_13509_b200 import _dev  # noqa: E402
+from paper_2602_13509_b200.strips import StripBatch  # noqa: E402
+from paper_2602_13509_b200.synth import Scene  # noqa: E402
+
+L, S, B = 16384, 900, 70
+sc = Scene(4000, S, B, 5)
+raw = sc.generate(0, L)
+if "--dead" in sys.argv:
+    raw.view(torch.int16)[:, 300, 35] = 5
+else:
+    g = torch.Generator(device="cuda").manual_seed(1)
+    flat = raw.view(torch.int16).view(-1)
+    flat[torch.randint(0, flat.numel(), (flat.numel() // 10000,), device="cuda", generator=g)] = 7
+tabs = [(_dev.to_device(sc.dark), _dev.to_device(sc.coeff))]
+gains = [_dev.to_device(np.ones(L, np.float32))]
+b = StripBatch(L, S, B, 1)
+for _ in range(2):
+    b.enqueue([raw], tabs, gains, [1.0])
+torch.cuda.synchronize()
+print("flags", b.flags())
