@@ -123,16 +123,16 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
   // this thread's fixed (sample, output) pairs e = tid + 256 q and their tables
   int rowoff[PO], kbv[PO][FMAX];
   float dkv[PO][FMAX], ckv[PO][FMAX];
-  int rgbc[PO];
+  int rgbm[PO];  // the RGB channels this output band feeds (several when targets share a band)
 #pragma unroll
   for (int q = 0; q < PO; ++q) {
     const int e = threadIdx.x + 256 * q;
     const int sl = e < nouts ? e / nout : 0, o = e < nouts ? e - sl * nout : 0;
     rowoff[q] = sl * bands;
-    rgbc[q] = -1;
+    rgbm[q] = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      if (rgb_idx.c[c] == o) rgbc[q] = c;
+      if (rgb_idx.c[c] == o) rgbm[q] |= 1 << c;
 #pragma unroll
     for (int j = 0; j < FMAX; ++j) {
       const int k = o * factor + (j < factor ? j : 0);
@@ -199,7 +199,12 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
           }
         }
         __stcs(o_line + e, acc);
-        if (rgb && rgbc[q] >= 0) rgb[(line * samples + s0 + rowoff[q] / bands) * 3 + rgbc[q]] = acc;
+        if (rgb && rgbm[q]) {
+          float* px = rgb + (line * samples + s0 + rowoff[q] / bands) * 3;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (rgbm[q] & (1 << c)) px[c] = acc;
+        }
       }
     }
   }

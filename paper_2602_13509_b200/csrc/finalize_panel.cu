@@ -1,0 +1,375 @@
+// K3 for B <= 128 — blocked (panel) factorisation of one background per CTA.
+//
+// Replaces rx.py:56-86 (mu, unbiased symmetric sigma, ridge ladder eps * trace / B over
+// RIDGE_EPSILONS rx.py:23, Cholesky, sigma_inv = cho_solve(L, I) symmetrised) and
+// produces W = L^-1 (f64 and the f32 transposed copy K4 reads).
+//
+// finalize_small.cu advances the factor one column per CTA barrier (70 barriers plus a
+// pivot chain per step at B = 70).  Here the columns come in panels of kFpPanel:
+//   phase 1  warp 0 factors panel p in registers (lanes own rows; the pivot is broadcast
+//            by a shuffle and every lane takes sqrt / 1 / l itself, so a column costs
+//            one shuffle + the pivot chain + one shuffle per later panel column), while
+//            warps 1..15 apply W panel p-1 to the rows of R below it;
+//   phase 2  warp 0 forms W panel p (rows j of W = R_j / l_jj, lanes own columns), while
+//            warps 1..15 apply L panel p to the trailing submatrix of A;
+// two CTA barriers per panel instead of one per column.  Every entry sees exactly the
+// operations of the right-looking column algorithm in the same order (a_it -= l_ij l_tj,
+// R_it -= l_ij W_jt for ascending j, FMA-free like potrf so an exactly rank-deficient
+// input meets an exactly zero pivot), so mu, sigma, L and W are bit-identical to
+// finalize_small_kernel and finalize_kernel (tests/test_gpu_finalize.py); sigma_inv =
+// W^T W is summed in the same 4 x 4 register tiles as finalize_small.
+#include "common.cuh"
+
+namespace skyrx {
+
+constexpr int kFpThreads = 512;
+constexpr int kFpWarps = kFpThreads / 32;
+constexpr int kFpPanel = 8;
+__constant__ double kFpRidgeEps[6] = {0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6};  // rx.py:23
+
+// -DSKYRX_FIN_PROFILE: clock64 at the phase boundaries of matrix 0 plus the cycles warp 0
+// spends in its panels and warp 1 in its trailing updates (skyrx_fp_profile)
+#ifdef SKYRX_FIN_PROFILE
+__device__ long long fp_prof[16];
+#define FP_T(k)                                                     \
+  do {                                                              \
+    __syncthreads();                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) fp_prof[k] = clock64(); \
+  } while (0)
+#define FP_ACC(k, ...)                                                          \
+  do {                                                                          \
+    const long long t0_ = clock64();                                            \
+    __VA_ARGS__;                                                                \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)&fp_prof[k], \
+                                                    (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int skyrx_fp_profile(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fp_prof, sizeof(fp_prof));
+}
+#else
+#define FP_T(k) \
+  do {          \
+  } while (0)
+#define FP_ACC(k, ...) __VA_ARGS__
+#endif
+
+__device__ __forceinline__ int fp_tri_row(int e) {
+  int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while (i * (i + 1) / 2 > e) --i;
+  while ((i + 1) * (i + 2) / 2 <= e) ++i;
+  return i;
+}
+__device__ __forceinline__ int tri(int i) { return i * (i + 1) / 2; }
+
+// warp 0: factor columns [j0, j0 + np) of A (packed lower, already updated by every
+// earlier column); the panel's L entries replace them in place, pivots go to dg.
+// Returns false (uniformly) on a non-positive or NaN pivot.
+template <int RPL>
+__device__ __forceinline__ bool chol_panel(double* Ap, double* dg, int B, int j0) {
+  constexpr int P = kFpPanel;
+  const int lane = threadIdx.x & 31;
+  const int np = min(P, B - j0);
+  double a[RPL][P];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = j0 + lane + 32 * r;
+#pragma unroll
+    for (int c = 0; c < P; ++c)
+      a[r][c] = (i < B && c < np && j0 + c <= i) ? Ap[tri(i) + j0 + c] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    if (c >= np) break;
+    const int j = j0 + c;
+    const double v = __shfl_sync(0xffffffffu, a[0][c], c);  // a_jj: row j is lane c
+    if (!(v > 0.0)) return false;                           // potrf's failure (uniform)
+    const double l = sqrt(v);
+    const double rl = 1.0 / l;
+    if (lane == 0) dg[j] = l, dg[B + j] = rl;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = j0 + lane + 32 * r;
+      if (i > j && i < B) {
+        a[r][c] = a[r][c] * rl;  // l_ij
+        Ap[tri(i) + j] = a[r][c];
+      }
+    }
+#pragma unroll
+    for (int c2 = c + 1; c2 < P; ++c2) {
+      if (c2 >= np) break;
+      const int j2 = j0 + c2;
+      const double ltj = __shfl_sync(0xffffffffu, a[0][c], c2);  // l_{j2, j}
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = j0 + lane + 32 * r;
+        if (i >= j2 && i < B) a[r][c2] = __dsub_rn(a[r][c2], __dmul_rn(a[r][c], ltj));
+      }
+    }
+  }
+  return true;
+}
+
+// warp 0: rows [j0, j0 + np) of W = L^-1 from R (already holding every earlier row's
+// contribution): W_jt = R_jt / l_jj (R_jj = 1), then the panel's later rows take
+// R_j2,t -= l_j2,j W_jt.  Lanes own columns t.
+template <int RPL>
+__device__ __forceinline__ void w_panel(const double* Ap, double* Rp, const double* dg, int B,
+                                        int j0) {
+  constexpr int P = kFpPanel;
+  const int lane = threadIdx.x & 31;
+  const int np = min(P, B - j0);
+  double rr[RPL][P];
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int t = lane + 32 * k;
+#pragma unroll
+    for (int c = 0; c < P; ++c) rr[k][c] = (c < np && t < j0 + c) ? Rp[tri(j0 + c) + t] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    if (c >= np) break;
+    const int j = j0 + c;
+    const double rl = dg[B + j];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int t = lane + 32 * k;
+      if (t <= j) {
+        rr[k][c] = (t == j ? 1.0 : rr[k][c]) * rl;
+        Rp[tri(j) + t] = rr[k][c];
+      }
+    }
+#pragma unroll
+    for (int c2 = c + 1; c2 < P; ++c2) {
+      if (c2 >= np) break;
+      const double lj = Ap[tri(j0 + c2) + j];  // l_{j2, j}, a broadcast
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int t = lane + 32 * k;
+        if (t <= j) rr[k][c2] = __dsub_rn(rr[k][c2], __dmul_rn(lj, rr[k][c]));
+      }
+    }
+  }
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(kFpThreads, 1) finalize_panel_kernel(
+    const double* __restrict__ moments_all, const double* __restrict__ shift_all,
+    const int32_t* __restrict__ flags_all, int B, double* __restrict__ mu_all,
+    double* __restrict__ sigma_all, double* __restrict__ chol_all,
+    double* __restrict__ inv_all, double* __restrict__ w64_all, float* __restrict__ wf_all,
+    int ld_w, float* __restrict__ mhl_all, double* __restrict__ ridge_all,
+    int32_t* __restrict__ status_all) {
+  constexpr int P = kFpPanel;
+  extern __shared__ __align__(16) double fp[];
+  __shared__ double red[kFpWarps];
+  __shared__ int fail;
+  const int T = B * (B + 1) / 2;
+  double* Sp = fp;        // packed lower sigma
+  double* Ap = Sp + T;    // packed lower A (+ ridge) -> L, panel by panel, in place
+  double* Rp = Ap + T;    // packed lower R -> W = L^-1 (diagonal: W_jj = 1 / l_jj)
+  double* dg = Rp + T;    // [l_jj | 1 / l_jj]
+  const size_t BB = (size_t)B * B;
+  const int m = blockIdx.x;
+  const double* mom = moments_all + (size_t)m * (1 + B + BB);
+  const double* shift = shift_all + (size_t)m * B;
+  double* mu = mu_all + (size_t)m * B;
+  double* sigma = sigma_all + (size_t)m * BB;
+  double* chol = chol_all + (size_t)m * BB;
+  double* inv = inv_all + (size_t)m * BB;
+  double* w64 = w64_all + (size_t)m * BB;
+  float* wf = wf_all + (size_t)m * ld_w * ld_w;
+  float* mhl = mhl_all + (size_t)m * 2 * B;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  FP_T(0);
+
+  const double n = mom[0];
+  const double* s = mom + 1;
+  const double* q = mom + 1 + B;
+  int status = SKYRX_OK;
+  if (flags_all && flags_range(flags_all[m])) status = SKYRX_ERR_RANGE;
+  if (flags_all && (flags_all[m] & 1)) status = SKYRX_ERR_NONFINITE;
+  if (!(n > (double)B)) status = SKYRX_ERR_INSUFFICIENT;  // rx.py:51 checks size first
+  if (status != SKYRX_OK) {
+    if (tid == 0) {
+      status_all[m] = status;
+      ridge_all[m] = 0.0;
+    }
+    return;
+  }
+  for (int b = tid; b < B; b += kFpThreads) {  // rx.py:59
+    const double mb = shift[b] + s[b] / n;
+    mu[b] = mb;
+    const float hi = (float)mb;
+    mhl[b] = hi;
+    mhl[B + b] = (float)(mb - (double)hi);
+  }
+  // sigma (rx.py:65-66), symmetric by construction, and its trace
+  for (int e = tid; e < T; e += kFpThreads) {
+    const int i = fp_tri_row(e), k = e - tri(i);
+    const double vik = (q[(size_t)i * B + k] - s[i] * s[k] / n) / (n - 1.0);
+    const double vki = (q[(size_t)k * B + i] - s[k] * s[i] / n) / (n - 1.0);
+    const double v = (vik + vki) / 2.0;
+    Sp[e] = v;
+    sigma[(size_t)i * B + k] = v;
+    sigma[(size_t)k * B + i] = v;
+  }
+  __syncthreads();
+  // the trace in the general kernel's order (ridge = eps * trace / B must match it bitwise)
+  double tr = 0.0;
+  for (int b = tid; b < B; b += kFpThreads) tr += Sp[tri(b) + b];
+  tr = warp_sum(tr);
+  if (lane == 0) red[warp] = tr;
+  __syncthreads();
+  double trace = 0.0;
+  for (int w = 0; w < kFpWarps; ++w) trace += red[w];  // fixed order: deterministic
+  const double scale = trace > 0.0 ? trace / B : 1.0;
+  FP_T(1);
+
+  double ridge = 0.0;
+  bool ok = false;
+  const int wt = tid - 32, nwt = kFpThreads - 32;  // warps 1..15: the trailing updates
+#pragma unroll 1
+  for (int a = 0; a < 6 && !ok; ++a) {
+    ridge = kFpRidgeEps[a] * scale;
+    __syncthreads();  // every read of `fail` from the previous attempt is done
+    for (int e = tid; e < T; e += kFpThreads) {
+      const int i = fp_tri_row(e), t = e - tri(i);
+      Ap[e] = Sp[e] + (i == t ? ridge : 0.0);
+      Rp[e] = 0.0;
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    bool failed = false;
+    for (int j0 = 0; j0 < B; j0 += P) {
+      // ---- phase 1: factor panel p | R rows >= j0 take W panel p-1
+      if (warp == 0) {
+        bool okp;
+        FP_ACC(5, okp = chol_panel<RPL>(Ap, dg, B, j0));
+        if (!okp && lane == 0) fail = 1;
+      } else if (j0 > 0) FP_ACC(7, {
+        const int p0 = j0 - P;
+        const int cnt = (B - j0) * j0;
+        for (int e = wt; e < cnt; e += nwt) {
+          const int i = j0 + e / j0, t = e - (e / j0) * j0;
+          const double* li = Ap + tri(i);
+          double x = Rp[tri(i) + t];
+          for (int j = max(p0, t); j < j0; ++j) x = __dsub_rn(x, __dmul_rn(li[j], Rp[tri(j) + t]));
+          Rp[tri(i) + t] = x;
+        }
+      });
+      __syncthreads();
+      if (fail) {
+        failed = true;
+        break;
+      }
+      // ---- phase 2: W panel p | the trailing submatrix takes L panel p
+      const int j1 = min(j0 + P, B);
+      if (warp == 0) {
+        FP_ACC(6, w_panel<RPL>(Ap, Rp, dg, B, j0));
+      } else FP_ACC(8, {
+        const int mm = B - j1;
+        const int cnt = mm * (mm + 1) / 2;
+        for (int e = wt; e < cnt; e += nwt) {
+          const int ii = fp_tri_row(e), tt = e - tri(ii);
+          const int i = j1 + ii, t = j1 + tt;
+          const double* li = Ap + tri(i);
+          const double* lt = Ap + tri(t);
+          double x = li[t];
+          for (int j = j0; j < j1; ++j) x = __dsub_rn(x, __dmul_rn(li[j], lt[j]));
+          Ap[tri(i) + t] = x;
+        }
+      });
+      __syncthreads();
+    }
+    ok = !failed;
+  }
+  if (!ok) {
+    if (tid == 0) {
+      status_all[m] = SKYRX_ERR_NOT_PD;
+      ridge_all[m] = ridge;
+    }
+    return;
+  }
+  FP_T(2);
+  const double* Wp = Rp;
+  // sigma_inv = W^T W (= cho_solve(L, I)): inv_ij = sum_{k >= i} W_ki W_kj over 4 x 4
+  // tiles (i in I..I+3 >= j in J..J+3), 8 loads per 16 products (finalize_small's order)
+  const int nb = (B + 3) >> 2;
+  for (int tile = tid; tile < nb * (nb + 1) / 2; tile += kFpThreads) {
+    const int ta = fp_tri_row(tile), tb = tile - tri(ta);
+    const int I = 4 * ta, J = 4 * tb;
+    double acc[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[p][r] = 0.0;
+    for (int k = I; k < B; ++k) {
+      const double* row = Wp + tri(k);
+      double wa[4], wb[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        wa[p] = (I + p <= k) ? row[I + p] : 0.0;  // W_ki = 0 above the diagonal
+        wb[p] = (J + p <= k) ? row[J + p] : 0.0;
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[p][r] += wa[p] * wb[r];
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = I + p, jj = J + r;
+        if (i < B && jj <= i) {
+          inv[(size_t)i * B + jj] = acc[p][r];
+          inv[(size_t)jj * B + i] = acc[p][r];
+        }
+      }
+  }
+  FP_T(3);
+  // L (upper zeros), W (f64, upper zeros), the f32 transposed copy for K4
+  for (int e = tid; e < (int)BB; e += kFpThreads) {
+    const int i = e / B, c = e - i * B;
+    chol[e] = c < i ? Ap[tri(i) + c] : (c == i ? dg[i] : 0.0);
+    w64[e] = c <= i ? Wp[tri(i) + c] : 0.0;
+  }
+  for (int e = tid; e < ld_w * ld_w; e += kFpThreads) {
+    const int k = e / ld_w, j = e - k * ld_w;
+    wf[e] = (j < B && k < B && k <= j) ? (float)Wp[tri(j) + k] : 0.0f;
+  }
+  FP_T(4);
+  if (tid == 0) {
+    status_all[m] = SKYRX_OK;
+    ridge_all[m] = ridge;
+  }
+}
+
+size_t finalize_panel_smem(int B) {
+  const size_t T = (size_t)B * (B + 1) / 2;
+  return (3 * T + 2 * (size_t)B) * sizeof(double);
+}
+
+// launched by skyrx_stats_finalize for 1 <= B <= 128
+int launch_finalize_panel(const double* moments, const double* shift, const int32_t* flags,
+                          int B, int batch, double* mu, double* sigma, double* chol,
+                          double* sigma_inv, double* w64, float* wf, int ld_w, float* mhl,
+                          double* ridge, int32_t* status, cudaStream_t st) {
+  const size_t sm = finalize_panel_smem(B);
+#define SKYRX_FP(rpl)                                                                          \
+  if (B <= 32 * (rpl)) {                                                                       \
+    cudaFuncSetAttribute(finalize_panel_kernel<rpl>,                                           \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);                \
+    finalize_panel_kernel<rpl><<<batch, kFpThreads, sm, st>>>(                                 \
+        moments, shift, flags, B, mu, sigma, chol, sigma_inv, w64, wf, ld_w, mhl, ridge,       \
+        status);                                                                               \
+    SKYRX_CHECK_LAUNCH("skyrx_stats_finalize/panel");                                          \
+    return SKYRX_OK;                                                                           \
+  }
+  SKYRX_FP(1) SKYRX_FP(2) SKYRX_FP(3) SKYRX_FP(4)
+#undef SKYRX_FP
+  set_error("finalize_panel: B = %d too large", B);
+  return SKYRX_ERR_ARG;
+}
+
+}  // namespace skyrx

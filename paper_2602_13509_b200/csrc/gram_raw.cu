@@ -243,7 +243,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
     }
   } else if (warp == 9) {
-    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+#ifdef GRX_LANE0_ISSUE  // experiment: the issuing loop on lane 0 alone
+    if ((tid & 31) == 0) {
+#else
+    {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
+#endif
       constexpr uint32_t id = idesc_u8_s32(128, TWO_M ? 128 : NW);
       constexpr uint32_t id2 = idesc_u8_s32(128, ONES ? 64 : (N2 > 0 ? N2 : 16));
       int t = 0, unit = 0;
@@ -262,6 +266,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           GR_PW(2, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
           tc_fence_after();
           const uint8_t* base = stages + st * STAGE;
+#ifdef GRX_LANE0_ISSUE
+          if (true) {
+#else
+          if (elect_one()) {
+#endif
 #pragma unroll
           for (int ks = 0; ks < kGrLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
@@ -288,8 +297,16 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             }
           }
           mma_commit(&empty[st]);
+          }
+#ifdef GRX_LANE0_ISSUE
         }
         mma_commit(&acc_full[buf]);
+#else
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&acc_full[buf]);
+        __syncwarp();
+#endif
       }
     }
   } else if (warp < 4) {  // ---------------------------------------------- scan

@@ -32,11 +32,13 @@ constexpr int kMaxStages = 4;
 constexpr int kMaxAtoms = 5;        // window <= 640 bytes
 constexpr uint32_t kAtom = kLb * 128u;
 
+constexpr int kMaxPass = 4;
+
 struct Params {
   const float* dark;
   const float* coeff;
   double ginv;
-  double* part;          // per CTA: Sxx[B*B] (lower), Sx[B], n  (zeroed before pass 0)
+  double* part;          // per CTA: Sxx[B*B] (lower), Sx[B], n  (zeroed before the launch)
   const uint32_t* usum;  // per unit: column sums of the window's u16 lanes [units][NW/2]
   int64_t L;
   int32_t S, B;
@@ -44,14 +46,33 @@ struct Params {
   int32_t nw16;          // u16 lanes per window (= 64 * na)
   int64_t split_lines;
   int64_t units;
-  int32_t nblk;          // blocks in this pass (<= 4)
-  int32_t blk_r[4], blk_c[4];  // their (row atom, column atom) of the window
-  int32_t natom;         // window atoms this pass loads (the ones its blocks use)
-  int32_t atom_id[kMaxAtoms];  // ... which, in stage-slot order
-  int32_t blk_rs[4], blk_cs[4];  // the blocks' row / column atoms as stage slots
-  int32_t nstages;       // TMA ring depth (<= kMaxStages)
-  int32_t first_pass;    // also accumulate Sx and n
+  // All passes run in ONE launch: CTA c takes pass c % npass of the units of its group
+  // c / npass (the npass CTAs of a group walk the same units in the same order, so the
+  // tiles one of them fetches are L2 hits for the others: the cube streams from HBM
+  // about once instead of once per pass).
+  int32_t npass, ngroups;
+  int32_t nblk[kMaxPass];                 // blocks in each pass (<= 4)
+  int32_t blk_r[kMaxPass][4], blk_c[kMaxPass][4];  // their (row atom, column atom)
+  int32_t natom[kMaxPass];                // window atoms each pass loads
+  int32_t atom_id[kMaxPass][kMaxAtoms];   // ... which, in stage-slot order
+  int32_t blk_rs[kMaxPass][4], blk_cs[kMaxPass][4];  // the blocks' atoms as stage slots
+  int32_t nstages[kMaxPass];              // TMA ring depth (<= kMaxStages)
+  // group pacing: CTA c publishes the tiles its producer has issued in progress[c]; no
+  // producer runs more than `pace` tiles ahead of the slowest CTA of its group, so the
+  // group's reads of a tile stay within the L2 residency window (the passes' epilogues
+  // differ in cost, and unpaced CTAs drift apart by far more than L2 holds)
+  uint32_t* progress;
+  int32_t pace;
 };
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void unit_geom(const Params& p, int64_t u, int& s, int64_t& l0,
                                           int64_t& nl) {
@@ -135,8 +156,11 @@ __global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restri
 __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
     const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const uint32_t STAGE = (uint32_t)p.natom * kAtom;
-  const int kStages = p.nstages;
+  const int ps = blockIdx.x % p.npass;  // this CTA's pass (its blocks of the window)
+  const bool first_pass = ps == 0;
+  const int nblk = p.nblk[ps], natom = p.natom[ps];
+  const uint32_t STAGE = (uint32_t)natom * kAtom;
+  const int kStages = p.nstages[ps];
   uint8_t* stages = sm;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * STAGE);
   uint64_t* full = bars;
@@ -147,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int B = p.B;
-  const int64_t u0 = blockIdx.x, ustep = gridDim.x;
+  const int64_t u0 = blockIdx.x / p.npass, ustep = p.ngroups;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     mbar_init(acc_full, 1), mbar_init(acc_empty, 128);
@@ -171,17 +195,45 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kStages;
           mbar_wait(&empty[st], ((t / kStages) & 1) ^ 1);
+          if (p.pace > 0 && t >= p.pace) {
+            // wait (bounded: pacing is a cache hint, never a dependency) until every CTA of
+            // the group has issued tile t - pace
+            const int g0 = (int)(blockIdx.x / p.npass) * p.npass;
+            for (int q = 0; q < p.npass; ++q) {
+              if (g0 + q == (int)blockIdx.x) continue;
+              for (int spin = 0; spin < (1 << 16); ++spin) {
+                if ((int)ld_acquire(p.progress + g0 + q) >= t - p.pace) break;
+                __nanosleep(128);
+              }
+            }
+          }
           mbar_arrive_expect_tx(&full[st], STAGE);
-          for (int a = 0; a < p.natom; ++a)  // only the atoms this pass's blocks use
-            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * p.atom_id[a],
+          for (int a = 0; a < natom; ++a)  // only the atoms this pass's blocks use
+            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * p.atom_id[ps][a],
                         (int)(l0 + (int64_t)k * kLb), &full[st]);
+          if (p.pace > 0) st_release(p.progress + blockIdx.x, (uint32_t)(t + 1));
         }
       }
+      if (p.pace > 0) st_release(p.progress + blockIdx.x, 0x7fffffffu);  // done: never wait on me
     }
   } else if (warp == 5) {
-    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+    {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t id = idesc_u8(128, 128);
-      int t = 0, unit = 0;
+      // every operand descriptor is the stage-0 / atom-0 / k-step-0 one plus an offset in
+      // its start-address field (16-byte units, bits 0-13; smem < 256 KB never carries):
+      // one add per MMA instead of rebuilding both descriptors from parameter-space loads
+      // (the single issuing thread, not the tensor core, bounded the kernel:
+      // ~30 instructions per 64-clock MMA)
+      const uint64_t d0 = smem_desc_sw128(stages, kAtom, 1024);
+      uint32_t ao[4], bo[4];
+#pragma unroll
+      for (int bk = 0; bk < 4; ++bk) {
+        ao[bk] = bk < nblk ? (uint32_t)p.blk_rs[ps][bk] * (kAtom >> 4) : 0u;
+        bo[bk] = bk < nblk ? (uint32_t)p.blk_cs[ps][bk] * (kAtom >> 4) : 0u;
+      }
+      const uint32_t stage16 = STAGE >> 4;
+      int t = 0, unit = 0, st = 0;
+      uint32_t sph = 0;
       for (int64_t u = u0; u < p.units; u += ustep, ++unit) {
         int s;
         int64_t l0, nl;
@@ -190,21 +242,25 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         mbar_wait(acc_empty, (unit & 1) ^ 1);
         tc_fence_after();
         for (int k = 0; k < ntile; ++k, ++t) {
-          const int st = t % kStages;
-          mbar_wait(&full[st], (t / kStages) & 1);
+          mbar_wait(&full[st], sph);
           tc_fence_after();
-          const uint8_t* base = stages + st * STAGE;
-          for (int ks = 0; ks < kLb / 32; ++ks) {
-            const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-            for (int bk = 0; bk < p.nblk; ++bk) {
-              const uint64_t da = smem_desc_sw128(base + p.blk_rs[bk] * kAtom + ks * 4096, kAtom, 1024);
-              const uint64_t db = smem_desc_sw128(base + p.blk_cs[bk] * kAtom + ks * 4096, kAtom, 1024);
-              mma_i8(tmem + 128 * bk, da, db, id, acc);
+          const uint64_t ds = d0 + (uint64_t)(st * stage16);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < kLb / 32; ++ks) {
+              const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+              const uint64_t dk = ds + (uint64_t)(ks * (4096 >> 4));
+#pragma unroll
+              for (int bk = 0; bk < 4; ++bk)
+                if (bk < nblk) mma_i8(tmem + 128 * bk, dk + ao[bk], dk + bo[bk], id, acc);
             }
+            mma_commit(&empty[st]);
           }
-          mma_commit(&empty[st]);
+          __syncwarp();
+          if (++st == kStages) st = 0, sph ^= 1;
         }
-        mma_commit(acc_full);
+        if (elect_one()) mma_commit(acc_full);
+        __syncwarp();
       }
     }
   } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
@@ -233,8 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
       asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(acc_full, unit & 1);
       tc_fence_after();
-      for (int bk = 0; bk < p.nblk; ++bk) {
-        const int mr = p.blk_r[bk], mc = p.blk_c[bk];
+      for (int bk = 0; bk < nblk; ++bk) {
+        const int mr = p.blk_r[ps][bk], mc = p.blk_c[ps][bk];
         const int m = 128 * mr + te;
         const int rel = m - off;
         const bool in_band = rel >= 0 && rel < 2 * B;
@@ -275,12 +331,15 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
                   4503599627370496.0;
               const double C2 = bandC[b2], d2 = bandD[b2], S2 = bandS[b2];
               const double xx = gv - db * S2 - Sb * d2 + Lu * db * d2;
-              part[(size_t)b * B + b2] += Cb * C2 * xx;
+              // fire-and-forget RED: one thread owns each entry of this CTA's partial,
+              // so the adds land in program (unit) order — deterministic — and the
+              // epilogue never waits on a global read-modify-write round trip
+              atomicAdd(part + (size_t)b * B + b2, Cb * C2 * xx);
             }
           }
         }
       }
-      if (p.first_pass) {  // band sums: sum x = C_b (m_b - L d_b)
+      if (first_pass) {  // band sums: sum x = C_b (m_b - L d_b)
         for (int b = te; b < B; b += 128)
           part[(size_t)B * B + b] += bandC[b] * (bandS[b] - Lu * bandD[b]);
         nsum += Lu;
@@ -289,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
       mbar_arrive(acc_empty);
       asm volatile("bar.sync 1, 128;" ::: "memory");  // band terms reused by the next unit
     }
-    if (p.first_pass && tid == 0) part[(size_t)B * B + B] = nsum;
+    if (first_pass && tid == 0) part[(size_t)B * B + B] = nsum;
   }
   tc_fence_before();
   __syncthreads();
@@ -325,24 +384,32 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
   p.na = raww_atoms(bands);
   SKYRX_REQUIRE(p.na <= kMaxAtoms, "wide raw-byte moments support windows <= 640 bytes");
   p.nw16 = 64 * p.na;
+  // pass plan first (see below): the grid is npass CTAs per group of units
+  const int npass_w = p.na == 3 ? 2 : (p.na == 4 ? 3 : (p.na == 5 ? 4 : 1));
   // long units: the epilogue (integer blocks -> calibrated f64) is not overlapped with the
-  // tensor core (the pass's blocks fill TMEM), so fewer, longer units (>= 4 per SM)
+  // tensor core (the pass's blocks fill TMEM), so fewer, longer units (>= 4 per group)
+  const int ngroups_max = kSMs / npass_w;
   int64_t nsplit = (lines + 16383) / 16384;
-  while ((int64_t)samples * nsplit < 4 * kSMs && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
+  while ((int64_t)samples * nsplit < 4 * ngroups_max && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
   p.split_lines = (lines + nsplit - 1) / nsplit;
   p.split_lines = (p.split_lines + kLb - 1) / kLb * kLb;
   nsplit = (lines + p.split_lines - 1) / p.split_lines;
   p.units = (int64_t)samples * nsplit;
-  int grid = kSMs;
-  if (p.units < grid) grid = (int)p.units;
+  p.ngroups = p.units < ngroups_max ? (int)p.units : ngroups_max;
+  p.npass = npass_w;
+  const int grid = p.ngroups * p.npass;
   const size_t stride = (size_t)bands * bands + bands + 1;
   cudaMemsetAsync(p.part, 0, (size_t)grid * stride * sizeof(double), st);
   uint32_t* usum = nullptr;
-  SKYRX_REQUIRE(cudaMallocAsync(&usum, (size_t)p.units * p.nw16 * sizeof(uint32_t), st) ==
+  const size_t usum_n = (size_t)p.units * p.nw16;
+  SKYRX_REQUIRE(cudaMallocAsync(&usum, (usum_n + grid) * sizeof(uint32_t), st) ==
                     cudaSuccess,
                 "cudaMallocAsync failed");
   p.usum = usum;
-  cudaMemsetAsync(usum, 0, (size_t)p.units * p.nw16 * sizeof(uint32_t), st);
+  cudaMemsetAsync(usum, 0, (usum_n + grid) * sizeof(uint32_t), st);
+  p.progress = usum + usum_n;
+  p.pace = 0;  // pacing cut DRAM reads 10.3 -> 5.4 GB but stalled the groups (3.1 -> 6.8 ms)
+  if (const char* e = getenv("SKYRX_RAWW_PACE")) p.pace = atoi(e);  // experiment hook
   raww_scan_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, dark, usum, flags);
   SKYRX_CHECK_LAUNCH("raww_scan_kernel");
   // 2-D byte view of the cube, 128-byte x 128-line swizzled boxes
@@ -382,28 +449,29 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
     for (; nb < 4; ++nb) gen[0][nb][0] = gen[0][nb][1] = -1;
     plan = gen, npass = 1;
   }
+  SKYRX_REQUIRE(npass == p.npass, "raww pass plan mismatch");
+  size_t smem = 0;
   for (int ps = 0; ps < npass; ++ps) {
-    p.nblk = 0;
-    p.natom = 0;
+    p.nblk[ps] = 0;
+    p.natom[ps] = 0;
     auto slot = [&](int atom) {
-      for (int i = 0; i < p.natom; ++i)
-        if (p.atom_id[i] == atom) return i;
-      p.atom_id[p.natom] = atom;
-      return p.natom++;
+      for (int i = 0; i < p.natom[ps]; ++i)
+        if (p.atom_id[ps][i] == atom) return i;
+      p.atom_id[ps][p.natom[ps]] = atom;
+      return p.natom[ps]++;
     };
     for (int i = 0; i < 4 && plan[ps][i][0] >= 0; ++i) {
-      p.blk_r[i] = plan[ps][i][0], p.blk_c[i] = plan[ps][i][1];
-      p.blk_rs[i] = slot(p.blk_r[i]), p.blk_cs[i] = slot(p.blk_c[i]);
-      ++p.nblk;
+      p.blk_r[ps][i] = plan[ps][i][0], p.blk_c[ps][i] = plan[ps][i][1];
+      p.blk_rs[ps][i] = slot(p.blk_r[ps][i]), p.blk_cs[ps][i] = slot(p.blk_c[ps][i]);
+      ++p.nblk[ps];
     }
-    const size_t stage = (size_t)p.natom * kAtom;
-    p.nstages = (int)std::min<size_t>(kMaxStages, (kSmemMax - 12288) / stage);
-    const size_t smem = p.nstages * stage + 16 * 8 + 3 * (size_t)bands * 8 + 1024;
-    p.first_pass = ps == 0;
-    cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    raww_gram_kernel<<<grid, kThreads, smem, st>>>(map, p);
-    SKYRX_CHECK_LAUNCH("raww_gram_kernel");
+    const size_t stage = (size_t)p.natom[ps] * kAtom;
+    p.nstages[ps] = (int)std::min<size_t>(kMaxStages, (kSmemMax - 12288) / stage);
+    smem = std::max(smem, p.nstages[ps] * stage + 16 * 8 + 3 * (size_t)bands * 8 + 1024);
   }
+  cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raww_gram_kernel<<<grid, kThreads, smem, st>>>(map, p);
+  SKYRX_CHECK_LAUNCH("raww_gram_kernel");
   cudaFreeAsync(usum, st);
   return gram_raw_sum_and_center(p.part, grid, bands, shift, own, moments, st, nullptr, 0,
                                  nullptr);

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       }
     }
   } else if (warp == 9) {
-    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+    {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t id2 = idesc_s8_s32(128, N2, 1, 1);
       constexpr uint32_t id1 = idesc_s8_s32(128, N1, 1, 1);
       constexpr uint32_t id0 = idesc_s8_s32(128, N0, 1, 1);
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         mbar_wait(&op_full[os], (t / kGtOpStages) & 1);
         tc_fence_after();
         const uint8_t* base = op_ring + os * OP_BYTES;
+        if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {  // 4 x 32 pixels
           const uint8_t* kb = base + ks * 4 * LBO;
@@ -142,6 +143,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         }
         mma_commit(&op_empty[os]);
         if ((t % kGtFlushTiles) == kGtFlushTiles - 1 || t == n - 1) mma_commit(acc_full);
+        }
+        __syncwarp();
       }
     }
   } else {  // ------------------------------------------------------------ workers

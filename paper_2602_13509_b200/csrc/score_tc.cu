@@ -399,7 +399,11 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
       }
     }
   } else if (warp == kMmaWarp) {
-    if ((tid & 31) == 0) {  // ------------------------------------------- MMA issuer
+#ifdef SCX_LANE0_ISSUE  // experiment: the issuing loop on lane 0 alone
+    if ((tid & 31) == 0) {
+#else
+    {  // ------------------------------- MMA issuer (whole warp, the elected lane issues)
+#endif
       mbar_wait(w_bar, 0);
       int as = 0, acs = 0;
       uint32_t aph = 0, cph = 0;
@@ -409,6 +413,11 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
         tc_fence_after();
         const uint32_t abase = tmem + kScoreABase + as * KP;  // A from TMEM
         const uint32_t d = tmem + acs * AW;
+#ifdef SCX_LANE0_ISSUE
+        if (true) {
+#else
+        if (elect_one()) {
+#endif
         // W = L^-1 is lower triangular: k-step ks (k in [16ks, 16ks+16)) only feeds
         // outputs j >= 16ks, so its MMAs cover N = KP - 16ks columns from column 16ks
         // (40 % fewer tensor cycles at KP = 80); k-step 0 spans every column and
@@ -439,6 +448,10 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
         }
         mma_commit(&a_empty[as]);
         mma_commit(&acc_full[acs]);
+        }
+#ifndef SCX_LANE0_ISSUE
+        __syncwarp();
+#endif
         if (++as == kScoreAStages) as = 0, aph ^= 1;
         if (++acs == kScoreAcc) acs = 0, cph ^= 1;
       }

@@ -270,7 +270,7 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
       }
     }
   } else if (warp == MMAW) {
-    if (lane == 0) {  // ------------------------------------------------- MMA issuer
+    {  // ------------------------------- MMA issuer (whole warp, the elected lane issues)
       int as = 0, acs = 0, ui = 0;
       uint32_t aph = 0, cph = 0;
       for (int64_t u = u0; u < p.units; u += ustep, ++ui) {
@@ -288,6 +288,7 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
           tc_fence_after();
           const uint32_t abase = tmem + ABASE + as * KP;
           const uint32_t d = tmem + acs * AW;
+          if (elect_one()) {
           // V lower triangular: k-step ks feeds outputs j >= 16 ks only
 #pragma unroll
           for (int ks = 0; ks < KP / 16; ++ks) {
@@ -314,10 +315,13 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
           }
           mma_commit(&a_empty[as]);
           mma_commit(&acc_full[acs]);
+          }
+          __syncwarp();
           if (++as == kAStages) as = 0, aph ^= 1;
           if (++acs == NACC) acs = 0, cph ^= 1;
         }
-        mma_commit(&rec_empty[rb]);
+        if (elect_one()) mma_commit(&rec_empty[rb]);
+        __syncwarp();
       }
     }
   } else if (warp >= EPI0) {  // --------------------------------------- epilogue

@@ -216,7 +216,7 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
       }
     }
   } else if (warp == MMAW) {
-    if (lane == 0) {  // ------------------------------------------------- MMA issuer
+    {  // ------------------------------- MMA issuer (whole warp, the elected lane issues)
       int ui = 0, bs = 0, acs = 0;
       uint32_t aph = 0, bph = 0, cph = 0;
       const uint32_t ahi = tmem + kABase, alo = tmem + kABase + KP / 2;
@@ -239,6 +239,7 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
             const uint8_t* bh = bring + bs * BSTAGE;
             const uint32_t id = idesc_f16_f32(128, rows, 0, 0);
             const uint32_t d = tmem + kAccBase + acs * kNB;
+            if (elect_one()) {
             for (int ks = 0; ks < kend / 16; ++ks) {
               const uint64_t bhi = smem_desc(bh + ks * 256, 128, sbo);
               const uint64_t blo = smem_desc(bh + half + ks * 256, 128, sbo);
@@ -250,6 +251,8 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
             mma_commit(&b_empty[bs]);
             mma_commit(&acc_full[acs]);
             if (nb == NNB - 1) mma_commit(a_empty);  // the tile's digits are consumed
+            }
+            __syncwarp();
             if (++bs == 2) bs = 0, bph ^= 1;
             if (++acs == 2) acs = 0, cph ^= 1;
           }

@@ -736,6 +736,10 @@ __global__ void whiten_prepare_kernel(const double* __restrict__ L, const double
   }
 }
 
+int launch_finalize_panel(const double* moments, const double* shift, const int32_t* flags,
+                          int B, int batch, double* mu, double* sigma, double* chol,
+                          double* sigma_inv, double* w64, float* wf, int ld_w, float* mhl,
+                          double* ridge, int32_t* status, cudaStream_t st);
 int launch_finalize_small(const double* moments, const double* shift, const int32_t* flags,
                           int B, int batch, double* mu, double* sigma, double* chol,
                           double* sigma_inv, double* w64, float* wf, int ld_w, float* mhl,
@@ -856,7 +860,12 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
   SKYRX_REQUIRE(bands > 0 && bands <= 1024, "bands %d outside [1, 1024]", bands);
   SKYRX_REQUIRE(batch >= 1, "batch must be >= 1");
   SKYRX_REQUIRE(ld_w >= bands, "ld_w %d < bands %d", ld_w, bands);
-  if (bands <= 80 && getenv("SKYRX_B200_FIN_GENERAL") == nullptr)  // latency kernel (finalize_small.cu)
+  const bool general = getenv("SKYRX_B200_FIN_GENERAL") != nullptr;
+  if (bands <= 128 && !general && getenv("SKYRX_B200_FIN_SLOT") == nullptr)  // finalize_panel.cu
+    return launch_finalize_panel(moments, shift, flags, bands, batch, mu, sigma, chol, sigma_inv,
+                                 whiten64, whiten, ld_w, mu_hilo, ridge, status,
+                                 as_stream(stream));
+  if (bands <= 80 && !general)  // the per-column latency kernel (finalize_small.cu)
     return launch_finalize_small(moments, shift, flags, bands, batch, mu, sigma, chol, sigma_inv,
                                  whiten64, whiten, ld_w, mu_hilo, ridge, status,
                                  as_stream(stream));

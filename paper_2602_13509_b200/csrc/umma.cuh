@@ -197,6 +197,18 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// one lane of a converged warp (elect.sync): the tcgen05 issue sites run the whole warp
+// through warp-uniform loops and let the elected lane issue, so their descriptors stay in
+// uniform registers (a `lane == 0` region makes ptxas wrap every MMA in a per-lane
+// R2UR / BRA.U.ANY loop, ~25 instructions per MMA on the single issuing thread)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(e));
+  return e != 0;
+}
+
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(

@@ -1,4 +1,4 @@
-"""K3 latency kernel (csrc/finalize_small.cu, B <= 128) against the general
+"""K3 latency kernels (csrc/finalize_panel.cu, B <= 128; finalize_small.cu) against the general
 finalize_kernel (stats.cu, SKYRX_B200_FIN_GENERAL=1) and the oracle.
 
 Same operands, order and rounding for the factor: mu, sigma, L and W must be
@@ -64,7 +64,7 @@ def finalize(P, mom, shift, B, monkeypatch, general):
             ("mu", "sigma", "chol", "sigma_inv", "w64", "whiten", "mu_hilo", "ridge", "status")}
 
 
-@pytest.mark.parametrize("B", [1, 3, 16, 44, 45, 63, 70, 79, 80])
+@pytest.mark.parametrize("B", [1, 3, 16, 31, 32, 33, 44, 45, 63, 70, 79, 80, 96, 97, 119, 128])
 def test_small_equals_general(P, monkeypatch, B):
     rng = np.random.default_rng(B)
     mom, shift = moments_batch(B, rng)
@@ -121,3 +121,20 @@ def test_nonfinite_and_range_flags(P):
     from paper_2602_13509_b200 import _lib
 
     assert st[0] == _lib.ERR_NONFINITE and st[1] == _lib.ERR_RANGE and st[2] == _lib.ERR_RANGE
+
+
+@pytest.mark.parametrize("B", [16, 45, 70, 80])
+def test_panel_equals_slot(P, monkeypatch, B):
+    """The panel kernel and the per-column slot kernel: bit-identical outputs."""
+    rng = np.random.default_rng(100 + B)
+    mom, shift = moments_batch(B, rng)
+    a = finalize(P, mom, shift, B, monkeypatch, general=False)
+    monkeypatch.setenv("SKYRX_B200_FIN_SLOT", "1")
+    b = finalize(P, mom, shift, B, monkeypatch, general=False)
+    monkeypatch.delenv("SKYRX_B200_FIN_SLOT", raising=False)
+    for key in ("status", "ridge", "mu", "sigma", "chol", "w64", "whiten", "mu_hilo", "sigma_inv"):
+        for m in range(mom.shape[0]):
+            if key not in ("status", "ridge") and a["status"][m] != 0:
+                continue
+            assert np.array_equal(np.atleast_1d(a[key][m]).view(np.uint8),
+                                  np.atleast_1d(b[key][m]).view(np.uint8)), (key, m)

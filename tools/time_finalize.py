@@ -1,4 +1,4 @@
-"""Latency of skyrx_stats_finalize (K3): small-B kernel vs the general one.
+"""Latency of skyrx_stats_finalize (K3): panel (B <= 128), slot (B <= 80) and general kernels.
 
     python tools/time_finalize.py   -> one line per (B, batch, kernel): us per call
 """
@@ -20,11 +20,15 @@ for B in (16, 70, 128):
         mom = np.concatenate([[float(n)], X.sum(0) * 0, q.ravel()])
         ds = P.DeviceStats(B, batch=batch)
         ds.moments.copy_(torch.from_numpy(np.tile(mom, (batch, 1))))
-        for general in (False, True):
-            if general:
+        for kind in ("panel", "slot", "general"):
+            os.environ.pop("SKYRX_B200_FIN_GENERAL", None)
+            os.environ.pop("SKYRX_B200_FIN_SLOT", None)
+            if kind == "general":
                 os.environ["SKYRX_B200_FIN_GENERAL"] = "1"
-            else:
-                os.environ.pop("SKYRX_B200_FIN_GENERAL", None)
+            elif kind == "slot":
+                if B > 80:
+                    continue
+                os.environ["SKYRX_B200_FIN_SLOT"] = "1"
             for _ in range(3):
                 ds.finalize()
             torch.cuda.synchronize()
@@ -34,5 +38,5 @@ for B in (16, 70, 128):
                 ds.finalize()
             b.record()
             torch.cuda.synchronize()
-            print(f"B={B} batch={batch} {'general' if general else 'small  '}: "
+            print(f"B={B} batch={batch} {kind:8s}: "
                   f"{a.elapsed_time(b) / 20 * 1e3:.1f} us per call", flush=True)
