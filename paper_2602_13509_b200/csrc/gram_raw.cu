@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
     }
   } else if (warp == 9) {
-#ifdef GRX_LANE0_ISSUE  // experiment: the issuing loop on lane 0 alone
+#ifndef GRX_ELECT_ISSUE  // lane 0 issues: 0.537 vs 0.563 ms per c4 strip for the
+    // warp-converged / elected-lane form (tools/time_gr_libs.py, round 2): the slower issue
+    // spaces the MMAs' shared-memory operand reads out against the scan warps' loads
     if ((tid & 31) == 0) {
 #else
     {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           GR_PW(2, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
           tc_fence_after();
           const uint8_t* base = stages + st * STAGE;
-#ifdef GRX_LANE0_ISSUE
+#ifndef GRX_ELECT_ISSUE
           if (true) {
 #else
           if (elect_one()) {
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           }
           mma_commit(&empty[st]);
           }
-#ifdef GRX_LANE0_ISSUE
+#ifndef GRX_ELECT_ISSUE
         }
         mma_commit(&acc_full[buf]);
 #else
