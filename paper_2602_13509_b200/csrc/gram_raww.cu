@@ -26,9 +26,14 @@ using namespace umma;
 
 namespace raww {
 
-constexpr int kLb = 128;            // lines per tile
+#ifndef RAWW_LB
+#define RAWW_LB 64
+#endif
+// lines per tile: 64, so a stage (every window atom: 5 x 8 KB at B = 270) leaves room for
+// five stages in flight (2.24 ms against 2.76 ms for 2 stages of 128 lines, B = 270)
+constexpr int kLb = RAWW_LB;
 constexpr int kThreads = 192;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 6;
 constexpr int kMaxAtoms = 5;        // window <= 640 bytes
 constexpr uint32_t kAtom = kLb * 128u;
 
@@ -46,33 +51,18 @@ struct Params {
   int32_t nw16;          // u16 lanes per window (= 64 * na)
   int64_t split_lines;
   int64_t units;
-  // All passes run in ONE launch: CTA c takes pass c % npass of the units of its group
-  // c / npass (the npass CTAs of a group walk the same units in the same order, so the
-  // tiles one of them fetches are L2 hits for the others: the cube streams from HBM
-  // about once instead of once per pass).
+  // All passes run in ONE launch, as a thread-block CLUSTER of npass CTAs per group of
+  // units: CTA rank r of a cluster computes pass r's blocks of the window for every unit
+  // of its group.  Each tile's window atoms are fetched once per cluster and multicast
+  // into every CTA's stage (rank r issues atoms a = r mod npass), and a stage is refilled
+  // only after the MMAs of all npass CTAs released it (multicast commits), so the cube
+  // streams from HBM once for all passes (ncu: 5.1 GB of DRAM reads at B = 270 against
+  // 10.3 GB for unicast CTA groups and 4 x 4.6 GB for one launch per pass).
   int32_t npass, ngroups;
   int32_t nblk[kMaxPass];                 // blocks in each pass (<= 4)
   int32_t blk_r[kMaxPass][4], blk_c[kMaxPass][4];  // their (row atom, column atom)
-  int32_t natom[kMaxPass];                // window atoms each pass loads
-  int32_t atom_id[kMaxPass][kMaxAtoms];   // ... which, in stage-slot order
-  int32_t blk_rs[kMaxPass][4], blk_cs[kMaxPass][4];  // the blocks' atoms as stage slots
-  int32_t nstages[kMaxPass];              // TMA ring depth (<= kMaxStages)
-  // group pacing: CTA c publishes the tiles its producer has issued in progress[c]; no
-  // producer runs more than `pace` tiles ahead of the slowest CTA of its group, so the
-  // group's reads of a tile stay within the L2 residency window (the passes' epilogues
-  // differ in cost, and unpaced CTAs drift apart by far more than L2 holds)
-  uint32_t* progress;
-  int32_t pace;
+  int32_t nstages;                        // TMA ring depth (<= kMaxStages), all atoms per stage
 };
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ void unit_geom(const Params& p, int64_t u, int& s, int64_t& l0,
                                           int64_t& nl) {
@@ -156,11 +146,12 @@ __global__ void __launch_bounds__(256) raww_scan_kernel(const uint16_t* __restri
 __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
     const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const int ps = blockIdx.x % p.npass;  // this CTA's pass (its blocks of the window)
+  const int ps = blockIdx.x % p.npass;  // this CTA's pass = its rank in the cluster
   const bool first_pass = ps == 0;
-  const int nblk = p.nblk[ps], natom = p.natom[ps];
-  const uint32_t STAGE = (uint32_t)natom * kAtom;
-  const int kStages = p.nstages[ps];
+  const int nblk = p.nblk[ps];
+  const uint32_t STAGE = (uint32_t)p.na * kAtom;  // every atom of the window, slot = atom
+  const int kStages = p.nstages;
+  const uint16_t all_ctas = (uint16_t)((1u << p.npass) - 1u);
   uint8_t* stages = sm;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + kStages * STAGE);
   uint64_t* full = bars;
@@ -173,13 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   const int B = p.B;
   const int64_t u0 = blockIdx.x / p.npass, ustep = p.ngroups;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    // full: this CTA's producer arms it; empty: one multicast commit per cluster CTA
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], p.npass);
     mbar_init(acc_full, 1), mbar_init(acc_empty, 128);
     fence_mbar_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // every CTA's barriers exist before any multicast lands on them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -194,27 +186,13 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         const int ntile = (int)((nl + kLb - 1) / kLb);
         for (int k = 0; k < ntile; ++k, ++t) {
           const int st = t % kStages;
-          mbar_wait(&empty[st], ((t / kStages) & 1) ^ 1);
-          if (p.pace > 0 && t >= p.pace) {
-            // wait (bounded: pacing is a cache hint, never a dependency) until every CTA of
-            // the group has issued tile t - pace
-            const int g0 = (int)(blockIdx.x / p.npass) * p.npass;
-            for (int q = 0; q < p.npass; ++q) {
-              if (g0 + q == (int)blockIdx.x) continue;
-              for (int spin = 0; spin < (1 << 16); ++spin) {
-                if ((int)ld_acquire(p.progress + g0 + q) >= t - p.pace) break;
-                __nanosleep(128);
-              }
-            }
-          }
-          mbar_arrive_expect_tx(&full[st], STAGE);
-          for (int a = 0; a < natom; ++a)  // only the atoms this pass's blocks use
-            tma_load_2d(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * p.atom_id[ps][a],
-                        (int)(l0 + (int64_t)k * kLb), &full[st]);
-          if (p.pace > 0) st_release(p.progress + blockIdx.x, (uint32_t)(t + 1));
+          mbar_wait(&empty[st], ((t / kStages) & 1) ^ 1);  // every cluster CTA released st
+          mbar_arrive_expect_tx(&full[st], STAGE);          // all atoms land here
+          for (int a = ps; a < p.na; a += p.npass)
+            tma_load_2d_mc(stages + st * STAGE + a * kAtom, &tmap, c0 + 128 * a,
+                           (int)(l0 + (int64_t)k * kLb), &full[st], all_ctas);
         }
       }
-      if (p.pace > 0) st_release(p.progress + blockIdx.x, 0x7fffffffu);  // done: never wait on me
     }
   } else if (warp == 5) {
     {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
@@ -228,8 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
       uint32_t ao[4], bo[4];
 #pragma unroll
       for (int bk = 0; bk < 4; ++bk) {
-        ao[bk] = bk < nblk ? (uint32_t)p.blk_rs[ps][bk] * (kAtom >> 4) : 0u;
-        bo[bk] = bk < nblk ? (uint32_t)p.blk_cs[ps][bk] * (kAtom >> 4) : 0u;
+        ao[bk] = bk < nblk ? (uint32_t)p.blk_r[ps][bk] * (kAtom >> 4) : 0u;
+        bo[bk] = bk < nblk ? (uint32_t)p.blk_c[ps][bk] * (kAtom >> 4) : 0u;
       }
       const uint32_t stage16 = STAGE >> 4;
       int t = 0, unit = 0, st = 0;
@@ -254,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
               for (int bk = 0; bk < 4; ++bk)
                 if (bk < nblk) mma_i8(tmem + 128 * bk, dk + ao[bk], dk + bo[bk], id, acc);
             }
-            mma_commit(&empty[st]);
+            mma_commit_mc(&empty[st], all_ctas);  // release st in every cluster CTA
           }
           __syncwarp();
           if (++st == kStages) st = 0, sph ^= 1;
@@ -354,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem, 512);
+  cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
 }
 
 }  // namespace raww
@@ -384,32 +363,77 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
   p.na = raww_atoms(bands);
   SKYRX_REQUIRE(p.na <= kMaxAtoms, "wide raw-byte moments support windows <= 640 bytes");
   p.nw16 = 64 * p.na;
-  // pass plan first (see below): the grid is npass CTAs per group of units
-  const int npass_w = p.na == 3 ? 2 : (p.na == 4 ? 3 : (p.na == 5 ? 4 : 1));
+  // lower-triangle blocks (row atom >= column atom), at most four per pass (TMEM)
+  static const int8_t plan3[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {-1, -1}},
+                                       {{2, 0}, {2, 1}, {2, 2}, {-1, -1}}};
+  static const int8_t plan4[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
+                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
+                                       {{3, 0}, {3, 3}, {-1, -1}, {-1, -1}}};
+  static const int8_t plan5[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
+                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
+                                       {{3, 0}, {3, 3}, {4, 0}, {4, 3}},
+                                       {{4, 1}, {4, 2}, {4, 4}, {-1, -1}}};
+  int8_t gen[1][4][2];
+  const int8_t(*plan)[4][2] = nullptr;
+  int npass = 0;
+  if (p.na == 3) plan = plan3, npass = 2;
+  else if (p.na == 4) plan = plan4, npass = 3;
+  else if (p.na == 5) plan = plan5, npass = 4;
+  else {  // one or two atoms: every block in one pass
+    int nb = 0;
+    for (int a = 0; a < p.na; ++a)
+      for (int c = 0; c <= a; ++c) gen[0][nb][0] = (int8_t)a, gen[0][nb][1] = (int8_t)c, ++nb;
+    for (; nb < 4; ++nb) gen[0][nb][0] = gen[0][nb][1] = -1;
+    plan = gen, npass = 1;
+  }
+  p.npass = npass;
+  for (int ps = 0; ps < npass; ++ps) {
+    p.nblk[ps] = 0;
+    for (int i = 0; i < 4 && plan[ps][i][0] >= 0; ++i) {
+      p.blk_r[ps][i] = plan[ps][i][0], p.blk_c[ps][i] = plan[ps][i][1];
+      ++p.nblk[ps];
+    }
+  }
+  const size_t stage = (size_t)p.na * kAtom;
+  p.nstages = (int)std::min<size_t>(kMaxStages, (kSmemMax - 12288) / stage);
+  const size_t smem = p.nstages * stage + 16 * 8 + 3 * (size_t)bands * 8 + 1024;
+  cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // one wave of clusters: as many as fit at once (a cluster's CTAs share a GPC)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)npass;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(npass * (kSMs / npass));
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, raww_gram_kernel, &cfg) != cudaSuccess ||
+      nclusters < 1)
+    nclusters = kSMs / npass;
   // long units: the epilogue (integer blocks -> calibrated f64) is not overlapped with the
   // tensor core (the pass's blocks fill TMEM), so fewer, longer units (>= 4 per group)
-  const int ngroups_max = kSMs / npass_w;
   int64_t nsplit = (lines + 16383) / 16384;
-  while ((int64_t)samples * nsplit < 4 * ngroups_max && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
+  while ((int64_t)samples * nsplit < 4 * nclusters && lines / (nsplit + 1) >= 4 * kLb) ++nsplit;
   p.split_lines = (lines + nsplit - 1) / nsplit;
   p.split_lines = (p.split_lines + kLb - 1) / kLb * kLb;
   nsplit = (lines + p.split_lines - 1) / p.split_lines;
   p.units = (int64_t)samples * nsplit;
-  p.ngroups = p.units < ngroups_max ? (int)p.units : ngroups_max;
-  p.npass = npass_w;
+  p.ngroups = p.units < nclusters ? (int)p.units : nclusters;
   const int grid = p.ngroups * p.npass;
+  cfg.gridDim = dim3(grid);
   const size_t stride = (size_t)bands * bands + bands + 1;
   cudaMemsetAsync(p.part, 0, (size_t)grid * stride * sizeof(double), st);
   uint32_t* usum = nullptr;
   const size_t usum_n = (size_t)p.units * p.nw16;
-  SKYRX_REQUIRE(cudaMallocAsync(&usum, (usum_n + grid) * sizeof(uint32_t), st) ==
-                    cudaSuccess,
+  SKYRX_REQUIRE(cudaMallocAsync(&usum, usum_n * sizeof(uint32_t), st) == cudaSuccess,
                 "cudaMallocAsync failed");
   p.usum = usum;
-  cudaMemsetAsync(usum, 0, (usum_n + grid) * sizeof(uint32_t), st);
-  p.progress = usum + usum_n;
-  p.pace = 0;  // pacing cut DRAM reads 10.3 -> 5.4 GB but stalled the groups (3.1 -> 6.8 ms)
-  if (const char* e = getenv("SKYRX_RAWW_PACE")) p.pace = atoi(e);  // experiment hook
+  cudaMemsetAsync(usum, 0, usum_n * sizeof(uint32_t), st);
   raww_scan_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, dark, usum, flags);
   SKYRX_CHECK_LAUNCH("raww_scan_kernel");
   // 2-D byte view of the cube, 128-byte x 128-line swizzled boxes
@@ -424,53 +448,8 @@ int stats_raw_wide(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SKYRX_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  // lower-triangle blocks (row atom >= column atom), at most four per pass (TMEM), grouped so
-  // each pass touches few atoms: a pass streams only the atoms its blocks use (B = 270:
-  // 4 passes x 3 of the 5 atoms instead of 4 x 5)
-  static const int8_t plan3[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {-1, -1}},
-                                       {{2, 0}, {2, 1}, {2, 2}, {-1, -1}}};
-  static const int8_t plan4[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
-                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
-                                       {{3, 0}, {3, 3}, {-1, -1}, {-1, -1}}};
-  static const int8_t plan5[][4][2] = {{{0, 0}, {1, 0}, {1, 1}, {2, 0}},
-                                       {{2, 1}, {2, 2}, {3, 1}, {3, 2}},
-                                       {{3, 0}, {3, 3}, {4, 0}, {4, 3}},
-                                       {{4, 1}, {4, 2}, {4, 4}, {-1, -1}}};
-  int8_t gen[16][4][2];
-  const int8_t(*plan)[4][2] = nullptr;
-  int npass = 0;
-  if (p.na == 3) plan = plan3, npass = 2;
-  else if (p.na == 4) plan = plan4, npass = 3;
-  else if (p.na == 5) plan = plan5, npass = 4;
-  else {  // one or two atoms: every block in one pass
-    int nb = 0;
-    for (int a = 0; a < p.na; ++a)
-      for (int c = 0; c <= a; ++c) gen[0][nb][0] = (int8_t)a, gen[0][nb][1] = (int8_t)c, ++nb;
-    for (; nb < 4; ++nb) gen[0][nb][0] = gen[0][nb][1] = -1;
-    plan = gen, npass = 1;
-  }
-  SKYRX_REQUIRE(npass == p.npass, "raww pass plan mismatch");
-  size_t smem = 0;
-  for (int ps = 0; ps < npass; ++ps) {
-    p.nblk[ps] = 0;
-    p.natom[ps] = 0;
-    auto slot = [&](int atom) {
-      for (int i = 0; i < p.natom[ps]; ++i)
-        if (p.atom_id[ps][i] == atom) return i;
-      p.atom_id[ps][p.natom[ps]] = atom;
-      return p.natom[ps]++;
-    };
-    for (int i = 0; i < 4 && plan[ps][i][0] >= 0; ++i) {
-      p.blk_r[ps][i] = plan[ps][i][0], p.blk_c[ps][i] = plan[ps][i][1];
-      p.blk_rs[ps][i] = slot(p.blk_r[ps][i]), p.blk_cs[ps][i] = slot(p.blk_c[ps][i]);
-      ++p.nblk[ps];
-    }
-    const size_t stage = (size_t)p.natom[ps] * kAtom;
-    p.nstages[ps] = (int)std::min<size_t>(kMaxStages, (kSmemMax - 12288) / stage);
-    smem = std::max(smem, p.nstages[ps] * stage + 16 * 8 + 3 * (size_t)bands * 8 + 1024);
-  }
-  cudaFuncSetAttribute(raww_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  raww_gram_kernel<<<grid, kThreads, smem, st>>>(map, p);
+  SKYRX_REQUIRE(cudaLaunchKernelEx(&cfg, raww_gram_kernel, map, p) == cudaSuccess,
+                "raww_gram_kernel cluster launch failed");
   SKYRX_CHECK_LAUNCH("raww_gram_kernel");
   cudaFreeAsync(usum, st);
   return gram_raw_sum_and_center(p.part, grid, bands, shift, own, moments, st, nullptr, 0,
