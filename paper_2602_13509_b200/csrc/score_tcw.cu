@@ -386,7 +386,15 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
       if (shist[i]) atomicAdd(&p.hist0[i], shist[i]);
 }
 
-// one CTA per (sample, background): the wide record (N-blocked V_s, T, q', inv)
+// one CTA per (kPackS consecutive samples, background): the wide records (N-blocked V_s,
+// T, q', inv).  Every element of W is read once per CTA and serves all its samples (the
+// per-sample form read the 0.6 MB W four times per sample: 0.43 ms per c3 cube).  Per
+// sample the arithmetic and its order are unchanged.
+#ifndef TCW_PACK_S
+#define TCW_PACK_S 8
+#endif
+constexpr int kPackS = TCW_PACK_S;
+
 template <int KP>
 __global__ void __launch_bounds__(256) tcw_pack_kernel(const double* __restrict__ w64,
                                                        const float* __restrict__ mu_hilo, int B,
@@ -394,66 +402,116 @@ __global__ void __launch_bounds__(256) tcw_pack_kernel(const double* __restrict_
                                                        const float* __restrict__ coeff, double gain,
                                                        uint8_t* __restrict__ out) {
   constexpr int NNB = nblocks(KP);
-  const int s = blockIdx.x;
+  const int s0 = blockIdx.x * kPackS;
+  const int ns = min(kPackS, S - s0);
   const int bg = blockIdx.y;
   const double* W = w64 + (size_t)bg * B * B;
   const float* mh = mu_hilo + (size_t)bg * 2 * B;
-  uint8_t* o = out + ((size_t)bg * S + s) * rec_bytes(KP);
-  uint8_t* tail = o + nb_offset(KP, NNB);
-  __shared__ double cs[KP], es[KP], red[256];
-  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
-    double c = 0.0, e = 0.0;
+  __shared__ double cs[kPackS][KP], es[kPackS][KP], red[kPackS][8], scs[kPackS];
+  __shared__ int exs[kPackS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < kPackS * KP; e += blockDim.x) {
+    const int q = e / KP, k = e - q * KP;
+    double c = 0.0, ev = 0.0;
     uint16_t t = 0;
-    if (k < B) {
+    if (k < B && q < ns) {
+      const int s = s0 + q;
       const double mu = (double)mh[k] + (double)mh[B + k];
       const double cg = (double)coeff[(size_t)s * B + k] / gain;
       const double d = (double)dark[(size_t)s * B + k];
       double R = rint(d + mu / cg);
       R = R < 0.0 ? 0.0 : (R > 4095.0 ? 4095.0 : R);
       c = cg;
-      e = cg * (R - d) - mu;
+      ev = cg * (R - d) - mu;
       t = (uint16_t)(4096.0 - R);
     }
-    cs[k] = c;
-    es[k] = e;
-    reinterpret_cast<uint16_t*>(tail)[k] = t;
+    cs[q][k] = c;
+    es[q][k] = ev;
+    if (q < ns)
+      reinterpret_cast<uint16_t*>(out + ((size_t)bg * S + s0 + q) * rec_bytes(KP) +
+                                  nb_offset(KP, NNB))[k] = t;
   }
   __syncthreads();
-  double m0 = 0.0;
-  for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
-    const int j = e / B, k = e - j * B;
-    if (k <= j) m0 = fmax(m0, fabs(W[e] * cs[k]));
+  // per sample: the largest |W_jk c_k| -> one power-of-two scale for V_s
+  double m0[kPackS];
+#pragma unroll
+  for (int q = 0; q < kPackS; ++q) m0[q] = 0.0;
+  for (int j = warp; j < B; j += 8)
+    for (int k = lane; k <= j; k += 32) {
+      const double w = W[(size_t)j * B + k];
+#pragma unroll
+      for (int q = 0; q < kPackS; ++q) m0[q] = fmax(m0[q], fabs(w * cs[q][k]));
+    }
+#pragma unroll
+  for (int q = 0; q < kPackS; ++q) {
+    double m = m0[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[q][warp] = m;
   }
-  red[threadIdx.x] = m0;
   __syncthreads();
-  double mx = 0.0;
-  for (int i = 0; i < 256; ++i) mx = fmax(mx, red[i]);
-  int ex = 0;
-  if (mx > 0.0) frexp(mx, &ex);
-  const double sc = ldexp(1.0, 14 - ex);
-  float* q = reinterpret_cast<float*>(tail + 2 * KP);
-  for (int j = threadIdx.x; j < KP; j += blockDim.x) {
-    double qj = 0.0;
-    for (int k = 0; k <= j && k < B; ++k)
-      if (j < B) qj += W[(size_t)j * B + k] * es[k];
-    q[j] = (float)(qj * sc);
+  if (tid < kPackS) {
+    double mx = 0.0;
+    for (int w = 0; w < 8; ++w) mx = fmax(mx, red[tid][w]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);
+    exs[tid] = ex;
+    scs[tid] = ldexp(1.0, 14 - ex);
   }
-  if (threadIdx.x == 0) q[KP] = (float)ldexp(1.0, ex - 14);
+  __syncthreads();
+  // q'_j = sum_k W_jk e_k (ascending k, as before), scaled
+  for (int j = tid; j < KP; j += blockDim.x) {
+    double qj[kPackS];
+#pragma unroll
+    for (int q = 0; q < kPackS; ++q) qj[q] = 0.0;
+    if (j < B) {
+      // the row's loads eight at a time ahead of the (ascending, serial) sums
+      const double* wr = W + (size_t)j * B;
+      int k = 0;
+      for (; k + 8 <= j + 1; k += 8) {
+        double w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = wr[k + i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int q = 0; q < kPackS; ++q) qj[q] += w[i] * es[q][k + i];
+      }
+      for (; k <= j; ++k) {
+        const double w = wr[k];
+#pragma unroll
+        for (int q = 0; q < kPackS; ++q) qj[q] += w * es[q][k];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kPackS; ++q)
+      if (q < ns) {
+        float* qo = reinterpret_cast<float*>(out + ((size_t)bg * S + s0 + q) * rec_bytes(KP) +
+                                             nb_offset(KP, NNB) + 2 * KP);
+        qo[j] = (float)(qj[q] * scs[q]);
+        if (j == 0) qo[KP] = (float)ldexp(1.0, exs[q] - 14);
+      }
+  }
   // N-block operands: block nb = rows [64 nb, 64 nb + rows) x K [0, kend), K-major
   for (int nb = 0; nb < NNB; ++nb) {
     const int rows = nb_rows(KP, nb), kend = nb_kend(KP, nb);
     const uint32_t sbo = (uint32_t)(kend / 8) * 128u;
-    uint8_t* hi = o + nb_offset(KP, nb);
-    uint8_t* lo = hi + (size_t)rows * kend * 2;
-    for (int e = threadIdx.x; e < rows * kend; e += blockDim.x) {
-      const int jj = e / kend, k = e - jj * kend;
+    for (int jj = warp; jj < rows; jj += 8) {
       const int j = kNB * nb + jj;
-      const double v = (j < B && k < B && k <= j) ? W[(size_t)j * B + k] * cs[k] * sc : 0.0;
-      const __half hh = __double2half(v);
-      const __half l = __double2half(v - (double)__half2float(hh));
-      const uint32_t off = (jj >> 3) * sbo + (k >> 3) * 128u + (jj & 7) * 16u + (k & 7) * 2u;
-      *reinterpret_cast<__half*>(hi + off) = hh;
-      *reinterpret_cast<__half*>(lo + off) = l;
+      for (int k = lane; k < kend; k += 32) {
+        const double w = (j < B && k < B && k <= j) ? W[(size_t)j * B + k] : 0.0;
+        const uint32_t off = (jj >> 3) * sbo + (k >> 3) * 128u + (jj & 7) * 16u + (k & 7) * 2u;
+#pragma unroll
+        for (int q = 0; q < kPackS; ++q) {
+          if (q >= ns) break;
+          const double v = w * cs[q][k] * scs[q];
+          const __half hh = __double2half(v);
+          const __half l = __double2half(v - (double)__half2float(hh));
+          uint8_t* hi = out + ((size_t)bg * S + s0 + q) * rec_bytes(KP) + nb_offset(KP, nb);
+          *reinterpret_cast<__half*>(hi + off) = hh;
+          *reinterpret_cast<__half*>(hi + (size_t)rows * kend * 2 + off) = l;
+        }
+      }
     }
   }
 }
@@ -522,7 +580,7 @@ extern "C" int skyrx_scorew_prep(const double* whiten64, const float* mu_hilo, i
                 "scorew_prep supports 128 < B <= 272");
   SKYRX_REQUIRE(gain > 0.0, "every line gain must be positive");
   cudaStream_t st = as_stream(stream);
-  const dim3 grid(samples, batch);
+  const dim3 grid((samples + tcw::kPackS - 1) / tcw::kPackS, batch);
   switch (tcw_kp(bands)) {
 #define SKYRX_KP(k)                                                                        \
   case k:                                                                                  \

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "raw_byte_moments or wide" tests/test_gpu_geometry.py::test_c3_full_cube -q -p no:randomly -x 2>&1 | tail -2
+C3="python bench.py --config c3 --steps 1 --warmup 1 --no-e2e --no-cpu --no-parity --no-graph"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s16_launches_c3.csv $C3 > /dev/null 2>&1; echo "ncu rc=$?"
+python tools/launch_summary.py gpurun_out/s16_launches_c3.csv 2>/dev/null | head -14
+timeout 300 python bench.py --config c3 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/s16_c3.json 2>/dev/null
+python -c "import json;d=json.load(open('gpurun_out/s16_c3.json'));print('c3', d['value']/1e9, d['ms_per_step'], d['roofline']['frac'], d['roofline']['other_pass'], d.get('parity',{}).get('pass'))"
