@@ -114,6 +114,15 @@ int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t samples, int32_t 
                    const float* qinv, double* moments, int32_t* flags, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* The same quantised-digit tensor-core moments of an already calibrated f32 radiance cube
+ * (replaces compute_stats(cube) rx.py:42-66 for mode="fast" on a RadianceCube, B <= 79,
+ * samples*bands*4 % 16 == 0); shift / qinv from skyrx_quant_shift(SKYRX_IN_F32, ...).
+ * flags |= 1 on a non-finite value, |= 2 if the quantiser range overflowed (then use
+ * skyrx_stats_accumulate). */
+int skyrx_stats_tc_f32(const float* pixels, int64_t lines, int32_t samples, int32_t bands,
+                       const double* shift, const float* qinv, double* moments, int32_t* flags,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* Raw-byte tensor-core moments (RAW cubes, one constant line gain, B <= 128,
  * samples*bands*2 % 16 == 0): exact integer byte Grams per sample column
  * (tcgen05 kind::i8, TMA-fed), calibration applied per sample in f64.  Same

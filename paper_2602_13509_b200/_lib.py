@@ -48,6 +48,7 @@ SIGNATURES = {
     "skyrx_stats_tc_workspace": (sz, [i32]),
     "skyrx_quant_shift": (C.c_int, [i32, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp]),
     "skyrx_stats_tc": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "skyrx_stats_tc_f32": (C.c_int, [vp, i64, i32, i32, vp, vp, vp, vp, vp, sz, vp]),
     "skyrx_stats_raw_supported": (C.c_int, [i64, i32, i32, vp]),
     "skyrx_stats_raw_workspace": (sz, [i32]),
     "skyrx_stats_raw_workspace_for": (sz, [i64, i32, i32]),

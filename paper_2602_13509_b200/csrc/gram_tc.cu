@@ -51,8 +51,12 @@ struct GramTcParams {
   uint32_t raw_stage_bytes;
 };
 
-template <int BPG>
+// KIND: SKYRX_IN_RAW_U16 (calibrate on the fly, the fused path) or SKYRX_IN_F32 (an
+// already calibrated radiance cube: compute_stats(mode="fast") on a RadianceCube)
+template <int BPG, int KIND = SKYRX_IN_RAW_U16>
 __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) {
+  constexpr bool kF32 = KIND == SKYRX_IN_F32;
+  constexpr uint32_t ESZ = kF32 ? 4u : 2u;  // bytes per band value in the ring
   constexpr int NG = BPG / 16;
   constexpr uint32_t LBO = 3u * NG * 128u;
   // 16 pixel groups (128 px) + pad for the M=128 A reads past the last group
@@ -110,11 +114,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         const int s = t % kGtRawStages;
         mbar_wait(&raw_empty[s], ((t / kGtRawStages) & 1) ^ 1);
         const TileInfo ti = tile_info(p.ts, it0 + t);
-        const uint32_t seg = (uint32_t)ti.w * B * 2u;
+        const uint32_t seg = (uint32_t)ti.w * B * ESZ;
         mbar_arrive_expect_tx(&raw_full[s], seg * (uint32_t)ti.nlines);
         uint8_t* dst = raw_ring + s * p.raw_stage_bytes;
         for (int li = 0; li < ti.nlines; ++li) {
-          const uint16_t* src = p.raw + ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(p.raw) +
+                               ((ti.line0 + li) * (int64_t)p.ts.S + ti.s0) * B * ESZ;
           bulk_g2s(dst + li * seg, src, seg, &raw_full[s]);
         }
       }
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
     };
     for (int t = 0; t < n; ++t) {
       const TileInfo ti = tile_info(p.ts, it0 + t);
-      if (ti.block != cur_block) {
+      if (!kF32 && ti.block != cur_block) {
         asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
         for (int e = tid; e < ti.w * B; e += kGtWorkers) {
           const int j = e / B, b = e - j * B;
@@ -219,11 +224,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       if (valid) {
         const int li = r / ti.w;
         j = r - li * ti.w;
-        g = __ldg(p.gain + ti.line0 + li);
+        if (!kF32) g = __ldg(p.gain + ti.line0 + li);
         const uint64_t pix = (uint64_t)(ti.line0 + li) * (uint64_t)p.ts.S + (uint64_t)(ti.s0 + j);
         pixkey = (uint32_t)(pix * 0x9E3779B97F4A7C15ull >> 32) * 0x85EBCA6Bu;
       }
       const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
+      const float* fp = reinterpret_cast<const float*>(raw_ring + s * p.raw_stage_bytes) + r * B;
       const float* dk = dark_s + j * (B + 1);
       const float* ck = coeff_s + j * (B + 1);
       uint8_t* ob = op_ring + os * OP_BYTES + (uint32_t)(r >> 3) * LBO + (uint32_t)(r & 7) * 16u;
@@ -237,9 +243,14 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
             const int k = gi * 16 + q4 * 4 + q;
             int D = 0;
             if (valid && k < B) {
-              const float t = __fsub_rn((float)rp[k], dk[k]);
-              float x = __fmul_rn(t < 0.0f ? 0.0f : t, ck[k]);
-              if (g != 1.0f) x = __fdiv_rn(x, g);
+              float x;
+              if constexpr (kF32) {
+                x = fp[k];
+              } else {
+                const float t = __fsub_rn((float)rp[k], dk[k]);
+                x = __fmul_rn(t < 0.0f ? 0.0f : t, ck[k]);
+                if (g != 1.0f) x = __fdiv_rn(x, g);
+              }
               finite_ok &= isfinite(x);
               const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);
               range_ok &= fabsf(tq) < 2064383.0f;  // keeps D2 within int8
@@ -370,9 +381,10 @@ __global__ void quant_shift_kernel(const void* pixels, int64_t npix, int32_t sam
 
 static int bpg_for(int B) { return ((B + 1 + 15) / 16) * 16; }
 
-template <int BPG>
+template <int BPG, int KIND = SKYRX_IN_RAW_U16>
 static int launch_gram_tc(GramTcParams p, double* moments, cudaStream_t st) {
-  p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * 2u) + 127u) & ~127u);
+  constexpr uint32_t ESZ = KIND == SKYRX_IN_F32 ? 4u : 2u;
+  p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * ESZ) + 127u) & ~127u);
   constexpr uint32_t LBO = 3u * (BPG / 16) * 128u;
   const size_t smem = kGtRawStages * (size_t)p.raw_stage_bytes + kGtOpStages * (16u * LBO + 1024u) +
                       2 * (size_t)kGtWmax * (p.ts.B + 1) * 4 + 2 * BPG * 4 + 16 * 8 + 64;
@@ -380,8 +392,9 @@ static int launch_gram_tc(GramTcParams p, double* moments, cudaStream_t st) {
   if (p.ts.items < grid) grid = (int)p.ts.items;
   if (grid < 1) grid = 1;
   p.per_cta = (p.ts.items + grid - 1) / grid;
-  cudaFuncSetAttribute(gram_tc_kernel<BPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  gram_tc_kernel<BPG><<<grid, kGtThreads, smem, st>>>(p);
+  cudaFuncSetAttribute(gram_tc_kernel<BPG, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  gram_tc_kernel<BPG, KIND><<<grid, kGtThreads, smem, st>>>(p);
   SKYRX_CHECK_LAUNCH("gram_tc_kernel");
   gram_tc_reduce_kernel<BPG><<<ceil_div(BPG * BPG, 256), 256, 0, st>>>(p.part, grid, p.ts.B, p.qinv,
                                                                         moments);
@@ -446,6 +459,36 @@ extern "C" int skyrx_stats_tc(const uint16_t* raw, int64_t lines, int32_t sample
     case 48: return launch_gram_tc<48>(p, moments, st);
     case 64: return launch_gram_tc<64>(p, moments, st);
     case 80: return launch_gram_tc<80>(p, moments, st);
+  }
+  set_error("unsupported band count %d", bands);
+  return SKYRX_ERR_ARG;
+}
+
+// compute_stats(mode="fast") on an f32 radiance cube (rx.py:42-66 on a RadianceCube): the
+// same quantised-digit tensor-core Gram, the values read as they are.  shift / qinv from
+// skyrx_quant_shift(SKYRX_IN_F32, ...).
+extern "C" int skyrx_stats_tc_f32(const float* pixels, int64_t lines, int32_t samples,
+                                  int32_t bands, const double* shift, const float* qinv,
+                                  double* moments, int32_t* flags, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  SKYRX_REQUIRE(skyrx_stats_tc_supported(lines, samples, bands, pixels),
+                "tensor-core moments path unsupported for this shape/alignment");
+  SKYRX_REQUIRE(workspace_bytes >= skyrx_stats_tc_workspace(bands), "workspace too small");
+  SKYRX_REQUIRE(((int64_t)samples * bands * 4) % 16 == 0, "f32 lines must be 16-byte multiples");
+  GramTcParams p{};
+  p.raw = reinterpret_cast<const uint16_t*>(pixels);  // byte address; the kernel reads f32
+  p.shift = shift;
+  p.qinv = qinv;
+  p.part = reinterpret_cast<double*>(workspace);
+  p.flags = flags;
+  tc_sched(lines, samples, bands, kGtWmax, p.ts);
+  cudaStream_t st = as_stream(stream);
+  switch (bpg_for(bands)) {
+    case 16: return launch_gram_tc<16, SKYRX_IN_F32>(p, moments, st);
+    case 32: return launch_gram_tc<32, SKYRX_IN_F32>(p, moments, st);
+    case 48: return launch_gram_tc<48, SKYRX_IN_F32>(p, moments, st);
+    case 64: return launch_gram_tc<64, SKYRX_IN_F32>(p, moments, st);
+    case 80: return launch_gram_tc<80, SKYRX_IN_F32>(p, moments, st);
   }
   set_error("unsupported band count %d", bands);
   return SKYRX_ERR_ARG;

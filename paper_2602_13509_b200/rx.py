@@ -149,10 +149,36 @@ def compute_stats(cube, chunk: int = 65536, *, mode: str = "precise") -> CubeSta
         raise ValueError(f"insufficient samples: {n} pixels for {bands} bands")
     ds = DeviceStats(bands)
     px = _radiance_device(cube)
-    accumulate_moments(ds, 0, _lib.IN_F32, px, cube.lines, cube.samples,
-                       precise=(mode == "precise"))
+    L, S = cube.lines, cube.samples
+    if mode == "fast" and _tc_f32_moments(ds, px, L, S):
+        ds.finalize()
+        if int(ds.status[0].item()) != _lib.ERR_RANGE:
+            return ds.host(0, n)
+        ds.flags.zero_()  # the quantiser's range overflowed: the f32-run kernel below
+    accumulate_moments(ds, 0, _lib.IN_F32, px, L, S, precise=(mode == "precise"))
     ds.finalize()
     return ds.host(0, n)
+
+
+def _tc_f32_moments(ds: DeviceStats, px: torch.Tensor, L: int, S: int) -> bool:
+    """mode="fast" moments of an f32 radiance cube on the tensor cores (skyrx_stats_tc_f32:
+    quantised int8 digits, exact int32 digit Gram); False where the kernel does not apply
+    (B > 79, small cubes whose quantiser noise does not average out, unaligned rows)."""
+    B = ds.bands
+    lib = _lib.load()
+    if (B > 79 or L * S < TC_MIN_PIXELS or (S * B * 4) % 16 != 0
+            or not lib.skyrx_stats_tc_supported(L, S, B, px.data_ptr())):
+        return False
+    s = _dev.stream_ptr()
+    qinv = _dev.empty((B,), torch.float32)
+    nbytes = int(lib.skyrx_stats_tc_workspace(B))
+    ws = _dev.empty((nbytes,), torch.uint8)
+    _lib.call("skyrx_quant_shift", _lib.IN_F32, px.data_ptr(), L, S, B, None, None, None,
+              ds.shift[0].data_ptr(), qinv.data_ptr(), s)
+    _lib.call("skyrx_stats_tc_f32", px.data_ptr(), L, S, B, ds.shift[0].data_ptr(),
+              qinv.data_ptr(), ds.moments[0].data_ptr(), ds.flags[0:1].data_ptr(),
+              ws.data_ptr(), nbytes, s)
+    return True
 
 
 def _device_whitening(stats: CubeStats, bands: int):

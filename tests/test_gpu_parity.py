@@ -290,6 +290,36 @@ class TestFastMode:
         want = g[f"{name}/scores"]
         assert (np.abs(sc - want) / np.maximum(want, 1e-12)).max() < SCORE_RTOL_FAST
 
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 1000), (256, 48, 2048), (900, 72, 400)])
+    def test_radiance_cube_moments_on_tensor_cores(self, P, monkeypatch, S, B, L):
+        """compute_stats(RadianceCube, mode="fast") takes the quantised-digit tensor-core
+        Gram (skyrx_stats_tc_f32) and meets the 1e-5 statistics tolerance; the paper's
+        binned cube shape (1000 x 900 x 70) first."""
+        from paper_2602_13509_b200 import _lib
+
+        t = osynth.make_tables(51, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L)
+        rad = O.apply_calibration(raw, t.dark, t.coeff, np.ones(L))
+        calls = []
+        real = _lib.call
+        monkeypatch.setattr(_lib, "call", lambda name, *a: (calls.append(name), real(name, *a))[1])
+        st = P.compute_stats(rad_cube(P, rad), mode="fast")
+        assert "skyrx_stats_tc_f32" in calls
+        want = O.compute_stats(rad)
+        assert normwise(st.mu, want.mu) < STATS_RTOL_FAST
+        assert normwise(st.sigma, want.sigma) < STATS_RTOL_FAST
+        inv = normwise(st.sigma_inv, want.sigma_inv)
+        print(f"PARITY tc-f32 moments {S}x{B}x{L} sigma_inv {inv:.3e}")
+        assert inv < INV_RTOL_FAST, inv
+        assert st.ridge_used == want.ridge_used
+
+    def test_radiance_cube_nonfinite_on_tensor_cores(self, P):
+        t = osynth.make_tables(52, 900, 70, 5)
+        rad = O.apply_calibration(osynth.generate_lines(t, 0, 400), t.dark, t.coeff, np.ones(400))
+        rad[123, 45, 6] = np.inf
+        with pytest.raises(ValueError, match="non-finite"):
+            P.compute_stats(rad_cube(P, rad), mode="fast")
+
 
 # ----------------------------------------------------------------------------- normalise etc.
 class TestNormalize:
