@@ -396,7 +396,7 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
 constexpr int kPackS = TCW_PACK_S;
 
 template <int KP>
-__global__ void __launch_bounds__(256) tcw_pack_kernel(const double* __restrict__ w64,
+__global__ void __launch_bounds__(256, 1) tcw_pack_kernel(const double* __restrict__ w64,
                                                        const float* __restrict__ mu_hilo, int B,
                                                        int S, const float* __restrict__ dark,
                                                        const float* __restrict__ coeff, double gain,
@@ -493,24 +493,41 @@ __global__ void __launch_bounds__(256) tcw_pack_kernel(const double* __restrict_
       }
   }
   // N-block operands: block nb = rows [64 nb, 64 nb + rows) x K [0, kend), K-major
+  // a thread takes one 16-byte core-matrix row (output row jj, k = 8 k8 .. 8 k8 + 7) for every
+  // sample of the CTA; consecutive threads write consecutive 16-byte rows (the canonical
+  // layout's (jj & 7) then k8 order), so each warp stores 512 contiguous bytes per sample
   for (int nb = 0; nb < NNB; ++nb) {
     const int rows = nb_rows(KP, nb), kend = nb_kend(KP, nb);
-    const uint32_t sbo = (uint32_t)(kend / 8) * 128u;
-    for (int jj = warp; jj < rows; jj += 8) {
-      const int j = kNB * nb + jj;
-      for (int k = lane; k < kend; k += 32) {
-        const double w = (j < B && k < B && k <= j) ? W[(size_t)j * B + k] : 0.0;
-        const uint32_t off = (jj >> 3) * sbo + (k >> 3) * 128u + (jj & 7) * 16u + (k & 7) * 2u;
+    const int nk8 = kend / 8;
+    const uint32_t sbo = (uint32_t)nk8 * 128u;
+    for (int g = tid; g < rows * nk8; g += blockDim.x) {
+      const int jb = (g >> 3) / nk8, k8 = (g >> 3) - jb * nk8;
+      const int jj = 8 * jb + (g & 7), j = kNB * nb + jj, k0 = 8 * k8;
+      double w[8];
 #pragma unroll
-        for (int q = 0; q < kPackS; ++q) {
-          if (q >= ns) break;
-          const double v = w * cs[q][k] * scs[q];
-          const __half hh = __double2half(v);
-          const __half l = __double2half(v - (double)__half2float(hh));
-          uint8_t* hi = out + ((size_t)bg * S + s0 + q) * rec_bytes(KP) + nb_offset(KP, nb);
-          *reinterpret_cast<__half*>(hi + off) = hh;
-          *reinterpret_cast<__half*>(hi + (size_t)rows * kend * 2 + off) = l;
+      for (int i = 0; i < 8; ++i) {
+        const int k = k0 + i;
+        w[i] = (j < B && k < B && k <= j) ? W[(size_t)j * B + k] : 0.0;
+      }
+      const uint32_t off = (uint32_t)jb * sbo + (uint32_t)k8 * 128u + (uint32_t)(g & 7) * 16u;
+#pragma unroll
+      for (int q = 0; q < kPackS; ++q) {
+        if (q >= ns) break;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const double v0 = w[i] * cs[q][k0 + i] * scs[q];
+          const double v1 = w[i + 1] * cs[q][k0 + i + 1] * scs[q];
+          const __half h0 = __double2half(v0), h1 = __double2half(v1);
+          const __half l0 = __double2half(v0 - (double)__half2float(h0));
+          const __half l1 = __double2half(v1 - (double)__half2float(h1));
+          hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+          lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
         }
+        uint8_t* hi = out + ((size_t)bg * S + s0 + q) * rec_bytes(KP) + nb_offset(KP, nb);
+        *reinterpret_cast<uint4*>(hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(hi + (size_t)rows * kend * 2 + off) =
+            make_uint4(lw[0], lw[1], lw[2], lw[3]);
       }
     }
   }

@@ -736,6 +736,19 @@ __global__ void whiten_prepare_kernel(const double* __restrict__ L, const double
   }
 }
 
+// sigma_inv = W^T W and the f32 whitening copy for the wide paths
+static int launch_wide_inv(const double* w64, int B, int batch, double* sigma_inv, float* wf,
+                           int ld_w, const int32_t* status, cudaStream_t st) {
+  const int64_t work = std::max((int64_t)B * B, (int64_t)ld_w * ld_w);
+  wide_inv_kernel<<<dim3((int)ceil_div<int64_t>(work, 256), batch), 256, 0, st>>>(
+      w64, B, sigma_inv, wf, ld_w, status);
+  SKYRX_CHECK_LAUNCH("skyrx_stats_finalize/wide");
+  return SKYRX_OK;
+}
+
+int launch_finalize_wide(const double* moments, const double* shift, const int32_t* flags, int B,
+                         int batch, double* mu, double* sigma, double* chol, double* w64,
+                         float* mhl, double* ridge, int32_t* status, cudaStream_t st);
 int launch_finalize_panel(const double* moments, const double* shift, const int32_t* flags,
                           int B, int batch, double* mu, double* sigma, double* chol,
                           double* sigma_inv, double* w64, float* wf, int ld_w, float* mhl,
@@ -869,14 +882,20 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
     return launch_finalize_small(moments, shift, flags, bands, batch, mu, sigma, chol, sigma_inv,
                                  whiten64, whiten, ld_w, mu_hilo, ridge, status,
                                  as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  const bool wide = bands > kSmemInvMaxB;
+  if (bands > 128 && bands <= 288 && !general) {  // finalize_wide.cu, then W^T W below
+    const int rc = launch_finalize_wide(moments, shift, flags, bands, batch, mu, sigma, chol,
+                                        whiten64, mu_hilo, ridge, status, st);
+    if (rc != SKYRX_OK) return rc;
+    return launch_wide_inv(whiten64, bands, batch, sigma_inv, whiten, ld_w, status, st);
+  }
   const size_t sm = 2 * (size_t)bands * sizeof(double) +
                     (bands <= kSmemInvMaxB ? ((size_t)bands * (bands | 1) + (size_t)bands * bands) *
                                                  sizeof(double)
                      : bands <= kSmemCholMaxB
                          ? (size_t)bands * (bands | 1) * sizeof(double)
                          : (size_t)(bands <= 750 ? 32 : 16) * bands * sizeof(double));  // panel
-  const bool wide = bands > kSmemInvMaxB;
-  cudaStream_t st = as_stream(stream);
   cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   finalize_kernel<<<batch, kFinThreads, sm, st>>>(moments, shift, flags, bands, mu, sigma, chol,
                                                   sigma_inv, whiten64, whiten, ld_w, mu_hilo,
@@ -887,10 +906,7 @@ extern "C" int skyrx_stats_finalize(const double* moments, const double* shift,
     cudaFuncSetAttribute(wide_trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
     wide_trinv_kernel<<<dim3(ceil_div(bands, 32), batch), 1024, xs, st>>>(chol, bands, whiten64,
                                                                           status);
-    const int64_t work = std::max((int64_t)bands * bands, (int64_t)ld_w * ld_w);
-    wide_inv_kernel<<<dim3((int)ceil_div<int64_t>(work, 256), batch), 256, 0, st>>>(
-        whiten64, bands, sigma_inv, whiten, ld_w, status);
-    SKYRX_CHECK_LAUNCH("skyrx_stats_finalize/wide");
+    return launch_wide_inv(whiten64, bands, batch, sigma_inv, whiten, ld_w, status, st);
   }
   return SKYRX_OK;
 }

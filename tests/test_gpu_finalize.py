@@ -1,4 +1,5 @@
-"""K3 latency kernels (csrc/finalize_panel.cu, B <= 128; finalize_small.cu) against the general
+"""K3 latency kernels (csrc/finalize_panel.cu, B <= 128; finalize_small.cu; finalize_wide.cu,
+128 < B <= 288) against the general
 finalize_kernel (stats.cu, SKYRX_B200_FIN_GENERAL=1) and the oracle.
 
 Same operands, order and rounding for the factor: mu, sigma, L and W must be
@@ -64,7 +65,8 @@ def finalize(P, mom, shift, B, monkeypatch, general):
             ("mu", "sigma", "chol", "sigma_inv", "w64", "whiten", "mu_hilo", "ridge", "status")}
 
 
-@pytest.mark.parametrize("B", [1, 3, 16, 31, 32, 33, 44, 45, 63, 70, 79, 80, 96, 97, 119, 128])
+@pytest.mark.parametrize("B", [1, 3, 16, 31, 32, 33, 44, 45, 63, 70, 79, 80, 96, 97, 119, 128,
+                               129, 160, 161, 200, 255, 270, 272, 288])
 def test_small_equals_general(P, monkeypatch, B):
     rng = np.random.default_rng(B)
     mom, shift = moments_batch(B, rng)
@@ -74,18 +76,22 @@ def test_small_equals_general(P, monkeypatch, B):
     assert np.array_equal(a["ridge"], b["ridge"])
     ok = a["status"] == 0
     # B > 118: the general path takes W from its column-wise multi-CTA kernel (another
-    # summation order), so W and its f32 copy are compared to rounding there
+    # summation order; finalize_wide.cu: a blocked one), so W and its f32 copy are compared
+    # to rounding there
     exact = ("mu", "sigma", "chol") + (("w64", "whiten", "mu_hilo") if B <= 118 else ("mu_hilo",))
     for key in exact:
         for m in np.flatnonzero(ok):
             assert np.array_equal(a[key][m].view(np.uint8), b[key][m].view(np.uint8)), (key, m)
+    # two backward-stable triangular inverses agree to rounding x cond(L); the ridged
+    # rank-deficient matrix (m = 1, cond(L) ~ 1e5) widens that for the blocked wide kernel
+    tol = 1e-13 if B <= 128 else 1e-11
     if B > 118:
         for m in np.flatnonzero(ok):
             d = np.abs(a["w64"][m] - b["w64"][m]).max()
-            assert d <= 1e-13 * np.abs(b["w64"][m]).max(), (m, d)
+            assert d <= tol * np.abs(b["w64"][m]).max(), (m, d)
     for m in np.flatnonzero(ok):
         d = np.abs(a["sigma_inv"][m] - b["sigma_inv"][m]).max()
-        assert d <= 1e-14 * np.abs(b["sigma_inv"][m]).max(), (m, d)
+        assert d <= tol / 10 * np.abs(b["sigma_inv"][m]).max(), (m, d)
         assert np.array_equal(a["sigma_inv"][m], a["sigma_inv"][m].T)
     # and the oracle's factorisation of the same moments (rx.py:56-86); the ridged
     # rank-deficient case (cond ~ 1e10) only on its ridge

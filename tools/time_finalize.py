@@ -1,4 +1,5 @@
-"""Latency of skyrx_stats_finalize (K3): panel (B <= 128), slot (B <= 80) and general kernels.
+"""Latency of skyrx_stats_finalize (K3): panel (B <= 128), slot (B <= 80), wide (128 < B <= 288)
+and general kernels.
 
     python tools/time_finalize.py   -> one line per (B, batch, kernel): us per call
 """
@@ -12,7 +13,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import paper_2602_13509_b200 as P  # noqa: E402
 
 rng = np.random.default_rng(0)
-for B in (16, 70, 128):
+for B in [int(b) for b in os.environ.get("BANDS", "16,70,128,270").split(",")]:
     for batch in (1, 64):
         n = 100000
         X = rng.standard_normal((4096, B)) @ np.diag(np.linspace(1, 30, B))
