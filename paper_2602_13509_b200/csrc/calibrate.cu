@@ -103,7 +103,17 @@ __global__ void __launch_bounds__(256) calibrate_bin_kernel(
 // SB x bands raw words are one contiguous range (16-byte loads into shared memory) and
 // its SB x nout outputs another (coalesced stores).  Same ops, same order as calib()
 // and the left-to-right band sum, so bit-identical.
-constexpr int kBinBufs = 2;
+// kBinBufs line buffers per CTA, kBinBufs - 1 lines in flight: at 2 CTAs per SM (121
+// registers) one line in flight per CTA kept ~17 KB per SM outstanding, 0.28 of the HBM
+// bandwidth at paper geometry (Little's law wants ~45 KB per SM)
+#ifndef SKYRX_BIN_BUFS
+#define SKYRX_BIN_BUFS 3
+#endif
+constexpr int kBinBufs = SKYRX_BIN_BUFS;
+#ifndef SKYRX_BIN_LPS
+#define SKYRX_BIN_LPS 4
+#endif
+constexpr int kBinLps = SKYRX_BIN_LPS;  // lines per ring slot
 
 template <int KIND, int PO, int FMAX>
 __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
@@ -124,6 +134,11 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
   int rowoff[PO], kbv[PO][FMAX];
   float dkv[PO][FMAX], ckv[PO][FMAX];
   int rgbm[PO];  // the RGB channels this output band feeds (several when targets share a band)
+  bool tab_ok = true;  // every table word of this thread admits calib_fast
+  // the output's FMAX bands are consecutive from an even word (discard_oob_bands keeps one
+  // contiguous range): its raw counts come as FMAX/2 32-bit words
+  bool pairs[PO];
+  uint32_t soff[PO];  // byte offset of the output's first band word in a line buffer
 #pragma unroll
   for (int q = 0; q < PO; ++q) {
     const int e = threadIdx.x + 256 * q;
@@ -133,18 +148,33 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       if (rgb_idx.c[c] == o) rgbm[q] |= 1 << c;
+    pairs[q] = kRaw && factor == FMAX && FMAX % 2 == 0;
+    soff[q] = 0;
 #pragma unroll
     for (int j = 0; j < FMAX; ++j) {
       const int k = o * factor + (j < factor ? j : 0);
       const int b = keep ? __ldg(keep + k) : k;
       kbv[q][j] = b;
+      pairs[q] = pairs[q] && b == kbv[q][0] + j && ((rowoff[q] + kbv[q][0]) & 1) == 0;
+      if (j == 0) soff[q] = (uint32_t)(rowoff[q] + b) * (uint32_t)sizeof(T);
       if (kRaw) {
         const int64_t tb = (int64_t)(s0 + sl) * bands + b;
         dkv[q][j] = __ldg(dark + tb);
         ckv[q][j] = __ldg(coeff + tb);
+        tab_ok = tab_ok && (dkv[q][j] == 0.0f || calib_fast_range(dkv[q][j])) &&
+                 calib_fast_range(ckv[q][j]);
       }
     }
   }
+  // CTA-uniform path choices (every thread's tables / band layout admit them)
+  bool vec_all = kRaw;
+#pragma unroll
+  for (int q = 0; q < PO; ++q) vec_all = vec_all && (pairs[q] || threadIdx.x + 256 * q >= nouts);
+  const bool vec_cta = __syncthreads_and(vec_all) != 0;
+  const bool fast_cta = kRaw && __syncthreads_and(tab_ok) != 0;
+  if (!rgb)
+#pragma unroll
+    for (int q = 0; q < PO; ++q) rgbm[q] = 0;
   const T* in = reinterpret_cast<const T*>(src);
   const int64_t l0 = blockIdx.y * lines_per_cta;
   const int64_t l1 = min(lines, l0 + lines_per_cta);
@@ -152,60 +182,103 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
   const int bufw = (nrow + 15) & ~15;  // words per buffer (16-byte aligned)
   const bool vec = ((((uintptr_t)in) | ((uintptr_t)samples * bands * sizeof(T)) |
                      ((uintptr_t)s0 * bands * sizeof(T))) & 15) == 0 && (nbytes & 15) == 0;
-  auto fetch = [&](int64_t line, T* dst) {
-    const T* g = in + (line * samples + s0) * (int64_t)bands;
-    if (vec) {
-      const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
-      for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + 16 * v),
-                     "l"(reinterpret_cast<const char*>(g) + 16 * (size_t)v));
-    } else {
-      for (int e = threadIdx.x; e < nrow; e += blockDim.x) dst[e] = g[e];
+  // a ring slot holds kBinLps consecutive lines: one barrier, one wait and one fetch round
+  // per kBinLps lines (the per-line control work was half the kernel's instructions)
+  const int64_t nsteps = (l1 - l0 + kBinLps - 1) / kBinLps;
+  auto fetch = [&](int64_t step, T* dst) {
+#pragma unroll
+    for (int h = 0; h < kBinLps; ++h) {
+      const int64_t line = l0 + step * kBinLps + h;
+      if (line >= l1) break;
+      const T* g = in + (line * samples + s0) * (int64_t)bands;
+      if (vec) {
+        const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst + h * bufw);
+        for (int v = threadIdx.x; v < nbytes / 16; v += blockDim.x)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0 + 16 * v),
+                       "l"(reinterpret_cast<const char*>(g) + 16 * (size_t)v));
+      } else {
+        for (int e = threadIdx.x; e < nrow; e += blockDim.x) dst[h * bufw + e] = g[e];
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  // kBinBufs line buffers: lines l+1 .. l+kBinBufs-1 are in flight while line l is
-  // calibrated (about 6 lines per SM cover the HBM latency at full bandwidth)
+  // kBinBufs slots: steps s+1 .. s+kBinBufs-1 are in flight while step s is calibrated
   for (int b = 0; b < kBinBufs - 1; ++b) {
-    if (l0 + b < l1) fetch(l0 + b, tile + b * bufw);
+    if (b < nsteps) fetch(b, tile + b * kBinLps * bufw);
     else asm volatile("cp.async.commit_group;\n" ::);
   }
-  for (int64_t line = l0; line < l1; ++line) {
-    const int cur = (int)((line - l0) % kBinBufs);
+  for (int64_t step = 0; step < nsteps; ++step) {
+    const int cur = (int)(step % kBinBufs);
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kBinBufs - 2));
-    __syncthreads();  // line `line` is in tile[cur]; the buffer fetched next is free
-    const int64_t nxt = line + kBinBufs - 1;
-    if (nxt < l1) fetch(nxt, tile + (int)((nxt - l0) % kBinBufs) * bufw);
+    __syncthreads();  // step `step` is in slot cur; the slot fetched next is free
+    const int64_t nxt = step + kBinBufs - 1;
+    if (nxt < nsteps) fetch(nxt, tile + (int)(nxt % kBinBufs) * kBinLps * bufw);
     else asm volatile("cp.async.commit_group;\n" ::);
-    const T* tl = tile + cur * bufw;
+#pragma unroll
+    for (int h = 0; h < kBinLps; ++h) {
+    const int64_t line = l0 + step * kBinLps + h;
+    if (line >= l1) break;
+    const T* tl = tile + (cur * kBinLps + h) * bufw;
     const float gl = kRaw ? __ldg(gain + line) : 1.0f;
+    const float gi = __frcp_rn(gl);
     float* o_line = out + (line * samples + s0) * (int64_t)nout;
+    float* rgb_line = rgb ? rgb + (line * samples + s0) * 3 : nullptr;
+    // CTA-uniform variants: whole-word raw loads (VEC), calib_fast (FAST); the band loop is
+    // fully unrolled over FMAX == factor bands with no per-element branching
+    const uint32_t tl32 = (uint32_t)__cvta_generic_to_shared(tl);
+    auto body = [&](auto vec_c, auto fast_c, auto one_c) {
+      constexpr bool VEC = decltype(vec_c)::value, FAST = decltype(fast_c)::value;
+      constexpr bool ONE = decltype(one_c)::value;  // gain 1: x / 1 == x, no division
 #pragma unroll
-    for (int q = 0; q < PO; ++q) {
-      const int e = threadIdx.x + 256 * q;
-      if (e < nouts) {
-        const T* row = tl + rowoff[q];
-        float acc = 0.0f;
+      for (int q = 0; q < PO; ++q) {
+        const int e = threadIdx.x + 256 * q;
+        if (e < nouts) {
+          const T* row = tl + rowoff[q];
+          float rv[FMAX];
+          if constexpr (VEC) {  // exact u16 -> f32: (2^23 + r) - 2^23
 #pragma unroll
-        for (int j = 0; j < FMAX; ++j) {
-          if (j < factor) {
-            float x;
-            if constexpr (kRaw) {
-              x = calib((float)row[kbv[q][j]], dkv[q][j], ckv[q][j], gl);
-            } else {
-              x = row[kbv[q][j]];
+            for (int j = 0; j < FMAX; j += 2) {
+              uint32_t v;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(tl32 + soff[q] + 2 * j));
+              rv[j] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
+              rv[j + 1] = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
             }
-            acc = (j == 0) ? x : __fadd_rn(acc, x);
+          } else {
+#pragma unroll
+            for (int j = 0; j < FMAX; ++j) rv[j] = j < factor ? (float)row[kbv[q][j]] : 0.0f;
+          }
+          float acc = 0.0f;
+#pragma unroll
+          for (int j = 0; j < FMAX; ++j) {
+            if (VEC || j < factor) {
+              float x;
+              if constexpr (kRaw) {
+                x = ONE ? __fmul_rn(fmaxf(__fsub_rn(rv[j], dkv[q][j]), 0.0f), ckv[q][j])
+                    : FAST ? calib_fast(rv[j], dkv[q][j], ckv[q][j], gl, gi)
+                           : calib(rv[j], dkv[q][j], ckv[q][j], gl);
+              } else {
+                x = rv[j];
+              }
+              acc = (j == 0) ? x : __fadd_rn(acc, x);
+            }
+          }
+          __stcs(o_line + e, acc);
+          if (rgbm[q]) {
+            float* px = rgb_line + (rowoff[q] / bands) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (rgbm[q] & (1 << c)) px[c] = acc;
           }
         }
-        __stcs(o_line + e, acc);
-        if (rgb && rgbm[q]) {
-          float* px = rgb + (line * samples + s0 + rowoff[q] / bands) * 3;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            if (rgbm[q] & (1 << c)) px[c] = acc;
-        }
       }
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const bool fast = fast_cta && calib_fast_range(gl);
+    if (vec_cta && fast && gl == 1.0f) body(T_{}, T_{}, T_{});
+    else if (vec_cta && fast) body(T_{}, T_{}, F_{});
+    else if (fast) body(F_{}, T_{}, F_{});
+    else body(F_{}, F_{}, F_{});
     }
   }
 }
@@ -219,7 +292,7 @@ static bool launch_bin_tiled(const void* src, int64_t lines, int32_t samples, in
   if (factor > FMAX || nout > 256 * PO || lines < 1 || samples < 1) return false;
   const int sb = std::min(samples, (256 * PO) / nout);
   const size_t elem = KIND == SKYRX_IN_RAW_U16 ? 2 : 4;
-  const size_t sm = kBinBufs * (((size_t)sb * bands + 15) / 16 * 16) * elem;  // line buffers
+  const size_t sm = kBinBufs * kBinLps * (((size_t)sb * bands + 15) / 16 * 16) * elem;
   if (sm > 200 * 1024) return false;
   auto k = calibrate_bin_tiled_kernel<KIND, PO, FMAX>;
   if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

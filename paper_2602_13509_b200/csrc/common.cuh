@@ -49,6 +49,25 @@ __device__ __forceinline__ float calib(float raw, float dark, float coeff, float
   return __fdiv_rn(t, gain);
 }
 
+// calib() with the division by the line gain as a multiplication by y = RN(1/g) plus one
+// FMA correction (Markstein: y within half an ulp of 1/g and q within one ulp of t/g give
+// RN(q + (t - q g) y) = RN(t/g)), 4 instructions instead of the __fdiv_rn sequence.  Only
+// for operands that keep every intermediate normal and finite: the caller checks g, dark and
+// coeff (calib_fast_ok); tools/fastdiv_probe.cu compares it with __fdiv_rn bit for bit.
+__device__ __forceinline__ float calib_fast(float raw, float dark, float coeff, float gain,
+                                            float ginv) {
+  // finite operands (calib_fast_range): no NaN to keep, so max(t, 0) is one FMNMX
+  const float t = __fmul_rn(fmaxf(__fsub_rn(raw, dark), 0.0f), coeff);
+  const float q = __fmul_rn(t, ginv);
+  const float r = __fmaf_rn(-q, gain, t);
+  return __fmaf_rn(r, ginv, q);
+}
+// |x| in [2^-60, 2^60] (normal, finite); dark may also be 0
+__device__ __forceinline__ bool calib_fast_range(float x) {
+  const float a = fabsf(x);
+  return a >= 8.6736174e-19f && a <= 1.1529215e18f;
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return isfinite(x); }
 
 template <typename T>
