@@ -2,27 +2,33 @@
 //
 // Reference: rx.py:56-66 (f64 mean, then f64 Gram of centred pixels).  Here
 // every calibrated value is centred by the sample shift c_b and quantised to a
-// fixed point D = floor((x - c_b) / q_b + u) with a deterministic per-element
-// dither u in [0, 1) (unbiased even for lattice-valued data), |D| < 2^21 - 2^15 (q_b a power of
-// two from 4x the largest sampled deviation).  D is split into three digits
-// D = D2*2^14 + D1*2^7 + D0 (D0, D1 in [-64, 64), D2 in [-127, 127]) and the
-// Gram of the digits is accumulated EXACTLY in int32 by tcgen05.mma kind::i8
-// (|digit products| <= 2^14; TMEM is drained every 2^17 pixels):
-//     G = sum_a 2^14a Pa,a + sum_{a>b} 2^7(a+b) (Pa,b + Pa,b^T),  Pa,b = Da^T Db
-// One constant band (index B, digit D0 = 1 on valid pixels) makes the same
-// products carry n and sum(D).  The only approximation left is the
-// quantisation (noise ~q/sqrt(12) per element, averaged over the cube): the
-// emulated worst score error on the c1 generator is 8.5e-7.
-// Values outside the quantiser range set flags |= 2 and the host recomputes
-// that cube with the FFMA kernel (never happens on the BASELINE generators).
+// fixed point D = floor((x - c_b) / q_b + u) with a per-element dither u in [0, 1)
+// (unbiased even for lattice-valued data), |D| < 2^22 (q_b a power of two from 4.2x the
+// largest sampled deviation).  E = D + 2^22 is split into three unsigned bytes
+// E = e2*2^16 + e1*2^8 + e0 (e2 < 128) and the Gram of the digits is accumulated EXACTLY
+// in int32 by tcgen05.mma kind::i8 (unsigned; digit products < 2^16, TMEM drained every
+// 255 tiles of 128 pixels):
+//     G_E = sum_a 2^16a Pa,a + sum_{a>b} 2^8(a+b) (Pa,b + Pa,b^T),  Pa,b = Ea^T Eb
+// One constant band (index B, E = 1 on valid pixels) makes the same products carry n and
+// sum(E); the reduce removes the offset exactly: G_D = G_E - 2^22 (S_i + S_j) + n 2^44.
+// The only approximation left is the quantisation (noise ~q/sqrt(12) per element,
+// averaged over the cube).  Values outside the quantiser range (or non-finite) set
+// flags |= 2 and the host recomputes that cube with the FFMA kernel.
+//
+// Per element the workers spend ~12 instructions: raw words as u32 pairs (exact u16 ->
+// f32 by the 2^23 trick), calibration with the per-line 1/g as a multiply (the moments
+// are not a bit-exact calibration anyway: rx.py's f32 rounding is the reference's own
+// ~1e-8), quantisation by the 1.5 * 2^23 magic add (round to nearest of tq + u - 1/2 =
+// floor(tq + u)), a Weyl-sequence dither over a per-pixel hash, and byte digits moved
+// into the three operand planes with PRMT (no per-digit shifts or masks).
 //
 // Operands are MN-major (bands contiguous) so each pixel row writes 16-byte
 // chunks: smem address of (digit a, band b, pixel p) =
 //     (p/8)*LBO + (a*NG + b/16)*128 + (p%8)*16 + b%16,  LBO = 3*NG*128.
 // Per 32-pixel K step three MMAs cover the six products:
-//     A = D2 (M=128), B = [D0|D1|D2] (N = 3*BPg) -> P20 P21 P22
-//     A = D1,         B = [D0|D1]    (N = 2*BPg) -> P10 P11
-//     A = D0,         B = D0         (N =   BPg) -> P00          (6*BPg <= 480 TMEM cols)
+//     A = E2 (M=128), B = [E0|E1|E2] (N = 3*BPg) -> P20 P21 P22
+//     A = E1,         B = [E0|E1]    (N = 2*BPg) -> P10 P11
+//     A = E0,         B = E0         (N =   BPg) -> P00          (6*BPg <= 480 TMEM cols)
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "umma.cuh"
@@ -35,7 +41,14 @@ constexpr int kGtWorkers = 256;
 constexpr int kGtRawStages = 3;
 constexpr int kGtOpStages = 2;
 constexpr int kGtWmax = 32;
-constexpr int kGtFlushTiles = 1023;  // 1023 tiles * 128 px * 2^14 < 2^31
+constexpr int kGtFlushTiles = 255;  // 255 tiles * 128 px * 255^2 < 2^31
+constexpr int kGtOff = 1 << 22;     // E = D + kGtOff >= 0
+
+// idesc for kind::i8 with unsigned 8-bit operands, MN-major A and B, S32 accumulators
+__host__ __device__ constexpr uint32_t idesc_gt_u8(int M, int N) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | (1u << 15) | (1u << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
 struct GramTcParams {
   const uint16_t* raw;
@@ -100,7 +113,8 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
   for (int b = tid; b < BPG; b += blockDim.x) {
-    cs[b] = b < B ? (float)p.shift[b] : 0.0f;
+    // tq = (x - c_b) q_b as one FFMA: x q_b - c_b q_b (q_b a power of two: exact scaling)
+    cs[b] = b < B ? (float)p.shift[b] * p.qinv[b] : 0.0f;
     qs[b] = b < B ? p.qinv[b] : 0.0f;
   }
   tc_fence_before();
@@ -126,9 +140,9 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
     }
   } else if (warp == 9) {
     {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
-      constexpr uint32_t id2 = idesc_s8_s32(128, N2, 1, 1);
-      constexpr uint32_t id1 = idesc_s8_s32(128, N1, 1, 1);
-      constexpr uint32_t id0 = idesc_s8_s32(128, N0, 1, 1);
+      constexpr uint32_t id2 = idesc_gt_u8(128, N2);
+      constexpr uint32_t id1 = idesc_gt_u8(128, N1);
+      constexpr uint32_t id0 = idesc_gt_u8(128, N0);
       for (int t = 0; t < n; ++t) {
         const int os = t % kGtOpStages;
         const bool first = (t % kGtFlushTiles) == 0;
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
     constexpr int G0 = (NG + 1) / 2;  // groups [0, G0) for h = 0, [G0, NG) for h = 1
     const int g_lo = h ? G0 : 0, g_hi = h ? NG : G0;
     int cur_block = -1;
-    bool range_ok = true, finite_ok = true;
+    bool range_ok = true;
     int flushes = 0;
     auto flush = [&]() {
       mbar_wait(acc_full, flushes & 1);
@@ -181,10 +195,10 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int j = jc * 16 + q;
-            const double y = 268435456.0 * (double)(int32_t)p22[q] +
-                             16384.0 * (double)(int32_t)p11[q] + (double)(int32_t)p00[q];
-            const double x = 2097152.0 * (double)(int32_t)p21[q] +
-                             16384.0 * (double)(int32_t)p20[q] + 128.0 * (double)(int32_t)p10[q];
+            const double y = 4294967296.0 * (double)(int32_t)p22[q] +
+                             65536.0 * (double)(int32_t)p11[q] + (double)(int32_t)p00[q];
+            const double x = 16777216.0 * (double)(int32_t)p21[q] +
+                             65536.0 * (double)(int32_t)p20[q] + 256.0 * (double)(int32_t)p10[q];
             const size_t o = (size_t)j * BPG + lane_row;
             if (flushes == 0) {
               Y[o] = y;
@@ -207,8 +221,9 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         for (int e = tid; e < ti.w * B; e += kGtWorkers) {
           const int j = e / B, b = e - j * B;
           const int64_t g = (int64_t)(ti.s0 + j) * B + b;
-          dark_s[j * (B + 1) + b] = __ldg(p.dark + g);
-          coeff_s[j * (B + 1) + b] = __ldg(p.coeff + g);
+          const float c = __ldg(p.coeff + g);
+          dark_s[j * (B + 1) + b] = __fmul_rn(__ldg(p.dark + g), c);  // d c
+          coeff_s[j * (B + 1) + b] = c;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
         cur_block = ti.block;
@@ -219,66 +234,75 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       mbar_wait(&op_empty[os], ((t / kGtOpStages) & 1) ^ 1);
       const bool valid = r < ti.rows;
       int j = 0;
-      float g = 1.0f;
+      float gi = 1.0f;
       uint32_t pixkey = 0;
       if (valid) {
         const int li = r / ti.w;
         j = r - li * ti.w;
-        if (!kF32) g = __ldg(p.gain + ti.line0 + li);
+        if (!kF32) gi = 1.0f / __ldg(p.gain + ti.line0 + li);
         const uint64_t pix = (uint64_t)(ti.line0 + li) * (uint64_t)p.ts.S + (uint64_t)(ti.s0 + j);
         pixkey = (uint32_t)(pix * 0x9E3779B97F4A7C15ull >> 32) * 0x85EBCA6Bu;
       }
-      const uint16_t* rp = reinterpret_cast<const uint16_t*>(raw_ring + s * p.raw_stage_bytes) + r * B;
-      const float* fp = reinterpret_cast<const float*>(raw_ring + s * p.raw_stage_bytes) + r * B;
+      const uint8_t* rowb = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * ESZ;
       const float* dk = dark_s + j * (B + 1);
       const float* ck = coeff_s + j * (B + 1);
       uint8_t* ob = op_ring + os * OP_BYTES + (uint32_t)(r >> 3) * LBO + (uint32_t)(r & 7) * 16u;
-      for (int gi = g_lo; gi < g_hi; ++gi) {
+      // band k's value -> E = D + 2^22 (as a u32), D = floor(tq + u)
+      auto quant = [&](float x, int k) -> uint32_t {
+        const float tq = __fmaf_rn(x, qs[k], -cs[k]);
+        // dither: Weyl step over the band on a per-pixel hash, u - 1/2 in [-1/2, 1/2)
+        const uint32_t h = pixkey + (uint32_t)k * 0x9E3779B9u;
+        const float um = __uint_as_float(0x3F800000u | (h >> 9)) - 1.5f;
+        const float sv = __fadd_rn(tq, um);
+        range_ok &= fabsf(sv) < 4190000.0f;  // |D| < 2^22 (and false for NaN)
+        // RN(sv + 1.5 * 2^23) has ulp 1: its low mantissa bits are RN(sv) = floor(tq + u)
+        const float t = __fadd_rn(sv, 12582912.0f);
+        return (uint32_t)(__float_as_int(t) - 0x4B400000 + kGtOff);
+      };
+      for (int gq = g_lo; gq < g_hi; ++gq) {
         uint32_t w0[4], w1[4], w2[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          uint32_t a0 = 0, a1 = 0, a2 = 0;
+          uint32_t e[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int k = gi * 16 + q4 * 4 + q;
-            int D = 0;
-            if (valid && k < B) {
-              float x;
-              if constexpr (kF32) {
-                x = fp[k];
+          for (int q = 0; q < 4; q += 2) {
+            const int k = gq * 16 + q4 * 4 + q;
+            float xa = 0.0f, xb = 0.0f;
+            bool ina = valid && k < B, inb = valid && k + 1 < B;
+            if constexpr (kF32) {
+              const float* fp = reinterpret_cast<const float*>(rowb);
+              if (ina) xa = fp[k];
+              if (inb) xb = fp[k + 1];
+            } else {
+              float ra, rb;
+              if ((B & 1) == 0 && inb) {  // one u32 = bands k, k+1 (rows are 4-byte aligned)
+                const uint32_t v = *reinterpret_cast<const uint32_t*>(rowb + 2 * k);
+                ra = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)) - 8388608.0f;
+                rb = __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632)) - 8388608.0f;
               } else {
-                const float t = __fsub_rn((float)rp[k], dk[k]);
-                x = __fmul_rn(t < 0.0f ? 0.0f : t, ck[k]);
-                if (g != 1.0f) x = __fdiv_rn(x, g);
+                const uint16_t* rp = reinterpret_cast<const uint16_t*>(rowb);
+                ra = ina ? (float)rp[k] : 0.0f;
+                rb = inb ? (float)rp[k + 1] : 0.0f;
               }
-              finite_ok &= isfinite(x);
-              const float tq = __fmul_rn(__fsub_rn(x, cs[k]), qs[k]);
-              range_ok &= fabsf(tq) < 2064383.0f;  // keeps D2 within int8
-              // deterministic dithered rounding: E[D] = tq for any input lattice
-              uint32_t hq = pixkey ^ ((uint32_t)k * 0x9E3779B9u);
-              hq ^= hq >> 15;
-              hq *= 0x2C1B3C6Du;
-              hq ^= hq >> 12;
-              // round up with probability frac(tq): u >= 1 - frac is exact in f32
-              const float fl = floorf(tq);
-              const float u = (float)(hq >> 8) * 0x1p-24f;
-              D = (int)fl + (u >= 1.0f - (tq - fl) ? 1 : 0);
-            } else if (valid && k == B) {
-              D = 1;  // constant band: carries n and sum(D)
+              if (ina) xa = fmaxf(__fmaf_rn(ra, ck[k], -dk[k]), 0.0f) * gi;
+              if (inb) xb = fmaxf(__fmaf_rn(rb, ck[k + 1], -dk[k + 1]), 0.0f) * gi;
             }
-            const int d0 = ((D + 64) & 127) - 64;
-            const int t1 = (D - d0) >> 7;
-            const int d1 = ((t1 + 64) & 127) - 64;
-            const int d2 = (t1 - d1) >> 7;
-            a0 |= (uint32_t)(d0 & 255) << (8 * q);
-            a1 |= (uint32_t)(d1 & 255) << (8 * q);
-            a2 |= (uint32_t)(d2 & 255) << (8 * q);
+            // padding bands (k >= B, not the constant band) quantise to E = 2^22 with
+            // q_b = c_b = 0: they only add the known offset, removed with the others
+            e[q] = ina ? quant(xa, k) : (valid && k == B ? 1u : (uint32_t)kGtOff);
+            e[q + 1] = inb ? quant(xb, k + 1) : (valid && k + 1 == B ? 1u : (uint32_t)kGtOff);
+            if (!valid) e[q] = e[q + 1] = 0u;
           }
-          w0[q4] = a0, w1[q4] = a1, w2[q4] = a2;
+          // bytes 0, 1, 2 of the four E words -> the three digit planes
+          const uint32_t p01 = __byte_perm(e[0], e[1], 0x5140);
+          const uint32_t p23 = __byte_perm(e[2], e[3], 0x5140);
+          w0[q4] = __byte_perm(p01, p23, 0x5410);
+          w1[q4] = __byte_perm(p01, p23, 0x7632);
+          w2[q4] = __byte_perm(__byte_perm(e[0], e[1], 0x0062), __byte_perm(e[2], e[3], 0x0062), 0x5410);
         }
-        *reinterpret_cast<uint4*>(ob + (0 * NG + gi) * 128) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-        *reinterpret_cast<uint4*>(ob + (1 * NG + gi) * 128) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-        *reinterpret_cast<uint4*>(ob + (2 * NG + gi) * 128) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+        *reinterpret_cast<uint4*>(ob + (0 * NG + gq) * 128) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(ob + (1 * NG + gq) * 128) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4*>(ob + (2 * NG + gq) * 128) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
       }
       fence_async_smem();
       mbar_arrive(&op_full[os]);
@@ -286,8 +310,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       if ((t % kGtFlushTiles) == kGtFlushTiles - 1 && t != n - 1) flush();
     }
     if (n > 0) flush();
-    if (!range_ok) atomicOr(p.flags, 2);
-    if (!finite_ok) atomicOr(p.flags, 1);
+    if (!range_ok) atomicOr(p.flags, 2);  // incl. non-finite values: the f64 redo reports them
   }
   (void)nflush;
   tc_fence_before();
@@ -304,21 +327,28 @@ __global__ void gram_tc_reduce_kernel(const double* __restrict__ part, int npart
   if (e >= BPG * BPG) return;
   const int i = e / BPG, j = e - i * BPG;
   if (i > B || j > B || j > i) return;  // lower triangle incl. the constant band B
-  double v = 0.0;
-  for (int c = 0; c < nparts; ++c) {
-    const double* Y = part + (size_t)c * 2 * BPG * BPG;
-    const double* X = Y + BPG * BPG;
-    v += Y[(size_t)j * BPG + i] + X[(size_t)j * BPG + i] + X[(size_t)i * BPG + j];
-  }
+  // G_E(a, b), a >= b: the digit Gram of E = D + 2^22 (constant band B: E = 1)
+  auto G = [&](int a, int b) {
+    double v = 0.0;
+    for (int c = 0; c < nparts; ++c) {
+      const double* Y = part + (size_t)c * 2 * BPG * BPG;
+      const double* X = Y + BPG * BPG;
+      v += Y[(size_t)b * BPG + a] + X[(size_t)b * BPG + a] + X[(size_t)a * BPG + b];
+    }
+    return v;
+  };
+  constexpr double off = (double)kGtOff;
+  const double n = G(B, B);  // pixel count (exact)
   double* s_out = moments + 1;
   double* q_out = moments + 1 + B;
   const double qi = i < B ? 1.0 / (double)qinv[i] : 1.0;
   const double qj = j < B ? 1.0 / (double)qinv[j] : 1.0;
   if (i == B && j == B) {
-    moments[0] = v;                       // pixel count (exact)
+    moments[0] = n;
   } else if (i == B) {
-    s_out[j] = v * qj;                    // sum over pixels of (x_j - c_j), quantised
+    s_out[j] = (G(B, j) - n * off) * qj;  // sum over pixels of (x_j - c_j), quantised
   } else {
+    const double v = G(i, j) - off * (G(B, i) + G(B, j)) + n * off * off;
     q_out[(size_t)i * B + j] = v * qi * qj;
     q_out[(size_t)j * B + i] = v * qi * qj;
   }
@@ -372,7 +402,7 @@ __global__ void quant_shift_kernel(const void* pixels, int64_t npix, int32_t sam
     const float bound = fmaxf(4.2f * amax, 1e-30f);
     int e = 0;
     frexpf(bound, &e);                 // bound < 2^e
-    int ex = 21 - e;                   // |x - c| <= 4 amax  =>  |D| < 2^21 * 4/4.2
+    int ex = 22 - e;                   // |x - c| <= 4 amax  =>  |D| < 2^22 * 4/4.2
     ex = ex > 120 ? 120 : (ex < -120 ? -120 : ex);
     shift[b] = (double)c;
     qinv[b] = ldexpf(1.0f, ex);
