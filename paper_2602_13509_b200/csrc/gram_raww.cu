@@ -13,7 +13,7 @@
 //      - m d^T + L d d^T) and accumulate them into the CTA's partial in global
 //      memory (each band pair belongs to exactly one block, hence one pass);
 //   3. the partials are reduced and centred by gram_raw.cu's deterministic kernels.
-// Warps of the Gram kernel: 4 epilogue (TMEM lane quarters), TMA, MMA.
+// Warps of the Gram kernel: 4 x kEpiGroups epilogue (TMEM lane quarters), TMA, MMA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,7 +32,16 @@ namespace raww {
 // lines per tile: 64, so a stage (every window atom: 5 x 8 KB at B = 270) leaves room for
 // five stages in flight (2.24 ms against 2.76 ms for 2 stages of 128 lines, B = 270)
 constexpr int kLb = RAWW_LB;
-constexpr int kThreads = 192;
+// epilogue: kEpiGroups groups of 4 warps (one per TMEM lane quarter); group g takes the
+// pass's blocks g, g + kEpiGroups, ...  The pass's blocks fill TMEM, so the epilogue is
+// not overlapped with the tensor core: four groups drain a unit's four blocks in parallel
+#ifndef RAWW_EPI_GROUPS
+#define RAWW_EPI_GROUPS 4
+#endif
+constexpr int kEpiGroups = RAWW_EPI_GROUPS;
+constexpr int kEpiThreads = 128 * kEpiGroups;
+constexpr int kTmaWarp = kEpiThreads / 32, kMmaWarp = kTmaWarp + 1;
+constexpr int kThreads = kEpiThreads + 64;
 constexpr int kMaxStages = 6;
 constexpr int kMaxAtoms = 5;        // window <= 640 bytes
 constexpr uint32_t kAtom = kLb * 128u;
@@ -166,16 +175,16 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   if (tid == 0) {
     // full: this CTA's producer arms it; empty: one multicast commit per cluster CTA
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], p.npass);
-    mbar_init(acc_full, 1), mbar_init(acc_empty, 128);
+    mbar_init(acc_full, 1), mbar_init(acc_empty, kEpiThreads);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   cluster_sync_all();  // every CTA's barriers exist before any multicast lands on them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       int t = 0;
       for (int64_t u = u0; u < p.units; u += ustep) {
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t id = idesc_u8(128, 128);
       // every operand descriptor is the stage-0 / atom-0 / k-step-0 one plus an offset in
@@ -241,8 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         __syncwarp();
       }
     }
-  } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
-    const int te = tid;  // byte row within the row atom = TMEM lane
+  } else {  // ---------------------------------------------------- epilogue (warps 0..kTmaWarp-1)
+    const int te = tid & 127;  // byte row within the row atom = TMEM lane
+    const int grp = tid >> 7;
     double* part = p.part + (size_t)blockIdx.x * ((size_t)B * B + B + 1);
     double* bandC = reinterpret_cast<double*>(bars + 2 * kStages + 2 + 2);  // [B] per unit
     double* bandD = bandC + B;
@@ -259,15 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
       const float* drow = p.dark + (int64_t)s * B;
       const float* crow = p.coeff + (int64_t)s * B;
       // this unit's per-band terms, once, for the four epilogue warps
-      for (int b = te; b < B; b += 128) {
+      for (int b = tid; b < B; b += kEpiThreads) {
         bandC[b] = (double)crow[b] * p.ginv;
         bandD[b] = (double)drow[b];
         bandS[b] = (double)us[(off >> 1) + b];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
       mbar_wait(acc_full, unit & 1);
       tc_fence_after();
-      for (int bk = 0; bk < nblk; ++bk) {
+      for (int bk = grp; bk < nblk; bk += kEpiGroups) {
         const int mr = p.blk_r[ps][bk], mc = p.blk_c[ps][bk];
         const int m = 128 * mr + te;
         const int rel = m - off;
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         const int b = rel >> 1;
         double Cb = 0.0, db = 0.0, Sb = 0.0;
         if (in_band) Cb = bandC[b], db = bandD[b], Sb = bandS[b];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 128 * bk;
+        const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 128 * bk;
         for (int cc = 0; cc < 8; cc += 2) {  // two chunks per TMEM wait
           uint32_t v2[32];
           tmem_ld16(taddr + cc * 16, v2);
@@ -317,21 +327,21 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
           }
         }
       }
-      if (first_pass) {  // band sums: sum x = C_b (m_b - L d_b)
+      if (first_pass && grp == 0) {  // band sums: sum x = C_b (m_b - L d_b)
         for (int b = te; b < B; b += 128)
           part[(size_t)B * B + b] += bandC[b] * (bandS[b] - Lu * bandD[b]);
         nsum += Lu;
       }
       tc_fence_before();
       mbar_arrive(acc_empty);
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // band terms reused by the next unit
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // band terms reused next unit
     }
     if (first_pass && tid == 0) part[(size_t)B * B + B] = nsum;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
   cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
 }
 
