@@ -284,8 +284,16 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
                 ra = ina ? (float)rp[k] : 0.0f;
                 rb = inb ? (float)rp[k + 1] : 0.0f;
               }
-              if (ina) xa = fmaxf(__fmaf_rn(ra, ck[k], -dk[k]), 0.0f) * gi;
-              if (inb) xb = fmaxf(__fmaf_rn(rb, ck[k + 1], -dk[k + 1]), 0.0f) * gi;
+              // max(., 0) that keeps NaN (np.maximum, calibrate.py:99): a NaN dark or coeff
+              // must reach the range check below (flags |= 2 -> the f64 redo reports it)
+              if (ina) {
+                const float ta = __fmaf_rn(ra, ck[k], -dk[k]);
+                xa = (ta < 0.0f ? 0.0f : ta) * gi;
+              }
+              if (inb) {
+                const float tb = __fmaf_rn(rb, ck[k + 1], -dk[k + 1]);
+                xb = (tb < 0.0f ? 0.0f : tb) * gi;
+              }
             }
             // padding bands (k >= B, not the constant band) quantise to E = 2^22 with
             // q_b = c_b = 0: they only add the known offset, removed with the others
