@@ -650,11 +650,15 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
 // true radiance (x'_b = 0 where r_b < d_b), dx = x' - x is -x on the clamped bands and
 //     sum x' x'^T = sum x x^T + sum (x dx^T + dx x^T + dx dx^T),   sum x' = sum x + sum dx.
 // Two kernels, both no-ops (one flags read per CTA) when nothing clamped:
-//  clamp_mark_kernel  streams the flagged units' lines (bit u of unit_clamp, set by the
-//                     Gram epilogue from its per-band minima; sample-major units of one
-//                     sample are skipped 16 B at a time when unflagged) with coalesced
-//                     16-byte loads and sets bit (line * S + s) of a pixel bitmap for
-//                     every pixel with a value below dark (atomicOr: order-free);
+//  clamp_mark_lines_kernel  (more than a quarter of the units flagged) streams the flagged
+//                     units' lines with coalesced 16-byte loads;
+//  clamp_mark_kernel  otherwise, work items (flagged unit, line chunk): the unit's window of every
+//                     line in the chunk (coalesced 2-byte loads, 8 in flight per thread)
+//                     against the sample's dark row; sets bit (line * S + s) of a pixel
+//                     bitmap for every pixel with a value below dark (atomicOr: order-free).
+//                     Unflagged units cost one bit test (a dead detector element flags the
+//                     units of one sample: ~0.69 ms for the old line-major pass over the
+//                     whole cube, which spent it on per-vector unit lookups);
 //  clamp_fix_kernel   CTA c walks a fixed contiguous range of the bitmap in pixel order,
 //                     stages the clamped pixels 32 at a time and adds, pixel by pixel,
 //                     only the row / column of each clamped band into a shared-memory
@@ -664,10 +668,91 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
 constexpr int kFixThreads = 256;
 constexpr int kFixBatch = 32;  // clamped pixels staged per round
 
+// unit u's sample and line range: gram_raw_kernel's unit_geom (regular units, then the tail
+// pieces of the leftover units)
+__device__ __forceinline__ void gr_unit_geom(const GramRawParams& p, int64_t u, int& s,
+                                             int64_t& l0, int64_t& nl) {
+  const int64_t ur = u < p.units_main ? u : p.units_main + (u - p.units_main) / p.tail_k;
+  s = (int)(ur % p.S);
+  l0 = (ur / p.S) * p.split_lines;
+  nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
+  if (u >= p.units_main) {
+    const int64_t piece = (u - p.units_main) % p.tail_k;
+    const int64_t a = piece * p.tail_lines;
+    const int64_t b = a + p.tail_lines < nl ? a + p.tail_lines : nl;
+    l0 += a;
+    nl = b > a ? b - a : 0;
+  }
+}
+
+constexpr int kMarkChunks = 16;  // line chunks per unit
+
+// more than a quarter of the units flagged (random sparse sub-dark counts flag every unit):
+// one coalesced line-major pass over the cube (clamp_mark_lines_kernel) beats per-unit
+// column reads; otherwise (a dead detector element flags the units of one sample)
+// clamp_mark_kernel reads only the flagged units.  Both kernels count the same bits.
+__device__ __forceinline__ bool clamp_many(const GramRawParams& p) {
+  if (p.units >= kGrMaxUnitBits) return true;
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int64_t i = threadIdx.x; i < (p.units + 31) / 32; i += blockDim.x)
+    c += __popc(p.unit_clamp[i]);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&cnt, c);
+  __syncthreads();
+  return 4 * (int64_t)cnt > p.units;
+}
+
 __global__ void __launch_bounds__(256) clamp_mark_kernel(const uint16_t* __restrict__ raw,
                                                          GramRawParams p,
                                                          uint32_t* __restrict__ pixbits) {
+  if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;  // nothing clamped
+  if (clamp_many(p)) return;
+  const int B = p.B;
+  const int lpp = blockDim.x / B;  // lines per pass (B <= 128 on this path)
+  const int b = threadIdx.x % B, lo = threadIdx.x / B;
+  const int64_t pitch = (int64_t)p.S * B;
+  constexpr int kUnroll = 8;  // loads in flight per thread
+  // persistent: work items (unit, line chunk), unflagged units skipped by one bit test
+  for (int64_t it = blockIdx.x; it < p.units * kMarkChunks; it += gridDim.x) {
+    const int64_t u = it / kMarkChunks;
+    const int ch = (int)(it - u * kMarkChunks);
+    if (!((p.unit_clamp[u >> 5] >> (u & 31)) & 1u)) continue;
+    int s;
+    int64_t l0, nl;
+    gr_unit_geom(p, u, s, l0, nl);
+    const int64_t per = (nl + kMarkChunks - 1) / kMarkChunks;
+    const int64_t la = l0 + ch * per;
+    const int64_t lb = min(l0 + nl, la + per);
+    if (lo >= lpp || la >= lb) continue;
+    const float dk = __ldg(p.dark + (int64_t)s * B + b);
+    const uint16_t* base = raw + (int64_t)s * B + b;
+    for (int64_t line = la + lo; line < lb; line += (int64_t)kUnroll * lpp) {
+      uint16_t v[kUnroll];
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        const int64_t l = line + (int64_t)k * lpp;
+        v[k] = l < lb ? __ldcs(base + l * pitch) : (uint16_t)0xFFFF;
+      }
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        const int64_t l = line + (int64_t)k * lpp;
+        if (l < lb && (float)v[k] < dk) {  // rare
+          const int64_t pix = l * p.S + s;
+          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) clamp_mark_lines_kernel(const uint16_t* __restrict__ raw,
+                                                         GramRawParams p,
+                                                         uint32_t* __restrict__ pixbits) {
   if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;
+  if (!clamp_many(p)) return;  // few flagged units: clamp_mark_kernel
   const int B = p.B;
   const int vpl = p.S * B / 8;  // 16-B vectors per line (S B 2 % 16 == 0)
   // line-major: CTA rows walk lines, threads the line's vectors; element e of a line is
@@ -936,10 +1021,12 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   const int work = p.B * p.B + p.B + 1;
   if (p.pixbits != nullptr) {
     cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
+    clamp_mark_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, p.pixbits);
+    SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
     const int vpl = p.S * p.B / 8;
     const int gx = (vpl + 255) / 256;
     const int gy = (int)std::min<int64_t>(p.L, std::max<int64_t>(1, (int64_t)kSMs * 8 / gx));
-    clamp_mark_kernel<<<dim3(gx, gy), 256, 0, st>>>(raw, p, p.pixbits);
+    clamp_mark_lines_kernel<<<dim3(gx, gy), 256, 0, st>>>(raw, p, p.pixbits);
     SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
   }
   const size_t fsm = clamp_fix_smem(p.B);
