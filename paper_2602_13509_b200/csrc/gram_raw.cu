@@ -763,7 +763,6 @@ __global__ void __launch_bounds__(256) clamp_mark_lines_kernel(const uint16_t* _
   const bool dark16 = (reinterpret_cast<uintptr_t>(p.dark) & 15) == 0;
   for (int vx = blockIdx.x * blockDim.x + threadIdx.x; vx < vpl; vx += gridDim.x * blockDim.x) {
     const int e0 = vx * 8;
-    const int s0 = e0 / B, s1 = (e0 + 7) / B;
     float dv[8];
     if (dark16) {
       const float4 d0 = __ldg(reinterpret_cast<const float4*>(p.dark + e0));
@@ -774,23 +773,15 @@ __global__ void __launch_bounds__(256) clamp_mark_lines_kernel(const uint16_t* _
 #pragma unroll
       for (int q = 0; q < 8; ++q) dv[q] = __ldg(p.dark + e0 + q);
     }
-    auto flagged = [&](int64_t sp, int64_t lin, int s) {
-      int64_t u = sp * p.S + s;  // regular units: u = split * S + s
-      if (u >= p.units_main)     // a leftover unit cut into tail pieces
-        u = p.units_main + (u - p.units_main) * p.tail_k + lin / p.tail_lines;
-      return u >= kGrMaxUnitBits || ((p.unit_clamp[u >> 5] >> (u & 31)) & 1u);
-    };
     for (int64_t l0 = blockIdx.y; l0 < p.L; l0 += (int64_t)kLines * gridDim.y) {
       uint4 w[kLines];
       bool on[kLines];
 #pragma unroll
       for (int k = 0; k < kLines; ++k) {
         const int64_t line = l0 + (int64_t)k * gridDim.y;
-        on[k] = false;
-        if (line < p.L) {
-          const int64_t sp = line / p.split_lines, lin = line - sp * p.split_lines;
-          on[k] = flagged(sp, lin, s0) || (s1 != s0 && flagged(sp, lin, s1));
-        }
+        // most units are flagged here: stream every line (an unflagged unit holds no value
+        // below dark, so comparing it marks nothing) instead of a unit lookup per vector
+        on[k] = line < p.L;
         if (on[k])
           w[k] = __ldcs(reinterpret_cast<const uint4*>(raw + line * p.S * (int64_t)B) + vx);
       }
