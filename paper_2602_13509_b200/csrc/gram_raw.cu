@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   } else {  // ------------------------------------------------------------ epilogue (warps 4-7)
     const int te = tid - kGrWorkers;  // TMEM lane = byte row of the Gram
     const int we = warp & 3;
+    const uint32_t tq = warp_uniform(tmem + ((uint32_t)(32 * we) << 16));  // lane quarter
     int unit = 0;
     for (int64_t u = u0; u < u1; u += ustep, ++unit) {
       int s;
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         for (int part = 0; part < 2; ++part) {
           if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
           uint32_t sv[16];
-          tmem_ld16(tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? 224u : 160u), sv);
+          tmem_ld16(tq + buf * BUFC + (part ? 224u : 160u), sv);
           tmem_ld_wait();
           const uint32_t partner = __shfl_xor_sync(0xffffffffu, sv[0], 1);
           const int rel = 128 * part + te - off;
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         double Cb = 0.0, db = 0.0, Sb = 0.0;
         if (in_band) Cb = bandC[b], db = bandD[b], Sb = bandS[b];
         // part 0: byte columns 0..NW-1 of the full-width block; part 1: columns 128..NW-1
-        const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + buf * BUFC + (part ? P1OFF : 0);
+        const uint32_t taddr = tq + buf * BUFC + (part ? P1OFF : 0);
         const int cc0 = part ? 8 : 0;
         // chunks this warp's rows need (warp-uniform): the lower triangle reaches byte
         // column 128 part + 32 we + 31; part-0 rows also own every column past byte 128

@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
   } else {  // ---------------------------------------------------- epilogue (warps 0..kTmaWarp-1)
     const int te = tid & 127;  // byte row within the row atom = TMEM lane
     const int grp = tid >> 7;
+    const uint32_t tq = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16));
     double* part = p.part + (size_t)blockIdx.x * ((size_t)B * B + B + 1);
     double* bandC = reinterpret_cast<double*>(bars + 2 * kStages + 2 + 2);  // [B] per unit
     double* bandD = bandC + B;
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) raww_gram_kernel(
         const int b = rel >> 1;
         double Cb = 0.0, db = 0.0, Sb = 0.0;
         if (in_band) Cb = bandC[b], db = bandD[b], Sb = bandS[b];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 128 * bk;
+        const uint32_t taddr = tq + 128 * bk;
         for (int cc = 0; cc < 8; cc += 2) {  // two chunks per TMEM wait
           uint32_t v2[32];
           tmem_ld16(taddr + cc * 16, v2);

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       tc_fence_after();
       // warp w reads TMEM lanes 32*(w%4).., columns split by h
       const int lane_row = 32 * (warp & 3) + (tid & 31);  // band row i
-      const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+      const uint32_t tl = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16));
       double* Y = p.part + (size_t)blockIdx.x * 2 * BPG * BPG;
       double* X = Y + BPG * BPG;
       for (int jc = h; jc < NG; jc += 2) {

@@ -19,6 +19,8 @@
 // Each worker keeps its row's per-sample calibration constants in registers.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 #include "tma.cuh"
@@ -251,9 +253,10 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
   if (n > 0) load_row_tables(ti);  // the CTA never leaves this block
   // A stage `as` lives in TMEM columns [kScoreABase + as*KP, + KP): hi in the first
   // KP/2 (two f16 per column), lo in the next KP/2; this thread's lane = its row
-  const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase + 4 * c_lo;
+  const uint32_t tl =
+      warp_uniform(tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase + 4 * c_lo);
   if (h == 0) {  // zero the all-padding chunks of both A stages (never rewritten)
-    const uint32_t tz = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase;
+    const uint32_t tz = warp_uniform(tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kScoreABase);
     for (int st = 0; st < kScoreAStages; ++st)
       for (int c = nchr; c < NCH; ++c) {
         tmem_st4(tz + st * KP + 4 * c, 0u, 0u, 0u, 0u);
@@ -265,9 +268,14 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
   const uint32_t ring32 = smem_u32(raw_ring), raw_full32 = smem_u32(raw_full);
   const uint32_t raw_empty32 = smem_u32(raw_empty), a_full32 = smem_u32(a_full);
   const uint32_t a_empty32 = smem_u32(a_empty);
-  int s = 0, as = 0;
+  int s = 0;
   uint32_t ph = 0, aph = 0;
-  for (int t = 0; t < n; ++t) {
+  // the tile loop is unrolled over the two A stages: with the stage a compile-time constant
+  // every tcgen05.st address is the loop-invariant uniform base plus an immediate (one R2UR
+  // per warp for the whole loop instead of ~5 R2UR + NOPs per tile)
+  static_assert(kScoreAStages == 2, "the transform loop is unrolled over two A stages");
+  auto tile = [&](int t, auto as_c) {
+    constexpr int AS = decltype(as_c)::value;
     if (t > 0) tile_next_in_block(p.ts, ti, gstep);
     // rows past the tile's end transform stale ring bytes (finite u16 counts): the
     // TMEM stores are warp-collective, and the epilogue drops those rows
@@ -277,10 +285,10 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
       g = __ldg(p.gain + (line < p.ts.L ? line : p.ts.L - 1));
     }
     SC_PW(0, mbar_wait(raw_full32 + 8 * s, ph));
-    SC_PW(1, mbar_wait(a_empty32 + 8 * as, aph ^ 1));
+    SC_PW(1, mbar_wait(a_empty32 + 8 * AS, aph ^ 1));
     tc_fence_after();
     const uint32_t roff = s * p.raw_stage_bytes + r * B * 2 + 16 * c_lo;
-    const uint32_t thi = tl + as * KP;
+    const uint32_t thi = tl + AS * KP;
 #ifndef SCX_NO_XFORM  // ablation switches (tools/build_sc_var.sh), off in the product
     if constexpr (BATCHED) {
       SC_PW(2, transform_row_batched<CHT>(ring32 + roff, tco, tnof, thi, thi + KP / 2));
@@ -293,11 +301,15 @@ __device__ __forceinline__ void transform_loop(const ScoreTcParams& p, int n, in
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {  // one arrival per warp
-      mbar_arrive(a_full32 + 8 * as);
+      mbar_arrive(a_full32 + 8 * AS);
       mbar_arrive(raw_empty32 + 8 * s);
     }
     if (++s == NR) s = 0, ph ^= 1;
-    if (++as == kScoreAStages) as = 0, aph ^= 1;
+    if (AS == kScoreAStages - 1) aph ^= 1;
+  };
+  for (int t = 0; t < n; t += 2) {
+    tile(t, std::integral_constant<int, 0>{});
+    if (t + 1 < n) tile(t + 1, std::integral_constant<int, 1>{});
   }
 }
 
@@ -461,30 +473,33 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
     const int lane = tid & 31;
     mbar_wait(w_bar, 0);
     const float ws2 = colscale[0] * colscale[0];  // one power-of-two scale for all of W
-    const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tbase = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16));
     uint32_t local_max = 0;
     TileInfo ti = tile_at(p.ts, blk, g0);
     // the CTA never leaves its block, so a row's (line, sample) offsets are fixed
     const int li = n > 0 ? r / ti.w : 0;
     const int sc = r - li * ti.w;
     const uint32_t acc_full32 = smem_u32(acc_full), acc_empty32 = smem_u32(acc_empty);
-    int acs = 0;
     uint32_t cph = 0;
-    for (int t = 0; t < n; ++t) {
+    // unrolled over the two accumulators (constant TMEM addresses, as in the transform)
+    static_assert(kScoreAcc == 2, "the epilogue loop is unrolled over two accumulators");
+    auto tile = [&](int t, auto acs_c) {
+      constexpr int acs = decltype(acs_c)::value;
       if (t > 0) tile_next_in_block(p.ts, ti, gstep);
       SC_PW(6, mbar_wait(acc_full32 + 8 * acs, cph));
       tc_fence_after();
       float2 acc = make_float2(0.0f, 0.0f);
+      const uint32_t tacc = tbase + acs * AW;
 #ifdef SCX_NO_EPI
       if (false)
 #endif
 #pragma unroll
       for (int c = 0; c < NCH; c += 2) {
         uint32_t v[16];
-        tmem_ld16(tbase + acs * AW + c * 8, v);
+        tmem_ld16(tacc + c * 8, v);
         if constexpr (kScoreNcat) {
           uint32_t w[16];
-          tmem_ld16(tbase + acs * AW + NP + c * 8, w);
+          tmem_ld16(tacc + NP + c * 8, w);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 16; q += 2) {
@@ -517,7 +532,11 @@ __global__ void __maxnreg__(sc_maxreg(KP)) score_tc_kernel(
         const uint32_t peers = __match_any_sync(0xffffffffu, bin);
         if (valid && lane == __ffs(peers) - 1) atomicAdd(&shist[bin], __popc(peers));
       }
-      if (++acs == kScoreAcc) acs = 0, cph ^= 1;
+      if (acs == kScoreAcc - 1) cph ^= 1;
+    };
+    for (int t = 0; t < n; t += 2) {
+      tile(t, std::integral_constant<int, 0>{});
+      if (t + 1 < n) tile(t + 1, std::integral_constant<int, 1>{});
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)

@@ -326,7 +326,7 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
     }
   } else if (warp >= EPI0) {  // --------------------------------------- epilogue
     const int r = tid & 127;
-    const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tb = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16));
     uint32_t local_max = 0;
     int acs = 0, ui = 0;
     uint32_t cph = 0;
@@ -407,7 +407,7 @@ __global__ void __maxnreg__(maxreg(KP)) score_tcs_kernel(const __grid_constant__
     const int cpg = (nchr + NG - 1) / NG;
     const int c_lo = cpg * g;
     const int cnt = min(cpg, nchr - c_lo);
-    const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + ABASE;
+    const uint32_t tl = warp_uniform(tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + ABASE);
     if (g == 0) {  // all-padding chunks of both A stages: zero once, never rewritten
       for (int st = 0; st < kAStages; ++st)
         for (int c = nchr; c < NCH; ++c) {

@@ -261,7 +261,7 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
     }
   } else if (warp >= EPI0) {  // --------------------------------------- epilogue
     const int r = tid & 127;
-    const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + kAccBase;
+    const uint32_t tbase = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + kAccBase);
     uint32_t local_max = 0;
     int ui = 0, acs = 0;
     uint32_t cph = 0;
@@ -331,7 +331,7 @@ __global__ void __maxnreg__(kMaxReg) score_tcw_kernel(const __grid_constant__ CU
     const int cpg = (nchr + kGroups - 1) / kGroups;
     const int c_lo = cpg * g;
     const int cnt = min(cpg, nchr - c_lo);
-    const uint32_t tl = tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kABase;
+    const uint32_t tl = warp_uniform(tmem + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + kABase);
     if (g == 0) {  // all-padding chunks of A: zero once
       for (int c = nchr; c < NCH; ++c) {
         tmem_st4(tl + 4 * c, 0u, 0u, 0u, 0u);

@@ -259,6 +259,13 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// a warp-uniform value (e.g. a TMEM lane-quarter base derived from threadIdx) passed through
+// a shuffle: ptxas then keeps it, and every tcgen05.ld/st address built from it, in uniform
+// registers (one R2UR per warp instead of one R2UR + NOPs per TMEM access: ~110 of the
+// ~3150 instructions a score_tc tile took)
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) {
+  return __shfl_sync(0xffffffffu, v, 0);
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
