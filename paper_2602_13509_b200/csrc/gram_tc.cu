@@ -36,8 +36,18 @@
 namespace skyrx {
 using namespace umma;
 
-constexpr int kGtThreads = 320;  // 8 worker warps (2 per pixel row) + TMA + MMA
-constexpr int kGtWorkers = 256;
+// worker warps: kGtH threads per pixel row (each a contiguous run of 16-band groups), then the
+// TMA and MMA warps.  What bounds the kernel is shared memory, not issue: per 128-pixel tile
+// the MMAs read ~108 KB of digit planes, the workers' per-pixel calibration rows ~80 KB, plus
+// the plane writes and the raw ring (4 workers per row, 4 operand stages, or 40 % fewer
+// instructions, measured: none faster than 3.67 ms per c4 strip, profiles/r02_ablation.md)
+#ifndef GTC_H
+#define GTC_H 2
+#endif
+constexpr int kGtH = GTC_H;
+constexpr int kGtWorkers = 128 * kGtH;
+constexpr int kGtThreads = kGtWorkers + 64;
+constexpr int kGtTmaWarp = kGtWorkers / 32, kGtMmaWarp = kGtTmaWarp + 1;
 constexpr int kGtRawStages = 3;
 constexpr int kGtOpStages = 2;
 constexpr int kGtWmax = 32;
@@ -80,9 +90,9 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
   const int B = p.ts.B;
   uint8_t* raw_ring = sm;
   uint8_t* op_ring = raw_ring + kGtRawStages * p.raw_stage_bytes;
-  float* dark_s = reinterpret_cast<float*>(op_ring + kGtOpStages * OP_BYTES);
-  float* coeff_s = dark_s + kGtWmax * (B + 1);
-  float* cs = coeff_s + kGtWmax * (B + 1);
+  // per (sample of the block, band pair): {c q, -(d c) q} x 2, the quantiser scale folded in
+  float4* tab4 = reinterpret_cast<float4*>(op_ring + kGtOpStages * OP_BYTES);  // [Wmax][BPG/2]
+  float* cs = reinterpret_cast<float*>(tab4 + kGtWmax * (BPG / 2));  // [BPG] -c_b q_b
   float* qs = cs + BPG;
   uint64_t* bars = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(qs + BPG) + 7) & ~uintptr_t(7));
@@ -111,10 +121,10 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
     mbar_init(acc_empty, kGtWorkers);
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == kGtMmaWarp) tmem_alloc(tmem_slot, 512);
   for (int b = tid; b < BPG; b += blockDim.x) {
     // tq = (x - c_b) q_b as one FFMA: x q_b - c_b q_b (q_b a power of two: exact scaling)
-    cs[b] = b < B ? (float)p.shift[b] * p.qinv[b] : 0.0f;
+    cs[b] = b < B ? -((float)p.shift[b] * p.qinv[b]) : 0.0f;
     qs[b] = b < B ? p.qinv[b] : 0.0f;
   }
   tc_fence_before();
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == kGtTmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       for (int t = 0; t < n; ++t) {
         const int s = t % kGtRawStages;
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kGtMmaWarp) {
     {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t id2 = idesc_gt_u8(128, N2);
       constexpr uint32_t id1 = idesc_gt_u8(128, N1);
@@ -169,8 +179,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
   } else {  // ------------------------------------------------------------ workers
     const int r = tid & 127;          // pixel row
     const int h = tid >> 7;           // which band groups this thread packs
-    constexpr int G0 = (NG + 1) / 2;  // groups [0, G0) for h = 0, [G0, NG) for h = 1
-    const int g_lo = h ? G0 : 0, g_hi = h ? NG : G0;
+    const int g_lo = h * NG / kGtH, g_hi = (h + 1) * NG / kGtH;  // this thread's groups
     int cur_block = -1;
     bool range_ok = true;
     int flushes = 0;
@@ -182,30 +191,34 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       const uint32_t tl = warp_uniform(tmem + ((uint32_t)(32 * (warp & 3)) << 16));
       double* Y = p.part + (size_t)blockIdx.x * 2 * BPG * BPG;
       double* X = Y + BPG * BPG;
-      for (int jc = h; jc < NG; jc += 2) {
-        uint32_t p20[16], p21[16], p22[16], p10[16], p11[16], p00[16];
-        tmem_ld16(tl + 0 * BPG + jc * 16, p20);
-        tmem_ld16(tl + 1 * BPG + jc * 16, p21);
-        tmem_ld16(tl + 2 * BPG + jc * 16, p22);
-        tmem_ld16(tl + N2 + 0 * BPG + jc * 16, p10);
-        tmem_ld16(tl + N2 + 1 * BPG + jc * 16, p11);
-        tmem_ld16(tl + N2 + N1 + jc * 16, p00);
-        tmem_ld_wait();
-        if (lane_row < BPG) {
+      for (int jc = h; jc < NG; jc += kGtH) {
+#pragma unroll 1
+        for (int hc = 0; hc < 2; ++hc) {  // 8 columns at a time (registers)
+          const uint32_t col = jc * 16 + hc * 8;
+          uint32_t p20[8], p21[8], p22[8], p10[8], p11[8], p00[8];
+          tmem_ld8(tl + 0 * BPG + col, p20);
+          tmem_ld8(tl + 1 * BPG + col, p21);
+          tmem_ld8(tl + 2 * BPG + col, p22);
+          tmem_ld8(tl + N2 + 0 * BPG + col, p10);
+          tmem_ld8(tl + N2 + 1 * BPG + col, p11);
+          tmem_ld8(tl + N2 + N1 + col, p00);
+          tmem_ld_wait();
+          if (lane_row < BPG) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int j = jc * 16 + q;
-            const double y = 4294967296.0 * (double)(int32_t)p22[q] +
-                             65536.0 * (double)(int32_t)p11[q] + (double)(int32_t)p00[q];
-            const double x = 16777216.0 * (double)(int32_t)p21[q] +
-                             65536.0 * (double)(int32_t)p20[q] + 256.0 * (double)(int32_t)p10[q];
-            const size_t o = (size_t)j * BPG + lane_row;
-            if (flushes == 0) {
-              Y[o] = y;
-              X[o] = x;
-            } else {
-              Y[o] += y;
-              X[o] += x;
+            for (int q = 0; q < 8; ++q) {
+              const int j = (int)col + q;
+              const double y = 4294967296.0 * (double)(int32_t)p22[q] +
+                               65536.0 * (double)(int32_t)p11[q] + (double)(int32_t)p00[q];
+              const double x = 16777216.0 * (double)(int32_t)p21[q] +
+                               65536.0 * (double)(int32_t)p20[q] + 256.0 * (double)(int32_t)p10[q];
+              const size_t o = (size_t)j * BPG + lane_row;
+              if (flushes == 0) {
+                Y[o] = y;
+                X[o] = x;
+              } else {
+                Y[o] += y;
+                X[o] += x;
+              }
             }
           }
         }
@@ -218,12 +231,20 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       const TileInfo ti = tile_info(p.ts, it0 + t);
       if (!kF32 && ti.block != cur_block) {
         asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
-        for (int e = tid; e < ti.w * B; e += kGtWorkers) {
-          const int j = e / B, b = e - j * B;
-          const int64_t g = (int64_t)(ti.s0 + j) * B + b;
-          const float c = __ldg(p.coeff + g);
-          dark_s[j * (B + 1) + b] = __fmul_rn(__ldg(p.dark + g), c);  // d c
-          coeff_s[j * (B + 1) + b] = c;
+        for (int e = tid; e < ti.w * (BPG / 2); e += kGtWorkers) {
+          const int j = e / (BPG / 2), pr = e - j * (BPG / 2);
+          float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int b = 2 * pr + h;
+            if (b < B) {
+              const int64_t g = (int64_t)(ti.s0 + j) * B + b;
+              const float c = __ldg(p.coeff + g);
+              v[2 * h] = c * qs[b];
+              v[2 * h + 1] = -(__fmul_rn(__ldg(p.dark + g), c) * qs[b]);  // -(d c) q
+            }
+          }
+          tab4[e] = make_float4(v[0], v[1], v[2], v[3]);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kGtWorkers) : "memory");
         cur_block = ti.block;
@@ -244,12 +265,12 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
         pixkey = (uint32_t)(pix * 0x9E3779B97F4A7C15ull >> 32) * 0x85EBCA6Bu;
       }
       const uint8_t* rowb = raw_ring + s * p.raw_stage_bytes + (size_t)r * B * ESZ;
-      const float* dk = dark_s + j * (B + 1);
-      const float* ck = coeff_s + j * (B + 1);
+      const float4* tj = tab4 + j * (BPG / 2);
       uint8_t* ob = op_ring + os * OP_BYTES + (uint32_t)(r >> 3) * LBO + (uint32_t)(r & 7) * 16u;
       // band k's value -> E = D + 2^22 (as a u32), D = floor(tq + u)
+      // x: the calibrated value already in quantiser units (RAW) or the radiance (F32)
       auto quant = [&](float x, int k) -> uint32_t {
-        const float tq = __fmaf_rn(x, qs[k], -cs[k]);
+        const float tq = kF32 ? __fmaf_rn(x, qs[k], cs[k]) : __fmaf_rn(x, gi, cs[k]);
         // dither: Weyl step over the band on a per-pixel hash, u - 1/2 in [-1/2, 1/2)
         const uint32_t h = pixkey + (uint32_t)k * 0x9E3779B9u;
         const float um = __uint_as_float(0x3F800000u | (h >> 9)) - 1.5f;
@@ -261,6 +282,40 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
       };
       for (int gq = g_lo; gq < g_hi; ++gq) {
         uint32_t w0[4], w1[4], w2[4];
+        if (!kF32 && (B & 1) == 0 && valid && gq * 16 + 16 <= B) {
+          // a full group of 16 bands: no per-element conditions, band pairs in f32x2
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t e[4];
+#pragma unroll
+            for (int q = 0; q < 4; q += 2) {
+              const int k = gq * 16 + q4 * 4 + q;
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(rowb + 2 * k);
+              const float2 rf = fadd2(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7610)),
+                                                  __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7632))),
+                                      make_float2(-8388608.0f, -8388608.0f));
+              const float4 tb4 = tj[k >> 1];
+              const float2 c2 = *reinterpret_cast<const float2*>(cs + k);
+              float2 x = ffma2(rf, make_float2(tb4.x, tb4.z), make_float2(tb4.y, tb4.w));
+              x.x = x.x < 0.0f ? 0.0f : x.x;  // keeps NaN
+              x.y = x.y < 0.0f ? 0.0f : x.y;
+              const float2 tq = ffma2(x, make_float2(gi, gi), c2);
+              const uint32_t h0 = pixkey + (uint32_t)k * 0x9E3779B9u, h1 = h0 + 0x9E3779B9u;
+              const float2 sv = fadd2(tq, fadd2(make_float2(__uint_as_float(0x3F800000u | (h0 >> 9)),
+                                                            __uint_as_float(0x3F800000u | (h1 >> 9))),
+                                                make_float2(-1.5f, -1.5f)));
+              range_ok &= fabsf(sv.x) < 4190000.0f && fabsf(sv.y) < 4190000.0f;
+              const float2 tt = fadd2(sv, make_float2(12582912.0f, 12582912.0f));
+              e[q] = (uint32_t)(__float_as_int(tt.x) - 0x4B400000 + kGtOff);
+              e[q + 1] = (uint32_t)(__float_as_int(tt.y) - 0x4B400000 + kGtOff);
+            }
+            const uint32_t p01 = __byte_perm(e[0], e[1], 0x5140);
+            const uint32_t p23 = __byte_perm(e[2], e[3], 0x5140);
+            w0[q4] = __byte_perm(p01, p23, 0x5410);
+            w1[q4] = __byte_perm(p01, p23, 0x7632);
+            w2[q4] = __byte_perm(__byte_perm(e[0], e[1], 0x0062), __byte_perm(e[2], e[3], 0x0062), 0x5410);
+          }
+        } else {
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           uint32_t e[4];
@@ -286,13 +341,14 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
               }
               // max(., 0) that keeps NaN (np.maximum, calibrate.py:99): a NaN dark or coeff
               // must reach the range check below (flags |= 2 -> the f64 redo reports it)
+              const float4 tb4 = tj[k >> 1];  // k even
               if (ina) {
-                const float ta = __fmaf_rn(ra, ck[k], -dk[k]);
-                xa = (ta < 0.0f ? 0.0f : ta) * gi;
+                const float ta = __fmaf_rn(ra, tb4.x, tb4.y);
+                xa = ta < 0.0f ? 0.0f : ta;
               }
               if (inb) {
-                const float tb = __fmaf_rn(rb, ck[k + 1], -dk[k + 1]);
-                xb = (tb < 0.0f ? 0.0f : tb) * gi;
+                const float tb = __fmaf_rn(rb, tb4.z, tb4.w);
+                xb = tb < 0.0f ? 0.0f : tb;
               }
             }
             // padding bands (k >= B, not the constant band) quantise to E = 2^22 with
@@ -307,6 +363,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
           w0[q4] = __byte_perm(p01, p23, 0x5410);
           w1[q4] = __byte_perm(p01, p23, 0x7632);
           w2[q4] = __byte_perm(__byte_perm(e[0], e[1], 0x0062), __byte_perm(e[2], e[3], 0x0062), 0x5410);
+        }
         }
         *reinterpret_cast<uint4*>(ob + (0 * NG + gq) * 128) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
         *reinterpret_cast<uint4*>(ob + (1 * NG + gq) * 128) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
@@ -324,7 +381,7 @@ __global__ void __launch_bounds__(kGtThreads, 1) gram_tc_kernel(GramTcParams p) 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) tmem_dealloc(tmem, 512);
+  if (warp == kGtMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // Gram (units) = sum over CTAs of Y + X + X^T, then scale to moments [n, s, Q]
@@ -425,7 +482,7 @@ static int launch_gram_tc(GramTcParams p, double* moments, cudaStream_t st) {
   p.raw_stage_bytes = (uint32_t)(((128u * p.ts.B * ESZ) + 127u) & ~127u);
   constexpr uint32_t LBO = 3u * (BPG / 16) * 128u;
   const size_t smem = kGtRawStages * (size_t)p.raw_stage_bytes + kGtOpStages * (16u * LBO + 1024u) +
-                      2 * (size_t)kGtWmax * (p.ts.B + 1) * 4 + 2 * BPG * 4 + 16 * 8 + 64;
+                      (size_t)kGtWmax * (BPG / 2) * 16 + 2 * BPG * 4 + 16 * 8 + 64;
   int grid = kSMs;
   if (p.ts.items < grid) grid = (int)p.ts.items;
   if (grid < 1) grid = 1;

@@ -57,6 +57,19 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(int iters, unsigned long l
             mma_f16_ts(tm + 16 * ks, tm + 360 + ks * 8, bd + ks * 64,
                        idesc_f16_f32(128, 80 - 16 * ks, 0, 0), 1);
           }
+        } else if constexpr (MODE == 5 || MODE == 6) {
+          // gram_tc's operand layout: MN-major, no swizzle, LBO = 3 NG 128 (NG = 5), SBO = 128
+          // (MODE 5) vs MN-major SWIZZLE_128B (MODE 6), i8, M = 128, N = 240 / 160 / 80
+          const uint32_t lbo = MODE == 5 ? 1920u : 8192u, sbo = MODE == 5 ? 128u : 1024u;
+          const uint64_t b = MODE == 5 ? smem_desc(sm, lbo, sbo) : smem_desc_sw128(sm, lbo, sbo);
+          const uint64_t a = MODE == 5 ? smem_desc(sm + 1280, lbo, sbo) : smem_desc_sw128(sm + 16384, lbo, sbo);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint32_t o = MODE == 5 ? ks * 4 * 1920 / 16 : ks * 4096 / 16;
+            mma_i8(tm, a + o, b + o, (2u << 4) | (1u << 15) | (1u << 16) | (30u << 17) | (8u << 24), 1);
+            mma_i8(tm + 240, a + o, b + o, (2u << 4) | (1u << 15) | (1u << 16) | (20u << 17) | (8u << 24), 1);
+            mma_i8(tm + 400, a + o, b + o, (2u << 4) | (1u << 15) | (1u << 16) | (10u << 17) | (8u << 24), 1);
+          }
         } else {
 #pragma unroll
           for (int ks = 0; ks < 5; ++ks) {
@@ -120,5 +133,7 @@ int main() {
   run<2, 256>("i8 ss M128 K32 sw128", 8);
   run<3, 0>("score_tc tile ts (10 MMAs)", 10);
   run<4, 0>("score_tc tile ss (10 MMAs)", 10);
+  run<5, 0>("gram_tc tile i8 noswz (12 MMAs)", 12);
+  run<6, 0>("gram_tc tile i8 sw128 (12 MMAs)", 12);
   return 0;
 }
