@@ -56,8 +56,18 @@ __device__ unsigned long long gr_prof[160][12];
 #ifndef GRX_L2PROMO  // experiment switch: the TMA boxes' L2 promotion
 #define GRX_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
-constexpr int kGrThreads = 320;
-constexpr int kGrWorkers = 128;   // scan threads (warps 0-3); epilogue = warps 4-7
+// warps: 4 scan, 4 x kGrEpiGroups epilogue (group g takes every kGrEpiGroups-th pair of
+// 16-column chunks of a unit's byte Gram), TMA, MMA.  Short units (a 249-line c2 chunk: two
+// tiles per unit) are epilogue-bound (84 % of the kernel, tools/gr_profile.py), so the
+// epilogue is split over two groups
+#ifndef GRX_EPI_GROUPS
+#define GRX_EPI_GROUPS 2
+#endif
+constexpr int kGrEpiGroups = GRX_EPI_GROUPS;
+constexpr int kGrWorkers = 128;   // scan threads (warps 0-3)
+constexpr int kGrEpi = 128 * kGrEpiGroups;  // epilogue threads (warps 4..)
+constexpr int kGrTmaWarp = (kGrWorkers + kGrEpi) / 32, kGrMmaWarp = kGrTmaWarp + 1;
+constexpr int kGrThreads = kGrWorkers + kGrEpi + 64;
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
 // TMA ring depth (stage = 128 lines x (128 + second-box) bytes) within the shared memory
 // left beside the f64 accumulator: 8 stages, 5 for windows > 160 B, 2 for > 192 B
@@ -182,12 +192,12 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   if (tid == 0) {
     for (int s = 0; s < kGrStages; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], kGrWorkers + 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&acc_full[b], 1), mbar_init(&acc_empty[b], kGrWorkers);
-      mbar_init(&scan_full[b], 1), mbar_init(&scan_empty[b], kGrWorkers);
+      mbar_init(&acc_full[b], 1), mbar_init(&acc_empty[b], kGrEpi);
+      mbar_init(&scan_full[b], 1), mbar_init(&scan_empty[b], kGrEpi);
     }
     fence_mbar_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == kGrMmaWarp) tmem_alloc(tmem_slot, 512);
   // bit 8: this cube's clamp check ran (bit 4 would report a value below dark)
   if (blockIdx.x == 0 && tid == 0) atomicOr(p.flags, 8);
   for (int e = tid; e < B * B + B; e += blockDim.x) qacc[e] = 0.0;
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     }
   };
 
-  if (warp == 8) {
+  if (warp == kGrTmaWarp) {
     if ((tid & 31) == 0) {  // ------------------------------------------- TMA producer
       int t = 0;
       for (int64_t u = u0; u < u1; u += ustep) {
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kGrMmaWarp) {
 #ifndef GRX_ELECT_ISSUE  // lane 0 issues: 0.537 vs 0.563 ms per c4 strip for the
     // warp-converged / elected-lane form (tools/time_gr_libs.py, round 2): the slower issue
     // spaces the MMAs' shared-memory operand reads out against the scan warps' loads
@@ -384,8 +394,9 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
       if (tid == 0) mbar_arrive(&scan_full[ub]);
     }
-  } else {  // ------------------------------------------------------------ epilogue (warps 4-7)
-    const int te = tid - kGrWorkers;  // TMEM lane = byte row of the Gram
+  } else {  // ------------------------------------------------------- epilogue (warps 4 .. 4 + 4G)
+    const int te = (tid - kGrWorkers) & 127;  // TMEM lane = byte row of the Gram
+    const int eg = (tid - kGrWorkers) >> 7;   // epilogue group
     const int we = warp & 3;
     const uint32_t tq = warp_uniform(tmem + ((uint32_t)(32 * we) << 16));  // lane quarter
     int unit = 0;
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       const float* crow = p.coeff + (int64_t)s * B;
       bool clamp = false;
       // this unit's per-band terms, once, for every epilogue thread
-      if (ONES) {  // band sums = 256 sum(hi) + sum(lo) from the ones columns
+      if (ONES && eg == 0) {  // band sums = 256 sum(hi) + sum(lo) from the ones columns
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
           if (part == 1 && 128 + 32 * we >= off + 2 * B) continue;  // warp-uniform
@@ -431,13 +442,13 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
             bandS[rel >> 1] = 256.0 * (double)partner + (double)sv[0];
         }
       }
-      for (int bb = te; bb < B; bb += kGrWorkers) {
+      for (int bb = tid - kGrWorkers; bb < B; bb += kGrEpi) {
         bandC[bb] = (double)crow[bb] * p.ginv;
         bandD[bb] = (double)drow[bb];
         if (!ONES) bandS[bb] = (double)smv[(off >> 1) + bb];
         clamp |= (float)mnv[(off >> 1) + bb] < drow[bb];
       }
-      asm volatile("bar.sync 2, %0;" ::"n"(kGrWorkers) : "memory");
+      asm volatile("bar.sync 2, %0;" ::"n"(kGrEpi) : "memory");
 #ifdef SKYRX_GR_PROFILE
       const unsigned long long et1 = clock64();
       if (tid == kGrWorkers) gr_prof[blockIdx.x][8] += et1 - et0;
@@ -465,7 +476,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           return cc < NCH && (cc * 16 <= cmax || (part == 0 && TWO_M && cc >= 8));
         };
         // two chunks per TMEM wait: the loads queue behind the next unit's MMAs
-        for (int cc = cc0; cc < NCH; cc += 2) {
+        for (int cc = cc0 + 2 * eg; cc < NCH; cc += 2 * kGrEpiGroups) {
           const bool n0 = needed(cc), n1 = needed(cc + 1);
           if (!n0 && !n1) continue;
           uint32_t v2[32];
@@ -511,13 +522,13 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           }
           }
         }
-        if (in_band && !hi) sacc[b] += Cb * (Sb - Lu * db);
+        if (in_band && !hi && eg == 0) sacc[b] += Cb * (Sb - Lu * db);
 #ifdef SKYRX_GR_PROFILE
         if (tid == kGrWorkers) gr_prof[blockIdx.x][9 + part] += clock64() - et1;
 #endif
       }
       // the band terms are rewritten by the next unit only after every thread is done here
-      asm volatile("bar.sync 2, %0;" ::"n"(kGrWorkers) : "memory");
+      asm volatile("bar.sync 2, %0;" ::"n"(kGrEpi) : "memory");
 #ifdef SKYRX_GR_PROFILE
       if (tid == kGrWorkers) gr_prof[blockIdx.x][6] += clock64() - et0;
 #endif
@@ -552,7 +563,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #ifdef SKYRX_GR_PROFILE
   if (tid == 0) gr_prof[blockIdx.x][7] += clock64() - kt0;
 #endif
-  if (warp == 9) tmem_dealloc(tmem, 512);
+  if (warp == kGrMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 #ifdef SKYRX_GR_PROFILE

@@ -12,7 +12,7 @@ from paper_2602_13509_b200 import _lib
 if os.environ.get('SKYRX_LIB'):
     _lib.load(os.environ['SKYRX_LIB'])
 from paper_2602_13509_b200.synth import Scene
-L, S, B = 16384, 900, 70
+L, S, B = int(os.environ.get('GR_L', 16384)), 900, 70
 sc = Scene(4000, S, B, 5)
 raw = sc.generate(0, L)
 d, c = torch.from_numpy(sc.dark).cuda(), torch.from_numpy(sc.coeff).cuda()
