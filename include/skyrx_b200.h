@@ -152,6 +152,10 @@ int skyrx_stats_raw_own_shift(const uint16_t* raw, int64_t lines, int32_t sample
 /* state = forget * state + chunk (R-STREAM exponential forgetting) */
 int skyrx_moments_fold(double* state, const double* chunk, int32_t bands, double forget,
                        void* stream);
+/* the same, copying the pre-fold state to prev (StreamingRX's undo point for a chunk whose
+ * moments must be redone) in the same launch */
+int skyrx_moments_fold_keep(double* state, const double* chunk, int32_t bands, double forget,
+                            double* prev, void* stream);
 
 /* ---------------------------------------------------------------- K3 factorisation
  * Replaces rx.py:56-86 finalisation: mu, unbiased symmetric sigma, ridge

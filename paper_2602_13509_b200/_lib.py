@@ -55,6 +55,7 @@ SIGNATURES = {
     "skyrx_stats_raw": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "skyrx_stats_raw_own_shift": (C.c_int, [vp, i64, i32, i32, vp, vp, f64, vp, vp, vp, vp, sz, vp]),
     "skyrx_moments_fold":(C.c_int, [vp, vp, i32, f64, vp]),
+    "skyrx_moments_fold_keep":(C.c_int, [vp, vp, i32, f64, vp, vp]),
     "skyrx_stats_finalize": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp,
                                        vp, vp, vp]),
     "skyrx_whiten_prepare": (C.c_int, [vp, vp, i32, vp, vp, i32, vp, vp]),

@@ -59,9 +59,9 @@ __device__ unsigned long long gr_prof[160][12];
 // warps: 4 scan, 4 x kGrEpiGroups epilogue (group g takes every kGrEpiGroups-th pair of
 // 16-column chunks of a unit's byte Gram), TMA, MMA.  Short units (a 249-line c2 chunk: two
 // tiles per unit) are epilogue-bound (84 % of the kernel, tools/gr_profile.py), so the
-// epilogue is split over two groups
+// epilogue is split over three groups (1 / 2 / 3 / 4 groups: 124 / 101 / 97 / 103 us per chunk)
 #ifndef GRX_EPI_GROUPS
-#define GRX_EPI_GROUPS 2
+#define GRX_EPI_GROUPS 3
 #endif
 constexpr int kGrEpiGroups = GRX_EPI_GROUPS;
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3)
@@ -662,9 +662,8 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
 // true radiance (x'_b = 0 where r_b < d_b), dx = x' - x is -x on the clamped bands and
 //     sum x' x'^T = sum x x^T + sum (x dx^T + dx x^T + dx dx^T),   sum x' = sum x + sum dx.
 // Two kernels, both no-ops (one flags read per CTA) when nothing clamped:
-//  clamp_mark_lines_kernel  (more than a quarter of the units flagged) streams the flagged
-//                     units' lines with coalesced 16-byte loads;
-//  clamp_mark_kernel  otherwise, work items (flagged unit, line chunk): the unit's window of every
+//  clamp_mark_kernel  more than a quarter of the units flagged: streams every line with
+//                     coalesced 16-byte loads; otherwise work items (flagged unit, line chunk): the unit's window of every
 //                     line in the chunk (coalesced 2-byte loads, 8 in flight per thread)
 //                     against the sample's dark row; sets bit (line * S + s) of a pixel
 //                     bitmap for every pixel with a value below dark (atomicOr: order-free).
@@ -700,9 +699,8 @@ __device__ __forceinline__ void gr_unit_geom(const GramRawParams& p, int64_t u, 
 constexpr int kMarkChunks = 16;  // line chunks per unit
 
 // more than a quarter of the units flagged (random sparse sub-dark counts flag every unit):
-// one coalesced line-major pass over the cube (clamp_mark_lines_kernel) beats per-unit
-// column reads; otherwise (a dead detector element flags the units of one sample)
-// clamp_mark_kernel reads only the flagged units.  Both kernels count the same bits.
+// one coalesced line-major pass over the cube beats per-unit column reads; otherwise (a dead
+// detector element flags the units of one sample) only the flagged units are read.
 __device__ __forceinline__ bool clamp_many(const GramRawParams& p) {
   if (p.units >= kGrMaxUnitBits) return true;
   __shared__ int cnt;
@@ -717,11 +715,75 @@ __device__ __forceinline__ bool clamp_many(const GramRawParams& p) {
   return 4 * (int64_t)cnt > p.units;
 }
 
+// the line-major pass as CTA (bx, by) of a gx x gy grid (clamp_mark_kernel's CTAs, re-indexed)
+__device__ __forceinline__ void clamp_mark_lines(const uint16_t* __restrict__ raw,
+                                                 const GramRawParams& p,
+                                                 uint32_t* __restrict__ pixbits, int bx, int gx,
+                                                 int by, int gy) {
+  const int B = p.B;
+  const int vpl = p.S * B / 8;  // 16-B vectors per line (S B 2 % 16 == 0)
+  // line-major: CTA rows walk lines, threads the line's vectors; element e of a line is
+  // sample e / B, band e % B, and its dark word is dark[e] (the (S, B) table, row-major).
+  // Four lines per round, their loads issued together (one load in flight per thread
+  // left the kernel latency-bound at 1.1 ms per c4 strip).
+  constexpr int kLines = 4;
+  const bool dark16 = (reinterpret_cast<uintptr_t>(p.dark) & 15) == 0;
+  for (int vx = bx * blockDim.x + threadIdx.x; vx < vpl; vx += gx * blockDim.x) {
+    const int e0 = vx * 8;
+    float dv[8];
+    if (dark16) {
+      const float4 d0 = __ldg(reinterpret_cast<const float4*>(p.dark + e0));
+      const float4 d1 = __ldg(reinterpret_cast<const float4*>(p.dark + e0 + 4));
+      dv[0] = d0.x, dv[1] = d0.y, dv[2] = d0.z, dv[3] = d0.w;
+      dv[4] = d1.x, dv[5] = d1.y, dv[6] = d1.z, dv[7] = d1.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dv[q] = __ldg(p.dark + e0 + q);
+    }
+    for (int64_t l0 = by; l0 < p.L; l0 += (int64_t)kLines * gy) {
+      uint4 w[kLines];
+      bool on[kLines];
+#pragma unroll
+      for (int k = 0; k < kLines; ++k) {
+        const int64_t line = l0 + (int64_t)k * gy;
+        // most units are flagged here: stream every line (an unflagged unit holds no value
+        // below dark, so comparing it marks nothing) instead of a unit lookup per vector
+        on[k] = line < p.L;
+        if (on[k])
+          w[k] = __ldcs(reinterpret_cast<const uint4*>(raw + line * p.S * (int64_t)B) + vx);
+      }
+#pragma unroll
+      for (int k = 0; k < kLines; ++k) {
+        if (!on[k]) continue;
+        const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+        uint32_t hit = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t r = (q & 1) ? (ws[q >> 1] >> 16) : (ws[q >> 1] & 0xffffu);
+          hit |= (uint32_t)((float)r < dv[q]) << q;
+        }
+        while (hit) {  // rare
+          const int q = __ffs(hit) - 1;
+          hit &= hit - 1;
+          const int64_t pix = (l0 + (int64_t)k * gy) * p.S + (e0 + q) / B;
+          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) clamp_mark_kernel(const uint16_t* __restrict__ raw,
                                                          GramRawParams p,
                                                          uint32_t* __restrict__ pixbits) {
   if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;  // nothing clamped
-  if (clamp_many(p)) return;
+  if (clamp_many(p)) {  // one launch for both forms: the CTAs re-indexed as a 2-D grid
+    const int gx = (p.S * p.B / 8 + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int gy = (int)gridDim.x / gx;
+    if ((int)blockIdx.x < gx * gy)
+      clamp_mark_lines(raw, p, pixbits, blockIdx.x % gx, gx, blockIdx.x / gx, gy);
+    return;
+  }
   const int B = p.B;
   const int lpp = blockDim.x / B;  // lines per pass (B <= 128 on this path)
   const int b = threadIdx.x % B, lo = threadIdx.x / B;
@@ -753,64 +815,6 @@ __global__ void __launch_bounds__(256) clamp_mark_kernel(const uint16_t* __restr
         const int64_t l = line + (int64_t)k * lpp;
         if (l < lb && (float)v[k] < dk) {  // rare
           const int64_t pix = l * p.S + s;
-          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
-        }
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) clamp_mark_lines_kernel(const uint16_t* __restrict__ raw,
-                                                         GramRawParams p,
-                                                         uint32_t* __restrict__ pixbits) {
-  if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;
-  if (!clamp_many(p)) return;  // few flagged units: clamp_mark_kernel
-  const int B = p.B;
-  const int vpl = p.S * B / 8;  // 16-B vectors per line (S B 2 % 16 == 0)
-  // line-major: CTA rows walk lines, threads the line's vectors; element e of a line is
-  // sample e / B, band e % B, and its dark word is dark[e] (the (S, B) table, row-major).
-  // Four lines per round, their loads issued together (one load in flight per thread
-  // left the kernel latency-bound at 1.1 ms per c4 strip).
-  constexpr int kLines = 4;
-  const bool dark16 = (reinterpret_cast<uintptr_t>(p.dark) & 15) == 0;
-  for (int vx = blockIdx.x * blockDim.x + threadIdx.x; vx < vpl; vx += gridDim.x * blockDim.x) {
-    const int e0 = vx * 8;
-    float dv[8];
-    if (dark16) {
-      const float4 d0 = __ldg(reinterpret_cast<const float4*>(p.dark + e0));
-      const float4 d1 = __ldg(reinterpret_cast<const float4*>(p.dark + e0 + 4));
-      dv[0] = d0.x, dv[1] = d0.y, dv[2] = d0.z, dv[3] = d0.w;
-      dv[4] = d1.x, dv[5] = d1.y, dv[6] = d1.z, dv[7] = d1.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) dv[q] = __ldg(p.dark + e0 + q);
-    }
-    for (int64_t l0 = blockIdx.y; l0 < p.L; l0 += (int64_t)kLines * gridDim.y) {
-      uint4 w[kLines];
-      bool on[kLines];
-#pragma unroll
-      for (int k = 0; k < kLines; ++k) {
-        const int64_t line = l0 + (int64_t)k * gridDim.y;
-        // most units are flagged here: stream every line (an unflagged unit holds no value
-        // below dark, so comparing it marks nothing) instead of a unit lookup per vector
-        on[k] = line < p.L;
-        if (on[k])
-          w[k] = __ldcs(reinterpret_cast<const uint4*>(raw + line * p.S * (int64_t)B) + vx);
-      }
-#pragma unroll
-      for (int k = 0; k < kLines; ++k) {
-        if (!on[k]) continue;
-        const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
-        uint32_t hit = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t r = (q & 1) ? (ws[q >> 1] >> 16) : (ws[q >> 1] & 0xffffu);
-          hit |= (uint32_t)((float)r < dv[q]) << q;
-        }
-        while (hit) {  // rare
-          const int q = __ffs(hit) - 1;
-          hit &= hit - 1;
-          const int64_t pix = (l0 + (int64_t)k * gridDim.y) * p.S + (e0 + q) / B;
           atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
         }
       }
@@ -1025,11 +1029,6 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   if (p.pixbits != nullptr) {
     cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
     clamp_mark_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, p.pixbits);
-    SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
-    const int vpl = p.S * p.B / 8;
-    const int gx = (vpl + 255) / 256;
-    const int gy = (int)std::min<int64_t>(p.L, std::max<int64_t>(1, (int64_t)kSMs * 8 / gx));
-    clamp_mark_lines_kernel<<<dim3(gx, gy), 256, 0, st>>>(raw, p, p.pixbits);
     SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
   }
   const size_t fsm = clamp_fix_smem(p.B);

@@ -264,9 +264,13 @@ __global__ void __launch_bounds__(256) shift_kernel(CubeRef cube, double* __rest
 }
 
 __global__ void fold_kernel(double* __restrict__ state, const double* __restrict__ chunk,
-                            int64_t len, double forget) {
+                            int64_t len, double forget, double* __restrict__ prev) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < len) state[i] = forget * state[i] + chunk[i];
+  if (i < len) {
+    const double v = state[i];
+    if (prev) prev[i] = v;  // the undo point of a chunk that must be redone
+    state[i] = forget * v + chunk[i];
+  }
 }
 
 // ------------------------------------------------------------------ K3
@@ -859,8 +863,18 @@ extern "C" int skyrx_moments_fold(double* state, const double* chunk, int32_t ba
   SKYRX_REQUIRE(bands > 0, "bad bands");
   const int64_t len = (int64_t)skyrx_moments_len(bands);
   fold_kernel<<<(int)ceil_div<int64_t>(len, 256), 256, 0, as_stream(stream)>>>(state, chunk,
-                                                                               len, forget);
+                                                                               len, forget, nullptr);
   SKYRX_CHECK_LAUNCH("skyrx_moments_fold");
+  return SKYRX_OK;
+}
+
+extern "C" int skyrx_moments_fold_keep(double* state, const double* chunk, int32_t bands,
+                                       double forget, double* prev, void* stream) {
+  SKYRX_REQUIRE(bands > 0 && prev != nullptr, "bad bands or prev");
+  const int64_t len = (int64_t)skyrx_moments_len(bands);
+  fold_kernel<<<(int)ceil_div<int64_t>(len, 256), 256, 0, as_stream(stream)>>>(state, chunk,
+                                                                               len, forget, prev);
+  SKYRX_CHECK_LAUNCH("skyrx_moments_fold_keep");
   return SKYRX_OK;
 }
 

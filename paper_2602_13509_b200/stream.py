@@ -86,7 +86,6 @@ class StreamingRX:
         args = (self.raw.data_ptr(), L, S, B, self.dark.data_ptr(), self.coeff.data_ptr(),
                 self.gains.data_ptr())
         ds.flags.zero_()
-        self.prev_state.copy_(ds.moments[0])  # undo point if this chunk must be redone
         if first:
             _lib.call("skyrx_stats_shift", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(), s)
         use_raw = self.raw_ok and gain is not None and not precise
@@ -102,8 +101,9 @@ class StreamingRX:
             _lib.call("skyrx_stats_accumulate", _lib.IN_RAW_U16, *args, ds.shift[0].data_ptr(),
                       1, self.chunk_moments.data_ptr(), ds.flags.data_ptr(), plan.ws.data_ptr(),
                       plan.ws_bytes, s)
-        _lib.call("skyrx_moments_fold", ds.moments[0].data_ptr(), self.chunk_moments.data_ptr(),
-                  B, self.forget, s)
+        # fold, keeping the pre-chunk state as the undo point if this chunk must be redone
+        _lib.call("skyrx_moments_fold_keep", ds.moments[0].data_ptr(),
+                  self.chunk_moments.data_ptr(), B, self.forget, self.prev_state.data_ptr(), s)
         plan.finalize()
         plan.score(0, self.raw, self.dark, self.coeff, self.gains, self.k)
 
