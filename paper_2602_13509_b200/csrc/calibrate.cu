@@ -248,6 +248,23 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
             for (int j = 0; j < FMAX; ++j) rv[j] = j < factor ? (float)row[kbv[q][j]] : 0.0f;
           }
           float acc = 0.0f;
+          if constexpr (kRaw && VEC && FAST && FMAX % 2 == 0) {
+            // band pairs in f32x2 (same per-lane rounding), then the left-to-right sum
+#pragma unroll
+            for (int j = 0; j < FMAX; j += 2) {
+              const float2 rr = make_float2(rv[j], rv[j + 1]);
+              const float2 dd = make_float2(dkv[q][j], dkv[q][j + 1]);
+              const float2 cc = make_float2(ckv[q][j], ckv[q][j + 1]);
+              float2 x2;
+              if constexpr (ONE) {
+                const float2 t = fsub2(rr, dd);
+                x2 = fmul2(make_float2(fmaxf(t.x, 0.0f), fmaxf(t.y, 0.0f)), cc);
+              } else {
+                x2 = calib_fast2(rr, dd, cc, gl, gi);
+              }
+              acc = (j == 0) ? __fadd_rn(x2.x, x2.y) : __fadd_rn(__fadd_rn(acc, x2.x), x2.y);
+            }
+          } else {
 #pragma unroll
           for (int j = 0; j < FMAX; ++j) {
             if (VEC || j < factor) {
@@ -261,6 +278,7 @@ __global__ void __launch_bounds__(256) calibrate_bin_tiled_kernel(
               }
               acc = (j == 0) ? x : __fadd_rn(acc, x);
             }
+          }
           }
           __stcs(o_line + e, acc);
           if (rgbm[q]) {

@@ -102,6 +102,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   float2 r;
   asm("{\n\t.reg .b64 a, b, d;\n\t"
@@ -110,6 +119,17 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
+}
+
+// calib_fast on two values at once (f32x2 ops, each lane rounded like the scalar form)
+__device__ __forceinline__ float2 calib_fast2(float2 raw, float2 dark, float2 coeff, float gain,
+                                              float ginv) {
+  float2 t = fsub2(raw, dark);
+  t = fmul2(make_float2(fmaxf(t.x, 0.0f), fmaxf(t.y, 0.0f)), coeff);
+  const float2 gi2 = make_float2(ginv, ginv);
+  const float2 q = fmul2(t, gi2);
+  const float2 r = ffma2(make_float2(-q.x, -q.y), make_float2(gain, gain), t);
+  return ffma2(r, gi2, q);
 }
 
 // moments that must be recomputed: the int8 quantiser overflowed (2), or a value clamped

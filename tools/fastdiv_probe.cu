@@ -27,8 +27,16 @@ __global__ void probe(uint64_t seed, int iters) {
     if (!(calib_fast_range(gain) && calib_fast_range(coeff) && (dark == 0.0f || calib_fast_range(dark)))) continue;
     const float a = calib(raw, dark, coeff, gain);
     const float b = calib_fast(raw, dark, coeff, gain, __frcp_rn(gain));
-    ++chk;
-    if (__float_as_uint(a) != __float_as_uint(b)) {
+    // the f32x2 pair form, second lane from the next operand set's raw / dark / coeff
+    const float raw2 = (float)((h0 >> 16) & 0xFFFF);
+    const float dark2 = dark * 0.75f, coeff2 = coeff * 1.25f;
+    const float a2 = calib(raw2, dark2, coeff2, gain);
+    const float2 b2 = calib_fast2(make_float2(raw, raw2), make_float2(dark, dark2),
+                                  make_float2(coeff, coeff2), gain, __frcp_rn(gain));
+    chk += 3;
+    if (__float_as_uint(a) != __float_as_uint(b) || __float_as_uint(a) != __float_as_uint(b2.x) ||
+        (calib_fast_range(coeff2) && (dark2 == 0.0f || calib_fast_range(dark2)) &&
+         __float_as_uint(a2) != __float_as_uint(b2.y))) {
       if (bad < 3) printf("mismatch raw %g dark %a coeff %a gain %a: %a vs %a\n", raw, dark, coeff, gain, a, b);
       ++bad;
     }
