@@ -679,6 +679,23 @@ class TestDetect:
         assert normwise(det.stats.mu, exact.mu) < 1e-12
         check_detection(det, raw, t)
 
+    @pytest.mark.parametrize("S,B,L", [(900, 70, 2100), (128, 128, 1100)])
+    def test_dead_element_only(self, P, S, B, L):
+        """One dead detector element (a whole (sample, band) column below dark) and nothing
+        else: few units clamp, so the marking reads only the flagged units (the per-unit
+        form of clamp_mark_kernel); the corrected moments are exact."""
+        t = osynth.make_tables(47, S, B, 5)
+        raw = osynth.generate_lines(t, 0, L).copy()
+        raw[:, S // 2, B // 3] = 3
+        raw[L // 2, 5, 1] = 0  # and one isolated sub-dark count elsewhere
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(t.dark, t.coeff), plan=plan)
+        assert int(plan.ds.flags[0].item()) & (4 | 256) == (4 | 256)
+        exact = O.compute_stats_exact(raw, t.dark, t.coeff, np.ones(L))
+        assert normwise(det.stats.sigma, exact.sigma) < 1e-11
+        assert normwise(det.stats.mu, exact.mu) < 1e-12
+        check_detection(det, raw, t)
+
     def test_deterministic(self, P):
         t = osynth.make_tables(1, 900, 70)
         raw = osynth.generate_lines(t, 0, 128)
