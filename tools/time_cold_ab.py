@@ -23,8 +23,15 @@ if len(sys.argv) > 2 and sys.argv[1] == "--one":
                   plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(), None, _dev.stream_ptr())
     def gr(raw):
         plan.run(0, raw, d, c, g, gain_const=1.0)
+    hist = _lib.load().skyrx_topk_histogram(plan.topk_ws.data_ptr())
+    def tch(raw):  # with the fused digit-0 top-k histogram, as plan.score runs it
+        _lib.call("skyrx_score_tc", raw.data_ptr(), L, S, B, d.data_ptr(), c.data_ptr(), None,
+                  ds.mu_hilo[0].data_ptr(), plan.wpack[0].data_ptr(), ds.flags[0:1].data_ptr(),
+                  plan.scores[0].data_ptr(), plan.max_key[0:1].data_ptr(), hist, _dev.stream_ptr())
+    def full(raw):  # the whole score stage of the bench step (init, score + hist, mask pass)
+        plan.score(0, raw, d, c, g)
     out = {}
-    for name, fn in (("score_tc", tc), ("moments", gr)):
+    for name, fn in (("score_tc", tc), ("score_tc_hist", tch), ("score_stage", full), ("moments", gr)):
         fn(raws[0]); torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
