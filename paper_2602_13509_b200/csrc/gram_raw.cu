@@ -78,7 +78,6 @@ __host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 1
 __host__ __device__ constexpr int gr_stages() { return NCH >= 13 ? 2 : (NCH >= 11 ? 5 : GRX_STAGES); }
 #endif
 constexpr int64_t kGrMaxUnitLines = 32768;
-constexpr int64_t kGrMaxUnitBits = 1 << 20;  // units past this count are all re-scanned
 
 struct GramRawParams {
   const float* dark;
@@ -97,7 +96,6 @@ struct GramRawParams {
   int64_t units_main;   // regular units dealt in full rounds
   int32_t tail_k;       // pieces per leftover unit (1: no split)
   int64_t tail_lines;   // lines per piece (multiple of the tile)
-  uint32_t* unit_clamp;  // bit u: unit u holds a value below dark (clamp_mark_kernel)
   uint32_t* pixbits;     // bit (line * S + s): that pixel has a clamped value, or null
 };
 
@@ -128,6 +126,73 @@ __host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 51
 #else  // experiment: one accumulator (no MMA runs ahead of the epilogue loads)
 __host__ __device__ constexpr int gr_nbuf() { return 1; }
 #endif
+
+// The scan of one FULL tile (128 lines) by one thread of box 0 (BOX1 = false) or of the
+// second box: trip counts and line steps are compile-time, and the thread's 8..16 shared
+// loads go out in one or two batches instead of a loop whose runtime trip count cost a
+// division per tile and one shared-memory latency per four lines.  The scan warps sit on
+// the stage-release path (a stage is freed by the MMA commit AND the 128 scan arrivals), so
+// their per-tile latency is kernel time.  lw: the warp's index within its box's scanners.
+// below(v, th): some halfword of v is below its threshold (max(v, t) != v)
+__device__ __forceinline__ uint32_t gr_below(const uint4& v, const uint32_t (&th)[4]) {
+  return (__vmaxu2(v.x, th[0]) ^ v.x) | (__vmaxu2(v.y, th[1]) ^ v.y) |
+         (__vmaxu2(v.z, th[2]) ^ v.z) | (__vmaxu2(v.w, th[3]) ^ v.w);
+}
+// marking: when the minima say this thread's lines hold a value below dark, the lines are
+// tested one by one from the registers they are still in, and mark(l) is called for each hit
+template <int NCH, bool BOX1, bool SUMS, class Mark>
+__device__ __forceinline__ void gr_scan_full(uint32_t atom, int lane, int lw, uint32_t (&tm)[4],
+                                             uint32_t (&sm8)[8], bool marking,
+                                             const uint32_t (&th)[4], uint32_t always,
+                                             Mark&& mark) {
+  constexpr uint32_t W2B = gr_w2b<NCH>();
+  constexpr int W0 = NCH > 8 ? (W2B == 32 ? 3 : 2) : 4;
+  constexpr int NQ1 = W2B > 0 ? (int)W2B / 16 : 1;
+  constexpr int LPW = BOX1 ? 32 / NQ1 : 4;
+  constexpr int LSTEP = LPW * (BOX1 ? 4 - W0 : W0);
+  constexpr uint32_t WDT = BOX1 ? W2B : 128u;
+  constexpr int NITF = kGrLb / LSTEP, REM = kGrLb - NITF * LSTEP;
+#ifndef GRX_SCAN_NB
+#define GRX_SCAN_NB 11
+#endif
+  constexpr int NB = NITF > GRX_SCAN_NB ? (NITF + 1) / 2 : NITF;  // loads in flight per batch
+  const int q = BOX1 ? lane % NQ1 : lane & 7;
+  const int l0 = (BOX1 ? lane / NQ1 : lane >> 3) + LPW * lw;
+  auto ld = [&](int l) {
+    const uint32_t sw = ((uint32_t)l * WDT >> 7) & (WDT / 16 - 1);
+    return ld_shared_v4(atom + l * WDT + ((q ^ sw) << 4));
+  };
+  auto acc = [&](const uint4& v) {
+    tm[0] = __vminu2(tm[0], v.x), tm[1] = __vminu2(tm[1], v.y);
+    tm[2] = __vminu2(tm[2], v.z), tm[3] = __vminu2(tm[3], v.w);
+    if (SUMS) {
+      sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu;
+      sm8[3] += v.y >> 16, sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16;
+      sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
+    }
+  };
+  uint4 vr = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  const bool tail = REM > 0 && l0 < REM;  // lines 128 - REM ..: the first REM threads' extra line
+  if (tail) vr = ld(l0 + NITF * LSTEP);
+#pragma unroll
+  for (int i0 = 0; i0 < NITF; i0 += NB) {
+    uint4 v[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (i0 + j < NITF) v[j] = ld(l0 + (i0 + j) * LSTEP);
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (i0 + j < NITF) acc(v[j]);
+    if (i0 + NB >= NITF && tail) acc(vr);
+    const uint4 tmv = make_uint4(tm[0], tm[1], tm[2], tm[3]);
+    if (marking && (always | gr_below(tmv, th))) {  // rare
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (i0 + j < NITF && (always | gr_below(v[j], th))) mark(l0 + (i0 + j) * LSTEP);
+      if (i0 + NB >= NITF && tail && (always | gr_below(vr, th))) mark(l0 + NITF * LSTEP);
+    }
+  }
+}
 
 template <int NCH>
 __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -332,6 +397,11 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
     const int lstep = lpw * (box1 ? 4 - W0 : W0);
     const uint32_t wdt = box1 ? W2B : 128u;
     const bool scanner = c < NCH;
+#ifndef GRX_NO_MARK
+    const bool marking = p.pixbits != nullptr;
+#else  // timing experiment: the scan without the clamp marking
+    const bool marking = false;
+#endif
     int t = 0, unit = 0;
     for (int64_t u = u0; u < u1; u += ustep, ++unit) {
       int s;
@@ -340,6 +410,26 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
       uint32_t mn[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
       uint32_t sm8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      // clamp thresholds of this thread's 8 window halfwords: a count r calibrates to 0
+      // iff (float)r < dark, i.e. r < ceil(dark) (never for dark <= 0 or NaN; always for
+      // dark > 65535); halfwords outside the sample's bands get 0
+      uint32_t th[4] = {0u, 0u, 0u, 0u};
+      uint32_t always = 0u;
+      if (marking && scanner) {
+        const int off2 = (int)((((int64_t)s * B * 2) & 15) >> 1);
+        const float* drow = p.dark + (int64_t)s * B;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int b = 8 * c + i - off2;
+          uint32_t t16 = 0u;
+          if (b >= 0 && b < B) {
+            const float dk = __ldg(drow + b);
+            if (dk > 65535.0f) always = 1u;
+            else if (dk > 0.0f) t16 = (uint32_t)ceilf(dk);
+          }
+          th[i >> 1] |= t16 << (16 * (i & 1));
+        }
+      }
       for (int k = 0; k < ntile; ++k, ++t) {
         const int st = t % kGrStages;
         if (tid == 0) GR_PW(3, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
@@ -352,18 +442,48 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
           // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
           const uint32_t atom = stages32 + st * STAGE + (box1 ? ATOM : 0u);
+          uint32_t tm[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};  // tile minima
+          auto mark_line = [&](int l) {
+            const int64_t pix = (l0 + (int64_t)k * kGrLb + l) * p.S + s;
+            atomicOr(p.pixbits + (pix >> 5), 1u << (pix & 31));
+          };
+          const bool full_tile = valid == kGrLb;
+          if (full_tile) {
+            if (box1) {
+              if constexpr (TWO_M)
+                gr_scan_full<NCH, true, !ONES>(atom, lane, lw, tm, sm8, marking, th, always,
+                                               mark_line);
+            } else {
+              gr_scan_full<NCH, false, !ONES>(atom, lane, lw, tm, sm8, marking, th, always,
+                                              mark_line);
+            }
+          } else
 #pragma unroll 4
           for (int l = lr + lpw * lw; l < valid; l += lstep) {
             const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
             const uint4 v = ld_shared_v4(atom + l * wdt + ((q ^ sw) << 4));
-            mn[0] = __vminu2(mn[0], v.x), mn[1] = __vminu2(mn[1], v.y);
-            mn[2] = __vminu2(mn[2], v.z), mn[3] = __vminu2(mn[3], v.w);
+            tm[0] = __vminu2(tm[0], v.x), tm[1] = __vminu2(tm[1], v.y);
+            tm[2] = __vminu2(tm[2], v.z), tm[3] = __vminu2(tm[3], v.w);
             if (!ONES) {  // (ONES: the column sums come from the tensor core)
               sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu;
               sm8[3] += v.y >> 16, sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16;
               sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
             }
           }
+          // a minimum below its threshold: this thread's part of the tile holds a value
+          // below dark; its pixels are marked here for clamp_fix_kernel, so no second pass
+          // over the cube is needed
+          // (a partial tile: rescanned from shared memory, where it still is)
+          if (marking && !full_tile &&
+              (always | gr_below(make_uint4(tm[0], tm[1], tm[2], tm[3]), th))) {
+            for (int l = lr + lpw * lw; l < valid; l += lstep) {
+              const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
+              const uint4 v = ld_shared_v4(atom + l * wdt + ((q ^ sw) << 4));
+              if (always | gr_below(v, th)) mark_line(l);
+            }
+          }
+          mn[0] = __vminu2(mn[0], tm[0]), mn[1] = __vminu2(mn[1], tm[1]);
+          mn[2] = __vminu2(mn[2], tm[2]), mn[3] = __vminu2(mn[3], tm[3]);
         }
         mbar_arrive(empty32 + 8 * st);
       }
@@ -532,10 +652,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
 #ifdef SKYRX_GR_PROFILE
       if (tid == kGrWorkers) gr_prof[blockIdx.x][6] += clock64() - et0;
 #endif
-      if (clamp) {
-        atomicOr(p.flags, 4);
-        if (u < kGrMaxUnitBits) atomicOr(p.unit_clamp + (u >> 5), 1u << (u & 31));
-      }
+      if (clamp) atomicOr(p.flags, 4);
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       mbar_arrive(&scan_empty[ub]);
@@ -591,7 +708,15 @@ __device__ __forceinline__ double part_slice_sum(const double* __restrict__ part
     for (int k = 0; k < kSumBatch; ++k)
       if (c0 + k < c1) acc += v[k];
   } else {
-    for (int c = c0; c < c1; ++c) acc += part[(size_t)c * stride + e];
+    for (int cb = c0; cb < c1; cb += kSumBatch) {  // the same in-order sum, in batches
+      double v[kSumBatch];
+#pragma unroll
+      for (int k = 0; k < kSumBatch; ++k)
+        v[k] = cb + k < c1 ? __ldcg(part + (size_t)(cb + k) * stride + e) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kSumBatch; ++k)
+        if (cb + k < c1) acc += v[k];
+    }
   }
   return acc;
 }
@@ -661,166 +786,24 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
 // exact corrections are added to the uncentred sums: with x the unclamped and x' the
 // true radiance (x'_b = 0 where r_b < d_b), dx = x' - x is -x on the clamped bands and
 //     sum x' x'^T = sum x x^T + sum (x dx^T + dx x^T + dx dx^T),   sum x' = sum x + sum dx.
-// Two kernels, both no-ops (one flags read per CTA) when nothing clamped:
-//  clamp_mark_kernel  more than a quarter of the units flagged: streams every line with
-//                     coalesced 16-byte loads; otherwise work items (flagged unit, line chunk): the unit's window of every
-//                     line in the chunk (coalesced 2-byte loads, 8 in flight per thread)
-//                     against the sample's dark row; sets bit (line * S + s) of a pixel
-//                     bitmap for every pixel with a value below dark (atomicOr: order-free).
-//                     Unflagged units cost one bit test (a dead detector element flags the
-//                     units of one sample: ~0.69 ms for the old line-major pass over the
-//                     whole cube, which spent it on per-vector unit lookups);
+// The scan warps of gram_raw_kernel mark the pixels: a thread whose tile minima fall below
+// its thresholds rescans its part of the tile (still in shared memory) and sets bit
+// (line * S + s) of a pixel bitmap for every pixel with a value below dark (atomicOr:
+// order-free).  Round 2 had a separate marking launch that streamed the cube again (355 us
+// of the 0.01 %-sub-dark c4 strip).  Then, a no-op (one flags read per CTA) when nothing
+// clamped:
 //  clamp_fix_kernel   CTA c walks a fixed contiguous range of the bitmap in pixel order,
-//                     stages the clamped pixels 32 at a time and adds, pixel by pixel,
+//                     stages the clamped pixels 16 at a time and adds, pixel by pixel,
 //                     only the row / column of each clamped band into a shared-memory
 //                     triangle (thread t takes entry (t, c)): a deterministic per-CTA
 //                     partial, joined to the Gram partials in gram_raw_sum_kernel's
 //                     fixed-order sum.
 constexpr int kFixThreads = 256;
-constexpr int kFixBatch = 32;  // clamped pixels staged per round
-
-// unit u's sample and line range: gram_raw_kernel's unit_geom (regular units, then the tail
-// pieces of the leftover units)
-__device__ __forceinline__ void gr_unit_geom(const GramRawParams& p, int64_t u, int& s,
-                                             int64_t& l0, int64_t& nl) {
-  const int64_t ur = u < p.units_main ? u : p.units_main + (u - p.units_main) / p.tail_k;
-  s = (int)(ur % p.S);
-  l0 = (ur / p.S) * p.split_lines;
-  nl = p.L - l0 < p.split_lines ? p.L - l0 : p.split_lines;
-  if (u >= p.units_main) {
-    const int64_t piece = (u - p.units_main) % p.tail_k;
-    const int64_t a = piece * p.tail_lines;
-    const int64_t b = a + p.tail_lines < nl ? a + p.tail_lines : nl;
-    l0 += a;
-    nl = b > a ? b - a : 0;
-  }
-}
-
-constexpr int kMarkChunks = 16;  // line chunks per unit
-
-// more than a quarter of the units flagged (random sparse sub-dark counts flag every unit):
-// one coalesced line-major pass over the cube beats per-unit column reads; otherwise (a dead
-// detector element flags the units of one sample) only the flagged units are read.
-__device__ __forceinline__ bool clamp_many(const GramRawParams& p) {
-  if (p.units >= kGrMaxUnitBits) return true;
-  __shared__ int cnt;
-  if (threadIdx.x == 0) cnt = 0;
-  __syncthreads();
-  int c = 0;
-  for (int64_t i = threadIdx.x; i < (p.units + 31) / 32; i += blockDim.x)
-    c += __popc(p.unit_clamp[i]);
-  c = warp_sum(c);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&cnt, c);
-  __syncthreads();
-  return 4 * (int64_t)cnt > p.units;
-}
-
-// the line-major pass as CTA (bx, by) of a gx x gy grid (clamp_mark_kernel's CTAs, re-indexed)
-__device__ __forceinline__ void clamp_mark_lines(const uint16_t* __restrict__ raw,
-                                                 const GramRawParams& p,
-                                                 uint32_t* __restrict__ pixbits, int bx, int gx,
-                                                 int by, int gy) {
-  const int B = p.B;
-  const int vpl = p.S * B / 8;  // 16-B vectors per line (S B 2 % 16 == 0)
-  // line-major: CTA rows walk lines, threads the line's vectors; element e of a line is
-  // sample e / B, band e % B, and its dark word is dark[e] (the (S, B) table, row-major).
-  // Four lines per round, their loads issued together (one load in flight per thread
-  // left the kernel latency-bound at 1.1 ms per c4 strip).
-  constexpr int kLines = 4;
-  const bool dark16 = (reinterpret_cast<uintptr_t>(p.dark) & 15) == 0;
-  for (int vx = bx * blockDim.x + threadIdx.x; vx < vpl; vx += gx * blockDim.x) {
-    const int e0 = vx * 8;
-    float dv[8];
-    if (dark16) {
-      const float4 d0 = __ldg(reinterpret_cast<const float4*>(p.dark + e0));
-      const float4 d1 = __ldg(reinterpret_cast<const float4*>(p.dark + e0 + 4));
-      dv[0] = d0.x, dv[1] = d0.y, dv[2] = d0.z, dv[3] = d0.w;
-      dv[4] = d1.x, dv[5] = d1.y, dv[6] = d1.z, dv[7] = d1.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) dv[q] = __ldg(p.dark + e0 + q);
-    }
-    for (int64_t l0 = by; l0 < p.L; l0 += (int64_t)kLines * gy) {
-      uint4 w[kLines];
-      bool on[kLines];
-#pragma unroll
-      for (int k = 0; k < kLines; ++k) {
-        const int64_t line = l0 + (int64_t)k * gy;
-        // most units are flagged here: stream every line (an unflagged unit holds no value
-        // below dark, so comparing it marks nothing) instead of a unit lookup per vector
-        on[k] = line < p.L;
-        if (on[k])
-          w[k] = __ldcs(reinterpret_cast<const uint4*>(raw + line * p.S * (int64_t)B) + vx);
-      }
-#pragma unroll
-      for (int k = 0; k < kLines; ++k) {
-        if (!on[k]) continue;
-        const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
-        uint32_t hit = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint32_t r = (q & 1) ? (ws[q >> 1] >> 16) : (ws[q >> 1] & 0xffffu);
-          hit |= (uint32_t)((float)r < dv[q]) << q;
-        }
-        while (hit) {  // rare
-          const int q = __ffs(hit) - 1;
-          hit &= hit - 1;
-          const int64_t pix = (l0 + (int64_t)k * gy) * p.S + (e0 + q) / B;
-          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
-        }
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) clamp_mark_kernel(const uint16_t* __restrict__ raw,
-                                                         GramRawParams p,
-                                                         uint32_t* __restrict__ pixbits) {
-  if (!(*reinterpret_cast<volatile int32_t*>(p.flags) & 4)) return;  // nothing clamped
-  if (clamp_many(p)) {  // one launch for both forms: the CTAs re-indexed as a 2-D grid
-    const int gx = (p.S * p.B / 8 + (int)blockDim.x - 1) / (int)blockDim.x;
-    const int gy = (int)gridDim.x / gx;
-    if ((int)blockIdx.x < gx * gy)
-      clamp_mark_lines(raw, p, pixbits, blockIdx.x % gx, gx, blockIdx.x / gx, gy);
-    return;
-  }
-  const int B = p.B;
-  const int lpp = blockDim.x / B;  // lines per pass (B <= 128 on this path)
-  const int b = threadIdx.x % B, lo = threadIdx.x / B;
-  const int64_t pitch = (int64_t)p.S * B;
-  constexpr int kUnroll = 8;  // loads in flight per thread
-  // persistent: work items (unit, line chunk), unflagged units skipped by one bit test
-  for (int64_t it = blockIdx.x; it < p.units * kMarkChunks; it += gridDim.x) {
-    const int64_t u = it / kMarkChunks;
-    const int ch = (int)(it - u * kMarkChunks);
-    if (!((p.unit_clamp[u >> 5] >> (u & 31)) & 1u)) continue;
-    int s;
-    int64_t l0, nl;
-    gr_unit_geom(p, u, s, l0, nl);
-    const int64_t per = (nl + kMarkChunks - 1) / kMarkChunks;
-    const int64_t la = l0 + ch * per;
-    const int64_t lb = min(l0 + nl, la + per);
-    if (lo >= lpp || la >= lb) continue;
-    const float dk = __ldg(p.dark + (int64_t)s * B + b);
-    const uint16_t* base = raw + (int64_t)s * B + b;
-    for (int64_t line = la + lo; line < lb; line += (int64_t)kUnroll * lpp) {
-      uint16_t v[kUnroll];
-#pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        const int64_t l = line + (int64_t)k * lpp;
-        v[k] = l < lb ? __ldcs(base + l * pitch) : (uint16_t)0xFFFF;
-      }
-#pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        const int64_t l = line + (int64_t)k * lpp;
-        if (l < lb && (float)v[k] < dk) {  // rare
-          const int64_t pix = l * p.S + s;
-          atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
-        }
-      }
-    }
-  }
-}
+constexpr int kFixBatch = 16;  // clamped pixels staged per round
+// clamp_fix CTAs: the per-pixel chain (one barrier per clamped pixel, B threads busy) is
+// latency-bound, so four co-resident CTAs per SM walk a quarter of the bitmap range each
+// (0.01 % sub-dark c4 strip: 404 us with one CTA per SM)
+static inline int fix_grid(int B) { return B <= 80 ? 4 * kSMs : (B <= 128 ? 2 * kSMs : kSMs); }
 
 __global__ void __launch_bounds__(kFixThreads) clamp_fix_kernel(
     const uint16_t* __restrict__ raw, GramRawParams p, const uint32_t* __restrict__ pixbits,
@@ -944,7 +927,7 @@ int gram_raw_sum_and_center(const double* part, int grid, int bands, double* shi
                             double* moments, cudaStream_t st, const double* fix, int nfix,
                             const int32_t* flags) {
   const int work = bands * bands + bands + 1;
-  double* tot = const_cast<double*>(part) + (size_t)2 * kSMs * work;  // after the partials
+  double* tot = const_cast<double*>(part) + (size_t)(kSMs + fix_grid(bands)) * work;  // after the partials
   gram_raw_sum_kernel<<<ceil_div(work, 32), 256, 0, st>>>(part, grid, work, tot, fix, nfix,
                                                           flags);
   SKYRX_CHECK_LAUNCH("gram_raw_sum_kernel");
@@ -1019,18 +1002,14 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   }
   cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  const int64_t nbits = p.units < kGrMaxUnitBits ? p.units : kGrMaxUnitBits;
-  cudaMemsetAsync(p.unit_clamp, 0, (size_t)((nbits + 31) / 32) * 4, st);
+  // the scan warps mark every pixel holding a value below dark while its tile is on chip
+  if (p.pixbits != nullptr)
+    cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
   gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
   // exact corrections of the clamped pixels (no-op passes when nothing clamped)
-  const int fgrid = kSMs;
+  const int fgrid = fix_grid(p.B);
   const int work = p.B * p.B + p.B + 1;
-  if (p.pixbits != nullptr) {
-    cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
-    clamp_mark_kernel<<<kSMs * 8, 256, 0, st>>>(raw, p, p.pixbits);
-    SKYRX_CHECK_LAUNCH("clamp_mark_kernel");
-  }
   const size_t fsm = clamp_fix_smem(p.B);
   if (fsm > 48 * 1024)
     cudaFuncSetAttribute(clamp_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
@@ -1058,9 +1037,8 @@ extern "C" int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t
 }
 
 extern "C" size_t skyrx_stats_raw_workspace(int32_t bands) {
-  // [2 kSMs partials (Gram CTAs, clamp fix-up CTAs) | total] doubles, then the unit bitmap
-  return (size_t)(2 * kSMs + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double) +
-         (size_t)kGrMaxUnitBits / 8;
+  // [kSMs + fix_grid(B) partials (Gram CTAs, clamp fix-up CTAs) | total] doubles
+  return (size_t)(kSMs + fix_grid(bands) + 1) * ((size_t)bands * bands + bands + 1) * sizeof(double);
 }
 
 extern "C" size_t skyrx_stats_raw_workspace_for(int64_t lines, int32_t samples,
@@ -1098,10 +1076,9 @@ static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, i
   p.coeff = coeff;
   p.ginv = 1.0 / gain;
   p.part = reinterpret_cast<double*>(workspace);
-  p.unit_clamp = reinterpret_cast<uint32_t*>(
-      p.part + (size_t)(2 * kSMs + 1) * ((size_t)bands * bands + bands + 1));
   p.pixbits = workspace_bytes >= skyrx_stats_raw_workspace_for(lines, samples, bands)
-                  ? p.unit_clamp + kGrMaxUnitBits / 32
+                  ? reinterpret_cast<uint32_t*>(p.part + (size_t)(kSMs + fix_grid(bands) + 1) *
+                                                             ((size_t)bands * bands + bands + 1))
                   : nullptr;
   p.flags = flags;
   p.L = lines;

@@ -679,11 +679,42 @@ class TestDetect:
         assert normwise(det.stats.mu, exact.mu) < 1e-12
         check_detection(det, raw, t)
 
+    @pytest.mark.parametrize("S,B,L", [(64, 70, 700), (40, 33, 333)])
+    def test_clamp_marking_threshold_edges(self, P, S, B, L):
+        """The scan warps mark a pixel iff some count r has (float)r < dark, tested as
+        r < ceil(dark) on u16 pairs: integer and fractional darks at r = dark - 1, dark,
+        dark + 1, a dark <= 0 (never clamps) and a dark > 65535 (every count clamps),
+        in full and partial tiles, in box 0 and past byte 128.  calibrate.py:99."""
+        t = osynth.make_tables(48, S, B, 5)
+        dark = t.dark.copy()
+        raw = osynth.generate_lines(t, 0, L).copy()
+        dark[3, 2] = 100.0       # integer dark: 99 clamps, 100 and 101 do not
+        dark[5, B - 1] = 100.5   # fractional (the last band: past byte 128 when B > 64)
+        dark[7, 0] = 0.0
+        dark[8, 1] = -5.0
+        dark[9, B // 2] = 70000.0  # above every u16 count: the whole column clamps
+        raw[0:3, 3, 2] = (99, 100, 101)
+        raw[130:133, 5, B - 1] = (100, 101, 102)
+        raw[L - 1, 5, B - 1] = 7       # in the partial last tile
+        raw[200, 7, 0] = 0
+        raw[201, 8, 1] = 0
+        plan = P.DetectPlan(L, S, B)
+        det = P.detect(raw_cube(P, raw), P.CalibrationTables(dark, t.coeff), plan=plan)
+        assert int(plan.ds.flags[0].item()) & (4 | 256) == (4 | 256)
+        assert plan.used_raw[0]
+        exact = O.compute_stats_exact(raw, dark, t.coeff, np.ones(L))
+        assert normwise(det.stats.sigma, exact.sigma) < 1e-11
+        assert normwise(det.stats.mu, exact.mu) < 1e-12
+        rad = O.apply_calibration(raw, dark, t.coeff, np.ones(L))
+        assert rad[0, 3, 2] == 0.0 and rad[1, 3, 2] == 0.0 and rad[2, 3, 2] > 0.0
+        assert rad[130, 5, B - 1] == 0.0 and rad[131, 5, B - 1] > 0.0
+        assert (rad[:, 9, B // 2] == 0.0).all()
+
     @pytest.mark.parametrize("S,B,L", [(900, 70, 2100), (128, 128, 1100)])
     def test_dead_element_only(self, P, S, B, L):
         """One dead detector element (a whole (sample, band) column below dark) and nothing
         else: few units clamp, so the marking reads only the flagged units (the per-unit
-        form of clamp_mark_kernel); the corrected moments are exact."""
+        marking); the corrected moments are exact."""
         t = osynth.make_tables(47, S, B, 5)
         raw = osynth.generate_lines(t, 0, L).copy()
         raw[:, S // 2, B // 3] = 3
