@@ -29,6 +29,7 @@
 // needed: windows wider than 128 bytes add one M=128 x N=(NW-128) MMA for the
 // bottom-right block instead of a second full-width one.
 #include <algorithm>
+#include <type_traits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -127,71 +128,94 @@ __host__ __device__ constexpr int gr_nbuf() { return 2 * gr_bufcols<NCH>() <= 51
 __host__ __device__ constexpr int gr_nbuf() { return 1; }
 #endif
 
-// The scan of one FULL tile (128 lines) by one thread of box 0 (BOX1 = false) or of the
-// second box: trip counts and line steps are compile-time, and the thread's 8..16 shared
-// loads go out in one or two batches instead of a loop whose runtime trip count cost a
-// division per tile and one shared-memory latency per four lines.  The scan warps sit on
-// the stage-release path (a stage is freed by the MMA commit AND the 128 scan arrivals), so
-// their per-tile latency is kernel time.  lw: the warp's index within its box's scanners.
 // below(v, th): some halfword of v is below its threshold (max(v, t) != v)
 __device__ __forceinline__ uint32_t gr_below(const uint4& v, const uint32_t (&th)[4]) {
   return (__vmaxu2(v.x, th[0]) ^ v.x) | (__vmaxu2(v.y, th[1]) ^ v.y) |
          (__vmaxu2(v.z, th[2]) ^ v.z) | (__vmaxu2(v.w, th[3]) ^ v.w);
 }
-// marking: when the minima say this thread's lines hold a value below dark, the lines are
-// tested one by one from the registers they are still in, and mark(l) is called for each hit
-template <int NCH, bool BOX1, bool SUMS, class Mark>
-__device__ __forceinline__ void gr_scan_full(uint32_t atom, int lane, int lw, uint32_t (&tm)[4],
-                                             uint32_t (&sm8)[8], bool marking,
-                                             const uint32_t (&th)[4], uint32_t always,
-                                             Mark&& mark) {
-  constexpr uint32_t W2B = gr_w2b<NCH>();
-  constexpr int W0 = NCH > 8 ? (W2B == 32 ? 3 : 2) : 4;
-  constexpr int NQ1 = W2B > 0 ? (int)W2B / 16 : 1;
-  constexpr int LPW = BOX1 ? 32 / NQ1 : 4;
-  constexpr int LSTEP = LPW * (BOX1 ? 4 - W0 : W0);
-  constexpr uint32_t WDT = BOX1 ? W2B : 128u;
-  constexpr int NITF = kGrLb / LSTEP, REM = kGrLb - NITF * LSTEP;
-#ifndef GRX_SCAN_NB
-#define GRX_SCAN_NB 11
-#endif
-  constexpr int NB = NITF > GRX_SCAN_NB ? (NITF + 1) / 2 : NITF;  // loads in flight per batch
-  const int q = BOX1 ? lane % NQ1 : lane & 7;
-  const int l0 = (BOX1 ? lane / NQ1 : lane >> 3) + LPW * lw;
-  auto ld = [&](int l) {
-    const uint32_t sw = ((uint32_t)l * WDT >> 7) & (WDT / 16 - 1);
-    return ld_shared_v4(atom + l * WDT + ((q ^ sw) << 4));
-  };
-  auto acc = [&](const uint4& v) {
-    tm[0] = __vminu2(tm[0], v.x), tm[1] = __vminu2(tm[1], v.y);
-    tm[2] = __vminu2(tm[2], v.z), tm[3] = __vminu2(tm[3], v.w);
-    if (SUMS) {
-      sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu;
-      sm8[3] += v.y >> 16, sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16;
-      sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
-    }
-  };
-  uint4 vr = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-  const bool tail = REM > 0 && l0 < REM;  // lines 128 - REM ..: the first REM threads' extra line
-  if (tail) vr = ld(l0 + NITF * LSTEP);
+
+// One scan thread's state for one 16-byte chunk of the window: running minima, column sums
+// (windows whose sums do not come from the tensor core), clamp thresholds.
+struct GrChunkScan {
+  uint32_t tm[4];   // min(th, every count so far): differs from th once a count is below it
+  uint32_t sm[8];   // column sums
+  uint32_t th[4];   // r < th: the count calibrates to 0 (r < ceil(dark)); 0: never
+  uint32_t always;  // a dark above every u16 count
+  uint32_t hit;     // the unit held a value below dark in this chunk
+};
+
+// The scan of NL lines of one chunk, all loads in flight at once: line j of the thread sits
+// at addr + j * STRIDE (the thread's lines share their swizzle phase, so the offsets are
+// immediates).  The scan warps sit on the stage-release path (a stage is freed by the MMA
+// commit AND the 128 scan arrivals), so their instruction count per tile is kernel time:
+// the round-2 loop (runtime trip count: a division per tile, an address computation and a
+// shared-memory latency per four lines) cost 7 % of the kernel.  The running minima start
+// at the clamp thresholds, so "a count below its dark" is four XORs per tile (tm != th);
+// then gr_mark_chunk tests the thread's lines one by one.
+// The rare path, out of line so that it costs the scan loop no registers: the thread's lines
+// (still in shared memory) are tested one by one and the pixels holding a value below dark
+// get their bit.  pix0: pixel index of the tile's line 0 at this sample.
+template <int NL, uint32_t STRIDE>
+__device__ __noinline__ void gr_mark_chunk(uint32_t addr, int line0, int lstep, int valid,
+                                           uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                           uint32_t always, int64_t pix0, int S,
+                                           uint32_t* __restrict__ pixbits) {
+  const uint32_t th[4] = {t0, t1, t2, t3};
+  uint4 v[NL];
 #pragma unroll
-  for (int i0 = 0; i0 < NITF; i0 += NB) {
-    uint4 v[NB];
+  for (int j = 0; j < NL; ++j) {
+    v[j] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (line0 + j * lstep < valid) v[j] = ld_shared_v4(addr + j * STRIDE);
+  }
 #pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (i0 + j < NITF) v[j] = ld(l0 + (i0 + j) * LSTEP);
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (i0 + j < NITF) acc(v[j]);
-    if (i0 + NB >= NITF && tail) acc(vr);
-    const uint4 tmv = make_uint4(tm[0], tm[1], tm[2], tm[3]);
-    if (marking && (always | gr_below(tmv, th))) {  // rare
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (i0 + j < NITF && (always | gr_below(v[j], th))) mark(l0 + (i0 + j) * LSTEP);
-      if (i0 + NB >= NITF && tail && (always | gr_below(vr, th))) mark(l0 + NITF * LSTEP);
+  for (int j = 0; j < NL; ++j) {
+    if (line0 + j * lstep < valid && (always | gr_below(v[j], th))) {
+      const int64_t pix = pix0 + (int64_t)(line0 + j * lstep) * S;
+      atomicOr(pixbits + (pix >> 5), 1u << (pix & 31));
     }
   }
+}
+
+// the three steps of a chunk's scan, separate so that a thread's two chunks (box 0 and the
+// second box) have all their loads in flight before either is reduced or tested: one
+// shared-memory latency per tile instead of two
+template <int NL, uint32_t STRIDE, bool FULL>
+__device__ __forceinline__ void gr_scan_load(uint4 (&v)[NL], uint32_t addr, int line0, int lstep,
+                                             int valid) {
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    v[j] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (FULL || line0 + j * lstep < valid) v[j] = ld_shared_v4(addr + j * STRIDE);
+  }
+}
+template <int NL, bool SUMS, bool FULL>
+__device__ __forceinline__ void gr_scan_acc(GrChunkScan& c, const uint4 (&v)[NL], int line0,
+                                            int lstep, int valid) {
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    c.tm[0] = __vminu2(c.tm[0], v[j].x), c.tm[1] = __vminu2(c.tm[1], v[j].y);
+    c.tm[2] = __vminu2(c.tm[2], v[j].z), c.tm[3] = __vminu2(c.tm[3], v[j].w);
+    if (SUMS && (FULL || line0 + j * lstep < valid)) {
+      c.sm[0] += v[j].x & 0xffffu, c.sm[1] += v[j].x >> 16, c.sm[2] += v[j].y & 0xffffu;
+      c.sm[3] += v[j].y >> 16, c.sm[4] += v[j].z & 0xffffu, c.sm[5] += v[j].z >> 16;
+      c.sm[6] += v[j].w & 0xffffu, c.sm[7] += v[j].w >> 16;
+    }
+  }
+}
+__device__ __forceinline__ uint32_t gr_scan_test(const GrChunkScan& c) {
+  return c.always | (c.tm[0] ^ c.th[0]) | (c.tm[1] ^ c.th[1]) | (c.tm[2] ^ c.th[2]) |
+         (c.tm[3] ^ c.th[3]);
+}
+template <int NL, uint32_t STRIDE>
+__device__ __forceinline__ void gr_scan_hit(GrChunkScan& c, uint32_t addr, int line0, int lstep,
+                                            int valid, uint32_t* pixbits, int64_t pix0, int S) {
+  if (pixbits != nullptr)
+    gr_mark_chunk<NL, STRIDE>(addr, line0, lstep, valid, c.th[0], c.th[1], c.th[2], c.th[3],
+                              c.always, pix0, S, pixbits);
+  // the minima start afresh, so that later clean tiles skip the per-line test
+  c.hit = 1u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c.tm[i] = c.th[i];
 }
 
 template <int NCH>
@@ -210,10 +234,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   constexpr uint32_t ATOM1 = TWO_M ? kGrLb * W2B : 0u;
   constexpr uint32_t STAGE = ATOM + ATOM1;
   constexpr uint32_t LT1 = W2B == 32 ? 6u : (W2B == 64 ? 4u : 2u);
-  // scan mapping (conflict-free 128-bit shared loads): each thread owns one logical 16-B
-  // chunk of the window; a quarter-warp reads 128 contiguous bytes (one 128-B line of box 0,
-  // or 128/W2B lines of box 1). W0 warps scan box 0, the other 4 - W0 scan box 1.
-  constexpr int W0 = TWO_M ? (W2B == 32 ? 3 : 2) : 4;
+  // NQ1: 16-byte chunks per line of the second box
   constexpr int NQ1 = W2B > 0 ? (int)W2B / 16 : 1;
   constexpr int BUFC = gr_bufcols<NCH>();
   constexpr bool ONES = gr_ones<NCH>();
@@ -230,8 +251,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
   double* sacc = qacc + B * B;
   uint8_t* ones = reinterpret_cast<uint8_t*>(sacc + B);      // ONES: [128 lines][32 B] of 1
   uint32_t* smin = reinterpret_cast<uint32_t*>(ones + (ONES ? kGrLb * 32 : 0));  // [thread][4]
-  uint32_t* ssum = smin + kGrWorkers * 4;                    // [scan thread][8]
-  uint32_t* minv = ssum + kGrWorkers * 8;                    // [2][NCH*8]
+  uint32_t* ssum = smin + kGrWorkers * 4;                    // [scan thread][8] (not ONES)
+  uint32_t* smin1 = ssum + (ONES ? 0 : kGrWorkers * 8);      // the same for the second box
+  uint32_t* ssum1 = smin1 + (TWO_M ? kGrWorkers * 4 : 0);
+  uint32_t* minv = ssum1 + (TWO_M && !ONES ? kGrWorkers * 8 : 0);  // [2][NCH*8]
   uint32_t* sumv = minv + 2 * NCH * 8;                       // [2][NCH*8]
   double* bandC = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(sumv + 2 * NCH * 8) + 7) & ~uintptr_t(7));  // [B] per unit
@@ -387,126 +410,138 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
     }
   } else if (warp < 4) {  // ---------------------------------------------- scan
-    const int lane = tid & 31;
-    const bool box1 = warp >= W0;
-    const int q = box1 ? lane % NQ1 : lane & 7;            // logical chunk within the box
-    const int c = box1 ? 8 + q : q;                        // chunk of the window
-    const int lr = box1 ? lane / NQ1 : lane >> 3;          // line within a warp step
-    const int lpw = box1 ? 32 / NQ1 : 4;                   // lines per warp step
-    const int lw = box1 ? warp - W0 : warp;
-    const int lstep = lpw * (box1 ? 4 - W0 : W0);
-    const uint32_t wdt = box1 ? W2B : 128u;
-    const bool scanner = c < NCH;
-#ifndef GRX_NO_MARK
-    const bool marking = p.pixbits != nullptr;
-#else  // timing experiment: the scan without the clamp marking
-    const bool marking = false;
-#endif
+    // every thread scans one chunk of box 0 (chunk tid & 7, lines (tid >> 3) + 16 j, j < 8)
+    // and one of the second box (chunk 8 + tid % NQ1, lines tid / NQ1 + (128 / NQ1) j,
+    // j < NQ1): a quarter-warp reads 128 contiguous bytes (conflict-free), and a thread's
+    // lines share their swizzle phase, so their addresses differ by immediates
+    const int q0 = tid & 7, ls0 = tid >> 3;
+    const int q1 = tid % NQ1, ls1 = tid / NQ1;
+    constexpr int LSTEP1 = kGrLb / NQ1;
+    const uint32_t off0 = ls0 * 128u + ((uint32_t)(q0 ^ (ls0 & 7)) << 4);
+    const uint32_t off1 =
+        ATOM + ls1 * W2B + ((uint32_t)(q1 ^ (int)(((uint32_t)ls1 * W2B >> 7) & (NQ1 - 1))) << 4);
+    const bool scan0 = q0 < NCH;
+    const bool scan1 = TWO_M && 8 + q1 < NCH;
+    uint32_t* const pixbits = p.pixbits;  // null: no room for the bitmap, detection only
+    // dark levels of a chunk's 8 window halfwords at sample s (0 outside the sample's bands):
+    // a count r calibrates to 0 iff (float)r < dark, i.e. r < ceil(dark) (never for
+    // dark <= 0 or NaN; always for dark > 65535).  Fetched one unit ahead, before the
+    // per-unit reduction, so that the loads' latency is off the first tile's scan
+    auto fetch_dark = [&](float (&dk)[8], int s, int chunk, bool on) {
+      const int off2 = (int)((((int64_t)s * B * 2) & 15) >> 1);
+      const float* drow = p.dark + (int64_t)s * B;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = 8 * chunk + i - off2;
+        dk[i] = (on && b >= 0 && b < B) ? __ldg(drow + b) : 0.0f;
+      }
+    };
+    float dk0[8], dk1[8];
+    if (u0 < u1) {
+      int s;
+      int64_t l0, nl;
+      unit_geom(u0, s, l0, nl);
+      fetch_dark(dk0, s, q0, scan0);
+      if (TWO_M) fetch_dark(dk1, s, 8 + q1, scan1);
+    }
     int t = 0, unit = 0;
     for (int64_t u = u0; u < u1; u += ustep, ++unit) {
       int s;
       int64_t l0, nl;
       unit_geom(u, s, l0, nl);
       const int ntile = (int)((nl + kGrLb - 1) / kGrLb);
-      uint32_t mn[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-      uint32_t sm8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      // clamp thresholds of this thread's 8 window halfwords: a count r calibrates to 0
-      // iff (float)r < dark, i.e. r < ceil(dark) (never for dark <= 0 or NaN; always for
-      // dark > 65535); halfwords outside the sample's bands get 0
-      uint32_t th[4] = {0u, 0u, 0u, 0u};
-      uint32_t always = 0u;
-      if (marking && scanner) {
-        const int off2 = (int)((((int64_t)s * B * 2) & 15) >> 1);
-        const float* drow = p.dark + (int64_t)s * B;
+      const int last_valid = (int)(nl - (int64_t)(ntile - 1) * kGrLb);  // lines of the last tile
+      GrChunkScan c0, c1;
+      auto begin = [&](GrChunkScan& c, const float (&dk)[8]) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.th[i] = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c.sm[i] = 0u;
+        c.always = 0u, c.hit = 0u;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int b = 8 * c + i - off2;
           uint32_t t16 = 0u;
-          if (b >= 0 && b < B) {
-            const float dk = __ldg(drow + b);
-            if (dk > 65535.0f) always = 1u;
-            else if (dk > 0.0f) t16 = (uint32_t)ceilf(dk);
-          }
-          th[i >> 1] |= t16 << (16 * (i & 1));
+          if (dk[i] > 65535.0f) c.always = 1u;
+          else if (dk[i] > 0.0f) t16 = (uint32_t)ceilf(dk[i]);
+          c.th[i >> 1] |= t16 << (16 * (i & 1));
         }
-      }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.tm[i] = c.th[i];
+      };
+      begin(c0, dk0);
+      if (TWO_M) begin(c1, dk1);
       for (int k = 0; k < ntile; ++k, ++t) {
         const int st = t % kGrStages;
         if (tid == 0) GR_PW(3, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
         else mbar_wait(full32 + 8 * st, (t / kGrStages) & 1);
-#ifdef GRX_NO_SCAN
-        if (false) {
-#else
-        if (scanner) {
-#endif
-          const int valid = (int)(nl - (int64_t)k * kGrLb < kGrLb ? nl - (int64_t)k * kGrLb : kGrLb);
-          // 16-B chunk q of line l sits at chunk q ^ ((l * width) >> 7 & (width/16 - 1))
-          const uint32_t atom = stages32 + st * STAGE + (box1 ? ATOM : 0u);
-          uint32_t tm[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};  // tile minima
-          auto mark_line = [&](int l) {
-            const int64_t pix = (l0 + (int64_t)k * kGrLb + l) * p.S + s;
-            atomicOr(p.pixbits + (pix >> 5), 1u << (pix & 31));
+#ifndef GRX_NO_SCAN
+        {
+          const int valid = k == ntile - 1 ? last_valid : kGrLb;
+          const uint32_t base = stages32 + st * STAGE;
+          auto scan_tile = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            uint4 v0[8], v1[NQ1];
+            if (scan0) gr_scan_load<8, 2048u, FULL>(v0, base + off0, ls0, 16, valid);
+            if (TWO_M && scan1) gr_scan_load<NQ1, 2048u, FULL>(v1, base + off1, ls1, LSTEP1, valid);
+            if (scan0) gr_scan_acc<8, !ONES, FULL>(c0, v0, ls0, 16, valid);
+            if (TWO_M && scan1) gr_scan_acc<NQ1, !ONES, FULL>(c1, v1, ls1, LSTEP1, valid);
           };
-          const bool full_tile = valid == kGrLb;
-          if (full_tile) {
-            if (box1) {
-              if constexpr (TWO_M)
-                gr_scan_full<NCH, true, !ONES>(atom, lane, lw, tm, sm8, marking, th, always,
-                                               mark_line);
-            } else {
-              gr_scan_full<NCH, false, !ONES>(atom, lane, lw, tm, sm8, marking, th, always,
-                                              mark_line);
-            }
-          } else
-#pragma unroll 4
-          for (int l = lr + lpw * lw; l < valid; l += lstep) {
-            const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
-            const uint4 v = ld_shared_v4(atom + l * wdt + ((q ^ sw) << 4));
-            tm[0] = __vminu2(tm[0], v.x), tm[1] = __vminu2(tm[1], v.y);
-            tm[2] = __vminu2(tm[2], v.z), tm[3] = __vminu2(tm[3], v.w);
-            if (!ONES) {  // (ONES: the column sums come from the tensor core)
-              sm8[0] += v.x & 0xffffu, sm8[1] += v.x >> 16, sm8[2] += v.y & 0xffffu;
-              sm8[3] += v.y >> 16, sm8[4] += v.z & 0xffffu, sm8[5] += v.z >> 16;
-              sm8[6] += v.w & 0xffffu, sm8[7] += v.w >> 16;
-            }
+          if (valid == kGrLb) scan_tile(std::true_type{});
+          else scan_tile(std::false_type{});
+          // a count below its dark (rare): its pixels are marked for clamp_fix_kernel
+          const uint32_t x0 = scan0 ? gr_scan_test(c0) : 0u;
+          const uint32_t x1 = (TWO_M && scan1) ? gr_scan_test(c1) : 0u;
+          if (x0 | x1) {
+            const int64_t pix0 = (l0 + (int64_t)k * kGrLb) * p.S + s;
+            if (x0) gr_scan_hit<8, 2048u>(c0, base + off0, ls0, 16, valid, pixbits, pix0, p.S);
+            if (TWO_M && x1)
+              gr_scan_hit<NQ1, 2048u>(c1, base + off1, ls1, LSTEP1, valid, pixbits, pix0, p.S);
           }
-          // a minimum below its threshold: this thread's part of the tile holds a value
-          // below dark; its pixels are marked here for clamp_fix_kernel, so no second pass
-          // over the cube is needed
-          // (a partial tile: rescanned from shared memory, where it still is)
-          if (marking && !full_tile &&
-              (always | gr_below(make_uint4(tm[0], tm[1], tm[2], tm[3]), th))) {
-            for (int l = lr + lpw * lw; l < valid; l += lstep) {
-              const uint32_t sw = ((uint32_t)l * wdt >> 7) & (wdt / 16 - 1);
-              const uint4 v = ld_shared_v4(atom + l * wdt + ((q ^ sw) << 4));
-              if (always | gr_below(v, th)) mark_line(l);
-            }
-          }
-          mn[0] = __vminu2(mn[0], tm[0]), mn[1] = __vminu2(mn[1], tm[1]);
-          mn[2] = __vminu2(mn[2], tm[2]), mn[3] = __vminu2(mn[3], tm[3]);
         }
+#endif
         mbar_arrive(empty32 + 8 * st);
       }
-      // per-unit reduction of the scans (fixed member order per chunk) into buffer ub
-      for (int i = 0; i < 4; ++i) smin[tid * 4 + i] = mn[i];
-      for (int i = 0; i < 8; ++i) ssum[tid * 8 + i] = sm8[i];
+      if (u + ustep < u1) {  // the next unit's dark levels, in flight during the reduction
+        int sn;
+        int64_t l0n, nln;
+        unit_geom(u + ustep, sn, l0n, nln);
+        fetch_dark(dk0, sn, q0, scan0);
+        if (TWO_M) fetch_dark(dk1, sn, 8 + q1, scan1);
+      }
+      // per-unit reduction of the scans (fixed member order per chunk) into buffer ub; a
+      // chunk that held a value below dark publishes minima of 0 (below any dark that can
+      // clamp), the others 0xffff
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        smin[tid * 4 + i] = c0.hit ? 0u : 0xffffffffu;
+        if (TWO_M) smin1[tid * 4 + i] = c1.hit ? 0u : 0xffffffffu;
+      }
+      if (!ONES) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          ssum[tid * 8 + i] = c0.sm[i];
+          if (TWO_M) ssum1[tid * 8 + i] = c1.sm[i];
+        }
+      }
       const int ub = unit & 1;
       mbar_wait(&scan_empty[ub], ((unit >> 1) & 1) ^ 1);
       asm volatile("bar.sync 1, %0;" ::"n"(kGrWorkers) : "memory");
       if (tid < NCH * 8) {
         const int cc = tid >> 3, qq = tid & 7;
-        // members of chunk cc: box 0 -> threads cc + 8m (m < 4 W0); box 1 -> threads
-        // 32 W0 + (cc - 8) + NQ1 m (m < 32 (4 - W0) / NQ1)
+        // members of chunk cc: box 0 -> threads cc + 8 m (m < 16); second box -> threads
+        // (cc - 8) + NQ1 m (m < 128 / NQ1)
         const bool b1 = cc >= 8;
-        const int first = b1 ? 32 * W0 + (cc - 8) : cc;
+        const uint32_t* pm = b1 ? smin1 : smin;
+        const uint32_t* ps = b1 ? ssum1 : ssum;
+        const int first = b1 ? cc - 8 : cc;
         const int stride = b1 ? NQ1 : 8;
-        const int nmem = b1 ? 32 * (4 - W0) / NQ1 : 4 * W0;
+        const int nmem = b1 ? kGrWorkers / NQ1 : kGrWorkers / 8;
         uint32_t mv = 0xffffu, sv = 0;
         for (int m = 0; m < nmem; ++m) {
           const int mt = first + stride * m;
-          const uint32_t w = smin[mt * 4 + (qq >> 1)];
+          const uint32_t w = pm[mt * 4 + (qq >> 1)];
           mv = min(mv, (qq & 1) ? (w >> 16) : (w & 0xffffu));
-          sv += ssum[mt * 8 + qq];
+          if (!ONES) sv += ps[mt * 8 + qq];
         }
         minv[ub * NCH * 8 + tid] = mv;
         sumv[ub * NCH * 8 + tid] = sv;
@@ -975,7 +1010,7 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
   const size_t qbytes = 0;
 #endif
   const size_t smem = kGrStages * (size_t)STAGE + qbytes +
-                      (size_t)kGrWorkers * 12 * 4 + NCH * 8 * 16 + 3 * (size_t)p.B * 8 +
+                      (size_t)kGrWorkers * 16 * (NCH > 8 ? 2 : 1) * (gr_ones<NCH>() ? 1 : 3) + NCH * 8 * 16 + 3 * (size_t)p.B * 8 +
                       (gr_ones<NCH>() ? kGrLb * 32 : 0) +
                       16 * 8 + 1024;
   int grid = kSMs;
