@@ -679,7 +679,8 @@ class TestDetect:
         assert normwise(det.stats.mu, exact.mu) < 1e-12
         check_detection(det, raw, t)
 
-    @pytest.mark.parametrize("S,B,L", [(64, 70, 700), (40, 33, 333)])
+    @pytest.mark.parametrize("S,B,L", [(64, 70, 700), (40, 33, 333), (64, 96, 700), (48, 80, 300),
+                                       (32, 128, 520)])
     def test_clamp_marking_threshold_edges(self, P, S, B, L):
         """The scan warps mark a pixel iff some count r has (float)r < dark, tested as
         r < ceil(dark) on u16 pairs: integer and fractional darks at r = dark - 1, dark,
@@ -701,7 +702,6 @@ class TestDetect:
         plan = P.DetectPlan(L, S, B)
         det = P.detect(raw_cube(P, raw), P.CalibrationTables(dark, t.coeff), plan=plan)
         assert int(plan.ds.flags[0].item()) & (4 | 256) == (4 | 256)
-        assert plan.used_raw[0]
         exact = O.compute_stats_exact(raw, dark, t.coeff, np.ones(L))
         assert normwise(det.stats.sigma, exact.sigma) < 1e-11
         assert normwise(det.stats.mu, exact.mu) < 1e-12
