@@ -127,10 +127,11 @@ int skyrx_stats_tc_f32(const float* pixels, int64_t lines, int32_t samples, int3
  * samples*bands*2 % 16 == 0): exact integer byte Grams per sample column
  * (tcgen05 kind::i8, TMA-fed), calibration applied per sample in f64.  Same
  * [n, s, Q] moments about `shift`; flags |= 4 if any value clamps at 0.  For
- * windows <= 256 bytes (B <= 127) the clamped pixels are then corrected exactly
- * in the same call (a re-scan of the flagged units only) and flags |= 256: the
- * moments are final (finalize accepts 4 with 256).  Wider windows (B > 127) leave
- * 4 without 256: the caller recomputes with another path.  workspace >=
+ * windows <= 256 bytes (B <= 128) the clamped pixels are then corrected exactly
+ * in the same call (the moments kernel marks them while their tile is on chip,
+ * a sparse kernel adds their corrections) and flags |= 256: the moments are
+ * final (finalize accepts 4 with 256).  Wider windows (B > 128) leave 4
+ * without 256: the caller recomputes with another path.  workspace >=
  * skyrx_stats_raw_workspace(bands) (>= skyrx_stats_raw_workspace_for(L, S, B) for the
  * clamp correction). */
 int skyrx_stats_raw_supported(int64_t lines, int32_t samples, int32_t bands, const void* raw);
