@@ -64,11 +64,15 @@ __device__ unsigned long long gr_prof[160][12];
 #ifndef GRX_EPI_GROUPS
 #define GRX_EPI_GROUPS 3
 #endif
-constexpr int kGrEpiGroups = GRX_EPI_GROUPS;
+constexpr int kGrEpiGroups = GRX_EPI_GROUPS;  // default; long units of the c4 shape take 2
 constexpr int kGrWorkers = 128;   // scan threads (warps 0-3)
-constexpr int kGrEpi = 128 * kGrEpiGroups;  // epilogue threads (warps 4..)
-constexpr int kGrTmaWarp = (kGrWorkers + kGrEpi) / 32, kGrMmaWarp = kGrTmaWarp + 1;
-constexpr int kGrThreads = kGrWorkers + kGrEpi + 64;
+// EG epilogue groups: epilogue threads (warps 4..), then the TMA and MMA warps
+constexpr int gr_epi(int eg) { return 128 * eg; }
+constexpr int gr_threads(int eg) { return kGrWorkers + gr_epi(eg) + 64; }
+// MMA issue form: -1 = per window class (below), 0 = lane 0 alone, 1 = whole warp + elected lane
+#ifndef GRX_ELECT_MODE
+#define GRX_ELECT_MODE -1
+#endif
 constexpr int kGrLb = 128;        // lines per tile (4 x K=32)
 // TMA ring depth (stage = 128 lines x (128 + second-box) bytes) within the shared memory
 // left beside the f64 accumulator: 8 stages, 5 for windows > 160 B, 2 for > 192 B
@@ -220,11 +224,13 @@ __device__ __forceinline__ void gr_scan_hit(GrChunkScan& c, uint32_t addr, int l
   for (int i = 0; i < 4; ++i) c.tm[i] = c.th[i];
 }
 
-template <int NCH>
-__global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
+template <int NCH, int EG = kGrEpiGroups>
+__global__ void __launch_bounds__(gr_threads(EG), 1) gram_raw_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                  const __grid_constant__ CUtensorMap tmap1,
                                                                  GramRawParams p) {
   constexpr int kGrStages = gr_stages<NCH>();
+  constexpr int kGrEpi = gr_epi(EG);
+  constexpr int kGrTmaWarp = (kGrWorkers + kGrEpi) / 32, kGrMmaWarp = kGrTmaWarp + 1;
   constexpr int NW = 16 * NCH;                    // window bytes = MMA N
   constexpr bool TWO_M = NCH > 8;                 // rows 128.. need a second M=128 MMA
   constexpr int N2 = TWO_M ? NW - 128 : 0;        // ... only over columns 128..NW-1
@@ -343,13 +349,14 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
       }
     }
   } else if (warp == kGrMmaWarp) {
-#ifndef GRX_ELECT_ISSUE  // lane 0 issues: 0.537 vs 0.563 ms per c4 strip for the
-    // warp-converged / elected-lane form (tools/time_gr_libs.py, round 2): the slower issue
-    // spaces the MMAs' shared-memory operand reads out against the scan warps' loads
-    if ((tid & 31) == 0) {
-#else
-    {  // --------------------------------- MMA issuer (whole warp, one elected lane issues)
-#endif
+    // ------------------------------------------------------------------- MMA issuer
+    // Two issue forms, chosen per window class by measurement (tools/time_gr_direct.py,
+    // session 6, after the scan rewrite): the whole warp converged with one elected lane
+    // issuing is faster for the three-MMA ONES windows (c4 strip 0.487 -> 0.442 ms), lane 0
+    // alone for the others (B = 40 / 96 / 128: 0.390 / 0.558 / 1.015 against 0.400 / 0.610 /
+    // 1.042 ms).  (Before the scan rewrite lane 0 was faster for the c4 shape too.)
+    constexpr bool ELECT = GRX_ELECT_MODE < 0 ? ONES : (GRX_ELECT_MODE != 0);
+    if (ELECT || (tid & 31) == 0) {
       constexpr uint32_t id = idesc_u8_s32(128, TWO_M ? 128 : NW);
       constexpr uint32_t id2 = idesc_u8_s32(128, ONES ? 64 : (N2 > 0 ? N2 : 16));
       int t = 0, unit = 0;
@@ -368,11 +375,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           GR_PW(2, mbar_wait(full32 + 8 * st, (t / kGrStages) & 1));
           tc_fence_after();
           const uint8_t* base = stages + st * STAGE;
-#ifndef GRX_ELECT_ISSUE
-          if (true) {
-#else
-          if (elect_one()) {
-#endif
+          if (!ELECT || elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kGrLb / 32; ++ks) {
             const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
@@ -400,15 +403,10 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           }
           mma_commit(&empty[st]);
           }
-#ifndef GRX_ELECT_ISSUE
+          if (ELECT) __syncwarp();
         }
-        mma_commit(&acc_full[buf]);
-#else
-          __syncwarp();
-        }
-        if (elect_one()) mma_commit(&acc_full[buf]);
-        __syncwarp();
-#endif
+        if (!ELECT || elect_one()) mma_commit(&acc_full[buf]);
+        if (ELECT) __syncwarp();
       }
     }
   } else if (warp < 4) {  // ---------------------------------------------- scan
@@ -637,7 +635,7 @@ __global__ void __launch_bounds__(kGrThreads, 1) gram_raw_kernel(const __grid_co
           return cc < NCH && (cc * 16 <= cmax || (part == 0 && TWO_M && cc >= 8));
         };
         // two chunks per TMEM wait: the loads queue behind the next unit's MMAs
-        for (int cc = cc0 + 2 * eg; cc < NCH; cc += 2 * kGrEpiGroups) {
+        for (int cc = cc0 + 2 * eg; cc < NCH; cc += 2 * EG) {
           const bool n0 = needed(cc), n1 = needed(cc + 1);
           if (!n0 && !n1) continue;
           uint32_t v2[32];
@@ -989,7 +987,7 @@ static int nch_for(int B) {
   return (maxoff + 2 * B + 15) / 16;
 }
 
-template <int NCH>
+template <int NCH, int EG = kGrEpiGroups>
 static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawParams p,
                            double* moments, double* shift, int own, cudaStream_t st) {
   constexpr uint32_t W2B = gr_w2b<NCH>();
@@ -1041,12 +1039,12 @@ static int launch_gram_raw(const CUtensorMap& map, const uint16_t* raw, GramRawP
       }
     }
   }
-  cudaFuncSetAttribute(gram_raw_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gram_raw_kernel<NCH, EG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   // the scan warps mark every pixel holding a value below dark while its tile is on chip
   if (p.pixbits != nullptr)
     cudaMemsetAsync(p.pixbits, 0, (size_t)((p.L * p.S + 31) / 32) * 4, st);
-  gram_raw_kernel<NCH><<<grid, kGrThreads, smem, st>>>(map, map1, p);
+  gram_raw_kernel<NCH, EG><<<grid, gr_threads(EG), smem, st>>>(map, map1, p);
   SKYRX_CHECK_LAUNCH("gram_raw_kernel");
   // exact corrections of the clamped pixels (no-op passes when nothing clamped)
   const int fgrid = fix_grid(p.B);
@@ -1137,6 +1135,13 @@ static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, i
   p.nsplit = (int)((lines + p.split_lines - 1) / p.split_lines);
   p.units = (int64_t)samples * p.nsplit;
   cudaStream_t st = as_stream(stream);
+  // long units of the three-MMA windows: two epilogue groups are enough and leave the scan
+  // warps more issue slots (c4 strip 0.442 -> 0.435 ms); short units (c1, c2 chunks) are
+  // epilogue-bound and keep three
+  if (kGrEpiGroups == 3 && p.split_lines >= 32 * kGrLb) {
+    if (nch == 9) return launch_gram_raw<9, 2>(map, raw, p, moments, shift, own, st);
+    if (nch == 10) return launch_gram_raw<10, 2>(map, raw, p, moments, shift, own, st);
+  }
   switch (nch) {
 #define SKYRX_NCH(k) \
   case k:            \

@@ -3,12 +3,14 @@ compare its moments with the first library's (tools/build_gr_var.sh builds varia
   python tools/time_gr_direct.py [--bands B] lib0.so lib1.so ..."""
 import os, sys, json, subprocess
 args = sys.argv[1:]
-bands = 70
-if args and args[0] == "--bands":
-    bands = int(args[1]); args = args[2:]
+bands, lines = 70, 16384
+while args and args[0] in ("--bands", "--lines"):
+    if args[0] == "--bands": bands = int(args[1])
+    else: lines = int(args[1])
+    args = args[2:]
 if len(args) > 1:
     for l in args:
-        subprocess.run([sys.executable, __file__, "--bands", str(bands), l])
+        subprocess.run([sys.executable, __file__, "--bands", str(bands), "--lines", str(lines), l])
     sys.exit(0)
 import numpy as np, torch
 sys.path.insert(0, '.')
@@ -16,7 +18,7 @@ from paper_2602_13509_b200 import _lib
 _lib.load(args[0])
 import paper_2602_13509_b200 as P
 from paper_2602_13509_b200.synth import Scene
-L, S, B = 16384, 900, bands
+L, S, B = lines, 900, bands
 if (S * B * 2) % 16: S = 904
 sc = Scene(4000, S, B, 5)
 raws = [sc.generate(i, L) for i in range(4)]   # 4 strips: 8 GB cycled, larger than L2
@@ -39,7 +41,7 @@ a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 a.record()
 for i in range(20): fn(i)
 b.record(); torch.cuda.synchronize()
-ref = f"gpurun_out/gr_direct_ref_{B}.npy"
+ref = f"gpurun_out/gr_direct_ref_{B}_{L}.npy"
 os.makedirs("gpurun_out", exist_ok=True)
 if not os.path.exists(ref):
     np.save(ref, m0); rel = None
@@ -47,5 +49,5 @@ else:
     r = np.load(ref); rel = float(np.abs(m0 - r).max() / np.abs(r).max())
     nz = np.abs(r) > 0
     relel = float((np.abs(m0 - r)[nz] / np.abs(r)[nz]).max())
-print(json.dumps({"lib": args[0], "bands": B, "ms": a.elapsed_time(b) / 20, "flags": f0,
+print(json.dumps({"lib": args[0], "bands": B, "lines": L, "ms": a.elapsed_time(b) / 20, "flags": f0,
                   "rel_vs_first": rel, "rel_elementwise": None if rel is None else relel}), flush=True)
