@@ -838,11 +838,19 @@ __global__ void gram_raw_center_kernel(const double* __restrict__ tot, int B,
 //                     partial, joined to the Gram partials in gram_raw_sum_kernel's
 //                     fixed-order sum.
 constexpr int kFixThreads = 256;
-constexpr int kFixBatch = 16;  // clamped pixels staged per round
+#ifndef GRX_FIX_BATCH
+#define GRX_FIX_BATCH 16
+#endif
+#ifndef GRX_FIX_PER_SM
+#define GRX_FIX_PER_SM 5
+#endif
+constexpr int kFixBatch = GRX_FIX_BATCH;  // clamped pixels staged per round
 // clamp_fix CTAs: the per-pixel chain (one barrier per clamped pixel, B threads busy) is
-// latency-bound, so four co-resident CTAs per SM walk a quarter of the bitmap range each
+// latency-bound, so five co-resident CTAs per SM (what shared memory allows) walk a fifth of the bitmap range each
 // (0.01 % sub-dark c4 strip: 404 us with one CTA per SM)
-static inline int fix_grid(int B) { return B <= 80 ? 4 * kSMs : (B <= 128 ? 2 * kSMs : kSMs); }
+static inline int fix_grid(int B) {
+  return B <= 80 ? GRX_FIX_PER_SM * kSMs : (B <= 128 ? 2 * kSMs : kSMs);
+}
 
 __global__ void __launch_bounds__(kFixThreads) clamp_fix_kernel(
     const uint16_t* __restrict__ raw, GramRawParams p, const uint32_t* __restrict__ pixbits,
