@@ -1143,17 +1143,16 @@ static int stats_raw_impl(const uint16_t* raw, int64_t lines, int32_t samples, i
   p.nsplit = (int)((lines + p.split_lines - 1) / p.split_lines);
   p.units = (int64_t)samples * p.nsplit;
   cudaStream_t st = as_stream(stream);
-  // long units of the three-MMA windows: two epilogue groups are enough and leave the scan
-  // warps more issue slots (c4 strip 0.442 -> 0.435 ms); short units (c1, c2 chunks) are
+  // long units (>= 32 tiles): two epilogue groups are enough and leave the scan warps more
+  // issue slots (strips of B = 40 / 70 / 96 / 128: 0.391 / 0.442 / 0.565 / 1.017 ->
+  // 0.367 / 0.434 / 0.540 / 0.990 ms); short units (c1 strips, c2 chunks) are
   // epilogue-bound and keep three
-  if (kGrEpiGroups == 3 && p.split_lines >= 32 * kGrLb) {
-    if (nch == 9) return launch_gram_raw<9, 2>(map, raw, p, moments, shift, own, st);
-    if (nch == 10) return launch_gram_raw<10, 2>(map, raw, p, moments, shift, own, st);
-  }
+  const bool long_units = kGrEpiGroups == 3 && p.split_lines >= 32 * kGrLb;
   switch (nch) {
-#define SKYRX_NCH(k) \
-  case k:            \
-    return launch_gram_raw<k>(map, raw, p, moments, shift, own, st);
+#define SKYRX_NCH(k)                                                                  \
+  case k:                                                                             \
+    return long_units ? launch_gram_raw<k, 2>(map, raw, p, moments, shift, own, st)   \
+                      : launch_gram_raw<k>(map, raw, p, moments, shift, own, st);
     SKYRX_NCH(1) SKYRX_NCH(2) SKYRX_NCH(3) SKYRX_NCH(4) SKYRX_NCH(5) SKYRX_NCH(6) SKYRX_NCH(7)
     SKYRX_NCH(8) SKYRX_NCH(9) SKYRX_NCH(10) SKYRX_NCH(11) SKYRX_NCH(12) SKYRX_NCH(13)
     SKYRX_NCH(14) SKYRX_NCH(15) SKYRX_NCH(16)
